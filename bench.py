@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Throughput benchmark: trees/s to purity at 1M x 4096 (BASELINE.json), per B200 and aggregate.
+
+One step = one pass of the hot path over one batch: training --trees trees (default 100 per GPU,
+BASELINE config 3: synthetic 1M x 4096, 2-class, trained to purity, dynamic split switch with a
+fixed recorded breakeven) through the level-wise frontier scheduler and the sm_100a kernels.
+Multi-GPU (torchrun): trees are sharded tree-wise across ranks (weak scaling, no collective on
+the data path); rank r trains its own slice of the forest each step.
+
+value  device-timed trees/s over all ranks (CUDA events on the trainer's stream, max over ranks)
+e2e    the same through the C ABI with host buffers: every step uploads the 16.4 GB table from
+       page-locked memory (sofg_upload_dataset), trains, and reads the forest back.
+roofline  the histogram counting kernel (the dominant one), sector-model gather bytes / its
+       event-timed duration, against MEASURED_PEAKS.json's HBM copy bandwidth.
+cpu_baseline  the reference itself (oracle/_ref, compiled from the reference headers) training
+       trees of the same forest on this host's cores; those trees are also compared bit-for-bit
+       with the GPU's.
+
+`--impl reference` times the reference's CPU learner alone (all host threads).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trees/sec to purity at 1M x 4096 (2-class synthetic trunk, dynamic split switch)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=1_000_000)
+    p.add_argument("--d", type=int, default=4096)
+    p.add_argument("--trees", type=int, default=100, help="trees per GPU per step")
+    p.add_argument("--breakeven", type=int, default=1024)
+    p.add_argument("--seed", type=int, default=7)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--cpu-trees", type=int, default=0, help="CPU baseline sample (0 = one per core)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    sm, mx, reasons = [x.strip() for x in out.split(",")]
+                    self.samples.append((float(sm), float(mx), int(reasons, 16)))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x100: "display_clock_setting"}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        reasons = 0
+        for s in self.samples:
+            reasons |= s[2]
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": [v for k, v in names.items() if reasons & k and k != 0x1],
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_reference_sample(X, y, n_trees, args, threads):
+    """Reference learner (oracle/_ref) on this host: `n_trees` trees of the bench forest."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib
+
+    orc = oracle_lib.get("reference") if oracle_lib.have_reference() else oracle_lib.get("port")
+    ds = orc.dataset(X, y, 2)
+    cfg = oracle_lib.make_config(n_trees=n_trees, mode="dynamic", breakeven=args.breakeven, seed=args.seed,
+                                 n_workers=threads)
+    t0 = time.perf_counter()
+    forest = orc.train_forest_ds(ds, cfg)
+    dt = time.perf_counter() - t0
+    orc.dataset_free(ds)
+    return forest, dt, orc.kind
+
+
+def host_trunk(n, d, seed=1):
+    """Trunk-model table on the host for the reference arm (multi-threaded numpy)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    X = np.empty((d, n), np.float32)
+    mu = (1.0 / np.sqrt(np.arange(1, d + 1))).astype(np.float32)
+    sign = np.where(np.arange(n) % 2 == 0, 1.0, -1.0).astype(np.float32)
+
+    def fill(f0):
+        rng = np.random.default_rng([seed, f0])
+        for f in range(f0, min(d, f0 + 64)):
+            X[f] = rng.standard_normal(n, dtype=np.float32) + sign * mu[f]
+
+    with ThreadPoolExecutor(os.cpu_count() or 8) as ex:
+        list(ex.map(fill, range(0, d, 64)))
+    return X, (np.arange(n) % 2).astype(np.int32)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    X, y = host_trunk(args.n, args.d)
+    n_trees = args.cpu_trees or threads
+    steps = max(1, min(args.steps, 2))
+    times = []
+    for _ in range(steps):
+        _, dt, kind = cpu_reference_sample(X, y, n_trees, args, threads)
+        times.append(dt)
+    v = n_trees / statistics.median(times)
+    line = {"metric": METRIC, "value": v, "unit": "trees/s", "n_gpus": 0, "steps": steps,
+            "steps_requested": args.steps, "warmup": 0, "ms_per_step": 1000 * statistics.median(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+            "data": "synthetic trunk model (numpy, host)", "impl": "reference",
+            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, trees to purity (BASELINE config 3)",
+                       "n_samples": args.n, "n_features": args.d, "trees_per_step": n_trees,
+                       "breakeven": args.breakeven, "mode": "dynamic", "seed": args.seed},
+            "cpu_baseline": {"value": v, "unit": "trees/s", "cores": threads, "kind": kind,
+                             "sample": f"{n_trees} full trees of the 1M x 4096 forest on {threads} threads "
+                                       f"per step; {steps} step(s), no warm-up (each step ~{times[0]:.0f} s)"},
+            "e2e": {"value": v, "unit": "trees/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+
+    import paper_2603_00326_b200 as sofg
+
+    torch.cuda.set_device(local)
+    ctx = sofg.Context(local)
+    t0 = time.perf_counter()
+    ctx.generate_trunk(args.n, args.d, 2, seed=1)
+    gen_s = time.perf_counter() - t0
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
+    T = args.trees
+    per_step = T * world
+    total_trees = (args.warmup + args.steps + args.e2e_steps) * per_step
+
+    def cfg_for(step):
+        b = step * per_step + rank * T
+        return sofg.TrainConfig(n_trees=total_trees, mode="dynamic", breakeven=args.breakeven, seed=args.seed,
+                                n_workers=0, tree_begin=b, tree_end=b + T)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up ---------------------------------------------------------------------------------
+    first = None
+    for s in range(args.warmup):
+        f = ctx.train_forest(cfg_for(s))
+        if s == 0:
+            first = f
+    # ---- timed region ------------------------------------------------------------------------
+    ctx.set_stats(2)
+    ctx.reset_stats()
+    nodes = 0
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clocks:
+        ev0.record(stream)
+        for s in range(args.warmup, args.warmup + args.steps):
+            f = ctx.train_forest(cfg_for(s))
+            nodes += len(f.left)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms)
+    st = ctx.stats()
+    ctx.set_stats(0)
+    value = world * T * args.steps / (ms_max / 1000.0)
+
+    peak, peak_kind = measured_peak()
+    hist_ms = st["ms_hist_count"]
+    exact_ms = st["ms_exact"]
+    hist_launches = max(1, st["hist_count_launches"])
+    achieved = st["hist_sector_bytes"] / (hist_ms / 1000.0) / 1e9 if hist_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": "k_hist_count (projection + histogram, sector-model gathers)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "peak_kind": peak_kind, "traffic": None,
+                "algorithmic_bytes_per_launch": st["hist_sector_bytes"] / hist_launches,
+                "avg_launch_ms": hist_ms / hist_launches,
+                "strict_gbs": round(st["hist_strict_bytes"] / (hist_ms / 1000.0) / 1e9, 1) if hist_ms else 0.0,
+                "exact_kernel_gbs": round(st["exact_sector_bytes"] / (exact_ms / 1000.0) / 1e9, 1) if exact_ms else 0.0,
+                "phase_ms": {k: round(st[k], 2) for k in ("ms_sample", "ms_hist_rng", "ms_hist_count", "ms_exact",
+                                                          "ms_partition", "ms_waves_total", "ms_host_binomial",
+                                                          "ms_host_bootstrap", "ms_train_total")}}
+    gpu_launches = int(st["kernel_launches"])
+
+    # ---- end to end through the C ABI with host buffers ---------------------------------------
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        import ctypes as C
+
+        nbytes = args.n * args.d * 4
+        hptr = ctx.L.sofg_host_alloc(nbytes)
+        if not hptr:
+            raise RuntimeError("page-locked allocation failed")
+        Xh = np.ctypeslib.as_array((C.c_float * (args.n * args.d)).from_address(hptr)).reshape(args.d, args.n)
+        yh = np.zeros(args.n, np.int32)
+        ctx.download(Xh, yh)
+        barrier()
+        t_e = []
+        d2h = 0
+        for s in range(args.warmup + args.steps, args.warmup + args.steps + args.e2e_steps):
+            torch.cuda.synchronize()
+            ts = time.perf_counter()
+            ctx.upload_ptr(hptr, yh, args.n, args.d, 2)
+            f = ctx.train_forest(cfg_for(s))
+            torch.cuda.synchronize()
+            t_e.append(time.perf_counter() - ts)
+            d2h = sum(a.nbytes for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off, f.feat, f.weight))
+        e_s = max_over_ranks(sum(t_e))
+        e2e = {"value": world * T * len(t_e) / e_s, "unit": "trees/s", "h2d_bytes_per_step": nbytes + 4 * args.n,
+               "d2h_bytes_per_step": d2h, "timing": "host wall clock, cuda-synchronized, max over ranks"}
+    else:
+        Xh = None
+
+    # ---- CPU baseline (rank 0, N = 1) -----------------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n_cpu = min(args.cpu_trees or threads, T)
+        if Xh is None:
+            Xh = np.zeros((args.d, args.n), np.float32)
+            yh = np.zeros(args.n, np.int32)
+            ctx.download(Xh, yh)
+        forest, dt, kind = cpu_reference_sample(Xh, yh, n_cpu, args, threads)
+        import oracle_lib
+
+        ff = oracle_lib.FlatForest(first.tree_off, first.left, first.right, first.pred, first.thr, first.term_off,
+                                   first.feat, first.weight)
+        same = sum(ff.tree_equal(forest, t) for t in range(n_cpu))
+        cpu = {"value": n_cpu / dt, "unit": "trees/s", "cores": threads, "kind": kind,
+               "sample": f"trees 0..{n_cpu - 1} of the bench forest (full 1M x 4096 trees, one per thread), "
+                         f"{dt:.1f} s", "bitexact_trees": f"{same}/{n_cpu}"}
+
+    line = {"metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 values / f64 accumulate+gain",
+            "data": "synthetic trunk model generated in HBM (counter-based RNG), inputs > L2",
+            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, {T} trees per GPU to purity "
+                                   f"(BASELINE config 3)",
+                       "n_samples": args.n, "n_features": args.d, "trees_per_gpu_per_step": T,
+                       "mode": "dynamic", "breakeven": args.breakeven, "bin_count": 256, "seed": args.seed,
+                       "parallelism": f"tree-sharded x{world}", "l2": "inputs 16.4 GB > 126 MB L2",
+                       "nodes_per_step": nodes / args.steps, "datagen_s": round(gen_s, 2)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "clocks": clocks.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if Xh is not None and not args.no_e2e and args.e2e_steps > 0:
+        ctx.L.sofg_host_free(hptr)
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+/*
+ * sofg — C ABI of the B200-native sparse-oblique forest trainer (libsofg.so).
+ *
+ * The reference (soforest, arXiv 2603.00326) is a header-only C++ library with no plugin or FFI
+ * layer; its drop-in boundary is the train/predict API of proj/include/soforest/forest.hpp. Each
+ * entry point below replaces one reference function (cited), taking plain pointers and sizes so
+ * any FFI (ctypes, cgo, JNI, N-API) can bind it; see INTEGRATION.md.
+ *
+ * Conventions
+ *   - every call returns 0 on success, non-zero on failure; sofg_last_error() (thread-local)
+ *     describes the failure and keeps the reference's exception class as a prefix:
+ *       1 "invalid_argument: ..."  (std::invalid_argument in the reference)
+ *       2 "out_of_range: ..."      (std::out_of_range)
+ *       3 "runtime_error: ..."     (CUDA / resource failures)
+ *   - X is column-major float32: column f at X[f * n_samples .. (f+1) * n_samples)
+ *     (the reference's BasicColumnarDataset<float> columns, dataset.hpp:23-69)
+ *   - a context owns one GPU (one host thread per context); contexts are independent.
+ *   - no CPU fallback: if the CUDA kernels cannot run, calls fail.
+ */
+#ifndef SOFG_H
+#define SOFG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sofg_ctx sofg_ctx;
+typedef struct sofg_forest sofg_forest;
+
+/* Mirrors soforest::TrainConfig (forest.hpp:38-53); same field meaning and defaults. */
+typedef struct sofg_train_config {
+  uint64_t n_trees;            /* 100 */
+  int32_t mode;                /* 0 exact-only, 1 histogram-only, 2 dynamic (forest.hpp:20) */
+  int32_t two_level_binning;   /* accepted, results identical either way (histogram.hpp:118) */
+  uint64_t bin_count;          /* 256, 2..1024 */
+  int32_t has_breakeven;       /* Dynamic: histogram iff n > breakeven (split.hpp:46-48) */
+  int32_t has_max_depth;
+  uint64_t breakeven;          /* absent -> 1024 (calibrate.hpp:43 fallback) */
+  uint64_t max_depth;
+  double bootstrap_fraction;   /* 0.632 */
+  uint64_t min_samples_split;  /* 2 */
+  uint64_t max_split_retries;  /* 1 */
+  uint64_t n_workers;          /* host threads for the per-node binomial draws (0 = all) */
+  uint64_t seed;               /* 0 */
+  /* extensions */
+  uint64_t num_projections;    /* 0: ProjectionConfig::for_features (projection.hpp:39-50) */
+  double cell_density;         /* <= 0: for_features density */
+  uint64_t batch_trees;        /* trees grown together per level (0 = all / memory bound) */
+  uint64_t tree_begin;         /* train trees [tree_begin, tree_end) of the forest (sharding) */
+  uint64_t tree_end;           /* 0 = n_trees */
+} sofg_train_config;
+
+void sofg_default_config(sofg_train_config* cfg);
+const char* sofg_last_error(void);
+const char* sofg_version(void);
+
+/* ---- context / dataset ------------------------------------------------------------------ */
+int sofg_create(int device, sofg_ctx** out);
+int sofg_destroy(sofg_ctx* ctx);
+/* Upload a dataset (replaces constructing BasicColumnarDataset<float>, dataset.hpp:28-45).
+ * labels: int32 in [0, class_count). Validates like the reference constructor. */
+int sofg_upload_dataset(sofg_ctx* ctx, const float* X, uint64_t n_samples, uint64_t n_features,
+                        const int32_t* labels, int32_t class_count);
+/* Same, one pointer per column (the reference's vector<vector<float>> layout). */
+int sofg_upload_columns(sofg_ctx* ctx, const float* const* columns, uint64_t n_samples,
+                        uint64_t n_features, const int32_t* labels, int32_t class_count);
+/* Synthetic trunk-model table generated directly in HBM (bench input; not bit-identical to
+ * the reference's serial generate_trunk, dataset.hpp:306-329 — same model). */
+int sofg_generate_trunk(sofg_ctx* ctx, uint64_t n_samples, uint64_t n_features,
+                        int32_t class_count, uint64_t seed);
+/* Copy the resident table back (column-major) and the labels; either pointer may be NULL. */
+int sofg_download_dataset(sofg_ctx* ctx, float* X, int32_t* labels);
+
+/* ---- training ------------------------------------------------------------------------------ */
+/* train_forest (forest.hpp:267-313): trees tree_begin..tree_end-1 of the forest defined by cfg
+ * (tree t is a pure function of (data, cfg, t), forest.hpp:264-266, so shards concatenate). */
+int sofg_train_forest(sofg_ctx* ctx, const sofg_train_config* cfg, sofg_forest** out);
+/* train_tree (forest.hpp:250-262): one tree grown from an explicit sorted active set. */
+int sofg_train_tree(sofg_ctx* ctx, const uint32_t* active, uint64_t n_active,
+                    const sofg_train_config* cfg, uint64_t seed, uint64_t depth,
+                    sofg_forest** out);
+
+/* ---- forest access (layout shared with the CPU oracle, oracle/oracle_capi.h) --------------- */
+uint64_t sofg_forest_num_trees(const sofg_forest* f);
+uint64_t sofg_forest_num_nodes(const sofg_forest* f);
+uint64_t sofg_forest_num_terms(const sofg_forest* f);
+uint64_t sofg_forest_breakeven(const sofg_forest* f);
+void sofg_forest_export(const sofg_forest* f, int64_t* tree_off, int32_t* left, int32_t* right,
+                        int32_t* pred, float* thr, int64_t* term_off, uint32_t* feat,
+                        float* weight);
+/* Build a forest from flat arrays (e.g. an oracle forest) for sofg_predict. */
+int sofg_forest_import(uint64_t n_trees, uint64_t n_features, int32_t class_count,
+                       const int64_t* tree_off, const int32_t* left, const int32_t* right,
+                       const int32_t* pred, const float* thr, const int64_t* term_off,
+                       const uint32_t* feat, const float* weight, sofg_forest** out);
+void sofg_forest_free(sofg_forest* f);
+
+/* predict (forest.hpp:110-121) for n_rows row-major host samples on the GPU.
+ * labels[n_rows]; votes[n_rows * class_count] (may be NULL). */
+int sofg_predict(sofg_ctx* ctx, const sofg_forest* f, const float* rows, uint64_t n_rows,
+                 uint64_t n_features, int32_t* labels, double* votes);
+
+/* ---- per-function entry points (kernel-level parity with the reference) -------------------- */
+/* apply_projection (projection.hpp:86-108) on the resident table. */
+int sofg_apply_projection(sofg_ctx* ctx, const uint32_t* feat, const float* weight,
+                          uint64_t n_terms, const uint32_t* active, uint64_t n_active,
+                          float* out);
+/* sample_projection_matrix (projection.hpp:57-82) for n_nodes engines make_rng(seeds[i]) after
+ * skip[i] outputs: host binomial + device Floyd/coins. row_ptr[n_nodes][R+1] (node-local),
+ * feat/weight[n_nodes][cap], consumed[n_nodes] = outputs used by the call. */
+int sofg_sample_projection(sofg_ctx* ctx, uint64_t n_features, uint64_t num_projections,
+                           double cell_density, const uint64_t* seeds, const uint64_t* skip,
+                           uint64_t n_nodes, uint32_t* row_ptr, uint32_t* feat, float* weight,
+                           uint64_t cap, uint64_t* consumed);
+/* find_node_split (split.hpp:229-317) for one node on the device with a caller-supplied
+ * projection matrix and engine = make_rng(seed) after `skip` outputs. */
+typedef struct sofg_split {
+  int32_t found;
+  int32_t projection_index;
+  float threshold;
+  uint32_t n_left;   /* as reported by the split search */
+  uint32_t n_right;
+  uint32_t n_left_partition; /* values <= threshold (forest.hpp:205) */
+  double gain;
+  uint64_t consumed; /* engine outputs used (boundary picks) */
+} sofg_split;
+int sofg_find_node_split(sofg_ctx* ctx, const uint32_t* active, uint64_t n_active,
+                         const uint32_t* row_ptr, uint64_t n_rows, const uint32_t* feat,
+                         const float* weight, int32_t method, uint64_t bin_count, uint64_t seed,
+                         uint64_t skip, sofg_split* out);
+
+/* The context's CUDA stream (cudaStream_t) — for timing with events on the launching stream. */
+void* sofg_stream(sofg_ctx* ctx);
+/* Page-locked host buffers for end-to-end transfers (cudaMallocHost / cudaFreeHost). */
+void* sofg_host_alloc(uint64_t bytes);
+void sofg_host_free(void* p);
+
+/* ---- instrumentation ----------------------------------------------------------------------- */
+typedef struct sofg_stats {
+  double ms_sample, ms_hist_rng, ms_hist_count, ms_exact, ms_partition, ms_waves_total;
+  double ms_host_binomial, ms_host_bootstrap, ms_train_total;
+  uint64_t waves, nodes, hist_nodes, exact_nodes, kernel_launches, levels;
+  uint64_t hist_count_launches, exact_launches;
+  double hist_strict_bytes, exact_strict_bytes, hist_sector_bytes, exact_sector_bytes;
+} sofg_stats;
+/* enable: 1 = CUDA-event timing per phase (+ sector accounting when 2); 0 = off */
+int sofg_set_stats(sofg_ctx* ctx, int enable);
+int sofg_get_stats(sofg_ctx* ctx, sofg_stats* out);
+int sofg_reset_stats(sofg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

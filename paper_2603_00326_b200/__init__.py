@@ -1,0 +1,354 @@
+"""B200-native sparse-oblique split finding for the soforest learner (arXiv 2603.00326).
+
+Python host mirror of the reference's train/predict API (reference
+proj/include/soforest/forest.hpp): ``train_forest``, ``train_tree``, ``predict``, plus the
+per-function entry points the parity tests use (``find_node_split``, ``sample_projection``,
+``apply_projection``). Everything calls ``lib/libsofg.so`` (hand-written sm_100a CUDA behind the
+C ABI of ``include/sofg.h``). There is no CPU fallback: if the library or a GPU is missing, calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["TrainConfig", "Forest", "Context", "lib_path", "load", "SofgError"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "lib", "libsofg.so")
+
+
+class SofgError(RuntimeError):
+    pass
+
+
+class _Cfg(C.Structure):
+    _fields_ = [
+        ("n_trees", C.c_uint64), ("mode", C.c_int32), ("two_level_binning", C.c_int32),
+        ("bin_count", C.c_uint64), ("has_breakeven", C.c_int32), ("has_max_depth", C.c_int32),
+        ("breakeven", C.c_uint64), ("max_depth", C.c_uint64), ("bootstrap_fraction", C.c_double),
+        ("min_samples_split", C.c_uint64), ("max_split_retries", C.c_uint64),
+        ("n_workers", C.c_uint64), ("seed", C.c_uint64), ("num_projections", C.c_uint64),
+        ("cell_density", C.c_double), ("batch_trees", C.c_uint64), ("tree_begin", C.c_uint64),
+        ("tree_end", C.c_uint64),
+    ]
+
+
+class _Split(C.Structure):
+    _fields_ = [("found", C.c_int32), ("projection_index", C.c_int32), ("threshold", C.c_float),
+                ("n_left", C.c_uint32), ("n_right", C.c_uint32), ("n_left_partition", C.c_uint32),
+                ("gain", C.c_double), ("consumed", C.c_uint64)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("ms_sample", "ms_hist_rng", "ms_hist_count", "ms_exact",
+                                           "ms_partition", "ms_waves_total", "ms_host_binomial",
+                                           "ms_host_bootstrap", "ms_train_total")] + \
+               [(n, C.c_uint64) for n in ("waves", "nodes", "hist_nodes", "exact_nodes", "kernel_launches",
+                                           "levels", "hist_count_launches", "exact_launches")] + \
+               [(n, C.c_double) for n in ("hist_strict_bytes", "exact_strict_bytes", "hist_sector_bytes",
+                                          "exact_sector_bytes")]
+
+
+_MODES = {"exact": 0, "histogram": 1, "dynamic": 2}
+_lib = None
+
+
+def load():
+    """Loads libsofg.so (raises if it is missing — the product path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not os.path.exists(path):
+        raise SofgError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    vp, u64, i32, f64 = C.c_void_p, C.c_uint64, C.c_int32, C.c_double
+    P = C.POINTER
+    L.sofg_last_error.restype = C.c_char_p
+    L.sofg_version.restype = C.c_char_p
+    L.sofg_default_config.argtypes = [P(_Cfg)]
+    L.sofg_create.argtypes = [C.c_int, P(vp)]
+    L.sofg_destroy.argtypes = [vp]
+    L.sofg_upload_dataset.argtypes = [vp, vp, u64, u64, vp, i32]
+    L.sofg_upload_columns.argtypes = [vp, vp, u64, u64, vp, i32]
+    L.sofg_generate_trunk.argtypes = [vp, u64, u64, i32, u64]
+    L.sofg_download_dataset.argtypes = [vp, vp, vp]
+    L.sofg_train_forest.argtypes = [vp, P(_Cfg), P(vp)]
+    L.sofg_train_tree.argtypes = [vp, vp, u64, P(_Cfg), u64, u64, P(vp)]
+    for fn in ("sofg_forest_num_trees", "sofg_forest_num_nodes", "sofg_forest_num_terms",
+               "sofg_forest_breakeven"):
+        getattr(L, fn).restype = u64
+        getattr(L, fn).argtypes = [vp]
+    L.sofg_forest_export.argtypes = [vp] * 9
+    L.sofg_forest_import.argtypes = [u64, u64, i32] + [vp] * 8 + [P(vp)]
+    L.sofg_forest_free.argtypes = [vp]
+    L.sofg_predict.argtypes = [vp, vp, vp, u64, u64, vp, vp]
+    L.sofg_apply_projection.argtypes = [vp, vp, vp, u64, vp, u64, vp]
+    L.sofg_sample_projection.argtypes = [vp, u64, u64, f64, vp, vp, u64, vp, vp, vp, u64, vp]
+    L.sofg_find_node_split.argtypes = [vp, vp, u64, vp, u64, vp, vp, i32, u64, u64, u64, P(_Split)]
+    L.sofg_stream.restype = vp
+    L.sofg_stream.argtypes = [vp]
+    L.sofg_host_alloc.restype = vp
+    L.sofg_host_alloc.argtypes = [u64]
+    L.sofg_host_free.argtypes = [vp]
+    L.sofg_set_stats.argtypes = [vp, C.c_int]
+    L.sofg_get_stats.argtypes = [vp, P(_Stats)]
+    L.sofg_reset_stats.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def _check(rc: int, what: str):
+    if rc == 0:
+        return
+    msg = load().sofg_last_error().decode()
+    if rc == 1:
+        raise ValueError(f"{what}: {msg}")
+    if rc == 2:
+        raise IndexError(f"{what}: {msg}")
+    raise SofgError(f"{what}: {msg}")
+
+
+@dataclass
+class TrainConfig:
+    """soforest::TrainConfig (forest.hpp:38-53) plus GPU extensions."""
+
+    n_trees: int = 100
+    mode: str = "dynamic"
+    bin_count: int = 256
+    two_level_binning: bool = True
+    breakeven: int | None = None
+    bootstrap_fraction: float = 0.632
+    max_depth: int | None = None
+    min_samples_split: int = 2
+    max_split_retries: int = 1
+    n_workers: int = 0
+    seed: int = 0
+    num_projections: int = 0
+    cell_density: float = 0.0
+    batch_trees: int = 0
+    tree_begin: int = 0
+    tree_end: int = 0
+
+    def to_c(self) -> _Cfg:
+        c = _Cfg()
+        load().sofg_default_config(C.byref(c))
+        c.n_trees = self.n_trees
+        c.mode = _MODES[self.mode] if isinstance(self.mode, str) else int(self.mode)
+        c.two_level_binning = int(self.two_level_binning)
+        c.bin_count = self.bin_count
+        c.has_breakeven = int(self.breakeven is not None)
+        c.breakeven = self.breakeven or 0
+        c.has_max_depth = int(self.max_depth is not None)
+        c.max_depth = self.max_depth or 0
+        c.bootstrap_fraction = self.bootstrap_fraction
+        c.min_samples_split = self.min_samples_split
+        c.max_split_retries = self.max_split_retries
+        c.n_workers = self.n_workers
+        c.seed = self.seed
+        c.num_projections = self.num_projections
+        c.cell_density = self.cell_density
+        c.batch_trees = self.batch_trees
+        c.tree_begin = self.tree_begin
+        c.tree_end = self.tree_end
+        return c
+
+
+@dataclass
+class Forest:
+    """Flat forest; node ids follow the reference's depth-first split order."""
+
+    tree_off: np.ndarray
+    left: np.ndarray
+    right: np.ndarray
+    pred: np.ndarray
+    thr: np.ndarray
+    term_off: np.ndarray
+    feat: np.ndarray
+    weight: np.ndarray
+    breakeven: int = 0
+    class_count: int = 0
+    n_features: int = 0
+
+    @property
+    def n_trees(self) -> int:
+        return len(self.tree_off) - 1
+
+    def tree_nodes(self, t: int) -> int:
+        return int(self.tree_off[t + 1] - self.tree_off[t])
+
+
+def _export(h) -> Forest:
+    L = load()
+    T, N, Q = L.sofg_forest_num_trees(h), L.sofg_forest_num_nodes(h), L.sofg_forest_num_terms(h)
+    f = Forest(np.zeros(T + 1, np.int64), np.zeros(N, np.int32), np.zeros(N, np.int32), np.zeros(N, np.int32),
+               np.zeros(N, np.float32), np.zeros(N + 1, np.int64), np.zeros(Q, np.uint32), np.zeros(Q, np.float32),
+               int(L.sofg_forest_breakeven(h)))
+    L.sofg_forest_export(h, *(a.ctypes.data for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off,
+                                                       f.feat, f.weight)))
+    return f
+
+
+class Context:
+    """One GPU with a resident dataset (column-major float32 table + labels)."""
+
+    def __init__(self, device: int = 0):
+        self.L = load()
+        self.h = C.c_void_p()
+        _check(self.L.sofg_create(device, C.byref(self.h)), "sofg_create")
+        self.n_samples = 0
+        self.n_features = 0
+        self.class_count = 0
+
+    def close(self):
+        if self.h:
+            self.L.sofg_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- dataset ---------------------------------------------------------------------------------
+    def upload(self, X: np.ndarray, y: np.ndarray, class_count: int):
+        """X column-major [n_features][n_samples] float32 (the reference's column layout)."""
+        X = np.ascontiguousarray(X, np.float32)
+        y = np.ascontiguousarray(y, np.int32)
+        d, n = X.shape
+        _check(self.L.sofg_upload_dataset(self.h, X.ctypes.data, n, d, y.ctypes.data, class_count), "upload")
+        self.n_samples, self.n_features, self.class_count = n, d, class_count
+
+    def generate_trunk(self, n: int, d: int, class_count: int = 2, seed: int = 1):
+        _check(self.L.sofg_generate_trunk(self.h, n, d, class_count, seed), "generate_trunk")
+        self.n_samples, self.n_features, self.class_count = n, d, class_count
+
+    def download(self, X: np.ndarray | None = None, y: np.ndarray | None = None):
+        _check(self.L.sofg_download_dataset(self.h, X.ctypes.data if X is not None else None,
+                                            y.ctypes.data if y is not None else None), "download")
+
+    # -- training --------------------------------------------------------------------------------
+    def train_forest(self, cfg: TrainConfig) -> Forest:
+        c = cfg.to_c()
+        h = C.c_void_p()
+        _check(self.L.sofg_train_forest(self.h, C.byref(c), C.byref(h)), "train_forest")
+        try:
+            f = _export(h)
+        finally:
+            self.L.sofg_forest_free(h)
+        f.class_count, f.n_features = self.class_count, self.n_features
+        return f
+
+    def train_tree(self, active, cfg: TrainConfig, seed: int, depth: int = 0) -> Forest:
+        a = np.ascontiguousarray(active, np.uint32)
+        c = cfg.to_c()
+        h = C.c_void_p()
+        _check(self.L.sofg_train_tree(self.h, a.ctypes.data, len(a), C.byref(c), seed, depth, C.byref(h)),
+               "train_tree")
+        try:
+            f = _export(h)
+        finally:
+            self.L.sofg_forest_free(h)
+        f.class_count, f.n_features = self.class_count, self.n_features
+        return f
+
+    def predict(self, forest: Forest, rows: np.ndarray):
+        rows = np.ascontiguousarray(rows, np.float32)
+        n, d = rows.shape
+        h = C.c_void_p()
+        _check(self.L.sofg_forest_import(forest.n_trees, d, forest.class_count,
+                                         *(a.ctypes.data for a in (forest.tree_off, forest.left, forest.right,
+                                                                   forest.pred, forest.thr, forest.term_off,
+                                                                   forest.feat, forest.weight)), C.byref(h)),
+               "forest_import")
+        labels = np.zeros(n, np.int32)
+        votes = np.zeros((n, forest.class_count), np.float64)
+        try:
+            _check(self.L.sofg_predict(self.h, h, rows.ctypes.data, n, d, labels.ctypes.data, votes.ctypes.data),
+                   "predict")
+        finally:
+            self.L.sofg_forest_free(h)
+        return labels, votes
+
+    # -- per-function entry points ---------------------------------------------------------------
+    def apply_projection(self, feat, weight, active):
+        feat = np.ascontiguousarray(feat, np.uint32)
+        weight = np.ascontiguousarray(weight, np.float32)
+        active = np.ascontiguousarray(active, np.uint32)
+        out = np.zeros(len(active), np.float32)
+        _check(self.L.sofg_apply_projection(self.h, feat.ctypes.data, weight.ctypes.data, len(feat),
+                                            active.ctypes.data, len(active), out.ctypes.data), "apply_projection")
+        return out
+
+    def sample_projection(self, d, R, density, seeds, skips=None, cap=4096):
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        skips = np.zeros_like(seeds) if skips is None else np.ascontiguousarray(skips, np.uint64)
+        n = len(seeds)
+        row_ptr = np.zeros((n, R + 1), np.uint32)
+        feat = np.zeros((n, cap), np.uint32)
+        w = np.zeros((n, cap), np.float32)
+        used = np.zeros(n, np.uint64)
+        _check(self.L.sofg_sample_projection(self.h, d, R, density, seeds.ctypes.data, skips.ctypes.data, n,
+                                             row_ptr.ctypes.data, feat.ctypes.data, w.ctypes.data, cap,
+                                             used.ctypes.data), "sample_projection")
+        return row_ptr, feat, w, used
+
+    def find_node_split(self, active, row_ptr, feat, weight, method, bin_count, seed, skip=0):
+        a = np.ascontiguousarray(active, np.uint32)
+        rp = np.ascontiguousarray(row_ptr, np.uint32)
+        f = np.ascontiguousarray(feat, np.uint32)
+        w = np.ascontiguousarray(weight, np.float32)
+        s = _Split()
+        m = _MODES[method] if isinstance(method, str) else int(method)
+        _check(self.L.sofg_find_node_split(self.h, a.ctypes.data, len(a), rp.ctypes.data, len(rp) - 1, f.ctypes.data,
+                                           w.ctypes.data, m, bin_count, seed, skip, C.byref(s)), "find_node_split")
+        return s
+
+    def stream_ptr(self) -> int:
+        return int(self.L.sofg_stream(self.h) or 0)
+
+    def upload_ptr(self, x_ptr: int, y: np.ndarray, n: int, d: int, class_count: int):
+        """Upload from a raw (e.g. page-locked) column-major host pointer."""
+        y = np.ascontiguousarray(y, np.int32)
+        _check(self.L.sofg_upload_dataset(self.h, x_ptr, n, d, y.ctypes.data, class_count), "upload")
+        self.n_samples, self.n_features, self.class_count = n, d, class_count
+
+    # -- instrumentation -------------------------------------------------------------------------
+    def set_stats(self, mode: int = 1):
+        _check(self.L.sofg_set_stats(self.h, mode), "set_stats")
+
+    def reset_stats(self):
+        _check(self.L.sofg_reset_stats(self.h), "reset_stats")
+
+    def stats(self) -> dict:
+        s = _Stats()
+        _check(self.L.sofg_get_stats(self.h, C.byref(s)), "get_stats")
+        return {name: getattr(s, name) for name, _ in _Stats._fields_}
+
+
+def train_forest(X, y, class_count, cfg: TrainConfig, device: int = 0) -> Forest:
+    """soforest::train_forest (forest.hpp:267) on one GPU."""
+    with Context(device) as ctx:
+        ctx.upload(X, y, class_count)
+        return ctx.train_forest(cfg)
+
+
+def train_tree(X, y, class_count, active, cfg: TrainConfig, seed: int, depth: int = 0, device: int = 0) -> Forest:
+    """soforest::train_tree (forest.hpp:250)."""
+    with Context(device) as ctx:
+        ctx.upload(X, y, class_count)
+        return ctx.train_tree(active, cfg, seed, depth)

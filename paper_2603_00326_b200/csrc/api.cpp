@@ -1,0 +1,774 @@
+// C ABI (include/sofg.h) and C++ API (include/sofg/soforest_gpu.hpp) over the level-wise trainer.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/sofg.h"
+#include "../../include/sofg/soforest_gpu.hpp"
+#include "engine.hpp"
+#include "host_rng.hpp"
+#include "kernels.hpp"
+#include "trainer.hpp"
+
+struct sofg_ctx {
+  std::unique_ptr<sofg::WaveRunner> eng;
+  std::unique_ptr<sofg::ThreadPool> pool;
+  int pool_threads = 0;
+  sofg::HostTimes times;
+  int stats_mode = 0;
+};
+
+struct sofg_forest {
+  sofg::FlatForest f;
+};
+
+using sofg::cuda_check;
+using sofg::DevBuf;
+using sofg::launch_generate_trunk;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = std::string("invalid_argument: ") + e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = std::string("out_of_range: ") + e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = std::string("runtime_error: ") + e.what();
+    return 3;
+  }
+}
+
+void require_ctx(sofg_ctx* c) {
+  if (!c || !c->eng) throw std::invalid_argument("null context");
+}
+void require_data(sofg_ctx* c) {
+  require_ctx(c);
+  if (!c->eng->data().loaded()) throw std::invalid_argument("no dataset uploaded");
+}
+
+int hw_threads() {
+  const unsigned h = std::thread::hardware_concurrency();
+  return h ? int(h) : 4;
+}
+
+sofg::ThreadPool& pool_for(sofg_ctx* c, uint64_t n_workers) {
+  int want = n_workers ? int(n_workers) : hw_threads();
+  want = std::max(1, std::min(want, hw_threads()));
+  if (!c->pool || c->pool_threads != want) {
+    c->pool.reset(new sofg::ThreadPool(want));
+    c->pool_threads = want;
+  }
+  return *c->pool;
+}
+
+// Dataset staging into HBM: ld = n rounded up to 32 samples (128 B column alignment).
+void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t k,
+            const std::function<void(float* dev, uint64_t ld)>& copy_X) {
+  if (n < 1 || d < 1) throw std::invalid_argument("empty dataset");
+  if (n >= (1ull << 31)) throw std::invalid_argument("n_samples must be < 2^31");
+  if (k < 1) throw std::invalid_argument("class_count must be positive");
+  if (k > sofg::kMaxClasses)
+    throw std::invalid_argument("class_count > " + std::to_string(sofg::kMaxClasses) +
+                                " is not supported by the GPU splitter");
+  for (uint64_t i = 0; i < n; ++i)  // dataset.hpp:41-44
+    if (labels[i] < 0 || labels[i] >= k) throw std::invalid_argument("label id out of range");
+  sofg::DeviceData& D = c->eng->data();
+  cuda_check(cudaSetDevice(c->eng->device()), "cudaSetDevice");
+  D.n = n;
+  D.d = d;
+  D.k = k;
+  D.ld = (n + 31) / 32 * 32;
+  D.X.exact(D.ld * d);
+  copy_X(D.X.p, D.ld);
+  D.labels_host.assign(labels, labels + n);
+  std::vector<uint8_t> l8(n);
+  for (uint64_t i = 0; i < n; ++i) l8[i] = uint8_t(labels[i]);
+  D.lab.exact(n);
+  cuda_check(cudaMemcpy(D.lab.p, l8.data(), n, cudaMemcpyHostToDevice), "H2D labels");
+  const std::vector<double> xl = sofg::host::xlogx_table(n);
+  D.xl.exact(n + 1);
+  cuda_check(cudaMemcpy(D.xl.p, xl.data(), 8 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx");
+}
+
+struct PCfg {
+  uint32_t R;
+  double density;
+};
+PCfg projection_config(uint64_t d, uint64_t num_projections, double cell_density) {
+  // ProjectionConfig::for_features (projection.hpp:39-50)
+  const double sd = std::sqrt(double(d));
+  PCfg p;
+  p.R = uint32_t(std::ceil(1.5 * sd));
+  const double e = double(std::llround(3.0 * sd));
+  p.density = std::min(1.0, e / (double(p.R) * double(d)));
+  if (num_projections) p.R = uint32_t(num_projections);
+  if (cell_density > 0.0) p.density = cell_density;
+  return p;
+}
+
+void validate_cfg(const sofg_train_config* cfg, const sofg::DeviceData& D) {  // forest.hpp:270-276
+  if (cfg->n_trees < 1) throw std::invalid_argument("n_trees must be positive");
+  if (cfg->bin_count < 2) throw std::invalid_argument("bin_count must be at least 2");
+  if (cfg->min_samples_split < 2)
+    throw std::invalid_argument("min_samples_split must be at least 2");
+  if (!(cfg->bootstrap_fraction > 0.0) || cfg->bootstrap_fraction > 1.0)
+    throw std::invalid_argument("bootstrap fraction must be in (0, 1]");
+  if (D.n < 2) throw std::invalid_argument("need at least 2 samples");
+  if (D.k < 2) throw std::invalid_argument("need at least 2 classes");
+  if (cfg->bin_count > uint64_t(sofg::kMaxBins))
+    throw std::invalid_argument("bin_count > " + std::to_string(sofg::kMaxBins) +
+                                " is not supported by the GPU histogram splitter");
+  if (cfg->mode < 0 || cfg->mode > 2) throw std::invalid_argument("unknown split mode");
+}
+
+sofg::TrainParams params_for(const sofg_train_config* cfg, const sofg::DeviceData& D,
+                             bool forest) {
+  sofg::TrainParams P;
+  P.mode = cfg->mode;
+  P.bins = cfg->bin_count;
+  // train_forest stores the resolved breakeven only for Dynamic (forest.hpp:285-293);
+  // train_tree uses cfg.breakeven or the fallback regardless of mode (forest.hpp:258).
+  P.breakeven = cfg->has_breakeven ? cfg->breakeven : sofg::kFallbackBreakeven;
+  (void)forest;
+  if (cfg->has_max_depth) P.max_depth = cfg->max_depth;
+  P.min_samples_split = cfg->min_samples_split;
+  P.max_split_retries = cfg->max_split_retries;
+  const PCfg pc = projection_config(D.d, cfg->num_projections, cfg->cell_density);
+  P.R = pc.R;
+  P.density = pc.density;
+  P.batch_trees = cfg->batch_trees;
+  return P;
+}
+
+uint64_t auto_batch(uint64_t n_root, uint64_t n_trees) {
+  // level buffers: 2 x (4 B id + 1 B label) per root sample; keep them under ~6 GB
+  const uint64_t per_tree = 10 * std::max<uint64_t>(n_root, 1);
+  const uint64_t cap = std::max<uint64_t>(1, (6ull << 30) / per_tree);
+  return std::min(n_trees, cap);
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+void sofg_default_config(sofg_train_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->n_trees = 100;
+  c->mode = 2;
+  c->two_level_binning = 1;
+  c->bin_count = 256;
+  c->bootstrap_fraction = 0.632;
+  c->min_samples_split = 2;
+  c->max_split_retries = 1;
+  c->n_workers = 1;
+}
+
+const char* sofg_last_error(void) { return g_err.c_str(); }
+const char* sofg_version(void) { return "sofg 0.1 (sm_100a)"; }
+
+int sofg_create(int device, sofg_ctx** out) {
+  return guard([&] {
+    int n = 0;
+    cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) throw std::invalid_argument("no such CUDA device");
+    auto* c = new sofg_ctx;
+    try {
+      c->eng.reset(new sofg::WaveRunner(device));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int sofg_destroy(sofg_ctx* c) {
+  return guard([&] { delete c; });
+}
+
+int sofg_upload_dataset(sofg_ctx* c, const float* X, uint64_t n, uint64_t d, const int32_t* y,
+                        int32_t k) {
+  return guard([&] {
+    require_ctx(c);
+    upload(c, n, d, y, k, [&](float* dev, uint64_t ld) {
+      cuda_check(cudaMemcpy2D(dev, ld * 4, X, n * 4, n * 4, d, cudaMemcpyHostToDevice),
+                 "H2D table");
+    });
+  });
+}
+
+int sofg_upload_columns(sofg_ctx* c, const float* const* cols, uint64_t n, uint64_t d,
+                        const int32_t* y, int32_t k) {
+  return guard([&] {
+    require_ctx(c);
+    upload(c, n, d, y, k, [&](float* dev, uint64_t ld) {
+      for (uint64_t f = 0; f < d; ++f)
+        cuda_check(cudaMemcpyAsync(dev + f * ld, cols[f], n * 4, cudaMemcpyHostToDevice,
+                                   c->eng->stream()),
+                   "H2D column");
+      cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync columns");
+    });
+  });
+}
+
+int sofg_generate_trunk(sofg_ctx* c, uint64_t n, uint64_t d, int32_t k, uint64_t seed) {
+  return guard([&] {
+    require_ctx(c);
+    if (n < 2) throw std::invalid_argument("n_samples must be at least 2");
+    if (d == 0) throw std::invalid_argument("n_features must be positive");
+    std::vector<int32_t> y(n);
+    for (uint64_t i = 0; i < n; ++i) y[i] = int32_t(i % uint64_t(k));
+    upload(c, n, d, y.data(), k, [&](float* dev, uint64_t ld) {
+      DevBuf<uint8_t> tmp;
+      tmp.exact(n);
+      cuda_check(launch_generate_trunk(dev, ld, tmp.p, n, d, k, seed, c->eng->stream()),
+                 "generate_trunk");
+      cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync generate");
+    });
+  });
+}
+
+int sofg_download_dataset(sofg_ctx* c, float* X, int32_t* y) {
+  return guard([&] {
+    require_data(c);
+    const sofg::DeviceData& D = c->eng->data();
+    if (X)
+      cuda_check(cudaMemcpy2D(X, D.n * 4, D.X.p, D.ld * 4, D.n * 4, D.d, cudaMemcpyDeviceToHost),
+                 "D2H table");
+    if (y) std::memcpy(y, D.labels_host.data(), 4 * D.n);
+  });
+}
+
+int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** out) {
+  return guard([&] {
+    require_data(c);
+    const sofg::DeviceData& D = c->eng->data();
+    validate_cfg(cfg, D);
+    sofg::TrainParams P = params_for(cfg, D, true);
+    const uint64_t tb = cfg->tree_begin;
+    const uint64_t te = cfg->tree_end ? std::min(cfg->tree_end, cfg->n_trees) : cfg->n_trees;
+    if (tb > te) throw std::invalid_argument("tree_begin > tree_end");
+    sofg::ThreadPool& pool = pool_for(c, cfg->n_workers);
+    auto* res = new sofg_forest;
+    std::unique_ptr<sofg_forest> guard_res(res);
+    res->f.class_count = D.k;
+    res->f.n_features = D.d;
+    res->f.breakeven = cfg->mode == 2 ? P.breakeven : 0;
+    uint64_t k0 = uint64_t(std::llround(cfg->bootstrap_fraction * double(D.n)));
+    k0 = std::clamp<uint64_t>(k0, 1, D.n);
+    const uint64_t batch = P.batch_trees ? P.batch_trees : auto_batch(k0, te - tb);
+    for (uint64_t t0 = tb; t0 < te; t0 += batch) {
+      const uint64_t t1 = std::min(te, t0 + batch);
+      const size_t B = size_t(t1 - t0);
+      std::vector<std::vector<uint32_t>> roots(B);
+      std::vector<uint64_t> seeds(B);
+      const auto tbs = std::chrono::steady_clock::now();
+      pool.parallel_for(B, [&](size_t b) {
+        const uint64_t ts = sofg::host::derive_seed(cfg->seed, t0 + b + 1);  // forest.hpp:305
+        roots[b] = sofg::host::bootstrap_indices(D.n, cfg->bootstrap_fraction,
+                                                 sofg::host::derive_seed(ts, 0));
+        seeds[b] = sofg::host::derive_seed(ts, 1);
+      });
+      c->times.ms_bootstrap +=
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tbs).count();
+      sofg::grow_trees(*c->eng, P, pool, roots, seeds, 0, res->f, c->times);
+    }
+    *out = guard_res.release();
+  });
+}
+
+int sofg_train_tree(sofg_ctx* c, const uint32_t* active, uint64_t n_active,
+                    const sofg_train_config* cfg, uint64_t seed, uint64_t depth,
+                    sofg_forest** out) {
+  return guard([&] {
+    require_data(c);
+    const sofg::DeviceData& D = c->eng->data();
+    if (n_active == 0) throw std::invalid_argument("active sample set is empty");  // forest.hpp:254
+    for (uint64_t i = 0; i < n_active; ++i)
+      if (active[i] >= D.n) throw std::out_of_range("sample index out of range");  // :256
+    if (cfg->bin_count < 2) throw std::invalid_argument("bin_count must be at least 2");
+    if (cfg->bin_count > uint64_t(sofg::kMaxBins))
+      throw std::invalid_argument("bin_count exceeds the GPU histogram splitter");
+    sofg::TrainParams P = params_for(cfg, D, false);
+    sofg::ThreadPool& pool = pool_for(c, cfg->n_workers);
+    auto* res = new sofg_forest;
+    std::unique_ptr<sofg_forest> guard_res(res);
+    res->f.class_count = D.k;
+    res->f.n_features = D.d;
+    std::vector<std::vector<uint32_t>> roots{std::vector<uint32_t>(active, active + n_active)};
+    std::vector<uint64_t> seeds{seed};
+    sofg::grow_trees(*c->eng, P, pool, roots, seeds, uint32_t(depth), res->f, c->times);
+    *out = guard_res.release();
+  });
+}
+
+uint64_t sofg_forest_num_trees(const sofg_forest* f) { return f->f.n_trees(); }
+uint64_t sofg_forest_num_nodes(const sofg_forest* f) { return f->f.left.size(); }
+uint64_t sofg_forest_num_terms(const sofg_forest* f) { return f->f.feat.size(); }
+uint64_t sofg_forest_breakeven(const sofg_forest* f) { return f->f.breakeven; }
+
+void sofg_forest_export(const sofg_forest* fo, int64_t* tree_off, int32_t* left, int32_t* right,
+                        int32_t* pred, float* thr, int64_t* term_off, uint32_t* feat,
+                        float* weight) {
+  const sofg::FlatForest& f = fo->f;
+  std::memcpy(tree_off, f.tree_off.data(), 8 * f.tree_off.size());
+  std::memcpy(left, f.left.data(), 4 * f.left.size());
+  std::memcpy(right, f.right.data(), 4 * f.right.size());
+  std::memcpy(pred, f.pred.data(), 4 * f.pred.size());
+  std::memcpy(thr, f.thr.data(), 4 * f.thr.size());
+  std::memcpy(term_off, f.term_off.data(), 8 * f.term_off.size());
+  std::memcpy(feat, f.feat.data(), 4 * f.feat.size());
+  std::memcpy(weight, f.weight.data(), 4 * f.weight.size());
+}
+
+int sofg_forest_import(uint64_t n_trees, uint64_t n_features, int32_t k, const int64_t* tree_off,
+                       const int32_t* left, const int32_t* right, const int32_t* pred,
+                       const float* thr, const int64_t* term_off, const uint32_t* feat,
+                       const float* weight, sofg_forest** out) {
+  return guard([&] {
+    auto* r = new sofg_forest;
+    sofg::FlatForest& f = r->f;
+    const uint64_t N = uint64_t(tree_off[n_trees]);
+    const uint64_t Q = uint64_t(term_off[N]);
+    f.tree_off.assign(tree_off, tree_off + n_trees + 1);
+    f.left.assign(left, left + N);
+    f.right.assign(right, right + N);
+    f.pred.assign(pred, pred + N);
+    f.thr.assign(thr, thr + N);
+    f.term_off.assign(term_off, term_off + N + 1);
+    f.feat.assign(feat, feat + Q);
+    f.weight.assign(weight, weight + Q);
+    f.class_count = k;
+    f.n_features = n_features;
+    *out = r;
+  });
+}
+
+void sofg_forest_free(sofg_forest* f) { delete f; }
+
+int sofg_predict(sofg_ctx* c, const sofg_forest* fo, const float* rows, uint64_t n_rows,
+                 uint64_t d, int32_t* labels, double* votes) {
+  return guard([&] {
+    require_ctx(c);
+    const sofg::FlatForest& f = fo->f;
+    if (d != f.n_features)
+      throw std::invalid_argument("sample has " + std::to_string(d) + " features, model expects " +
+                                  std::to_string(f.n_features));  // forest.hpp:112-113
+    const int k = f.class_count;
+    const int T = int(f.n_trees());
+    if (n_rows == 0) return;
+    cudaStream_t st = c->eng->stream();
+    cuda_check(cudaSetDevice(c->eng->device()), "cudaSetDevice");
+    DevBuf<float> drows;
+    DevBuf<int64_t> dto, dqo;
+    DevBuf<int32_t> dl, dr, dp;
+    DevBuf<float> dt;
+    DevBuf<uint32_t> dq, dv;
+    std::vector<uint32_t> terms(f.feat.size());
+    for (size_t q = 0; q < terms.size(); ++q)
+      terms[q] = sofg::encode_term(f.feat[q], f.weight[q] < 0.f);
+    auto up = [&](auto& buf, const auto& vec) {
+      using T0 = typename std::decay_t<decltype(vec)>::value_type;
+      buf.exact(vec.size());
+      if (!vec.empty())
+        cuda_check(cudaMemcpyAsync(buf.p, vec.data(), sizeof(T0) * vec.size(),
+                                   cudaMemcpyHostToDevice, st),
+                   "H2D forest");
+    };
+    drows.exact(n_rows * d);
+    cuda_check(cudaMemcpyAsync(drows.p, rows, 4 * n_rows * d, cudaMemcpyHostToDevice, st), "H2D rows");
+    up(dto, f.tree_off);
+    up(dl, f.left);
+    up(dr, f.right);
+    up(dp, f.pred);
+    up(dt, f.thr);
+    up(dqo, f.term_off);
+    up(dq, terms);
+    dv.exact(n_rows * uint64_t(k));
+    cuda_check(cudaMemsetAsync(dv.p, 0, 4 * n_rows * uint64_t(k), st), "memset votes");
+    cuda_check(sofg::launch_predict(drows.p, n_rows, d, dto.p, T, dl.p, dr.p, dp.p, dt.p, dqo.p,
+                                    dq.p, k, dv.p, st),
+               "predict");
+    std::vector<uint32_t> hv(n_rows * uint64_t(k));
+    cuda_check(cudaMemcpyAsync(hv.data(), dv.p, 4 * hv.size(), cudaMemcpyDeviceToHost, st), "D2H votes");
+    cuda_check(cudaStreamSynchronize(st), "sync predict");
+    for (uint64_t i = 0; i < n_rows; ++i) {
+      int32_t best = 0;
+      for (int cc = 0; cc < k; ++cc) {
+        const double v = double(hv[i * k + cc]) / double(T);  // forest.hpp:116
+        if (votes) votes[i * k + cc] = v;
+        if (hv[i * k + cc] > hv[i * k + best]) best = cc;
+      }
+      labels[i] = best;
+    }
+  });
+}
+
+int sofg_apply_projection(sofg_ctx* c, const uint32_t* feat, const float* weight, uint64_t nt,
+                          const uint32_t* active, uint64_t n, float* out) {
+  return guard([&] {
+    require_data(c);
+    const sofg::DeviceData& D = c->eng->data();
+    for (uint64_t i = 0; i < n; ++i)
+      if (active[i] >= D.n) throw std::out_of_range("sample index out of range");
+    std::vector<uint32_t> t(nt);
+    for (uint64_t q = 0; q < nt; ++q) {
+      if (feat[q] >= D.d) throw std::out_of_range("feature index out of range");
+      t[q] = sofg::encode_term(feat[q], weight[q] < 0.f);
+    }
+    if (n == 0) return;
+    cudaStream_t st = c->eng->stream();
+    DevBuf<uint32_t> dt, da;
+    DevBuf<float> dout;
+    dt.exact(nt);
+    da.exact(n);
+    dout.exact(n);
+    if (nt) cuda_check(cudaMemcpyAsync(dt.p, t.data(), 4 * nt, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(da.p, active, 4 * n, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(sofg::launch_apply_projection(D.X.p, D.ld, dt.p, int(nt), da.p, n, dout.p, st),
+               "apply_projection");
+    cuda_check(cudaMemcpyAsync(out, dout.p, 4 * n, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int sofg_sample_projection(sofg_ctx* c, uint64_t d, uint64_t R, double density,
+                           const uint64_t* seeds, const uint64_t* skip, uint64_t n_nodes,
+                           uint32_t* row_ptr, uint32_t* feat, float* weight, uint64_t cap,
+                           uint64_t* consumed) {
+  return guard([&] {
+    require_ctx(c);
+    if (d == 0 || R == 0) throw std::invalid_argument("projection config is empty");
+    if (!(density >= 0.0) || density > 1.0)
+      throw std::invalid_argument("cell density must be in [0, 1]");
+    if (R * d >= (1ull << 32)) throw std::invalid_argument("projection matrix has >= 2^32 cells");
+    sofg::host::BinomialDraw binom(R * d, density);
+    std::vector<sofg::NodeIn> nodes(n_nodes);
+    uint64_t off = 0, zmax = 32;
+    for (uint64_t i = 0; i < n_nodes; ++i) {
+      uint64_t used;
+      const uint64_t z = binom(seeds[i], skip[i], &used);
+      if (z > cap) throw std::invalid_argument("projection nonzeros exceed output capacity");
+      nodes[i] = sofg::NodeIn{};
+      nodes[i].seed = seeds[i];
+      nodes[i].z = uint32_t(z);
+      nodes[i].pos = uint32_t(used);
+      nodes[i].term_off = uint32_t(off);
+      off += z;
+      zmax = std::max(zmax, z);
+    }
+    cudaStream_t st = c->eng->stream();
+    DevBuf<sofg::NodeIn> dn;
+    DevBuf<uint32_t> dterms, drp, dpos;
+    dn.exact(n_nodes);
+    dterms.exact(off + 1);
+    drp.exact(n_nodes * (R + 1));
+    dpos.exact(n_nodes);
+    cuda_check(cudaMemcpyAsync(dn.p, nodes.data(), sizeof(sofg::NodeIn) * n_nodes,
+                               cudaMemcpyHostToDevice, st),
+               "H2D nodes");
+    cuda_check(sofg::launch_sample_projection(dn.p, int(n_nodes), uint32_t(d), uint32_t(R),
+                                              uint32_t(zmax), dterms.p, drp.p, dpos.p, st),
+               "sample_projection");
+    std::vector<uint32_t> ht(off + 1), hrp(n_nodes * (R + 1)), hpos(n_nodes);
+    cuda_check(cudaMemcpyAsync(ht.data(), dterms.p, 4 * (off + 1), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(hrp.data(), drp.p, 4 * hrp.size(), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(hpos.data(), dpos.p, 4 * n_nodes, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync sample");
+    for (uint64_t i = 0; i < n_nodes; ++i) {
+      for (uint64_t r = 0; r <= R; ++r) row_ptr[i * (R + 1) + r] = hrp[i * (R + 1) + r];
+      for (uint32_t q = 0; q < nodes[i].z; ++q) {
+        const uint32_t t = ht[nodes[i].term_off + q];
+        feat[i * cap + q] = t >> 1;
+        weight[i * cap + q] = (t & 1u) ? -1.f : 1.f;
+      }
+      consumed[i] = uint64_t(hpos[i]) - skip[i];
+    }
+  });
+}
+
+int sofg_find_node_split(sofg_ctx* c, const uint32_t* active, uint64_t n, const uint32_t* row_ptr,
+                         uint64_t R, const uint32_t* feat, const float* weight, int32_t method,
+                         uint64_t bins, uint64_t seed, uint64_t skip, sofg_split* out) {
+  return guard([&] {
+    require_data(c);
+    const sofg::DeviceData& D = c->eng->data();
+    std::memset(out, 0, sizeof(*out));
+    if (n < 2) return;  // split.hpp:238
+    if (bins < 2) throw std::invalid_argument("bin_count must be at least 2");
+    if (bins > uint64_t(sofg::kMaxBins)) throw std::invalid_argument("bin_count too large");
+    for (uint64_t i = 0; i < n; ++i)
+      if (active[i] >= D.n) throw std::out_of_range("sample index out of range");
+    const uint64_t nnz = row_ptr[R];
+    sofg::WaveSpec w;
+    w.R = uint32_t(R);
+    w.d = uint32_t(D.d);
+    w.bins = uint32_t(bins);
+    w.k = D.k;
+    w.given_csr = true;
+    w.given_terms.resize(nnz);
+    for (uint64_t q = 0; q < nnz; ++q) {
+      if (feat[q] >= D.d) throw std::out_of_range("feature index out of range");
+      w.given_terms[q] = sofg::encode_term(feat[q], weight[q] < 0.f);
+    }
+    w.given_row_ptr.assign(row_ptr, row_ptr + R + 1);
+    w.given_pos = {uint32_t(skip)};
+    uint32_t counts[sofg::kMaxClasses] = {0};
+    std::vector<uint8_t> l8(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      l8[i] = uint8_t(D.labels_host[active[i]]);
+      counts[l8[i]]++;
+    }
+    sofg::NodeIn nd{};
+    nd.seed = seed;
+    nd.begin = 0;
+    nd.n = uint32_t(n);
+    nd.z = uint32_t(nnz);
+    nd.pos = uint32_t(skip);
+    nd.flags = sofg::kNodeGivenCsr | (method == 1 ? sofg::kNodeHist : 0u);
+    nd.parent = sofg::host::entropy(counts, D.k);
+    w.nodes = {nd};
+    cudaStream_t st = c->eng->stream();
+    DevBuf<uint32_t> di, dio;
+    DevBuf<uint8_t> dl, dlo;
+    di.exact(n);
+    dio.exact(n);
+    dl.exact(n);
+    dlo.exact(n);
+    cuda_check(cudaMemcpyAsync(di.p, active, 4 * n, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(dl.p, l8.data(), n, cudaMemcpyHostToDevice, st), "H2D");
+    w.idx_in = di.p;
+    w.lab_in = dl.p;
+    w.idx_out = dio.p;
+    w.lab_out = dlo.p;
+    std::vector<sofg::NodeRes> res;
+    c->eng->run(w, res);
+    const sofg::NodeRes& r = res[0];
+    out->found = r.row >= 0;
+    out->projection_index = r.row;
+    out->threshold = r.threshold;
+    out->gain = r.gain;
+    out->n_left = r.n_left_search;
+    out->n_right = r.row >= 0 ? uint32_t(n) - r.n_left_search : 0;
+    out->n_left_partition = r.n_left;
+    out->consumed = uint64_t(r.pos_after) - skip;
+  });
+}
+
+void* sofg_stream(sofg_ctx* c) { return c && c->eng ? (void*)c->eng->stream() : nullptr; }
+
+void* sofg_host_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void sofg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int sofg_set_stats(sofg_ctx* c, int enable) {
+  return guard([&] {
+    require_ctx(c);
+    c->stats_mode = enable;
+    c->eng->collect_stats = enable != 0;
+    c->eng->sector_accounting = enable >= 2;
+  });
+}
+
+int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
+  return guard([&] {
+    require_ctx(c);
+    std::memset(o, 0, sizeof(*o));
+    const sofg::WaveStats& s = c->eng->stats;
+    o->ms_sample = s.ms_sample;
+    o->ms_hist_rng = s.ms_hist_rng;
+    o->ms_hist_count = s.ms_hist_count;
+    o->ms_exact = s.ms_exact;
+    o->ms_partition = s.ms_partition;
+    o->ms_waves_total = s.ms_total;
+    o->ms_host_binomial = c->times.ms_binomial;
+    o->ms_host_bootstrap = c->times.ms_bootstrap;
+    o->ms_train_total = c->times.ms_total;
+    o->waves = s.waves;
+    o->nodes = s.nodes;
+    o->hist_nodes = s.hist_nodes;
+    o->exact_nodes = s.exact_nodes;
+    o->kernel_launches = s.launches;
+    o->levels = c->times.levels;
+    o->hist_count_launches = s.hist_count_launches;
+    o->exact_launches = s.exact_launches;
+    o->hist_strict_bytes = s.hist_strict_bytes;
+    o->exact_strict_bytes = s.exact_strict_bytes;
+    o->hist_sector_bytes = s.hist_sector_bytes;
+    o->exact_sector_bytes = s.exact_sector_bytes;
+  });
+}
+
+int sofg_reset_stats(sofg_ctx* c) {
+  return guard([&] {
+    require_ctx(c);
+    c->eng->stats = sofg::WaveStats{};
+    c->times = sofg::HostTimes{};
+  });
+}
+
+}  // extern "C"
+
+// =============================================================================== C++ API
+namespace sofg {
+
+ColumnarDataset::ColumnarDataset(std::vector<std::vector<float>> columns,
+                                 std::vector<std::int32_t> labels,
+                                 std::vector<std::string> label_names)
+    : columns_(std::move(columns)), labels_(std::move(labels)), label_names_(std::move(label_names)) {
+  for (const auto& col : columns_)  // dataset.hpp:35-44
+    if (col.size() != labels_.size())
+      throw std::invalid_argument("column length does not match label count");
+  for (std::int32_t y : labels_)
+    if (y < 0 || static_cast<std::size_t>(y) >= label_names_.size())
+      throw std::invalid_argument("label id out of range");
+}
+
+namespace {
+
+sofg_train_config to_c(const TrainConfig& t) {
+  sofg_train_config c;
+  sofg_default_config(&c);
+  c.n_trees = t.n_trees;
+  c.mode = t.mode == SplitMode::kExactOnly ? 0 : t.mode == SplitMode::kHistogramOnly ? 1 : 2;
+  c.two_level_binning = t.two_level_binning;
+  c.bin_count = t.bin_count;
+  c.has_breakeven = t.breakeven.has_value();
+  c.breakeven = t.breakeven.value_or(0);
+  c.has_max_depth = t.max_depth.has_value();
+  c.max_depth = t.max_depth.value_or(0);
+  c.bootstrap_fraction = t.bootstrap_fraction;
+  c.min_samples_split = t.min_samples_split;
+  c.max_split_retries = t.max_split_retries;
+  c.n_workers = t.n_workers;
+  c.seed = t.seed;
+  c.num_projections = t.num_projections;
+  c.cell_density = t.cell_density;
+  c.batch_trees = t.batch_trees;
+  return c;
+}
+
+void throw_last(int rc) {
+  const std::string m = sofg_last_error();
+  if (rc == 1) throw std::invalid_argument(m);
+  if (rc == 2) throw std::out_of_range(m);
+  throw std::runtime_error(m);
+}
+
+struct CtxHolder {
+  sofg_ctx* c = nullptr;
+  explicit CtxHolder(int dev) {
+    const int rc = sofg_create(dev, &c);
+    if (rc) throw_last(rc);
+  }
+  ~CtxHolder() { sofg_destroy(c); }
+};
+
+void upload_dataset(sofg_ctx* c, const ColumnarDataset& data) {
+  std::vector<const float*> cols(data.n_features());
+  for (std::size_t f = 0; f < cols.size(); ++f) cols[f] = data.column(f).data();
+  const int rc = sofg_upload_columns(c, cols.data(), data.n_samples(), data.n_features(),
+                                     data.labels().data(), data.class_count());
+  if (rc) throw_last(rc);
+}
+
+std::vector<Tree> to_trees(const sofg_forest* f) {
+  const FlatForest& F = f->f;
+  std::vector<Tree> out(F.n_trees());
+  for (std::size_t t = 0; t < out.size(); ++t) {
+    for (int64_t q = F.tree_off[t]; q < F.tree_off[t + 1]; ++q) {
+      TreeNode nd;
+      nd.left = F.left[size_t(q)];
+      nd.right = F.right[size_t(q)];
+      nd.predicted_class = F.pred[size_t(q)];
+      nd.threshold = F.thr[size_t(q)];
+      for (int64_t u = F.term_off[size_t(q)]; u < F.term_off[size_t(q) + 1]; ++u)
+        nd.projection.push_back({F.feat[size_t(u)], F.weight[size_t(u)]});
+      out[t].nodes.push_back(std::move(nd));
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+Forest train_forest(const ColumnarDataset& data, const TrainConfig& cfg) {
+  CtxHolder h(cfg.device);
+  upload_dataset(h.c, data);
+  const sofg_train_config c = to_c(cfg);
+  sofg_forest* f = nullptr;
+  const int rc = sofg_train_forest(h.c, &c, &f);
+  if (rc) throw_last(rc);
+  Forest out;
+  out.n_features = std::uint32_t(data.n_features());
+  out.class_count = data.class_count();
+  out.label_names = data.label_names();
+  out.config = cfg;
+  out.breakeven = f->f.breakeven;
+  out.trees = to_trees(f);
+  sofg_forest_free(f);
+  return out;
+}
+
+Tree train_tree(const ColumnarDataset& data, const SampleIndexSet& active, const TrainConfig& cfg,
+                std::uint64_t seed, std::size_t depth) {
+  CtxHolder h(cfg.device);
+  upload_dataset(h.c, data);
+  const sofg_train_config c = to_c(cfg);
+  sofg_forest* f = nullptr;
+  const int rc = sofg_train_tree(h.c, active.indices.data(), active.indices.size(), &c, seed,
+                                 depth, &f);
+  if (rc) throw_last(rc);
+  Tree t = std::move(to_trees(f)[0]);
+  sofg_forest_free(f);
+  return t;
+}
+
+Prediction predict(const Forest& forest, std::span<const float> sample) {  // forest.hpp:110-121
+  if (sample.size() != forest.n_features)
+    throw std::invalid_argument("sample has " + std::to_string(sample.size()) +
+                                " features, model expects " + std::to_string(forest.n_features));
+  FlatForest F;
+  F.class_count = forest.class_count;
+  F.n_features = forest.n_features;
+  for (const Tree& t : forest.trees) {
+    for (const TreeNode& nd : t.nodes) {
+      F.left.push_back(nd.left);
+      F.right.push_back(nd.right);
+      F.pred.push_back(nd.predicted_class);
+      F.thr.push_back(nd.threshold);
+      for (const auto& term : nd.projection) {
+        F.feat.push_back(term.feature);
+        F.weight.push_back(term.weight);
+      }
+      F.term_off.push_back(int64_t(F.feat.size()));
+    }
+    F.tree_off.push_back(int64_t(F.left.size()));
+  }
+  sofg_forest holder{std::move(F)};
+  CtxHolder h(forest.config.device);
+  Prediction p;
+  p.votes.assign(std::size_t(forest.class_count), 0.0);
+  const int rc = sofg_predict(h.c, &holder, sample.data(), 1, sample.size(), &p.label, p.votes.data());
+  if (rc) throw_last(rc);
+  return p;
+}
+
+}  // namespace sofg

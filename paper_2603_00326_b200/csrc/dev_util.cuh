@@ -1,0 +1,138 @@
+// Device helpers shared by the split-finding kernels: bit-exact restatements of the reference's
+// scalar helpers plus warp-level sorting / scanning primitives.
+#pragma once
+#include <cstdint>
+
+#include "common.hpp"
+
+namespace sofg {
+namespace dev {
+
+// split.hpp:126-134 — order-preserving float -> u32 map.
+__device__ __forceinline__ uint32_t order_key(float v) {
+  const uint32_t u = __float_as_uint(v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float order_key_inv(uint32_t k) {
+  const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+
+// histogram.hpp:23-28 as the reference's default build computes it (g++ -O2 -march=native
+// contracts a + (b - a) / 2 into vfmadd132ss): fma(b - a, 0.5f, a), clamped below b.
+__device__ __forceinline__ float midpoint_down(float a, float b) {
+  const float t = __fmaf_rn(__fsub_rn(b, a), 0.5f, a);
+  return (t < b) ? t : a;
+}
+
+// projection.hpp:86-108 for one sample: terms in ascending feature order, double accumulation,
+// first term assigns, later terms add, rounded to float once. Weights are +-1 so w*x is exact.
+__device__ __forceinline__ float project_sample(const float* __restrict__ X, uint64_t ld,
+                                                const uint32_t* __restrict__ terms, int nt,
+                                                uint32_t sample) {
+  if (nt == 0) return 0.f;
+  double acc = 0.0;
+  for (int t = 0; t < nt; ++t) {
+    const uint32_t tm = terms[t];
+    const float x = __ldg(X + uint64_t(tm >> 1) * ld + sample);
+    const double dx = (tm & 1u) ? -double(x) : double(x);
+    acc = (t == 0) ? dx : __dadd_rn(acc, dx);
+  }
+  return __double2float_rn(acc);
+}
+
+// Warp-cooperative bitonic sort of a[0..P), P a power of two >= 2, ascending.
+template <class K>
+__device__ __forceinline__ void warp_bitonic_sort(K* a, int P, int lane) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        const int p = i ^ j;
+        if (p > i) {
+          const K x = a[i], y = a[p];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[p] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Register bitonic sort of one key per lane (32 keys), ascending by lane.
+template <class K>
+__device__ __forceinline__ K warp_sort32(K v, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const K o = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool lower = (lane & j) == 0;
+      const bool up = (lane & k) == 0;
+      // keep min when (lower && up) || (!lower && !up)
+      const bool take_min = (lower == up);
+      v = take_min ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t v, int lane, uint32_t* total) {
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  *total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+__device__ __forceinline__ double warp_min_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Impurity sum of a candidate split: X = f(nl) - sum_c f(l_c) + f(nr) - sum_c f(r_c) with
+// f = xlogx, in the reference's operation order (split.hpp:66-76). gain = parent - X / n.
+// Division and subtraction are monotone, so the best gain is attained at min X; the exact
+// first-maximum position is then resolved among candidates whose X lies within a window of the
+// minimum (see first_best_in_window).
+template <int KC>
+__device__ __forceinline__ double impurity_sum(const double* __restrict__ xl, const uint32_t* left,
+                                               const uint32_t* total, int k, uint32_t nl,
+                                               uint32_t nr) {
+  double sl = 0.0, sr = 0.0;
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    if (c < k) {
+      sl = __dadd_rn(sl, xl[left[c]]);
+      sr = __dadd_rn(sr, xl[total[c] - left[c]]);
+    }
+  }
+  return __dsub_rn(__dadd_rn(__dsub_rn(xl[nl], sl), xl[nr]), sr);
+}
+
+__device__ __forceinline__ double gain_from_x(double parent, double X, double n) {
+  return __dsub_rn(parent, __ddiv_rn(X, n));
+}
+
+// Window around Xmin that contains every X whose gain rounds to the same double as Xmin's.
+// |q1 - q2| <= 2 ulp(max(parent, q)) for equal results; scaled back by n with a 2^10 margin.
+__device__ __forceinline__ double x_window(double parent, double xmin, double n) {
+  const double q = xmin / n;
+  const double mag = fmax(fabs(parent), fabs(q));
+  return xmin + (mag * n + fabs(xmin)) * 0x1p-40 + 1e-300;
+}
+
+}  // namespace dev
+}  // namespace sofg

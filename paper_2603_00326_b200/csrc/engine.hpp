@@ -1,0 +1,156 @@
+// Device context and the per-wave launch sequence.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace sofg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  T* ensure(size_t n) {
+    if (n <= cap && p) return p;
+    release();
+    size_t want = n < 64 ? 64 : n + n / 4;
+    cuda_check(cudaMalloc(&p, want * sizeof(T)), "cudaMalloc");
+    cap = want;
+    return p;
+  }
+  T* exact(size_t n) {  // no slack (large one-off buffers)
+    if (n <= cap && p) return p;
+    release();
+    cuda_check(cudaMalloc(&p, (n ? n : 1) * sizeof(T)), "cudaMalloc");
+    cap = n ? n : 1;
+    return p;
+  }
+};
+
+template <class T>
+struct PinnedBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  T* ensure(size_t n) {
+    if (n <= cap && p) return p;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    size_t want = n < 64 ? 64 : n + n / 4;
+    cuda_check(cudaMallocHost(&p, want * sizeof(T)), "cudaMallocHost");
+    cap = want;
+    return p;
+  }
+};
+
+// Dataset resident in HBM: column-major float table with a 32-sample-aligned leading dimension,
+// u8 labels, and the reference's xlogx table up to n.
+struct DeviceData {
+  DevBuf<float> X;
+  DevBuf<uint8_t> lab;
+  DevBuf<double> xl;
+  uint64_t n = 0, d = 0, ld = 0;
+  int k = 0;
+  std::vector<int32_t> labels_host;  // for root class counts
+  bool loaded() const { return n > 0; }
+};
+
+// One wave: a set of open nodes searched and partitioned together.
+struct WaveSpec {
+  uint32_t R = 0, d = 0, bins = 256;
+  int k = 2;
+  int chunk_cap = 8192;
+  std::vector<NodeIn> nodes;
+  // optional host-supplied projection matrices (kNodeGivenCsr on every node)
+  bool given_csr = false;
+  std::vector<uint32_t> given_terms;    // concatenated, node i at nodes[i].term_off
+  std::vector<uint32_t> given_row_ptr;  // [nodes][R+1]
+  std::vector<uint32_t> given_pos;      // stream position after the matrix (per node)
+  // level buffers
+  const uint32_t* idx_in = nullptr;
+  const uint8_t* lab_in = nullptr;
+  uint32_t* idx_out = nullptr;
+  uint8_t* lab_out = nullptr;
+};
+
+struct WaveStats {
+  double ms_sample = 0, ms_hist_rng = 0, ms_hist_count = 0, ms_exact = 0, ms_partition = 0;
+  double ms_total = 0;
+  uint64_t waves = 0, nodes = 0, hist_nodes = 0, exact_nodes = 0;
+  uint64_t launches = 0;
+  // algorithmic gather bytes (useful 4 B per gathered value; 32 B-sector model)
+  double hist_strict_bytes = 0, hist_sector_bytes = 0, exact_strict_bytes = 0,
+         exact_sector_bytes = 0;
+  uint64_t hist_count_launches = 0, exact_launches = 0;
+};
+
+class WaveRunner {
+ public:
+  explicit WaveRunner(int device);
+  ~WaveRunner();
+  WaveRunner(const WaveRunner&) = delete;
+  WaveRunner& operator=(const WaveRunner&) = delete;
+
+  cudaStream_t stream() const { return st_; }
+  int device() const { return device_; }
+  DeviceData& data() { return data_; }
+  const DeviceData& data() const { return data_; }
+
+  // Searches and partitions every node of `w`; res[i] receives node i's result.
+  void run(const WaveSpec& w, std::vector<NodeRes>& res);
+  // Terms of projection row `row` of node `node` of the last wave (for rows longer than the
+  // kWinTermsMax terms NodeRes carries inline).
+  std::vector<uint32_t> fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row);
+
+  WaveStats stats;
+  bool collect_stats = false;   // CUDA-event timing per phase + sector accounting
+  bool sector_accounting = false;
+
+ private:
+  int device_;
+  cudaStream_t st_ = nullptr;
+  cudaEvent_t ev_[6]{};
+  DeviceData data_;
+
+  // packed host->device inputs
+  PinnedBuf<unsigned char> h_in_;
+  DevBuf<unsigned char> d_in_;
+  PinnedBuf<NodeRes> h_res_;
+  // device scratch
+  DevBuf<uint32_t> terms_, row_ptr_, pos_proj_, pos_split_, draws_, nb_, flags_, tile_left_,
+      gcnt_, done_, sectors_;
+  DevBuf<float> bnd_;
+  DevBuf<RowRes> rowres_;
+  DevBuf<NodeRes> res_;
+  const uint32_t* last_terms_ = nullptr;
+  const uint32_t* last_rp_ = nullptr;
+};
+
+}  // namespace sofg

@@ -1,0 +1,127 @@
+// Host side of the per-node random stream.
+//
+// The reference seeds one std::mt19937_64 per node (make_rng, reference random.hpp:26) and draws
+// the projection nonzero count with std::binomial_distribution<long long> (projection.hpp:66-67),
+// whose rejection sampler uses glibc log/lgamma/exp — so that single draw stays on the host, on
+// the same libstdc++/libm as the reference. Everything after it (Floyd cells, coins, boundary
+// picks) is integer-only and is regenerated on the device from (seed, outputs consumed).
+//
+// LazyMt64 produces exactly std::mt19937_64's output sequence but only computes the seeding
+// recurrence as far as the requested outputs need it: output i < 156 of the first block depends
+// on seed words i, i+1 and i+156, so the handful of outputs a binomial draw consumes costs ~160
+// recurrence steps instead of 312 + a full twist.
+#pragma once
+#include <cstdint>
+#include <random>
+#include <vector>
+
+namespace sofg {
+namespace host {
+
+inline uint64_t split_mix64(uint64_t z) {  // reference random.hpp:13-18
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+inline uint64_t derive_seed(uint64_t seed, uint64_t key) {  // random.hpp:22-24
+  return split_mix64(seed ^ split_mix64(key + 0x632be59bd9b4e019ull));
+}
+
+class LazyMt64 {
+ public:
+  using result_type = uint64_t;
+  static constexpr result_type min() { return 0; }
+  static constexpr result_type max() { return ~0ull; }
+
+  explicit LazyMt64(uint64_t node_seed) {
+    s_[0] = split_mix64(node_seed);
+    seeded_ = 1;
+  }
+
+  result_type operator()() {
+    if (count_ < kN) {
+      const int i = int(count_);
+      uint64_t w;
+      if (i < kN - kM) {
+        need(i + kM);
+        w = mix(s_[i], s_[i + 1], s_[i + kM]);
+      } else {
+        need(kN - 1);
+        const uint64_t nxt = (i + 1 < kN) ? s_[i + 1] : b_[0];
+        w = mix(s_[i], nxt, b_[i - (kN - kM)]);
+      }
+      b_[i] = w;
+      ++count_;
+      return temper(w);
+    }
+    const int i = int(count_ % kN);
+    if (i == 0) twist_in_place();
+    ++count_;
+    return temper(b_[i]);
+  }
+
+  uint64_t consumed() const { return count_; }
+
+ private:
+  static constexpr int kN = 312, kM = 156;
+  static uint64_t mix(uint64_t cur, uint64_t nxt, uint64_t far) {
+    const uint64_t y = (cur & 0xFFFFFFFF80000000ull) | (nxt & 0x7FFFFFFFull);
+    return far ^ (y >> 1) ^ ((y & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+  }
+  static uint64_t temper(uint64_t y) {
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    return y ^ (y >> 43);
+  }
+  void need(int upto) {
+    while (seeded_ <= upto) {
+      const uint64_t p = s_[seeded_ - 1];
+      s_[seeded_] = 6364136223846793005ull * (p ^ (p >> 62)) + uint64_t(seeded_);
+      ++seeded_;
+    }
+  }
+  void twist_in_place() {
+    for (int k = 0; k < kN - kM; ++k) b_[k] = mix(b_[k], b_[k + 1], b_[k + kM]);
+    for (int k = kN - kM; k < kN - 1; ++k) b_[k] = mix(b_[k], b_[k + 1], b_[k - (kN - kM)]);
+    b_[kN - 1] = mix(b_[kN - 1], b_[0], b_[kM - 1]);
+  }
+
+  uint64_t s_[kN];  // seeding recurrence words (computed on demand)
+  uint64_t b_[kN];  // current raw block
+  int seeded_ = 0;
+  uint64_t count_ = 0;
+};
+
+// Binomial nonzero count of one projection matrix: a fresh distribution per draw (the
+// reference constructs it inside sample_projection_matrix, so no normal variate is carried
+// over between nodes); the parameter block is precomputed once.
+struct BinomialDraw {
+  std::binomial_distribution<long long>::param_type param;
+  BinomialDraw(uint64_t cells, double density) : param((long long)cells, density) {}
+
+  // Draw for engine make_rng(seed) after `skip` outputs. Returns z; *used = skip + consumed.
+  uint64_t operator()(uint64_t seed, uint64_t skip, uint64_t* used) const {
+    LazyMt64 g(seed);
+    for (uint64_t i = 0; i < skip; ++i) g();
+    std::binomial_distribution<long long> dist(param);
+    const long long z = dist(g);
+    *used = g.consumed();
+    return uint64_t(z);
+  }
+};
+
+// bootstrap_sample (reference dataset.hpp:332-349): std::sample selection sampling over iota(n)
+// with make_rng(seed); sorted output. Same libstdc++ algorithm as the reference by construction.
+std::vector<uint32_t> bootstrap_indices(uint64_t n, double fraction, uint64_t seed);
+
+// Entropy in bits of class counts (reference split.hpp:20-31), with the contraction the
+// reference's default -march=native build applies: h = fma(-p, log2(p), h).
+double entropy(const uint32_t* counts, int k);
+
+// xlogx table entries c * log2(c) (split.hpp:55-62), c = 0..n.
+std::vector<double> xlogx_table(uint64_t n);
+
+}  // namespace host
+}  // namespace sofg

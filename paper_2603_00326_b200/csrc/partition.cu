@@ -1,0 +1,204 @@
+// Stable two-way partition of every split node's segment (reference forest.hpp:197-212:
+// values <= threshold stay left in order, the rest follow in order).
+//
+//  k_part_flags    per 1024-element tile: recompute the winning row's projected value, flag
+//                  v <= thr, store the flag bits, count lefts per tile and per class.
+//  k_part_scan     per node: exclusive scan of tile left-counts; fills n_left, the stream
+//                  position after the attempt and the winning row's terms in NodeRes.
+//  k_part_scatter  per tile: rank inside the tile from the flag bits, scatter sample ids and
+//                  labels into the next level's buffers.
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "dev_util.cuh"
+#include "kernels.hpp"
+
+namespace sofg {
+namespace dev {
+
+__global__ void __launch_bounds__(256) k_part_flags(
+    const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, uint32_t R, int k,
+    const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
+    const uint32_t* __restrict__ idx, const uint8_t* __restrict__ lab, const float* __restrict__ X,
+    uint64_t ld, NodeRes* __restrict__ res, uint32_t* __restrict__ flags,
+    uint32_t* __restrict__ tile_left) {
+  __shared__ uint32_t s_cls[kMaxClasses];
+  __shared__ uint32_t s_left;
+  const Tile tl = tiles[blockIdx.x];
+  const NodeIn nd = nodes[tl.node];
+  const int row = res[tl.node].row;
+  if (row < 0) return;
+  const float thr = res[tl.node].threshold;
+  if (threadIdx.x < kMaxClasses) s_cls[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_left = 0;
+  __syncthreads();
+  const uint32_t* rp = row_ptr + size_t(tl.node) * (R + 1);
+  const uint32_t* rt = terms + nd.term_off + rp[row];
+  const int nt = int(rp[row + 1] - rp[row]);
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  uint32_t my_left = 0;
+  uint32_t cls[kMaxClasses];
+#pragma unroll
+  for (int c = 0; c < kMaxClasses; ++c) cls[c] = 0;
+  float v[4];
+  uint8_t y[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t l = uint32_t(e * 256 + threadIdx.x);
+    if (l < tl.len) {
+      const uint32_t p = nd.begin + tl.start + l;
+      v[e] = project_sample(X, ld, rt, nt, idx[p]);
+      y[e] = lab[p];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t l = uint32_t(e * 256 + threadIdx.x);
+    const bool f = l < tl.len && v[e] <= thr;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) flags[size_t(blockIdx.x) * 32 + e * 8 + w] = m;
+    if (f) {
+      ++my_left;
+#pragma unroll
+      for (int c = 0; c < kMaxClasses; ++c) cls[c] += (c == int(y[e]));
+    }
+  }
+  // reduce
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) my_left += __shfl_xor_sync(0xffffffffu, my_left, o);
+  if (lane == 0) atomicAdd(&s_left, my_left);
+#pragma unroll
+  for (int c = 0; c < kMaxClasses; ++c) {
+    uint32_t x = cls[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && c < k && x) atomicAdd(&s_cls[c], x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tile_left[blockIdx.x] = s_left;
+  if (threadIdx.x < uint32_t(k) && s_cls[threadIdx.x])
+    atomicAdd(&res[tl.node].left_counts[threadIdx.x], s_cls[threadIdx.x]);
+}
+
+// One warp per node: scan its tiles (tiles of a node are contiguous, first = tile_first[node]).
+__global__ void k_part_scan(const NodeIn* __restrict__ nodes, int n_nodes, uint32_t R,
+                            const uint32_t* __restrict__ tile_first,
+                            const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
+                            const uint32_t* __restrict__ pos_proj,
+                            const uint32_t* __restrict__ pos_split, uint32_t* __restrict__ tile_left,
+                            NodeRes* __restrict__ res) {
+  const int lane = threadIdx.x & 31;
+  const int node = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (node >= n_nodes) return;
+  const NodeIn nd = nodes[node];
+  NodeRes& o = res[node];
+  if (lane == 0) o.pos_after = (nd.flags & kNodeHist) ? pos_split[node] : pos_proj[node];
+  const int row = o.row;
+  if (row < 0) return;
+  const uint32_t t0 = tile_first[node], t1 = tile_first[node + 1];
+  uint32_t carry = 0;
+  for (uint32_t base = t0; base < t1; base += 32) {
+    const uint32_t t = base + lane;
+    const uint32_t c = t < t1 ? tile_left[t] : 0;
+    uint32_t tot;
+    const uint32_t ex = warp_excl_scan_u32(c, lane, &tot);
+    if (t < t1) tile_left[t] = carry + ex;  // becomes the tile's left offset
+    carry += tot;
+  }
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  const uint32_t nt = rp[row + 1] - rp[row];
+  const uint32_t* rt = terms + nd.term_off + rp[row];
+  if (lane == 0) {
+    o.n_left = carry;
+    o.n_terms = nt;
+  }
+  for (uint32_t q = lane; q < nt && q < uint32_t(kWinTermsMax); q += 32) o.terms[q] = rt[q];
+}
+
+__global__ void __launch_bounds__(256) k_part_scatter(
+    const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles,
+    const NodeRes* __restrict__ res, const uint32_t* __restrict__ flags,
+    const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ idx_in,
+    const uint8_t* __restrict__ lab_in, uint32_t* __restrict__ idx_out,
+    uint8_t* __restrict__ lab_out) {
+  __shared__ uint32_t s_wpre[32];
+  const Tile tl = tiles[blockIdx.x];
+  if (res[tl.node].row < 0) return;
+  const NodeIn nd = nodes[tl.node];
+  const uint32_t n_left = res[tl.node].n_left;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const uint32_t* fw = flags + size_t(blockIdx.x) * 32;
+  if (w == 0) {
+    uint32_t tot;
+    s_wpre[lane] = warp_excl_scan_u32(__popc(fw[lane]), lane, &tot);
+  }
+  __syncthreads();
+  const uint32_t off = tile_off[blockIdx.x];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t l = uint32_t(e * 256 + threadIdx.x);
+    if (l >= tl.len) continue;
+    const int word = e * 8 + w;
+    const uint32_t m = fw[word];
+    const uint32_t lrank = s_wpre[word] + __popc(m & ((1u << lane) - 1u));
+    const uint32_t p = tl.start + l;             // position inside the node
+    const uint32_t L = off + lrank;              // left elements before p
+    const bool left = (m >> lane) & 1u;
+    const uint32_t dst = left ? L : n_left + (p - L);
+    const uint32_t src = nd.begin + p;
+    idx_out[nd.begin + dst] = idx_in[src];
+    lab_out[nd.begin + dst] = lab_in[src];
+  }
+}
+
+// Roofline accounting: number of distinct 32-byte sectors {idx >> 3} in each node's (sorted)
+// sample-id set. Every projection term gathers one column over that set, so the node's gather
+// traffic in the sector model is 32 * sectors * z.
+__global__ void __launch_bounds__(256) k_sector_count(const NodeIn* __restrict__ nodes,
+                                                      const Tile* __restrict__ tiles,
+                                                      const uint32_t* __restrict__ idx,
+                                                      NodeRes* __restrict__ res) {
+  const Tile tl = tiles[blockIdx.x];
+  const NodeIn nd = nodes[tl.node];
+  uint32_t c = 0;
+  for (uint32_t l = threadIdx.x; l < tl.len; l += blockDim.x) {
+    const uint32_t p = tl.start + l;
+    const uint32_t s = idx[nd.begin + p] >> 3;
+    c += (p == 0 || (idx[nd.begin + p - 1] >> 3) != s) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&res[tl.node].sectors, c);
+}
+
+}  // namespace dev
+
+cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_tiles,
+                                const uint32_t* idx, NodeRes* res, cudaStream_t st) {
+  if (n_tiles == 0) return cudaSuccess;
+  dev::k_sector_count<<<n_tiles, 256, 0, st>>>(nodes, tiles, idx, res);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles, int n_tiles,
+                             const uint32_t* tile_first, uint32_t R, int k, const uint32_t* terms,
+                             const uint32_t* row_ptr, const uint32_t* pos_proj,
+                             const uint32_t* pos_split, const uint32_t* idx_in,
+                             const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
+                             const float* X, uint64_t ld, NodeRes* res, uint32_t* flags,
+                             uint32_t* tile_left, cudaStream_t st) {
+  if (n_nodes == 0) return cudaSuccess;
+  if (n_tiles > 0)
+    dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, idx_in, lab_in,
+                                               X, ld, res, flags, tile_left);
+  dev::k_part_scan<<<(n_nodes + 3) / 4, 128, 0, st>>>(nodes, n_nodes, R, tile_first, terms,
+                                                      row_ptr, pos_proj, pos_split, tile_left, res);
+  if (n_tiles > 0)
+    dev::k_part_scatter<<<n_tiles, 256, 0, st>>>(nodes, tiles, res, flags, tile_left, idx_in,
+                                                 lab_in, idx_out, lab_out);
+  return cudaGetLastError();
+}
+
+}  // namespace sofg

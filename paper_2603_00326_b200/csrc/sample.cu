@@ -1,0 +1,361 @@
+// Per-node random structure regenerated on the device from (seed, stream position):
+//
+//  k_sample_projection  — sample_projection_matrix (reference projection.hpp:57-82) after the
+//                         host's binomial draw: Floyd over R*d cells (random.hpp:31-45), ascending
+//                         cell order, one coin per cell. Output: CSR per node.
+//  k_hist_draws         — the Floyd position draws of sample_boundaries for every row of a
+//                         histogram node (histogram.hpp:47-53), consumed in row order from the
+//                         same engine (split.hpp:272-276), with Lemire rejections handled inline.
+//  k_hist_boundaries    — resolves each row's Floyd set, gathers the picked projected values,
+//                         sorts them and emits midpoint_down of distinct neighbours
+//                         (histogram.hpp:56-60).
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "dev_util.cuh"
+#include "kernels.hpp"
+#include "mt64.cuh"
+
+namespace sofg {
+namespace dev {
+
+// ------------------------------------------------------------------------------------------
+// Projection sampler: one warp per node.
+// smem per warp: 624 u64 (two engine blocks) + 2 * zpad u32 (sorted set, draw order).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_sample_projection(
+    const NodeIn* __restrict__ nodes, int n_nodes, uint32_t d, uint32_t R, int zpad,
+    uint32_t* __restrict__ terms, uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ pos_after) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int node = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (node >= n_nodes) return;
+  const size_t per_warp = size_t(2 * kMtN) * 8 + size_t(2 * zpad) * 4;
+  unsigned char* base = smem_raw + per_warp * wib;
+  uint64_t* blk = reinterpret_cast<uint64_t*>(base);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(base + size_t(2 * kMtN) * 8);
+  uint32_t* draws = keys + zpad;
+
+  const NodeIn nd = nodes[node];
+  uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  if (nd.flags & kNodeGivenCsr) return;  // host supplied the matrix and pos_after
+
+  const uint32_t z = nd.z;
+  const uint64_t cells = uint64_t(R) * d;
+  WarpStream s;
+  s.init_seeded(blk, nd.seed, lane);
+  s.skip(nd.pos, lane);
+  uint64_t used = nd.pos;
+
+  // Floyd draws t_q = uniform(0, cells - z + q), q = 0..z-1, in stream order.
+  uint32_t q = 0;
+  while (q < z) {
+    const uint32_t cnt = min(32u, z - q);
+    uint64_t t = 0;
+    bool ok = true;
+    const uint64_t x = s.window32(lane, lane);  // collective: every lane calls it
+    if (lane < int(cnt)) ok = lemire_accept(x, cells - z + q + lane + 1, &t);
+    const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+    const uint32_t take = bad ? uint32_t(__ffs(bad) - 1) : cnt;
+    if (lane < int(take)) draws[q + lane] = uint32_t(t);
+    s.advance(int(take), lane);
+    used += take;
+    q += take;
+    if (bad) {  // output rejected: it is consumed, the same draw retries on the next output
+      s.advance(1, lane);
+      used += 1;
+    }
+  }
+  __syncwarp();
+
+  // Set = {t_q} unless some t collides (prob ~ z^2 / 2 cells); sort and test neighbours.
+  for (int i = lane; i < zpad; i += 32) keys[i] = i < int(z) ? draws[i] : 0xffffffffu;
+  __syncwarp();
+  warp_bitonic_sort(keys, zpad, lane);
+  bool dup = false;
+  for (int i = lane + 1; i < int(z); i += 32) dup |= keys[i] == keys[i - 1];
+  if (__any_sync(0xffffffffu, dup)) {
+    // Exact Floyd resolution in draw order (random.hpp:36-44): a collision inserts j instead.
+    for (uint32_t i = 0; i < z; ++i) {
+      const uint32_t t = draws[i];
+      bool hit = false;
+      for (uint32_t p = lane; p < i; p += 32) hit |= keys[p] == t;
+      hit = __any_sync(0xffffffffu, hit);
+      __syncwarp();
+      if (lane == 0) keys[i] = hit ? uint32_t(cells - z + i) : t;
+      __syncwarp();
+    }
+    for (int i = lane; i < zpad; i += 32)
+      if (i >= int(z)) keys[i] = 0xffffffffu;
+    __syncwarp();
+    warp_bitonic_sort(keys, zpad, lane);
+  }
+
+  // Coins: cell i (ascending) gets the top bit of the next output (uniform_int<int>(0,1)).
+  uint32_t* out = terms + nd.term_off;
+  for (uint32_t b = 0; b < z; b += 32) {
+    const uint64_t x = s.window32(lane, lane);
+    const uint32_t i = b + lane;
+    if (i < z) {
+      const uint32_t cell = keys[i];
+      const bool plus = (x >> 63) != 0;
+      out[i] = encode_term(cell % d, !plus);
+    }
+    const uint32_t c = min(32u, z - b);
+    s.advance(int(c), lane);
+    used += c;
+  }
+  // row_ptr[r] = #cells < r*d
+  for (uint32_t r = lane; r <= R; r += 32) {
+    const uint64_t lim = uint64_t(r) * d;
+    uint32_t lo = 0, hi = z;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (uint64_t(keys[mid]) < lim) lo = mid + 1; else hi = mid;
+    }
+    rp[r] = lo;
+  }
+  if (lane == 0) pos_after[node] = uint32_t(used);
+}
+
+// ------------------------------------------------------------------------------------------
+// Histogram boundary draws: one CTA (256 threads) per histogram node. Generates the R*m Lemire
+// draws of the R consecutive sample_boundaries calls. Output: draws[slot][R*m] (u32),
+// pos_split[node] = stream position after the picks.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_hist_draws(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist,
+    uint32_t R, uint32_t bins, const uint32_t* __restrict__ pos_after_proj,
+    uint32_t* __restrict__ draws, uint32_t* __restrict__ pos_split) {
+  __shared__ uint64_t A[kMtN], B[kMtN];
+  __shared__ int s_first_bad;
+  const int h = blockIdx.x;
+  if (h >= n_hist) return;
+  const uint32_t node = hist_nodes[h];
+  const NodeIn nd = nodes[node];
+  const uint32_t n = nd.n;
+  const uint32_t start_pos = pos_after_proj[node];
+  const uint32_t m = min(bins, n);
+  const int tid = threadIdx.x;
+  if (n < 2 || bins < 2 || m == n) {  // histogram.hpp:42-49: no draws
+    if (tid == 0) pos_split[node] = start_pos;
+    return;
+  }
+  // seed + first twist
+  if (tid == 0) mt_seed_lane(B, split_mix64(nd.seed));
+  __syncthreads();
+  mt_twist_block(B, A, tid, blockDim.x);
+  uint64_t* cur_blk = A;
+  uint64_t* nxt_blk = B;
+  uint64_t pos = start_pos;
+  while (pos >= uint64_t(kMtN)) {
+    mt_twist_block(cur_blk, nxt_blk, tid, blockDim.x);
+    uint64_t* t = cur_blk;
+    cur_blk = nxt_blk;
+    nxt_blk = t;
+    pos -= kMtN;
+  }
+  int cur = int(pos);
+  uint64_t used = start_pos;
+  const uint64_t total = uint64_t(R) * m;
+  uint32_t* out = draws + size_t(h) * R * bins;  // fixed stride R*bins per histogram node
+  uint64_t q = 0;
+  while (q < total) {
+    const int avail = kMtN - cur;
+    const uint64_t want = min(uint64_t(avail), total - q);
+    if (tid == 0) s_first_bad = 0x7fffffff;
+    __syncthreads();
+    // first pass: find the first rejection within [cur, cur+want)
+    for (int o = tid; o < int(want); o += blockDim.x) {
+      const uint64_t x = mt_temper(cur_blk[cur + o]);
+      const uint64_t qq = q + uint64_t(o);
+      const uint32_t i = uint32_t(qq % m);
+      uint64_t t;
+      if (!lemire_accept(x, uint64_t(n - m + i) + 1, &t)) atomicMin(&s_first_bad, o);
+    }
+    __syncthreads();
+    const int fb = s_first_bad;
+    const int take = fb == 0x7fffffff ? int(want) : fb;
+    for (int o = tid; o < take; o += blockDim.x) {
+      const uint64_t x = mt_temper(cur_blk[cur + o]);
+      const uint64_t qq = q + uint64_t(o);
+      const uint32_t i = uint32_t(qq % m);
+      uint64_t t;
+      lemire_accept(x, uint64_t(n - m + i) + 1, &t);
+      out[qq] = uint32_t(t);
+    }
+    q += uint64_t(take);
+    cur += take + (fb == 0x7fffffff ? 0 : 1);
+    used += uint64_t(take) + (fb == 0x7fffffff ? 0 : 1);
+    if (cur >= kMtN) {
+      __syncthreads();
+      mt_twist_block(cur_blk, nxt_blk, tid, blockDim.x);
+      uint64_t* t = cur_blk;
+      cur_blk = nxt_blk;
+      nxt_blk = t;
+      cur -= kMtN;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) pos_split[node] = uint32_t(used);
+}
+
+// ------------------------------------------------------------------------------------------
+// Boundaries: one warp per (histogram node, row). smem per warp: mpad u64 + mpad floats(u32)
+// + mpad bytes.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_hist_boundaries(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist,
+    uint32_t R, uint32_t bins, int mpad, const uint32_t* __restrict__ draws,
+    const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
+    const uint32_t* __restrict__ idx, const float* __restrict__ X, uint64_t ld,
+    float* __restrict__ bnd, uint32_t* __restrict__ nb_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint64_t item = uint64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
+  if (item >= uint64_t(n_hist) * R) return;
+  const uint32_t h = uint32_t(item / R);
+  const uint32_t r = uint32_t(item % R);
+  const size_t per_warp = size_t(mpad) * 8 + size_t(mpad) * 4 + size_t(mpad);
+  unsigned char* base = smem_raw + per_warp * wib;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(base);
+  uint32_t* vk = reinterpret_cast<uint32_t*>(base + size_t(mpad) * 8);
+  uint8_t* col = reinterpret_cast<uint8_t*>(base + size_t(mpad) * 12);
+
+  const uint32_t node = hist_nodes[h];
+  const NodeIn nd = nodes[node];
+  const uint32_t n = nd.n;
+  float* out = bnd + (size_t(h) * R + r) * (bins - 1);
+  if (n < 2 || bins < 2) {
+    if (lane == 0) nb_out[size_t(h) * R + r] = 0;
+    return;
+  }
+  const uint32_t m = min(bins, n);
+  const uint32_t J0 = n - m;
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  const uint32_t* rt = terms + nd.term_off + rp[r];
+  const int nt = int(rp[r + 1] - rp[r]);
+  const uint32_t* seg = idx + nd.begin;
+
+  if (m < n) {
+    const uint32_t* t = draws + size_t(h) * R * bins + size_t(r) * m;
+    // C1: t_i equals an earlier t (sort (t, i) pairs; later duplicates collide).
+    for (int i = lane; i < mpad; i += 32)
+      keys[i] = i < int(m) ? ((uint64_t(t[i]) << 16) | uint64_t(i)) : ~0ull;
+    __syncwarp();
+    warp_bitonic_sort(keys, mpad, lane);
+    for (int i = lane; i < int(m); i += 32) {
+      const uint32_t me = uint32_t(keys[i] & 0xffffu);
+      const bool c1 = i > 0 && (keys[i] >> 16) == (keys[i - 1] >> 16);
+      col[me] = c1 ? 1 : 0;
+    }
+    __syncwarp();
+    // D_i = C1_i or (t_i - J0 < i and D_{t_i - J0}); monotone fixpoint over draw order.
+    bool changed = true;
+    while (changed) {
+      bool ch = false;
+      for (int i = lane; i < int(m); i += 32) {
+        if (col[i]) continue;
+        const uint32_t ti = t[i];
+        if (ti >= J0 && ti - J0 < uint32_t(i) && col[ti - J0]) {
+          col[i] = 1;
+          ch = true;
+        }
+      }
+      __syncwarp();
+      changed = __any_sync(0xffffffffu, ch);
+    }
+    // gather the picked values (positions in the node's active order)
+    for (int i = lane; i < mpad; i += 32) {
+      uint32_t key = 0xffffffffu;
+      if (i < int(m)) {
+        const uint32_t p = col[i] ? J0 + uint32_t(i) : t[i];
+        key = order_key(project_sample(X, ld, rt, nt, seg[p]));
+      }
+      vk[i] = key;
+    }
+  } else {
+    for (int i = lane; i < mpad; i += 32)
+      vk[i] = i < int(m) ? order_key(project_sample(X, ld, rt, nt, seg[i])) : 0xffffffffu;
+  }
+  __syncwarp();
+  warp_bitonic_sort(vk, mpad, lane);
+  // midpoints of consecutive distinct values (float comparison: -0 == +0)
+  uint32_t base_cnt = 0;
+  for (int i0 = 1; i0 < int(m); i0 += 32) {
+    const int i = i0 + lane;
+    bool emit = false;
+    float a = 0.f, b = 0.f;
+    if (i < int(m)) {
+      a = order_key_inv(vk[i - 1]);
+      b = order_key_inv(vk[i]);
+      emit = a < b;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, emit);
+    if (emit) out[base_cnt + __popc(mask & ((1u << lane) - 1))] = midpoint_down(a, b);
+    base_cnt += __popc(mask);
+  }
+  if (lane == 0) nb_out[size_t(h) * R + r] = base_cnt;
+}
+
+}  // namespace dev
+
+// ---------------------------------------------------------------------------- launchers
+static int next_pow2(int x) {
+  int p = 32;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t d, uint32_t R,
+                                     uint32_t zmax, uint32_t* terms, uint32_t* row_ptr,
+                                     uint32_t* pos_after, cudaStream_t st) {
+  if (n_nodes == 0) return cudaSuccess;
+  const int zpad = next_pow2(int(zmax));
+  const size_t per_warp = size_t(2 * dev::kMtN) * 8 + size_t(2 * zpad) * 4;
+  int warps = 4;
+  while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
+  const size_t smem = per_warp * warps;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(dev::k_sample_projection, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+  const int grid = (n_nodes + warps - 1) / warps;
+  dev::k_sample_projection<<<grid, warps * 32, smem, st>>>(nodes, n_nodes, d, R, zpad, terms,
+                                                           row_ptr, pos_after);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist_draws(const NodeIn* nodes, const uint32_t* hist_nodes, int n_hist,
+                              uint32_t R, uint32_t bins, const uint32_t* pos_after_proj,
+                              uint32_t* draws, uint32_t* pos_split, cudaStream_t st) {
+  if (n_hist == 0) return cudaSuccess;
+  dev::k_hist_draws<<<n_hist, 256, 0, st>>>(nodes, hist_nodes, n_hist, R, bins, pos_after_proj,
+                                            draws, pos_split);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nodes, int n_hist,
+                                   uint32_t R, uint32_t bins, const uint32_t* draws,
+                                   const uint32_t* terms, const uint32_t* row_ptr,
+                                   const uint32_t* idx, const float* X, uint64_t ld, float* bnd,
+                                   uint32_t* nb, cudaStream_t st) {
+  if (n_hist == 0) return cudaSuccess;
+  const int mpad = next_pow2(int(bins));
+  const size_t per_warp = size_t(mpad) * 13;
+  int warps = 4;
+  while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
+  const size_t smem = per_warp * warps;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(dev::k_hist_boundaries, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+  const uint64_t items = uint64_t(n_hist) * R;
+  const unsigned grid = unsigned((items + warps - 1) / warps);
+  dev::k_hist_boundaries<<<grid, warps * 32, smem, st>>>(nodes, hist_nodes, n_hist, R, bins, mpad,
+                                                         draws, terms, row_ptr, idx, X, ld, bnd,
+                                                         nb);
+  return cudaGetLastError();
+}
+
+}  // namespace sofg

@@ -1,0 +1,81 @@
+// Level-wise frontier scheduler: grows a batch of trees one depth at a time, every open node of
+// the depth searched and partitioned by one wave of kernels (engine.hpp). Replaces the
+// reference's depth-first per-node loop detail::TreeGrower::grow_from (forest.hpp:157-240) while
+// reproducing its trees exactly: per-node engines depend only on the node seed
+// (forest.hpp:183,226,228), so level order does not change any random stream, and node ids are
+// restored by replaying the reference's depth-first split order at the end.
+#pragma once
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <functional>
+#include <mutex>
+#include <optional>
+#include <thread>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace sofg {
+
+struct FlatForest {
+  std::vector<int64_t> tree_off{0};
+  std::vector<int32_t> left, right, pred;
+  std::vector<float> thr;
+  std::vector<int64_t> term_off{0};
+  std::vector<uint32_t> feat;
+  std::vector<float> weight;
+  uint64_t breakeven = 0;
+  int32_t class_count = 0;
+  uint64_t n_features = 0;
+  uint64_t n_trees() const { return tree_off.size() - 1; }
+};
+
+struct TrainParams {
+  int mode = 2;  // 0 exact-only, 1 histogram-only, 2 dynamic
+  uint64_t bins = 256;
+  uint64_t breakeven = 1024;
+  std::optional<uint64_t> max_depth;
+  uint64_t min_samples_split = 2;
+  uint64_t max_split_retries = 1;
+  uint32_t R = 0;          // projection rows
+  double density = 0.0;    // cell density
+  uint64_t batch_trees = 0;
+  int host_threads = 0;
+};
+
+// Minimal fork-join pool for the per-node host work (binomial draws, bootstraps).
+class ThreadPool {
+ public:
+  explicit ThreadPool(int n);
+  ~ThreadPool();
+  int size() const { return int(workers_.size()) + 1; }
+  // f(i) for i in [0, n), caller participates.
+  void parallel_for(size_t n, const std::function<void(size_t)>& f);
+
+ private:
+  void worker();
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(size_t)>* job_ = nullptr;
+  size_t job_n_ = 0;
+  std::atomic<size_t> next_{0};
+  int active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+struct HostTimes {
+  double ms_binomial = 0, ms_bootstrap = 0, ms_total = 0;
+  uint64_t levels = 0;
+};
+
+// Grows one tree per root (sorted active set + root seed) at depth offset root_depth and
+// appends them, renumbered in the reference's node order, to `out`.
+void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
+                const std::vector<std::vector<uint32_t>>& roots,
+                const std::vector<uint64_t>& root_seeds, uint32_t root_depth, FlatForest& out,
+                HostTimes& times);
+
+}  // namespace sofg

@@ -1,0 +1,219 @@
+"""GPU parity: every CUDA path against the CPU oracle on identical inputs and seeds.
+
+The oracle is the reference compiled as-is (oracle/_ref) when present, else the restated port;
+both are pinned to each other in tests/test_oracle.py. Integer/byte/index results and floats
+produced by identical IEEE operation sequences are compared bit-for-bit.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("d", [4, 8, 64, 512, 4096])
+def test_sample_projection_matches_oracle(gpu_ctx, oracle, d):
+    R, _, dens = oracle.projection_config(d)
+    seeds = np.array([oracle.derive_seed(7, i) for i in range(300)], np.uint64)
+    skips = np.array([(i * 13) % 700 for i in range(300)], np.uint64)
+    rp, feat, w, used = gpu_ctx.sample_projection(d, R, dens, seeds, skips)
+    for i in range(len(seeds)):
+        orp, ofeat, ow, oused = oracle.sample_projection(d, R, dens, int(seeds[i]), int(skips[i]))
+        assert np.array_equal(rp[i], orp), i
+        z = int(orp[-1])
+        assert np.array_equal(feat[i, :z], ofeat), i
+        assert np.array_equal(_bits(w[i, :z]), _bits(ow)), i
+        assert int(used[i]) == oused, i
+
+
+def test_sample_projection_dense_density(gpu_ctx, oracle):
+    # extension knob: denser matrices exercise long Floyd runs and collisions
+    d, R = 64, 12
+    for dens in (0.05, 0.3, 0.9):
+        seeds = np.arange(40, dtype=np.uint64) * 977 + 5
+        rp, feat, w, used = gpu_ctx.sample_projection(d, R, dens, seeds, cap=1024)
+        for i in range(len(seeds)):
+            orp, ofeat, ow, oused = oracle.sample_projection(d, R, dens, int(seeds[i]), 0)
+            assert np.array_equal(rp[i], orp)
+            z = int(orp[-1])
+            assert np.array_equal(feat[i, :z], ofeat)
+            assert np.array_equal(_bits(w[i, :z]), _bits(ow))
+            assert int(used[i]) == oused
+
+
+def test_apply_projection_goldens(gpu_ctx):
+    # projection_test.cpp:138-156
+    X = np.array([[1, 2, 3, 4], [10, 20, 30, 40], [100, 200, 300, 400]], np.float32)
+    gpu_ctx.upload(X, np.array([0, 1, 0, 1]), 2)
+    out = gpu_ctx.apply_projection([0, 2], [1, -1], [0, 1, 2, 3])
+    assert out.tolist() == [-99, -198, -297, -396]
+    assert gpu_ctx.apply_projection([0, 2], [1, -1], [3, 1]).tolist() == [-396, -198]
+    assert gpu_ctx.apply_projection([], [], [3, 1]).tolist() == [0, 0]
+    assert gpu_ctx.apply_projection([1], [-1], [0, 1, 2, 3]).tolist() == [-10, -20, -30, -40]
+
+
+def test_apply_projection_random(gpu_ctx, oracle):
+    rng = np.random.default_rng(3)
+    n, d = 5000, 50
+    X = (rng.standard_normal((d, n)) * rng.choice([1e-3, 1, 1e3], size=(d, 1))).astype(np.float32)
+    gpu_ctx.upload(X, rng.integers(0, 2, n), 2)
+    for it in range(30):
+        nt = int(rng.integers(0, 8))
+        feat = np.sort(rng.choice(d, nt, replace=False)).astype(np.uint32)
+        w = rng.choice([-1.0, 1.0], nt).astype(np.float32)
+        act = np.sort(rng.choice(n, int(rng.integers(1, n)), replace=False)).astype(np.uint32)
+        assert np.array_equal(_bits(gpu_ctx.apply_projection(feat, w, act)),
+                              _bits(oracle.apply_projection(X, feat, w, act)))
+
+
+def _split_eq(g, o):
+    assert bool(g.found) == bool(o.found)
+    if not o.found:
+        return
+    assert g.projection_index == o.projection_index
+    assert _bits(g.threshold) == _bits(o.threshold)
+    assert g.gain == o.gain
+    assert g.n_left == o.n_left
+
+
+@pytest.mark.parametrize("method,bins", [("exact", 256), ("histogram", 1024), ("histogram", 256),
+                                         ("histogram", 64), ("histogram", 8)])
+def test_find_node_split_trunk400(gpu_ctx, oracle, method, bins):
+    # FindNodeSplitTest fixture (split_test.cpp:231-240): generate_trunk(400, 8, 123), all rows
+    X, y = oracle.generate_trunk(400, 8, 123)
+    gpu_ctx.upload(X, y, 2)
+    R, _, dens = oracle.projection_config(8)
+    active = np.arange(400, dtype=np.uint32)
+    for seed in range(12):
+        rp, feat, w, used = oracle.sample_projection(8, R, dens, seed, 0)
+        g = gpu_ctx.find_node_split(active, rp, feat, w, method, bins, seed, used)
+        o, oused, _ = oracle.find_node_split(X, y, 2, active, rp, feat, w, method, bins, seed, used)
+        _split_eq(g, o)
+        assert int(g.consumed) == oused
+
+
+@pytest.mark.parametrize("n,method,bins", [(2, "exact", 256), (3, "exact", 256), (33, "exact", 256),
+                                           (700, "exact", 256), (2048, "exact", 256),
+                                           (300, "histogram", 256), (5000, "histogram", 256),
+                                           (20000, "histogram", 256), (9000, "histogram", 32)])
+def test_find_node_split_subsets(gpu_ctx, oracle, n, method, bins):
+    X, y = oracle.generate_trunk(30000, 16, 5)
+    gpu_ctx.upload(X, y, 2)
+    R, _, dens = oracle.projection_config(16)
+    rng = np.random.default_rng(n)
+    for it in range(4):
+        active = np.sort(rng.choice(30000, n, replace=False)).astype(np.uint32)
+        seed = int(rng.integers(1 << 60))
+        rp, feat, w, used = oracle.sample_projection(16, R, dens, seed, 0)
+        g = gpu_ctx.find_node_split(active, rp, feat, w, method, bins, seed, used)
+        o, oused, vals = oracle.find_node_split(X, y, 2, active, rp, feat, w, method, bins, seed, used)
+        _split_eq(g, o)
+        assert int(g.consumed) == oused
+        if o.found:
+            assert g.n_left_partition == int((vals <= o.threshold).sum())
+
+
+def test_find_node_split_quantized_ties(gpu_ctx, oracle):
+    # many equal projected values: grouping, signed zeros, first-max tie breaks
+    rng = np.random.default_rng(11)
+    n, d = 4000, 6
+    X = np.round(rng.standard_normal((d, n)) * 2).astype(np.float32) / 2
+    X[0, ::7] = -0.0
+    y = rng.integers(0, 3, n).astype(np.int32)
+    gpu_ctx.upload(X, y, 3)
+    R, _, dens = oracle.projection_config(d)
+    for it in range(20):
+        m = int(rng.integers(2, 1500))
+        active = np.sort(rng.choice(n, m, replace=False)).astype(np.uint32)
+        seed = it * 101 + 3
+        rp, feat, w, used = oracle.sample_projection(d, R, dens, seed, 0)
+        for method in ("exact", "histogram"):
+            if method == "exact" and m > 2048:
+                continue
+            g = gpu_ctx.find_node_split(active, rp, feat, w, method, 64, seed, used)
+            o, oused, _ = oracle.find_node_split(X, y, 3, active, rp, feat, w, method, 64, seed, used)
+            _split_eq(g, o)
+
+
+def _cfg(**kw):
+    import paper_2603_00326_b200 as sofg
+
+    return sofg.TrainConfig(**kw), oracle_lib.make_config(**{k: v for k, v in kw.items()
+                                                             if k not in ("batch_trees", "tree_begin", "tree_end")})
+
+
+def _forest_equal(g, o, t_g=None):
+    ff = oracle_lib.FlatForest(g.tree_off, g.left, g.right, g.pred, g.thr, g.term_off, g.feat, g.weight)
+    bad = [t for t in range(o.n_trees) if not ff.tree_equal(o, t)]
+    return bad
+
+
+@pytest.mark.parametrize("mode,breakeven", [("dynamic", 300), ("histogram", None), ("dynamic", 2048)])
+def test_train_forest_small(gpu_ctx, oracle, mode, breakeven):
+    X, y = oracle.generate_trunk(3000, 10, 21)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=6, mode=mode, breakeven=breakeven, seed=5, n_workers=4)
+    g = gpu_ctx.train_forest(gc)
+    o = oracle.train_forest(X, y, 2, oc)
+    assert g.n_trees == o.n_trees
+    assert _forest_equal(g, o) == []
+    assert g.breakeven == o.breakeven
+
+
+def test_train_forest_config1_10k_x_64(gpu_ctx, oracle):
+    # BASELINE config 1: 10K x 64, 10 trees to purity (dynamic, fixed breakeven)
+    X, y = oracle.generate_trunk(10000, 64, 1)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=10, mode="dynamic", breakeven=1024, seed=7, n_workers=8)
+    g = gpu_ctx.train_forest(gc)
+    o = oracle.train_forest(X, y, 2, oc)
+    assert _forest_equal(g, o) == []
+
+
+def test_train_tree_matches_forest_stream(gpu_ctx, oracle):
+    # forest_test.cpp:172-185: tree t equals train_tree on its derived stream
+    X, y = oracle.generate_trunk(600, 6, 13)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=1, mode="dynamic", breakeven=128, seed=77)
+    f = gpu_ctx.train_forest(gc)
+    ts = oracle.derive_seed(77, 1)
+    boot = oracle.bootstrap(600, 0.632, oracle.derive_seed(ts, 0))
+    t = gpu_ctx.train_tree(boot, gc, oracle.derive_seed(ts, 1))
+    o = oracle.train_tree(X, y, 2, boot, oc, oracle.derive_seed(ts, 1))
+    assert _forest_equal(t, o) == []
+    assert _forest_equal(f, o) == []
+
+
+def test_max_depth_and_min_samples(gpu_ctx, oracle):
+    X, y = oracle.generate_trunk(2000, 8, 3)
+    gpu_ctx.upload(X, y, 2)
+    for kw in (dict(max_depth=0), dict(max_depth=3), dict(min_samples_split=50), dict(max_split_retries=0)):
+        gc, oc = _cfg(n_trees=3, mode="dynamic", breakeven=200, seed=11, **kw)
+        assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, 2, oc)) == [], kw
+
+
+def test_multiclass_forest(gpu_ctx, oracle):
+    rng = np.random.default_rng(1)
+    n, d, k = 4000, 12, 4
+    y = (np.arange(n) % k).astype(np.int32)
+    X = (rng.standard_normal((d, n)) + 0.6 * (y[None, :] == (np.arange(d) % k)[:, None])).astype(np.float32)
+    gpu_ctx.upload(X, y, k)
+    gc, oc = _cfg(n_trees=4, mode="dynamic", breakeven=256, seed=2)
+    assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, k, oc)) == []
+
+
+def test_predict_matches_oracle(gpu_ctx, oracle):
+    X, y = oracle.generate_trunk(3000, 10, 4)
+    Xt, yt = oracle.generate_trunk(500, 10, 99)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=8, mode="dynamic", breakeven=256, seed=1)
+    g = gpu_ctx.train_forest(gc)
+    o, (olab, ovotes) = oracle.train_forest(X, y, 2, oc, predict_rows=Xt.T.copy())
+    lab, votes = gpu_ctx.predict(g, Xt.T.copy())
+    assert np.array_equal(lab, olab)
+    assert np.array_equal(votes, ovotes)
