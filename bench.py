@@ -262,7 +262,9 @@ def main():
                 "exact_kernel_gbs": round(st["exact_sector_bytes"] / (exact_ms / 1000.0) / 1e9, 1) if exact_ms else 0.0,
                 "phase_ms": {k: round(st[k], 2) for k in ("ms_sample", "ms_hist_rng", "ms_hist_count", "ms_exact",
                                                           "ms_partition", "ms_waves_total", "ms_host_binomial",
-                                                          "ms_host_bootstrap", "ms_train_total")}}
+                                                          "ms_host_bootstrap", "ms_train_total", "ms_host_roots",
+                                                          "ms_host_prep", "ms_host_submit", "ms_host_spec",
+                                                          "ms_host_wait", "ms_host_post", "ms_host_final")}}
     gpu_launches = int(st["kernel_launches"])
 
     # ---- end to end through the C ABI with host buffers ---------------------------------------

@@ -145,6 +145,9 @@ typedef struct sofg_stats {
   uint64_t waves, nodes, hist_nodes, exact_nodes, kernel_launches, levels;
   uint64_t hist_count_launches, exact_launches;
   double hist_strict_bytes, exact_strict_bytes, hist_sector_bytes, exact_sector_bytes;
+  /* host-side phases of the level loop (ms) */
+  double ms_host_roots, ms_host_prep, ms_host_submit, ms_host_spec, ms_host_wait, ms_host_post,
+      ms_host_final;
 } sofg_stats;
 /* enable: 1 = CUDA-event timing per phase (+ sector accounting when 2); 0 = off */
 int sofg_set_stats(sofg_ctx* ctx, int enable);

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "lib", "libsofg.so")
+    return os.path.join(_HERE, "lib", os.environ.get("SOFG_LIB", "libsofg.so"))
 
 
 class SofgError(RuntimeError):
@@ -53,7 +53,8 @@ class _Stats(C.Structure):
                [(n, C.c_uint64) for n in ("waves", "nodes", "hist_nodes", "exact_nodes", "kernel_launches",
                                            "levels", "hist_count_launches", "exact_launches")] + \
                [(n, C.c_double) for n in ("hist_strict_bytes", "exact_strict_bytes", "hist_sector_bytes",
-                                          "exact_sector_bytes")]
+                                          "exact_sector_bytes", "ms_host_roots", "ms_host_prep", "ms_host_submit",
+                                          "ms_host_spec", "ms_host_wait", "ms_host_post", "ms_host_final")]
 
 
 _MODES = {"exact": 0, "histogram": 1, "dynamic": 2}

@@ -613,6 +613,13 @@ int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
     o->exact_strict_bytes = s.exact_strict_bytes;
     o->hist_sector_bytes = s.hist_sector_bytes;
     o->exact_sector_bytes = s.exact_sector_bytes;
+    o->ms_host_roots = c->times.ms_roots;
+    o->ms_host_prep = c->times.ms_prep;
+    o->ms_host_submit = c->times.ms_submit;
+    o->ms_host_spec = c->times.ms_spec;
+    o->ms_host_wait = c->times.ms_wait;
+    o->ms_host_post = c->times.ms_post;
+    o->ms_host_final = c->times.ms_final;
   });
 }
 

@@ -25,6 +25,27 @@ __device__ __forceinline__ float midpoint_down(float a, float b) {
   return (t < b) ? t : a;
 }
 
+// Scattered 4-byte gathers from the column-major table. The cache operator matters: the
+// read-only path promotes L1 misses to whole lines, which multiplies HBM traffic for isolated
+// samples. SOFG_GATHER selects the operator (0 = ld.global.nc, 1 = .nc.L1::no_allocate,
+// 2 = .cg (L2 only), 3 = .cs (streaming)).
+#ifndef SOFG_GATHER
+#define SOFG_GATHER 2
+#endif
+__device__ __forceinline__ float gather(const float* p) {
+#if SOFG_GATHER == 0
+  return __ldg(p);
+#elif SOFG_GATHER == 1
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+#elif SOFG_GATHER == 2
+  return __ldcg(p);
+#else
+  return __ldcs(p);
+#endif
+}
+
 // projection.hpp:86-108 for one sample: terms in ascending feature order, double accumulation,
 // first term assigns, later terms add, rounded to float once. Weights are +-1 so w*x is exact.
 __device__ __forceinline__ float project_sample(const float* __restrict__ X, uint64_t ld,
@@ -34,8 +55,23 @@ __device__ __forceinline__ float project_sample(const float* __restrict__ X, uin
   double acc = 0.0;
   for (int t = 0; t < nt; ++t) {
     const uint32_t tm = terms[t];
-    const float x = __ldg(X + uint64_t(tm >> 1) * ld + sample);
+    const float x = gather(X + uint64_t(tm >> 1) * ld + sample);
     const double dx = (tm & 1u) ? -double(x) : double(x);
+    acc = (t == 0) ? dx : __dadd_rn(acc, dx);
+  }
+  return __double2float_rn(acc);
+}
+
+// The same value from the wave's gathered terms (csp.cu): Gn is the node's G block (term q of the
+// node at Gn[q*n + j]); the row's terms are q0..q0+nt-1 with signs in rt[t] & 1.
+__device__ __forceinline__ float combine_g(const float* __restrict__ Gn, uint32_t n,
+                                           const uint32_t* __restrict__ rt, int nt, uint32_t q0,
+                                           uint32_t j) {
+  if (nt == 0) return 0.f;
+  double acc = 0.0;
+  for (int t = 0; t < nt; ++t) {
+    const float x = Gn[uint64_t(q0 + uint32_t(t)) * n + j];
+    const double dx = (rt[t] & 1u) ? -double(x) : double(x);
     acc = (t == 0) ? dx : __dadd_rn(acc, dx);
   }
   return __double2float_rn(acc);

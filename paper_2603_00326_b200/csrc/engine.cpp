@@ -1,6 +1,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.hpp"
@@ -9,6 +10,14 @@ namespace sofg {
 
 WaveRunner::WaveRunner(int device) : device_(device) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  // The split search is a scattered 4-byte gather: ask L2 to fetch single 32-byte sectors from
+  // HBM instead of larger granules (override with SOFG_L2_FETCH=0..128 for experiments).
+  {
+    size_t gran = 32;
+    if (const char* e = std::getenv("SOFG_L2_FETCH")) gran = size_t(std::atoi(e));
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+    cudaGetLastError();
+  }
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
 }
@@ -39,11 +48,11 @@ int pow2_at_least(int x, int lo) {
 }
 }  // namespace
 
-void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
+void WaveRunner::submit(const WaveSpec& w) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   const DeviceData& D = data_;
   const int N = int(w.nodes.size());
-  res.assign(size_t(N), NodeRes{});
+  pend_n_ = N;
   if (N == 0) return;
   const uint32_t R = w.R;
   const int k = w.k;
@@ -52,10 +61,13 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
 
   // ---- derived work lists --------------------------------------------------------------
   std::vector<uint32_t> hist, exact, hist_slot(size_t(N), ~0u), multi_slot(size_t(N), ~0u);
+  std::vector<uint32_t> exact_b[7];
   std::vector<HistWork> work;
   std::vector<Tile> tiles;
   std::vector<uint32_t> tile_first(size_t(N) + 1, 0);
-  uint32_t zmax = 32, nmax_exact = 2, n_multi = 0;
+  uint32_t zmax = 32, n_multi = 0;
+  std::vector<uint64_t> gbase(static_cast<size_t>(N));
+  uint64_t g_total = 0, n_items = 0;
   uint64_t total_terms = 0;
   const uint32_t groups = (R + kHistRowsPerCta - 1) / kHistRowsPerCta;
   for (int i = 0; i < N; ++i) {
@@ -76,11 +88,14 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
     } else {
       if (nd.n > uint32_t(kExactSmemMax))
         throw std::invalid_argument("exact split of a node with " + std::to_string(nd.n) +
-                                    " samples exceeds the shared-memory exact splitter (" +
-                                    std::to_string(kExactSmemMax) + ")");
-      exact.push_back(uint32_t(i));
-      nmax_exact = std::max(nmax_exact, nd.n);
+                                    " samples exceeds the GPU exact splitter (" +
+                                    std::to_string(kExactSmemMax) + "); use a breakeven <= " +
+                                    std::to_string(kExactSmemMax));
+      exact_b[size_t(exact_bucket(nd.n))].push_back(uint32_t(i));
     }
+    gbase[size_t(i)] = g_total;
+    g_total += uint64_t(nd.z) * nd.n;
+    n_items += csp_items(nd.n, nd.z);
     tile_first[size_t(i)] = uint32_t(tiles.size());
     for (uint32_t s = 0, t = 0; s < nd.n; s += kTileElems, ++t)
       tiles.push_back({uint32_t(i), s, std::min(nd.n - s, uint32_t(kTileElems)), t});
@@ -92,7 +107,9 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
   Packer pk;
   const size_t o_nodes = pk.add(sizeof(NodeIn) * N);
   const size_t o_hist = pk.add(4 * hist.size());
+  for (auto& v : exact_b) exact.insert(exact.end(), v.begin(), v.end());
   const size_t o_exact = pk.add(4 * exact.size());
+  const size_t o_gbase = pk.add(8 * size_t(N));
   const size_t o_hslot = pk.add(4 * size_t(N));
   const size_t o_mslot = pk.add(4 * size_t(N));
   const size_t o_work = pk.add(sizeof(HistWork) * work.size());
@@ -111,6 +128,7 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
   put(o_nodes, w.nodes.data(), sizeof(NodeIn) * N);
   put(o_hist, hist.data(), 4 * hist.size());
   put(o_exact, exact.data(), 4 * exact.size());
+  put(o_gbase, gbase.data(), 8 * size_t(N));
   put(o_hslot, hist_slot.data(), 4 * size_t(N));
   put(o_mslot, multi_slot.data(), 4 * size_t(N));
   put(o_work, work.data(), sizeof(HistWork) * work.size());
@@ -127,6 +145,7 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
   const NodeIn* d_nodes = reinterpret_cast<const NodeIn*>(dp(o_nodes));
   const uint32_t* d_hist = reinterpret_cast<const uint32_t*>(dp(o_hist));
   const uint32_t* d_exact = reinterpret_cast<const uint32_t*>(dp(o_exact));
+  const uint64_t* d_gbase = reinterpret_cast<const uint64_t*>(dp(o_gbase));
   const uint32_t* d_hslot = reinterpret_cast<const uint32_t*>(dp(o_hslot));
   const uint32_t* d_mslot = reinterpret_cast<const uint32_t*>(dp(o_mslot));
   const HistWork* d_work = reinterpret_cast<const HistWork*>(dp(o_work));
@@ -157,6 +176,9 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
   uint32_t* d_gcnt = gcnt_.ensure(std::max<size_t>(1, size_t(n_multi) * R * bpad * k));
   uint32_t* d_done = done_.ensure(std::max<size_t>(1, size_t(n_multi) * groups));
   NodeRes* d_res = res_.ensure(size_t(N));
+  float* d_G = G_.ensure(std::max<uint64_t>(1, g_total));
+  uint64_t* d_items = items_.ensure(std::max<uint64_t>(1, n_items));
+  uint32_t* d_fcnt = fcnt_.ensure(w.d);
   uint32_t* d_flags = flags_.ensure(std::max<size_t>(1, tiles.size() * 32));
   uint32_t* d_tleft = tile_left_.ensure(std::max<size_t>(1, tiles.size()));
 
@@ -177,36 +199,46 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
                "sample_projection");
     ++launches;
   }
+  cuda_check(launch_csp(d_nodes, N, d_gbase, d_terms, w.d, n_items, d_fcnt, d_items, w.idx_in,
+                        D.X.p, D.ld, d_G, st_),
+             "column_sweep_gather");
+  launches += 4;
   if (timing) cudaEventRecord(ev_[1], st_);
   if (nh) {
     cuda_check(launch_hist_draws(d_nodes, d_hist, int(nh), R, bins, d_pos_proj, d_draws,
                                  d_pos_split, st_),
                "hist_draws");
     cuda_check(launch_hist_boundaries(d_nodes, d_hist, int(nh), R, bins, d_draws, d_terms, d_rp,
-                                      w.idx_in, D.X.p, D.ld, d_bnd, d_nb, st_),
+                                      d_gbase, d_G, d_bnd, d_nb, st_),
                "hist_boundaries");
     launches += 2;
   }
   if (timing) cudaEventRecord(ev_[2], st_);
   if (nh) {
     cuda_check(launch_hist_count(d_nodes, d_hslot, d_work, int(work.size()), d_mslot, R, bins, k,
-                                 w.chunk_cap, d_terms, d_rp, w.idx_in, w.lab_in, D.X.p, D.ld,
-                                 d_bnd, d_nb, D.xl.p, d_gcnt, d_done, d_rowres, st_),
+                                 w.chunk_cap, d_terms, d_rp, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
+                                 D.xl.p, d_gcnt, d_done, d_rowres, st_),
                "hist_count");
     cuda_check(launch_hist_select(d_hist, int(nh), R, d_rowres, d_res, st_), "hist_select");
     launches += 2;
   }
   if (timing) cudaEventRecord(ev_[3], st_);
-  if (!exact.empty()) {
-    cuda_check(launch_exact(d_nodes, d_exact, int(exact.size()), R, k, nmax_exact, d_terms, d_rp,
-                            w.idx_in, w.lab_in, D.X.p, D.ld, D.xl.p, d_res, st_),
-               "exact");
-    ++launches;
+  {
+    size_t off = 0;
+    for (int b = 0; b < 7; ++b) {
+      const size_t m = exact_b[b].size();
+      if (!m) continue;
+      cuda_check(launch_exact_bucket(b, d_nodes, d_exact + off, int(m), R, k, d_terms, d_rp,
+                                     w.lab_in, d_gbase, d_G, D.xl.p, d_res, st_),
+                 "exact_bucket");
+      off += m;
+      ++launches;
+    }
   }
   if (timing) cudaEventRecord(ev_[4], st_);
   cuda_check(launch_partition(d_nodes, N, d_tiles, int(tiles.size()), d_tfirst, R, k, d_terms,
                               d_rp, d_pos_proj, d_pos_split, w.idx_in, w.lab_in, w.idx_out,
-                              w.lab_out, D.X.p, D.ld, d_res, d_flags, d_tleft, st_),
+                              w.lab_out, d_gbase, d_G, d_res, d_flags, d_tleft, st_),
              "partition");
   launches += 3;
   if (timing) cudaEventRecord(ev_[5], st_);
@@ -214,16 +246,28 @@ void WaveRunner::run(const WaveSpec& w, std::vector<NodeRes>& res) {
   NodeRes* hr = h_res_.ensure(size_t(N));
   cuda_check(cudaMemcpyAsync(hr, d_res, sizeof(NodeRes) * N, cudaMemcpyDeviceToHost, st_),
              "D2H res");
-  cuda_check(cudaStreamSynchronize(st_), "wave sync");
-  std::memcpy(res.data(), hr, sizeof(NodeRes) * N);
+  pend_dres_ = d_res;
+  pend_launches_ = launches;
+  pend_hist_ = nh;
+  pend_exact_ = exact.size();
+}
 
+void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
+  const int N = pend_n_;
+  res.assign(size_t(N), NodeRes{});
+  if (N == 0) return;
+  cuda_check(cudaStreamSynchronize(st_), "wave sync");
+  std::memcpy(res.data(), h_res_.p, sizeof(NodeRes) * N);
+  const size_t nh = pend_hist_;
+  const int launches = pend_launches_;
+  const bool timing = collect_stats;
   stats.waves++;
   stats.nodes += uint64_t(N);
   stats.hist_nodes += nh;
-  stats.exact_nodes += exact.size();
+  stats.exact_nodes += pend_exact_;
   stats.launches += uint64_t(launches);
   if (nh) stats.hist_count_launches++;
-  if (!exact.empty()) stats.exact_launches++;
+  if (pend_exact_) stats.exact_launches++;
   if (timing) {
     float t[5];
     for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], ev_[i], ev_[i + 1]);

@@ -124,7 +124,16 @@ class WaveRunner {
   const DeviceData& data() const { return data_; }
 
   // Searches and partitions every node of `w`; res[i] receives node i's result.
-  void run(const WaveSpec& w, std::vector<NodeRes>& res);
+  void run(const WaveSpec& w, std::vector<NodeRes>& res) {
+    submit(w);
+    collect(w, res);
+  }
+  // Asynchronous halves of run(): submit() enqueues the wave's copies and kernels and returns;
+  // collect() waits for them and copies the node results out. `w` must stay alive in between.
+  void submit(const WaveSpec& w);
+  void collect(const WaveSpec& w, std::vector<NodeRes>& res);
+  // Page-locked staging reused across calls (root segments).
+  PinnedBuf<unsigned char> staging;
   // Terms of projection row `row` of node `node` of the last wave (for rows longer than the
   // kWinTermsMax terms NodeRes carries inline).
   std::vector<uint32_t> fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row);
@@ -149,8 +158,15 @@ class WaveRunner {
   DevBuf<float> bnd_;
   DevBuf<RowRes> rowres_;
   DevBuf<NodeRes> res_;
+  DevBuf<float> G_;        // gathered term values of the wave (csp.cu)
+  DevBuf<uint64_t> items_; // feature-sorted gather items
+  DevBuf<uint32_t> fcnt_;  // per-feature item counts / cursors
   const uint32_t* last_terms_ = nullptr;
   const uint32_t* last_rp_ = nullptr;
+  // submit -> collect state
+  NodeRes* pend_dres_ = nullptr;
+  int pend_n_ = 0, pend_launches_ = 0;
+  size_t pend_hist_ = 0, pend_exact_ = 0;
 };
 
 }  // namespace sofg

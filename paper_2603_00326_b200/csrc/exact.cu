@@ -1,0 +1,637 @@
+// Exact splitter, register-resident (reference best_split_exact, split.hpp:142-194, driven per
+// row by find_node_split, split.hpp:306-312).
+//
+// Nodes are bucketed by padded size P = 32*E (E keys per lane, blocked layout: lane l holds
+// sorted positions [l*E, (l+1)*E)). Per row a warp
+//   1. gathers the node's projected values, G rows at a time so G*E loads are in flight,
+//   2. builds keys (order_key(v) << 32 | label) — the reference's packed sort key,
+//   3. bitonic-sorts them in registers (intra-lane compare-exchange for strides < E, shuffles
+//      for strides >= E),
+//   4. scans class counts and evaluates the impurity sum at every gap between distinct values,
+//   5. resolves the reference's first-maximum position (see dev_util.cuh: impurity_sum).
+// E <= 4: one warp per node (four nodes per CTA). E >= 8: four warps per node, rows split
+// round-robin, reduced in shared memory (lowest row wins ties, as split.hpp:259-263).
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "dev_util.cuh"
+#include "kernels.hpp"
+
+namespace sofg {
+namespace dev {
+
+template <int E>
+__device__ __forceinline__ void reg_bitonic_sort(uint64_t (&key)[E], int lane) {
+  constexpr int P = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lm = j / E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, key[e], lm);
+          const int i = lane * E + e;
+          const bool up = (i & k) == 0;
+          const bool lower = (lane & lm) == 0;
+          const uint64_t mn = o < key[e] ? o : key[e];
+          const uint64_t mx = o < key[e] ? key[e] : o;
+          key[e] = (lower == up) ? mn : mx;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & j) == 0) {
+            const int i = lane * E + e;
+            const bool up = (i & k) == 0;
+            const uint64_t a = key[e], b = key[e | j];
+            const bool sw = (a > b) == up;
+            key[e] = sw ? b : a;
+            key[e | j] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
+struct Best {
+  double gain;
+  float thr;
+  uint32_t nl;
+  int row;
+};
+
+// Search one sorted row (keys in blocked layout). Updates `b` when this row's best gain is
+// strictly larger (rows are visited in increasing order by the calling warp).
+template <int E, int KC>
+__device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, int k,
+                                         const uint32_t* tot, double parent,
+                                         const double* __restrict__ xl, int row, int lane,
+                                         Best& b) {
+  // per-lane class counts
+  uint32_t loc[KC], pre[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) loc[c] = 0;
+  const int p0 = lane * E;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (uint32_t(p0 + e) < n) {
+      const int c = int(key[e] & 0xffu);
+#pragma unroll
+      for (int cc = 0; cc < KC; ++cc) loc[cc] += (cc == c);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    uint32_t t;
+    pre[c] = warp_excl_scan_u32(loc[c], lane, &t);
+  }
+  const uint64_t next_first = __shfl_down_sync(0xffffffffu, key[0], 1);
+  const double dn = double(n);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+
+  auto eval = [&](auto&& visit) {
+    uint32_t left[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) left[c] = pre[c];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t p = uint32_t(p0 + e);
+      if (p + 1 < n) {
+        const int c = int(key[e] & 0xffu);
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
+        const uint64_t kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
+        const float a = order_key_inv(uint32_t(key[e] >> 32));
+        const float bb = order_key_inv(uint32_t(kb >> 32));
+        if (a < bb) {
+          const uint32_t nl = p + 1;
+          double X;
+          if constexpr (KC == 2) {
+            const uint32_t l1 = left[1], l0 = nl - l1;
+            const double sl = __dadd_rn(__ldg(xl + l0), __ldg(xl + l1));
+            const double sr = __dadd_rn(__ldg(xl + tot[0] - l0), __ldg(xl + tot[1] - l1));
+            X = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+          } else {
+            double sl = 0.0, sr = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < KC; ++cc)
+              if (cc < k) {
+                sl = __dadd_rn(sl, __ldg(xl + left[cc]));
+                sr = __dadd_rn(sr, __ldg(xl + tot[cc] - left[cc]));
+              }
+            X = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+          }
+          if (visit(X, p, a, bb)) return;
+        }
+      }
+    }
+  };
+
+  double xmin = inf;
+  eval([&](double X, uint32_t, float, float) {
+    xmin = fmin(xmin, X);
+    return false;
+  });
+  xmin = warp_min_f64(xmin);
+  if (!(xmin < inf)) return;
+  const double g = gain_from_x(parent, xmin, dn);
+  if (!(g > 0.0)) return;
+  if (b.row >= 0 && !(g > b.gain)) return;
+  const double win = x_window(parent, xmin, dn);
+  uint32_t first = 0xffffffffu;
+  float fa = 0.f, fb = 0.f;
+  eval([&](double X, uint32_t p, float a, float bb) {
+    if (X <= win && gain_from_x(parent, X, dn) == g) {
+      first = p;
+      fa = a;
+      fb = bb;
+      return true;
+    }
+    return false;
+  });
+  const uint32_t fp = warp_min_u32(first);
+  const int src = __ffs(__ballot_sync(0xffffffffu, first == fp)) - 1;
+  fa = __shfl_sync(0xffffffffu, fa, src);
+  fb = __shfl_sync(0xffffffffu, fb, src);
+  b.row = row;
+  b.gain = g;
+  b.thr = midpoint_down(fa, fb);
+  b.nl = fp + 1;
+}
+
+// E keys per lane, G rows in flight per warp, WPN warps per node, KC class-count registers.
+template <int E, int GR, int WPN, int KC>
+__global__ void __launch_bounds__(128) k_exact_reg(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
+    int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
+    const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
+    const float* __restrict__ G, const double* __restrict__ xl, NodeRes* __restrict__ res) {
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int li = (WPN == 1) ? int(blockIdx.x) * 4 + w : int(blockIdx.x);
+  const int wr = (WPN == 1) ? 0 : w;  // rank of this warp within the node
+  __shared__ Best s_best[4];
+  if (li >= n_list) return;  // only reachable when WPN == 1 (whole warp exits)
+  const uint32_t node = list[li];
+  const NodeIn nd = nodes[node];
+  const uint32_t n = nd.n;
+
+  const float* Gn = G + gbase[node];
+  uint32_t cnt[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) cnt[c] = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t p = uint32_t(lane * E + e);
+    if (p < n) {
+      const int yy = lab[nd.begin + p];
+#pragma unroll
+      for (int c = 0; c < KC; ++c) cnt[c] += (c == yy);
+    }
+  }
+  uint32_t tot[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    uint32_t x = cnt[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    tot[c] = x;
+  }
+
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  const uint32_t* nterms = terms + nd.term_off;
+  Best best{0.0, 0.f, 0, -1};
+
+  for (uint32_t r0 = uint32_t(wr * GR); r0 < R; r0 += uint32_t(WPN * GR)) {
+    uint32_t tb[GR];
+    int nt[GR];
+    int ntmax = 0;
+#pragma unroll
+    for (int g = 0; g < GR; ++g) {
+      const uint32_t r = r0 + uint32_t(g);
+      if (r < R) {
+        tb[g] = rp[r];
+        nt[g] = int(rp[r + 1] - tb[g]);
+      } else {
+        tb[g] = 0;
+        nt[g] = 0;
+      }
+      ntmax = max(ntmax, nt[g]);
+    }
+    double acc[GR][E];
+    for (int t = 0; t < ntmax; ++t) {
+      float xv[GR][E];
+      uint32_t tm[GR];
+#pragma unroll
+      for (int g = 0; g < GR; ++g) tm[g] = t < nt[g] ? __ldg(nterms + tb[g] + t) : 0u;
+#pragma unroll
+      for (int g = 0; g < GR; ++g) {
+        const float* gq = Gn + uint64_t(tb[g] + uint32_t(t)) * n;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          xv[g][e] = (t < nt[g] && uint32_t(lane * E + e) < n) ? gq[lane * E + e] : 0.f;
+      }
+#pragma unroll
+      for (int g = 0; g < GR; ++g) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double dx = (tm[g] & 1u) ? -double(xv[g][e]) : double(xv[g][e]);
+          if (t == 0)
+            acc[g][e] = dx;
+          else if (t < nt[g])
+            acc[g][e] = __dadd_rn(acc[g][e], dx);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < GR; ++g) {
+      const uint32_t r = r0 + uint32_t(g);
+      if (r >= R || nt[g] == 0) continue;  // empty rows are skipped in exact mode (split.hpp:308)
+      uint64_t key[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (uint32_t(lane * E + e) < n) {
+          const float v = __double2float_rn(acc[g][e]);
+          key[e] = (uint64_t(order_key(v)) << 32) | uint64_t(__ldg(lab + nd.begin + lane * E + e));
+        } else {
+          key[e] = ~0ull;
+        }
+      }
+      reg_bitonic_sort<E>(key, lane);
+      scan_row<E, KC>(key, n, k, tot, nd.parent, xl, int(r), lane, best);
+    }
+  }
+
+  if (WPN == 1) {
+    if (lane == 0) {
+      NodeRes& o = res[node];
+      o.row = best.row;
+      o.gain = best.gain;
+      o.threshold = best.thr;
+      o.n_left_search = best.nl;
+    }
+    return;
+  }
+  if (lane == 0) s_best[w] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best bb{0.0, 0.f, 0, -1};
+    for (int i = 0; i < WPN; ++i) {
+      const Best& c = s_best[i];
+      if (c.row < 0) continue;
+      if (bb.row < 0 || c.gain > bb.gain || (c.gain == bb.gain && c.row < bb.row)) bb = c;
+    }
+    NodeRes& o = res[node];
+    o.row = bb.row;
+    o.gain = bb.gain;
+    o.threshold = bb.thr;
+    o.n_left_search = bb.nl;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Team variant for nodes of 257..2048 samples: a team of W warps (E = 8 keys per lane) sorts one
+// row together. Strides < 8 are intra-lane, < 256 shuffles, >= 256 go through shared memory
+// between the team's warps (named barrier per team). CTA = 8 warps = 8/W teams; teams take rows
+// round-robin, the CTA reduces the teams' bests (lowest row wins ties).
+// ------------------------------------------------------------------------------------------
+template <int W>
+__device__ __forceinline__ void team_sync(int team) {
+  if constexpr (W == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(W * 32) : "memory");
+  }
+}
+
+template <int W, int KC>
+__global__ void __launch_bounds__(256) k_exact_team(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
+    int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
+    const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
+    const float* __restrict__ G, const double* __restrict__ xl, NodeRes* __restrict__ res) {
+  constexpr int E = 8;
+  constexpr int TEAMS = 8 / W;
+  constexpr int P = 32 * E * W;
+  __shared__ uint64_t s_keys[8 * 32 * E];   // TEAMS * P == 2048 keys
+  __shared__ uint32_t s_cnt[8][KC];
+  __shared__ uint64_t s_first[8];
+  __shared__ double s_xmin[8];
+  __shared__ uint32_t s_pos[8];
+  __shared__ Best s_best[TEAMS];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int team = w / W;
+  const int wt = w % W;
+  uint64_t* buf = s_keys + team * P;
+  const uint32_t node = list[blockIdx.x];
+  const NodeIn nd = nodes[node];
+  const uint32_t n = nd.n;
+  const int p0 = (wt * 32 + lane) * E;  // first position held by this lane
+
+  const float* Gn = G + gbase[node];
+  uint32_t cnt[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) cnt[c] = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t p = uint32_t(p0 + e);
+    if (p < n) {
+      const int yy = lab[nd.begin + p];
+#pragma unroll
+      for (int c = 0; c < KC; ++c) cnt[c] += (c == yy);
+    }
+  }
+  // node class totals (whole CTA: every team holds the full node)
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    uint32_t x = cnt[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_cnt[w][c] = x;
+  }
+  __syncthreads();
+  uint32_t tot[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    uint32_t x = 0;
+    for (int i = 0; i < W; ++i) x += s_cnt[team * W + i][c];
+    tot[c] = x;
+  }
+  __syncthreads();
+
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  const uint32_t* nterms = terms + nd.term_off;
+  Best best{0.0, 0.f, 0, -1};
+  const double dn = double(n);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+
+  for (uint32_t r = uint32_t(team); r < R; r += uint32_t(TEAMS)) {
+    const uint32_t tb = rp[r];
+    const int nt = int(rp[r + 1] - tb);
+    if (nt == 0) continue;  // uniform per team; split.hpp:308
+    double acc[E];
+    for (int t = 0; t < nt; ++t) {
+      const uint32_t tm = __ldg(nterms + tb + t);
+      const float* gq = Gn + uint64_t(tb + uint32_t(t)) * n;
+      float xv[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) xv[e] = uint32_t(p0 + e) < n ? gq[p0 + e] : 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double dx = (tm & 1u) ? -double(xv[e]) : double(xv[e]);
+        acc[e] = t == 0 ? dx : __dadd_rn(acc[e], dx);
+      }
+    }
+    uint64_t key[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (uint32_t(p0 + e) < n) {
+        const float v = __double2float_rn(acc[e]);
+        key[e] = (uint64_t(order_key(v)) << 32) | uint64_t(__ldg(lab + nd.begin + p0 + e));
+      } else {
+        key[e] = ~0ull;
+      }
+    }
+    // ---- bitonic sort over the team's P positions
+#pragma unroll
+    for (int kk = 2; kk <= P; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        if (j >= 32 * E) {  // across warps, through shared memory
+#pragma unroll
+          for (int e = 0; e < E; ++e) buf[p0 + e] = key[e];
+          team_sync<W>(team);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = p0 + e;
+            const uint64_t o = buf[i ^ j];
+            const bool up = (i & kk) == 0;
+            const bool lower = (i & j) == 0;
+            const uint64_t mn = o < key[e] ? o : key[e];
+            const uint64_t mx = o < key[e] ? key[e] : o;
+            key[e] = (lower == up) ? mn : mx;
+          }
+          team_sync<W>(team);
+        } else if (j >= E) {
+          const int lm = j / E;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, key[e], lm);
+            const int i = p0 + e;
+            const bool up = (i & kk) == 0;
+            const bool lower = (lane & lm) == 0;
+            const uint64_t mn = o < key[e] ? o : key[e];
+            const uint64_t mx = o < key[e] ? key[e] : o;
+            key[e] = (lower == up) ? mn : mx;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            if ((e & j) == 0) {
+              const int i = p0 + e;
+              const bool up = (i & kk) == 0;
+              const uint64_t a = key[e], b = key[e | j];
+              const bool sw = (a > b) == up;
+              key[e] = sw ? b : a;
+              key[e | j] = sw ? a : b;
+            }
+          }
+        }
+      }
+    }
+    // ---- class prefix across the team
+    uint32_t loc[KC], pre[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) loc[c] = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (uint32_t(p0 + e) < n) {
+        const int c = int(key[e] & 0xffu);
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc) loc[cc] += (cc == c);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      uint32_t wtot;
+      pre[c] = warp_excl_scan_u32(loc[c], lane, &wtot);
+      if (lane == 0) s_cnt[w][c] = wtot;
+    }
+    if (lane == 0) s_first[w] = key[0];
+    team_sync<W>(team);
+#pragma unroll
+    for (int c = 0; c < KC; ++c)
+      for (int i = 0; i < wt; ++i) pre[c] += s_cnt[team * W + i][c];
+    uint64_t next_first = __shfl_down_sync(0xffffffffu, key[0], 1);
+    if (lane == 31) next_first = (wt + 1 < W) ? s_first[w + 1] : ~0ull;
+    team_sync<W>(team);
+
+    auto eval = [&](auto&& visit) {
+      uint32_t left[KC];
+#pragma unroll
+      for (int c = 0; c < KC; ++c) left[c] = pre[c];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t p = uint32_t(p0 + e);
+        if (p + 1 < n) {
+          const int c = int(key[e] & 0xffu);
+#pragma unroll
+          for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
+          const uint64_t kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
+          const float a = order_key_inv(uint32_t(key[e] >> 32));
+          const float bb = order_key_inv(uint32_t(kb >> 32));
+          if (a < bb) {
+            const uint32_t nl = p + 1;
+            double Xv;
+            if constexpr (KC == 2) {
+              const uint32_t l1 = left[1], l0 = nl - l1;
+              const double sl = __dadd_rn(__ldg(xl + l0), __ldg(xl + l1));
+              const double sr = __dadd_rn(__ldg(xl + tot[0] - l0), __ldg(xl + tot[1] - l1));
+              Xv = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+            } else {
+              double sl = 0.0, sr = 0.0;
+#pragma unroll
+              for (int cc = 0; cc < KC; ++cc)
+                if (cc < k) {
+                  sl = __dadd_rn(sl, __ldg(xl + left[cc]));
+                  sr = __dadd_rn(sr, __ldg(xl + tot[cc] - left[cc]));
+                }
+              Xv = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+            }
+            if (visit(Xv, p, a, bb)) return;
+          }
+        }
+      }
+    };
+    double xmin = inf;
+    eval([&](double Xv, uint32_t, float, float) {
+      xmin = fmin(xmin, Xv);
+      return false;
+    });
+    xmin = warp_min_f64(xmin);
+    if (lane == 0) s_xmin[w] = xmin;
+    team_sync<W>(team);
+    for (int i = 0; i < W; ++i) xmin = fmin(xmin, s_xmin[team * W + i]);
+    team_sync<W>(team);
+    if (!(xmin < inf)) continue;
+    const double g = gain_from_x(nd.parent, xmin, dn);
+    if (!(g > 0.0)) continue;
+    if (best.row >= 0 && !(g > best.gain)) continue;
+    const double win = x_window(nd.parent, xmin, dn);
+    uint32_t first = 0xffffffffu;
+    eval([&](double Xv, uint32_t p, float, float) {
+      if (Xv <= win && gain_from_x(nd.parent, Xv, dn) == g) {
+        first = p;
+        return true;
+      }
+      return false;
+    });
+    first = warp_min_u32(first);
+    if (lane == 0) s_pos[w] = first;
+    team_sync<W>(team);
+    uint32_t fp = first;
+    for (int i = 0; i < W; ++i) fp = min(fp, s_pos[team * W + i]);
+    // the two keys around the winning gap: positions fp, fp+1
+    if (uint32_t(p0) <= fp && fp < uint32_t(p0 + E)) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (uint32_t(p0 + e) == fp) s_first[team * W] = key[e];
+    }
+    if (uint32_t(p0) <= fp + 1 && fp + 1 < uint32_t(p0 + E)) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (uint32_t(p0 + e) == fp + 1) s_keys[team * P + 0] = key[e];
+    }
+    team_sync<W>(team);
+    const float a = order_key_inv(uint32_t(s_first[team * W] >> 32));
+    const float b = order_key_inv(uint32_t(s_keys[team * P + 0] >> 32));
+    team_sync<W>(team);
+    best.row = int(r);
+    best.gain = g;
+    best.thr = midpoint_down(a, b);
+    best.nl = fp + 1;
+  }
+  if (wt == 0 && lane == 0) s_best[team] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best bb{0.0, 0.f, 0, -1};
+    for (int i = 0; i < TEAMS; ++i) {
+      const Best& c = s_best[i];
+      if (c.row < 0) continue;
+      if (bb.row < 0 || c.gain > bb.gain || (c.gain == bb.gain && c.row < bb.row)) bb = c;
+    }
+    NodeRes& o = res[node];
+    o.row = bb.row;
+    o.gain = bb.gain;
+    o.threshold = bb.thr;
+    o.n_left_search = bb.nl;
+  }
+}
+
+template <int W, int KC>
+cudaError_t launch_team(const NodeIn* nodes, const uint32_t* list, int n, uint32_t R, int k,
+                        const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
+                        const uint64_t* gbase, const float* G, const double* xl, NodeRes* res,
+                        cudaStream_t st) {
+  k_exact_team<W, KC><<<n, 256, 0, st>>>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl,
+                                         res);
+  return cudaGetLastError();
+}
+
+template <int E, int GR, int WPN, int KC>
+cudaError_t launch_bucket(const NodeIn* nodes, const uint32_t* list, int n, uint32_t R, int k,
+                          const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
+                          const uint64_t* gbase, const float* G, const double* xl, NodeRes* res,
+                          cudaStream_t st) {
+  const int grid = WPN == 1 ? (n + 3) / 4 : n;
+  k_exact_reg<E, GR, WPN, KC><<<grid, 128, 0, st>>>(nodes, list, n, R, k, terms, row_ptr, lab,
+                                                     gbase, G, xl, res);
+  return cudaGetLastError();
+}
+
+template <int KC>
+cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
+                             uint32_t R, int k, const uint32_t* terms, const uint32_t* row_ptr,
+                             const uint8_t* lab, const uint64_t* gbase, const float* G,
+                             const double* xl, NodeRes* res, cudaStream_t st) {
+  switch (bucket) {
+    case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    case 3: return launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace dev
+
+int exact_bucket(uint32_t n) {
+  int b = 0;
+  uint32_t cap = 32;
+  while (cap < n) {
+    cap <<= 1;
+    ++b;
+  }
+  return b;  // 0..6 for n <= 2048
+}
+
+cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
+                                uint32_t R, int k, const uint32_t* terms,
+                                const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
+                                const float* G, const double* xl, NodeRes* res, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  if (k == 2)
+    return dev::launch_bucket_kc<2>(bucket, nodes, list, n, R, k, terms, row_ptr, lab, gbase, G,
+                                    xl, res, st);
+  return dev::launch_bucket_kc<kMaxClasses>(bucket, nodes, list, n, R, k, terms, row_ptr, lab,
+                                            gbase, G, xl, res, st);
+}
+
+}  // namespace sofg

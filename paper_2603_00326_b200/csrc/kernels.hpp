@@ -19,7 +19,7 @@ cudaError_t launch_hist_draws(const NodeIn* nodes, const uint32_t* hist_nodes, i
 cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nodes, int n_hist,
                                    uint32_t R, uint32_t bins, const uint32_t* draws,
                                    const uint32_t* terms, const uint32_t* row_ptr,
-                                   const uint32_t* idx, const float* X, uint64_t ld, float* bnd,
+                                   const uint64_t* gbase, const float* G, float* bnd,
                                    uint32_t* nb, cudaStream_t st);
 
 // split.cu
@@ -27,18 +27,25 @@ size_t hist_count_smem(uint32_t bins, int k, int chunk_cap);
 cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slot,
                               const HistWork* work, int n_work, const uint32_t* multi_slot,
                               uint32_t R, uint32_t bins, int k, int chunk_cap,
-                              const uint32_t* terms, const uint32_t* row_ptr, const uint32_t* idx,
-                              const uint8_t* lab, const float* X, uint64_t ld, const float* bnd,
+                              const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
+                              const uint64_t* gbase, const float* G, const float* bnd,
                               const uint32_t* nb, const double* xl, uint32_t* gcnt,
                               uint32_t* done, RowRes* rowres, cudaStream_t st);
 cudaError_t launch_hist_select(const uint32_t* hist_nodes, int n_hist, uint32_t R,
                                const RowRes* rowres, NodeRes* res, cudaStream_t st);
-size_t exact_smem(int npad_max, int warps);
-cudaError_t launch_exact(const NodeIn* nodes, const uint32_t* exact_nodes, int n_exact,
-                         uint32_t R, int k, uint32_t nmax, const uint32_t* terms,
-                         const uint32_t* row_ptr, const uint32_t* idx, const uint8_t* lab,
-                         const float* X, uint64_t ld, const double* xl, NodeRes* res,
-                         cudaStream_t st);
+// csp.cu — column-sweep gather into G (per node: z x n raw values, term-major)
+uint64_t csp_items(uint32_t n, uint32_t z);
+cudaError_t launch_csp(const NodeIn* nodes, int n_nodes, const uint64_t* gbase,
+                       const uint32_t* terms, uint32_t d, uint64_t n_items, uint32_t* cnt,
+                       uint64_t* items, const uint32_t* idx, const float* X, uint64_t ld, float* G,
+                       cudaStream_t st);
+
+// exact.cu — register-resident exact splitter, bucketed by node size (<= 2048 samples)
+int exact_bucket(uint32_t n);
+cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
+                                uint32_t R, int k, const uint32_t* terms,
+                                const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
+                                const float* G, const double* xl, NodeRes* res, cudaStream_t st);
 
 // partition.cu
 cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles, int n_tiles,
@@ -46,7 +53,7 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint32_t* row_ptr, const uint32_t* pos_proj,
                              const uint32_t* pos_split, const uint32_t* idx_in,
                              const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
-                             const float* X, uint64_t ld, NodeRes* res, uint32_t* flags,
+                             const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
                              uint32_t* tile_left, cudaStream_t st);
 
 cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_tiles,

@@ -19,8 +19,8 @@ namespace dev {
 __global__ void __launch_bounds__(256) k_part_flags(
     const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, uint32_t R, int k,
     const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
-    const uint32_t* __restrict__ idx, const uint8_t* __restrict__ lab, const float* __restrict__ X,
-    uint64_t ld, NodeRes* __restrict__ res, uint32_t* __restrict__ flags,
+    const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
+    const float* __restrict__ G, NodeRes* __restrict__ res, uint32_t* __restrict__ flags,
     uint32_t* __restrict__ tile_left) {
   __shared__ uint32_t s_cls[kMaxClasses];
   __shared__ uint32_t s_left;
@@ -33,8 +33,10 @@ __global__ void __launch_bounds__(256) k_part_flags(
   if (threadIdx.x == 0) s_left = 0;
   __syncthreads();
   const uint32_t* rp = row_ptr + size_t(tl.node) * (R + 1);
-  const uint32_t* rt = terms + nd.term_off + rp[row];
-  const int nt = int(rp[row + 1] - rp[row]);
+  const uint32_t q0 = rp[row];
+  const uint32_t* rt = terms + nd.term_off + q0;
+  const int nt = int(rp[row + 1] - q0);
+  const float* Gn = G + gbase[tl.node];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   uint32_t my_left = 0;
@@ -47,9 +49,8 @@ __global__ void __launch_bounds__(256) k_part_flags(
   for (int e = 0; e < 4; ++e) {
     const uint32_t l = uint32_t(e * 256 + threadIdx.x);
     if (l < tl.len) {
-      const uint32_t p = nd.begin + tl.start + l;
-      v[e] = project_sample(X, ld, rt, nt, idx[p]);
-      y[e] = lab[p];
+      v[e] = combine_g(Gn, nd.n, rt, nt, q0, tl.start + l);
+      y[e] = lab[nd.begin + tl.start + l];
     }
   }
 #pragma unroll
@@ -187,12 +188,12 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint32_t* row_ptr, const uint32_t* pos_proj,
                              const uint32_t* pos_split, const uint32_t* idx_in,
                              const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
-                             const float* X, uint64_t ld, NodeRes* res, uint32_t* flags,
+                             const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
                              uint32_t* tile_left, cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
   if (n_tiles > 0)
-    dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, idx_in, lab_in,
-                                               X, ld, res, flags, tile_left);
+    dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, lab_in, gbase,
+                                               G, res, flags, tile_left);
   dev::k_part_scan<<<(n_nodes + 3) / 4, 128, 0, st>>>(nodes, n_nodes, R, tile_first, terms,
                                                       row_ptr, pos_proj, pos_split, tile_left, res);
   if (n_tiles > 0)

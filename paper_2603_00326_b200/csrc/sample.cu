@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist,
     uint32_t R, uint32_t bins, int mpad, const uint32_t* __restrict__ draws,
     const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
-    const uint32_t* __restrict__ idx, const float* __restrict__ X, uint64_t ld,
+    const uint64_t* __restrict__ gbase, const float* __restrict__ G,
     float* __restrict__ bnd, uint32_t* __restrict__ nb_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -235,9 +235,10 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
   const uint32_t m = min(bins, n);
   const uint32_t J0 = n - m;
   const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
-  const uint32_t* rt = terms + nd.term_off + rp[r];
-  const int nt = int(rp[r + 1] - rp[r]);
-  const uint32_t* seg = idx + nd.begin;
+  const uint32_t q0 = rp[r];
+  const uint32_t* rt = terms + nd.term_off + q0;
+  const int nt = int(rp[r + 1] - q0);
+  const float* Gn = G + gbase[node];
 
   if (m < n) {
     const uint32_t* t = draws + size_t(h) * R * bins + size_t(r) * m;
@@ -272,13 +273,13 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
       uint32_t key = 0xffffffffu;
       if (i < int(m)) {
         const uint32_t p = col[i] ? J0 + uint32_t(i) : t[i];
-        key = order_key(project_sample(X, ld, rt, nt, seg[p]));
+        key = order_key(combine_g(Gn, n, rt, nt, q0, p));
       }
       vk[i] = key;
     }
   } else {
     for (int i = lane; i < mpad; i += 32)
-      vk[i] = i < int(m) ? order_key(project_sample(X, ld, rt, nt, seg[i])) : 0xffffffffu;
+      vk[i] = i < int(m) ? order_key(combine_g(Gn, n, rt, nt, q0, uint32_t(i))) : 0xffffffffu;
   }
   __syncwarp();
   warp_bitonic_sort(vk, mpad, lane);
@@ -339,7 +340,7 @@ cudaError_t launch_hist_draws(const NodeIn* nodes, const uint32_t* hist_nodes, i
 cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nodes, int n_hist,
                                    uint32_t R, uint32_t bins, const uint32_t* draws,
                                    const uint32_t* terms, const uint32_t* row_ptr,
-                                   const uint32_t* idx, const float* X, uint64_t ld, float* bnd,
+                                   const uint64_t* gbase, const float* G, float* bnd,
                                    uint32_t* nb, cudaStream_t st) {
   if (n_hist == 0) return cudaSuccess;
   const int mpad = next_pow2(int(bins));
@@ -353,7 +354,7 @@ cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nod
   const uint64_t items = uint64_t(n_hist) * R;
   const unsigned grid = unsigned((items + warps - 1) / warps);
   dev::k_hist_boundaries<<<grid, warps * 32, smem, st>>>(nodes, hist_nodes, n_hist, R, bins, mpad,
-                                                         draws, terms, row_ptr, idx, X, ld, bnd,
+                                                         draws, terms, row_ptr, gbase, G, bnd,
                                                          nb);
   return cudaGetLastError();
 }

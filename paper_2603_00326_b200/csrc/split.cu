@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(256) k_hist_count(
     const HistWork* __restrict__ work, const uint32_t* __restrict__ multi_slot,
     uint32_t R, uint32_t bins, int bpad, int k, int chunk_cap,
     const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
-    const uint32_t* __restrict__ idx, const uint8_t* __restrict__ lab,
-    const float* __restrict__ X, uint64_t ld, const float* __restrict__ bnd_g,
+    const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
+    const float* __restrict__ G, const float* __restrict__ bnd_g,
     const uint32_t* __restrict__ nb_g, const double* __restrict__ xl,
     uint32_t* __restrict__ gcnt, uint32_t* __restrict__ done, RowRes* __restrict__ rowres) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -139,8 +139,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
   // smem layout
   uint32_t* cnt_s = reinterpret_cast<uint32_t*>(smem_raw);                  // [8][bpad][k]
   float* bnd_s = reinterpret_cast<float*>(cnt_s + size_t(8) * bpad * k);      // [8][bpad]
-  uint32_t* idx_s = reinterpret_cast<uint32_t*>(bnd_s + size_t(8) * bpad);   // [chunk_cap]
-  uint8_t* lab_s = reinterpret_cast<uint8_t*>(idx_s + chunk_cap);            // [chunk_cap]
+  uint8_t* lab_s = reinterpret_cast<uint8_t*>(bnd_s + size_t(8) * bpad);     // [chunk_cap]
   __shared__ int s_last;
 
   const uint32_t r = wk.row0 + uint32_t(w);
@@ -152,19 +151,17 @@ __global__ void __launch_bounds__(256) k_hist_count(
   const float inf = __int_as_float(0x7f800000);
   const float* gb = bnd_g + (size_t(h) * R + (row_ok ? r : 0)) * (bins - 1);
   for (int i = lane; i < bpad; i += 32) my_bnd[i] = i < int(nb) ? gb[i] : inf;
-  // stage the chunk's sample ids and labels
-  const uint32_t* seg = idx + nd.begin + wk.start;
+  // stage the chunk's labels
   const uint8_t* lseg = lab + nd.begin + wk.start;
-  for (uint32_t j = threadIdx.x; j < wk.len; j += blockDim.x) {
-    idx_s[j] = seg[j];
-    lab_s[j] = lseg[j];
-  }
+  for (uint32_t j = threadIdx.x; j < wk.len; j += blockDim.x) lab_s[j] = lseg[j];
   __syncthreads();
 
   if (nb > 0) {
     const uint32_t* rp = row_ptr + size_t(wk.node) * (R + 1);
-    const uint32_t* rt = terms + nd.term_off + rp[r];
-    const int nt = int(rp[r + 1] - rp[r]);
+    const uint32_t q0 = rp[r];
+    const uint32_t* rt = terms + nd.term_off + q0;
+    const int nt = int(rp[r + 1] - q0);
+    const float* Gn = G + gbase[wk.node];
     for (uint32_t j0 = 0; j0 < wk.len; j0 += 128) {
       float v[4];
       uint8_t y[4];
@@ -172,7 +169,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
       for (int u = 0; u < 4; ++u) {
         const uint32_t j = j0 + uint32_t(u * 32 + lane);
         if (j < wk.len) {
-          v[u] = project_sample(X, ld, rt, nt, idx_s[j]);
+          v[u] = combine_g(Gn, nd.n, rt, nt, q0, wk.start + j);
           y[u] = lab_s[j];
         }
       }
@@ -255,170 +252,6 @@ __global__ void k_hist_select(const uint32_t* __restrict__ hist_nodes, int n_his
   o.n_left_search = nl;
 }
 
-// ------------------------------------------------------------------------------------------
-// Exact splitter: one CTA (8 warps) per node with n <= kExactSmemMax.
-// smem: xl[n+1] f64 | keys[8][npad] u64 | idx[n] u32 | lab[n] u8 | per-row results
-// ------------------------------------------------------------------------------------------
-struct RowBest {
-  double gain;
-  float thr;
-  uint32_t nl;
-};
-
-__global__ void __launch_bounds__(256) k_exact(
-    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ exact_nodes, int n_exact,
-    uint32_t R, int k, int npad_max, const uint32_t* __restrict__ terms,
-    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ idx,
-    const uint8_t* __restrict__ lab, const float* __restrict__ X, uint64_t ld,
-    const double* __restrict__ xl_g, NodeRes* __restrict__ res) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  const uint32_t node = exact_nodes[blockIdx.x];
-  const NodeIn nd = nodes[node];
-  const uint32_t n = nd.n;
-  int npad = 32;
-  while (npad < int(n)) npad <<= 1;
-  double* xl = reinterpret_cast<double*>(smem_raw);                           // [npad_max + 1]
-  uint64_t* keys_all = reinterpret_cast<uint64_t*>(xl + npad_max + 1);        // [nw][npad_max]
-  uint32_t* idx_s = reinterpret_cast<uint32_t*>(keys_all + size_t(nw) * npad_max);  // [npad_max]
-  uint8_t* lab_s = reinterpret_cast<uint8_t*>(idx_s + npad_max);             // [npad_max]
-  __shared__ RowBest s_best[8];
-  __shared__ int s_row[8];
-
-  for (uint32_t i = threadIdx.x; i <= n; i += blockDim.x) xl[i] = xl_g[i];
-  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
-    idx_s[j] = idx[nd.begin + j];
-    lab_s[j] = lab[nd.begin + j];
-  }
-  __syncthreads();
-
-  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
-  const uint32_t* nterms = terms + nd.term_off;
-  uint64_t* keys = keys_all + size_t(w) * npad_max;
-  const double dn = double(n);
-  const double parent = nd.parent;
-  const int E = npad / 32;
-  // warp-local best over its rows (rows visited in increasing order: strict '>' keeps lowest)
-  int wrow = -1;
-  RowBest wb{0.0, 0.f, 0};
-
-  for (uint32_t r = uint32_t(w); r < R; r += uint32_t(nw)) {
-    const int nt = int(rp[r + 1] - rp[r]);
-    if (nt == 0) continue;  // split.hpp:308: empty rows are skipped in exact mode
-    const uint32_t* rt = nterms + rp[r];
-    for (int j = lane; j < npad; j += 32) {
-      uint64_t key = ~0ull;
-      if (j < int(n)) {
-        const float v = project_sample(X, ld, rt, nt, idx_s[j]);
-        key = (uint64_t(order_key(v)) << 32) | uint64_t(lab_s[j]);
-      }
-      keys[j] = key;
-    }
-    __syncwarp();
-    warp_bitonic_sort(keys, npad, lane);
-    // per-lane class counts over its E consecutive sorted positions
-    uint32_t loc[kMaxClasses], pre[kMaxClasses], tot[kMaxClasses];
-#pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) loc[c] = 0;
-    const int p0 = lane * E;
-    for (int e = 0; e < E; ++e) {
-      const int p = p0 + e;
-      if (p < int(n)) {
-        const int c = int(keys[p] & 0xffu);
-#pragma unroll
-        for (int cc = 0; cc < kMaxClasses; ++cc) loc[cc] += (cc == c);
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) {
-      if (c < k) pre[c] = warp_excl_scan_u32(loc[c], lane, &tot[c]);
-      else pre[c] = tot[c] = 0;
-    }
-    // pass 1: min impurity over gaps p|p+1 with v_p < v_{p+1}
-    double xmin = __longlong_as_double(0x7ff0000000000000ll);
-    {
-      uint32_t left[kMaxClasses];
-#pragma unroll
-      for (int c = 0; c < kMaxClasses; ++c) left[c] = pre[c];
-      for (int e = 0; e < E; ++e) {
-        const int p = p0 + e;
-        if (p >= int(n) - 1) break;
-        const uint64_t ka = keys[p];
-        const int c = int(ka & 0xffu);
-#pragma unroll
-        for (int cc = 0; cc < kMaxClasses; ++cc) left[cc] += (cc == c);
-        const float a = order_key_inv(uint32_t(ka >> 32));
-        const float b = order_key_inv(uint32_t(keys[p + 1] >> 32));
-        if (!(a < b)) continue;
-        const uint32_t nl = uint32_t(p + 1);
-        const double Xv = impurity_sum<kMaxClasses>(xl, left, tot, k, nl, n - nl);
-        xmin = fmin(xmin, Xv);
-      }
-    }
-    xmin = warp_min_f64(xmin);
-    if (!(xmin < __longlong_as_double(0x7ff0000000000000ll))) continue;
-    const double gbest = gain_from_x(parent, xmin, dn);
-    if (!(gbest > 0.0)) continue;
-    if (wrow >= 0 && !(gbest > wb.gain)) continue;  // cannot beat an earlier row of this warp
-    const double win = x_window(parent, xmin, dn);
-    uint32_t first = 0xffffffffu;
-    {
-      uint32_t left[kMaxClasses];
-#pragma unroll
-      for (int c = 0; c < kMaxClasses; ++c) left[c] = pre[c];
-      for (int e = 0; e < E; ++e) {
-        const int p = p0 + e;
-        if (p >= int(n) - 1) break;
-        const uint64_t ka = keys[p];
-        const int c = int(ka & 0xffu);
-#pragma unroll
-        for (int cc = 0; cc < kMaxClasses; ++cc) left[cc] += (cc == c);
-        const float a = order_key_inv(uint32_t(ka >> 32));
-        const float b = order_key_inv(uint32_t(keys[p + 1] >> 32));
-        if (!(a < b)) continue;
-        const uint32_t nl = uint32_t(p + 1);
-        const double Xv = impurity_sum<kMaxClasses>(xl, left, tot, k, nl, n - nl);
-        if (Xv <= win && gain_from_x(parent, Xv, dn) == gbest) {
-          first = uint32_t(p);
-          break;
-        }
-      }
-    }
-    const uint32_t fp = warp_min_u32(first);
-    const float a = order_key_inv(uint32_t(keys[fp] >> 32));
-    const float b = order_key_inv(uint32_t(keys[fp + 1] >> 32));
-    wrow = int(r);
-    wb.gain = gbest;
-    wb.thr = midpoint_down(a, b);
-    wb.nl = fp + 1;
-    __syncwarp();
-  }
-  if (lane == 0) {
-    s_row[w] = wrow;
-    s_best[w] = wb;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // rows r were split across warps as r % nw == w; pick the lowest row among max gains
-    int best = -1;
-    RowBest bb{0.0, 0.f, 0};
-    for (int i = 0; i < nw; ++i) {
-      if (s_row[i] < 0) continue;
-      if (best < 0 || s_best[i].gain > bb.gain || (s_best[i].gain == bb.gain && s_row[i] < best)) {
-        best = s_row[i];
-        bb = s_best[i];
-      }
-    }
-    NodeRes& o = res[node];
-    o.row = best;
-    o.gain = bb.gain;
-    o.threshold = bb.thr;
-    o.n_left_search = bb.nl;
-  }
-}
-
 }  // namespace dev
 
 // ---------------------------------------------------------------------------- launchers
@@ -430,14 +263,14 @@ static int pow2_at_least(int x, int lo) {
 
 size_t hist_count_smem(uint32_t bins, int k, int chunk_cap) {
   const int bpad = pow2_at_least(int(bins), 32);
-  return size_t(8) * bpad * k * 4 + size_t(8) * bpad * 4 + size_t(chunk_cap) * 5 + 16;
+  return size_t(8) * bpad * k * 4 + size_t(8) * bpad * 4 + size_t(chunk_cap) + 16;
 }
 
 cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slot,
                               const HistWork* work, int n_work, const uint32_t* multi_slot,
                               uint32_t R, uint32_t bins, int k, int chunk_cap,
-                              const uint32_t* terms, const uint32_t* row_ptr, const uint32_t* idx,
-                              const uint8_t* lab, const float* X, uint64_t ld, const float* bnd,
+                              const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
+                              const uint64_t* gbase, const float* G, const float* bnd,
                               const uint32_t* nb, const double* xl, uint32_t* gcnt,
                               uint32_t* done, RowRes* rowres, cudaStream_t st) {
   if (n_work == 0) return cudaSuccess;
@@ -445,8 +278,8 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
   const size_t smem = hist_count_smem(bins, k, chunk_cap);
   cudaFuncSetAttribute(dev::k_hist_count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   dev::k_hist_count<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins,
-                                               bpad, k, chunk_cap, terms, row_ptr, idx, lab, X,
-                                               ld, bnd, nb, xl, gcnt, done, rowres);
+                                               bpad, k, chunk_cap, terms, row_ptr, lab, gbase, G,
+                                               bnd, nb, xl, gcnt, done, rowres);
   return cudaGetLastError();
 }
 
@@ -454,25 +287,6 @@ cudaError_t launch_hist_select(const uint32_t* hist_nodes, int n_hist, uint32_t 
                                const RowRes* rowres, NodeRes* res, cudaStream_t st) {
   if (n_hist == 0) return cudaSuccess;
   dev::k_hist_select<<<(n_hist + 127) / 128, 128, 0, st>>>(hist_nodes, n_hist, R, rowres, res);
-  return cudaGetLastError();
-}
-
-size_t exact_smem(int npad_max, int warps) {
-  return size_t(npad_max + 1) * 8 + size_t(warps) * npad_max * 8 + size_t(npad_max) * 5 + 16;
-}
-
-cudaError_t launch_exact(const NodeIn* nodes, const uint32_t* exact_nodes, int n_exact,
-                         uint32_t R, int k, uint32_t nmax, const uint32_t* terms,
-                         const uint32_t* row_ptr, const uint32_t* idx, const uint8_t* lab,
-                         const float* X, uint64_t ld, const double* xl, NodeRes* res,
-                         cudaStream_t st) {
-  if (n_exact == 0) return cudaSuccess;
-  const int npad_max = pow2_at_least(int(nmax), 32);
-  const int warps = 8;
-  const size_t smem = exact_smem(npad_max, warps);
-  cudaFuncSetAttribute(dev::k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  dev::k_exact<<<n_exact, warps * 32, smem, st>>>(nodes, exact_nodes, n_exact, R, k, npad_max,
-                                                  terms, row_ptr, idx, lab, X, ld, xl, res);
   return cudaGetLastError();
 }
 

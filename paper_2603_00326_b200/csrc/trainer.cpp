@@ -48,7 +48,7 @@ void ThreadPool::worker() {
 
 void ThreadPool::parallel_for(size_t n, const std::function<void(size_t)>& f) {
   if (n == 0) return;
-  if (workers_.empty() || n < 64) {
+  if (workers_.empty() || n < 2) {
     for (size_t i = 0; i < n; ++i) f(i);
     return;
   }
@@ -77,7 +77,7 @@ double ms_since(Clock::time_point t) {
 struct BNode {
   int32_t left = -1, right = -1, pred = -1;
   float thr = 0.f;
-  std::vector<uint32_t> terms;  // feature << 1 | negative
+  uint32_t term_off = 0, term_len = 0;  // into the tree's term pool
 };
 
 struct Open {
@@ -85,7 +85,10 @@ struct Open {
   int32_t bnode;
   uint32_t begin, n, depth, attempt;
   uint64_t seed;
-  uint64_t pos;  // engine outputs consumed before this attempt's binomial draw
+  uint64_t pos;   // engine outputs consumed before this attempt's binomial draw
+  uint32_t z;     // binomial draw for this attempt (valid when has_z)
+  uint32_t zpos;  // stream position after it
+  uint32_t has_z;
   uint32_t counts[kMaxClasses];
 };
 
@@ -112,6 +115,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   host::BinomialDraw binom(cells, P.density);
 
   // ---- root segments: tree b occupies [off[b], off[b+1]) of the level buffers -------------
+  auto t0 = Clock::now();
   std::vector<uint64_t> off(B + 1, 0);
   for (size_t b = 0; b < B; ++b) off[b + 1] = off[b] + roots[b].size();
   const uint64_t total = off[B];
@@ -123,23 +127,22 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     lab[i].exact(total);
   }
   {
-    PinnedBuf<uint32_t> hidx;
-    PinnedBuf<uint8_t> hlab;
-    uint32_t* hi = hidx.ensure(total);
-    uint8_t* hl = hlab.ensure(total);
-    for (size_t b = 0; b < B; ++b) {
+    unsigned char* stg = eng.staging.ensure(5 * total);
+    uint32_t* hi = reinterpret_cast<uint32_t*>(stg);
+    uint8_t* hl = stg + 4 * total;
+    pool.parallel_for(B, [&](size_t b) {
       std::memcpy(hi + off[b], roots[b].data(), 4 * roots[b].size());
       for (size_t j = 0; j < roots[b].size(); ++j) hl[off[b] + j] = uint8_t(D.labels_host[roots[b][j]]);
-    }
+    });
     cuda_check(cudaMemcpyAsync(idx[0].p, hi, 4 * total, cudaMemcpyHostToDevice, eng.stream()), "H2D idx");
     cuda_check(cudaMemcpyAsync(lab[0].p, hl, total, cudaMemcpyHostToDevice, eng.stream()), "H2D lab");
-    cuda_check(cudaStreamSynchronize(eng.stream()), "sync roots");
   }
 
   std::vector<std::vector<BNode>> trees(B);
-  std::vector<Open> frontier;
-  frontier.reserve(B);
-  for (size_t b = 0; b < B; ++b) {
+  std::vector<std::vector<uint32_t>> pools(B);
+  std::vector<Open> frontier(B);
+  pool.parallel_for(B, [&](size_t b) {
+    trees[b].reserve(1024);
     trees[b].emplace_back();
     Open o{};
     o.tree = uint32_t(b);
@@ -149,13 +152,13 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     o.depth = root_depth;
     o.seed = root_seeds[b];
     for (uint32_t s : roots[b]) o.counts[D.labels_host[s]]++;
-    frontier.push_back(o);
-  }
+    frontier[b] = o;
+  });
+  times.ms_roots += ms_since(t0);
 
   int cur = 0;
   std::vector<Open> split_list, retry, next;
-  std::vector<uint64_t> zs, poss;
-  std::vector<double> parents;
+  std::vector<uint32_t> spec_z, spec_pos;
   std::vector<NodeRes> res;
   WaveSpec w;
   w.R = P.R;
@@ -165,6 +168,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
 
   while (!frontier.empty()) {
     times.levels++;
+    t0 = Clock::now();
     split_list.clear();
     next.clear();
     for (const Open& o : frontier) {
@@ -177,21 +181,24 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       else
         trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
     }
+    times.ms_prep += ms_since(t0);
     while (!split_list.empty()) {
+      t0 = Clock::now();
       const size_t N = split_list.size();
-      zs.resize(N);
-      poss.resize(N);
-      parents.resize(N);
+      w.nodes.resize(N);
+      // binomial draws not done speculatively (roots, retries) + parent entropies
       const auto tb = Clock::now();
       pool.parallel_for(N, [&](size_t i) {
-        const Open& o = split_list[i];
-        uint64_t used;
-        zs[i] = binom(o.seed, o.pos, &used);
-        poss[i] = used;
-        parents[i] = host::entropy(o.counts, k);
+        Open& o = split_list[i];
+        if (!o.has_z) {
+          uint64_t used;
+          o.z = uint32_t(binom(o.seed, o.pos, &used));
+          o.zpos = uint32_t(used);
+          o.has_z = 1;
+        }
+        w.nodes[i].parent = host::entropy(o.counts, k);
       });
       times.ms_binomial += ms_since(tb);
-      w.nodes.resize(N);
       uint64_t term_off = 0;
       for (size_t i = 0; i < N; ++i) {
         const Open& o = split_list[i];
@@ -199,39 +206,65 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
         nd.seed = o.seed;
         nd.begin = o.begin;
         nd.n = o.n;
-        nd.z = uint32_t(zs[i]);
-        nd.pos = uint32_t(poss[i]);
+        nd.z = o.z;
+        nd.pos = o.zpos;
         const bool hist = P.mode == 1 || (P.mode == 2 && o.n > P.breakeven);  // split.hpp:46-48
         nd.flags = hist ? kNodeHist : 0u;
         nd.term_off = uint32_t(term_off);
         nd.hist_slot = 0;
         nd.tree = o.tree;
-        nd.parent = parents[i];
-        term_off += zs[i];
+        term_off += o.z;
       }
       if (term_off >= (1ull << 32)) throw std::runtime_error("wave term count overflow");
       w.idx_in = idx[cur].p;
       w.lab_in = lab[cur].p;
       w.idx_out = idx[cur ^ 1].p;
       w.lab_out = lab[cur ^ 1].p;
-      eng.run(w, res);
+      times.ms_prep += ms_since(t0);
+      t0 = Clock::now();
+      eng.submit(w);
+      times.ms_submit += ms_since(t0);
 
+      // While the GPU searches this wave: draw the children's attempt-0 binomials. They depend
+      // only on the child seeds derive_seed(seed, 1|2) (forest.hpp:226-228), known already.
+      t0 = Clock::now();
+      spec_z.resize(2 * N);
+      spec_pos.resize(2 * N);
+      pool.parallel_for(N, [&](size_t i) {
+        const Open& o = split_list[i];
+        for (int c = 0; c < 2; ++c) {
+          uint64_t used;
+          spec_z[2 * i + c] = uint32_t(binom(host::derive_seed(o.seed, uint64_t(c + 1)), 0, &used));
+          spec_pos[2 * i + c] = uint32_t(used);
+        }
+      });
+      times.ms_spec += ms_since(t0);
+      t0 = Clock::now();
+      eng.collect(w, res);
+      times.ms_wait += ms_since(t0);
+
+      t0 = Clock::now();
       retry.clear();
       for (size_t i = 0; i < N; ++i) {
         Open& o = split_list[i];
         const NodeRes& r = res[i];
         if (r.row >= 0 && r.n_left > 0 && r.n_left < o.n) {
           std::vector<BNode>& tr = trees[o.tree];
+          std::vector<uint32_t>& tp = pools[o.tree];
           const int32_t L = int32_t(tr.size());
           {
             BNode& p = tr[size_t(o.bnode)];
             p.thr = r.threshold;
             p.left = L;
             p.right = L + 1;
-            if (r.n_terms <= uint32_t(kWinTermsMax))
-              p.terms.assign(r.terms, r.terms + r.n_terms);
-            else
-              p.terms = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
+            p.term_off = uint32_t(tp.size());
+            p.term_len = r.n_terms;
+            if (r.n_terms <= uint32_t(kWinTermsMax)) {
+              tp.insert(tp.end(), r.terms, r.terms + r.n_terms);
+            } else {
+              const std::vector<uint32_t> t = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
+              tp.insert(tp.end(), t.begin(), t.end());
+            }
           }
           tr.emplace_back();
           tr.emplace_back();
@@ -246,6 +279,11 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
           rr.n = o.n - r.n_left;
           l.seed = host::derive_seed(o.seed, 1);  // forest.hpp:226-228
           rr.seed = host::derive_seed(o.seed, 2);
+          l.z = spec_z[2 * i];
+          l.zpos = spec_pos[2 * i];
+          rr.z = spec_z[2 * i + 1];
+          rr.zpos = spec_pos[2 * i + 1];
+          l.has_z = rr.has_z = 1;
           for (int c = 0; c < k; ++c) {
             l.counts[c] = r.left_counts[c];
             rr.counts[c] = o.counts[c] - r.left_counts[c];
@@ -255,29 +293,45 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
         } else if (o.attempt < P.max_split_retries) {  // forest.hpp:187,211: next attempt
           o.attempt++;
           o.pos = r.pos_after;
+          o.has_z = 0;
           retry.push_back(o);
         } else {
           trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
         }
       }
       split_list.swap(retry);
+      times.ms_post += ms_since(t0);
     }
     cur ^= 1;
     frontier.swap(next);
   }
 
   // ---- reference node order: ids assigned at split time in depth-first order (H4) ------------
+  t0 = Clock::now();
+  std::vector<uint64_t> node_base(B + 1, 0), term_base(B + 1, 0);
   for (size_t b = 0; b < B; ++b) {
+    node_base[b + 1] = node_base[b] + trees[b].size();
+    term_base[b + 1] = term_base[b] + pools[b].size();
+  }
+  const size_t N0 = out.left.size(), Q0 = out.feat.size(), T0 = out.tree_off.size();
+  out.left.resize(N0 + node_base[B]);
+  out.right.resize(N0 + node_base[B]);
+  out.pred.resize(N0 + node_base[B]);
+  out.thr.resize(N0 + node_base[B]);
+  out.term_off.resize(N0 + node_base[B] + 1);
+  out.feat.resize(Q0 + term_base[B]);
+  out.weight.resize(Q0 + term_base[B]);
+  out.tree_off.resize(T0 + B);
+  pool.parallel_for(B, [&](size_t b) {
     const std::vector<BNode>& tr = trees[b];
-    std::vector<int32_t> id(tr.size(), -1), order;
-    order.reserve(tr.size());
+    const std::vector<uint32_t>& tp = pools[b];
+    std::vector<int32_t> id(tr.size(), -1), by_id(tr.size());
     std::vector<int32_t> stack{0};
     id[0] = 0;
     int32_t next_id = 1;
     while (!stack.empty()) {
       const int32_t v = stack.back();
       stack.pop_back();
-      order.push_back(v);
       const BNode& nv = tr[size_t(v)];
       if (nv.left >= 0) {
         id[size_t(nv.left)] = next_id;
@@ -287,22 +341,25 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
         stack.push_back(nv.left);
       }
     }
-    std::vector<int32_t> by_id(tr.size());
     for (size_t v = 0; v < tr.size(); ++v) by_id[size_t(id[v])] = int32_t(v);
-    for (size_t q = 0; q < tr.size(); ++q) {
-      const BNode& nv = tr[size_t(by_id[q])];
-      out.left.push_back(nv.left >= 0 ? id[size_t(nv.left)] : -1);
-      out.right.push_back(nv.right >= 0 ? id[size_t(nv.right)] : -1);
-      out.pred.push_back(nv.pred);
-      out.thr.push_back(nv.left >= 0 ? nv.thr : 0.f);
-      for (uint32_t t : nv.terms) {
-        out.feat.push_back(t >> 1);
-        out.weight.push_back((t & 1u) ? -1.f : 1.f);
+    size_t q = N0 + node_base[b];
+    uint64_t tq = Q0 + term_base[b];
+    for (size_t u = 0; u < tr.size(); ++u, ++q) {
+      const BNode& nv = tr[size_t(by_id[u])];
+      out.left[q] = nv.left >= 0 ? id[size_t(nv.left)] : -1;
+      out.right[q] = nv.right >= 0 ? id[size_t(nv.right)] : -1;
+      out.pred[q] = nv.pred;
+      out.thr[q] = nv.left >= 0 ? nv.thr : 0.f;
+      for (uint32_t t = 0; t < nv.term_len; ++t, ++tq) {
+        const uint32_t e = tp[nv.term_off + t];
+        out.feat[tq] = e >> 1;
+        out.weight[tq] = (e & 1u) ? -1.f : 1.f;
       }
-      out.term_off.push_back(int64_t(out.feat.size()));
+      out.term_off[q + 1] = int64_t(tq);
     }
-    out.tree_off.push_back(int64_t(out.left.size()));
-  }
+    out.tree_off[T0 + b] = int64_t(N0 + node_base[b + 1]);
+  });
+  times.ms_final += ms_since(t0);
   times.ms_total += ms_since(t_start);
 }
 

@@ -97,8 +97,11 @@ def test_find_node_split_trunk400(gpu_ctx, oracle, method, bins):
         assert int(g.consumed) == oused
 
 
-@pytest.mark.parametrize("n,method,bins", [(2, "exact", 256), (3, "exact", 256), (33, "exact", 256),
-                                           (700, "exact", 256), (2048, "exact", 256),
+@pytest.mark.parametrize("n,method,bins", [(2, "exact", 256), (3, "exact", 256), (31, "exact", 256),
+                                           (32, "exact", 256), (33, "exact", 256), (64, "exact", 256),
+                                           (65, "exact", 256), (128, "exact", 256), (255, "exact", 256),
+                                           (512, "exact", 256), (700, "exact", 256), (1024, "exact", 256),
+                                           (1025, "exact", 256), (2048, "exact", 256),
                                            (300, "histogram", 256), (5000, "histogram", 256),
                                            (20000, "histogram", 256), (9000, "histogram", 32)])
 def test_find_node_split_subsets(gpu_ctx, oracle, n, method, bins):
