@@ -264,7 +264,8 @@ def main():
                                                           "ms_partition", "ms_waves_total", "ms_host_binomial",
                                                           "ms_host_bootstrap", "ms_train_total", "ms_host_roots",
                                                           "ms_host_prep", "ms_host_submit", "ms_host_spec",
-                                                          "ms_host_wait", "ms_host_post", "ms_host_final")}}
+                                                          "ms_host_wait", "ms_host_post", "ms_host_final")},
+                "kernel_ms": st.get("kernels", {})}
     gpu_launches = int(st["kernel_launches"])
 
     # ---- end to end through the C ABI with host buffers ---------------------------------------

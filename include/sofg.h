@@ -153,6 +153,9 @@ typedef struct sofg_stats {
 int sofg_set_stats(sofg_ctx* ctx, int enable);
 int sofg_get_stats(sofg_ctx* ctx, sofg_stats* out);
 int sofg_reset_stats(sofg_ctx* ctx);
+/* Per-launch-site CUDA-event times (stats mode): number of sites, then name/ms/launches of i. */
+int sofg_stats_kernels(sofg_ctx* ctx);
+int sofg_stats_kernel(sofg_ctx* ctx, int i, const char** name, double* ms, uint64_t* launches);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,8 @@ def load():
     L.sofg_set_stats.argtypes = [vp, C.c_int]
     L.sofg_get_stats.argtypes = [vp, P(_Stats)]
     L.sofg_reset_stats.argtypes = [vp]
+    L.sofg_stats_kernels.argtypes = [vp]
+    L.sofg_stats_kernel.argtypes = [vp, C.c_int, P(C.c_char_p), P(C.c_double), P(u64)]
     _lib = L
     return L
 
@@ -338,7 +340,14 @@ class Context:
     def stats(self) -> dict:
         s = _Stats()
         _check(self.L.sofg_get_stats(self.h, C.byref(s)), "get_stats")
-        return {name: getattr(s, name) for name, _ in _Stats._fields_}
+        out = {name: getattr(s, name) for name, _ in _Stats._fields_}
+        kern = {}
+        for i in range(self.L.sofg_stats_kernels(self.h)):
+            nm, ms, la = C.c_char_p(), C.c_double(), C.c_uint64()
+            _check(self.L.sofg_stats_kernel(self.h, i, C.byref(nm), C.byref(ms), C.byref(la)), "stats_kernel")
+            kern[nm.value.decode()] = {"ms": round(ms.value, 2), "launches": la.value}
+        out["kernels"] = kern
+        return out
 
 
 def train_forest(X, y, class_count, cfg: TrainConfig, device: int = 0) -> Forest:

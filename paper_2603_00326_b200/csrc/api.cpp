@@ -65,9 +65,11 @@ sofg::ThreadPool& pool_for(sofg_ctx* c, uint64_t n_workers) {
   int want = n_workers ? int(n_workers) : hw_threads();
   want = std::max(1, std::min(want, hw_threads()));
   if (!c->pool || c->pool_threads != want) {
+    c->eng->set_pool(nullptr);
     c->pool.reset(new sofg::ThreadPool(want));
     c->pool_threads = want;
   }
+  c->eng->set_pool(c->pool.get());
   return *c->pool;
 }
 
@@ -620,6 +622,19 @@ int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
     o->ms_host_wait = c->times.ms_wait;
     o->ms_host_post = c->times.ms_post;
     o->ms_host_final = c->times.ms_final;
+  });
+}
+
+int sofg_stats_kernels(sofg_ctx* c) { return c && c->eng ? int(c->eng->stats.per_kernel.size()) : 0; }
+
+int sofg_stats_kernel(sofg_ctx* c, int i, const char** name, double* ms, uint64_t* launches) {
+  return guard([&] {
+    require_ctx(c);
+    const auto& v = c->eng->stats.per_kernel;
+    if (i < 0 || size_t(i) >= v.size()) throw std::out_of_range("kernel stat index");
+    *name = v[size_t(i)].name;
+    *ms = v[size_t(i)].ms;
+    *launches = v[size_t(i)].launches;
   });
 }
 

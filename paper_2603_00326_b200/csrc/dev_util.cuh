@@ -170,5 +170,13 @@ __device__ __forceinline__ double x_window(double parent, double xmin, double n)
   return xmin + (mag * n + fabs(xmin)) * 0x1p-40 + 1e-300;
 }
 
+// Same window with q approximated by xmin * (1/n): the window only has to contain the candidates
+// whose exact gain can round to the best one, and the 2^-40 margin dwarfs the approximation.
+__device__ __forceinline__ double x_window_fast(double parent, double xmin, double n, double inv_n) {
+  const double q = xmin * inv_n;
+  const double mag = fmax(fabs(parent), fabs(q));
+  return xmin + (mag * n + fabs(xmin)) * 0x1p-40 + 1e-300;
+}
+
 }  // namespace dev
 }  // namespace sofg

@@ -5,6 +5,7 @@
 #include <cstring>
 
 #include "kernels.hpp"
+#include "trainer.hpp"
 
 namespace sofg {
 
@@ -20,11 +21,21 @@ WaveRunner::WaveRunner(int device) : device_(device) {
   }
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  for (auto& e : mk_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+}
+
+void WaveRunner::mark(const char* name) {
+  if (!collect_stats || n_marks_ >= kMaxMarks) return;
+  mk_name_[n_marks_] = name;
+  cudaEventRecord(mk_[n_marks_ + 1], st_);
+  ++n_marks_;
 }
 
 WaveRunner::~WaveRunner() {
   cudaSetDevice(device_);
   for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : mk_)
     if (e) cudaEventDestroy(e);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -59,62 +70,112 @@ void WaveRunner::submit(const WaveSpec& w) {
   const uint32_t bins = w.bins;
   const int bpad = pow2_at_least(int(bins), 32);
 
-  // ---- derived work lists --------------------------------------------------------------
-  std::vector<uint32_t> hist, exact, hist_slot(size_t(N), ~0u), multi_slot(size_t(N), ~0u);
-  std::vector<uint32_t> exact_b[7];
-  std::vector<HistWork> work;
-  std::vector<Tile> tiles;
-  std::vector<uint32_t> tile_first(size_t(N) + 1, 0);
-  uint32_t zmax = 32, n_multi = 0;
-  std::vector<uint64_t> gbase(static_cast<size_t>(N));
-  uint64_t g_total = 0, n_items = 0;
-  uint64_t total_terms = 0;
+  // ---- derived work lists (built straight into the page-locked staging buffer) ------------
+  // Per node: histogram work items (row groups x chunks), partition tiles, exact bucket, G block
+  // offset and gather-item count. Two parallel passes over node chunks: counts, then fills.
   const uint32_t groups = (R + kHistRowsPerCta - 1) / kHistRowsPerCta;
-  for (int i = 0; i < N; ++i) {
-    const NodeIn& nd = w.nodes[size_t(i)];
-    zmax = std::max(zmax, nd.z);
-    total_terms = std::max<uint64_t>(total_terms, uint64_t(nd.term_off) + nd.z);
-    if (nd.flags & kNodeHist) {
-      hist_slot[size_t(i)] = uint32_t(hist.size());
-      hist.push_back(uint32_t(i));
-      const uint32_t chunks = (nd.n + uint32_t(w.chunk_cap) - 1) / uint32_t(w.chunk_cap);
-      if (chunks > 1) multi_slot[size_t(i)] = n_multi++;
-      for (uint32_t g = 0; g < groups; ++g)
-        for (uint32_t c = 0; c < chunks; ++c) {
-          const uint32_t s = c * uint32_t(w.chunk_cap);
-          work.push_back({uint32_t(i), g * kHistRowsPerCta, s, std::min(nd.n - s, uint32_t(w.chunk_cap)),
-                          c, chunks});
-        }
+  const uint32_t cap = uint32_t(w.chunk_cap);
+  struct Cnt {
+    uint64_t hist = 0, multi = 0, work = 0, tiles = 0, g = 0, items = 0;
+    uint64_t exact[7] = {0, 0, 0, 0, 0, 0, 0};
+    uint32_t zmax = 32;
+    uint64_t terms_end = 0;
+    bool too_big = false;
+    uint32_t big_n = 0;
+  };
+  ThreadPool* pool = pool_;
+  std::vector<Cnt> cc;
+  std::vector<size_t> cb;
+  auto run_chunks = [&](const std::function<void(size_t, size_t, size_t)>& f) {
+    if (pool && N >= 4096) {
+      cb = pool->chunks(size_t(N), 2048, f);
     } else {
-      if (nd.n > uint32_t(kExactSmemMax))
-        throw std::invalid_argument("exact split of a node with " + std::to_string(nd.n) +
-                                    " samples exceeds the GPU exact splitter (" +
-                                    std::to_string(kExactSmemMax) + "); use a breakeven <= " +
-                                    std::to_string(kExactSmemMax));
-      exact_b[size_t(exact_bucket(nd.n))].push_back(uint32_t(i));
+      cb = {0, size_t(N)};
+      f(0, 0, size_t(N));
     }
-    gbase[size_t(i)] = g_total;
-    g_total += uint64_t(nd.z) * nd.n;
-    n_items += csp_items(nd.n, nd.z);
-    tile_first[size_t(i)] = uint32_t(tiles.size());
-    for (uint32_t s = 0, t = 0; s < nd.n; s += kTileElems, ++t)
-      tiles.push_back({uint32_t(i), s, std::min(nd.n - s, uint32_t(kTileElems)), t});
+  };
+  // pass 1: counts (chunk layout fixed by the first call)
+  {
+    std::vector<Cnt> tmp(pool ? size_t(pool->size()) * 4 + 1 : 1);
+    run_chunks([&](size_t c, size_t b0, size_t b1) {
+      Cnt& t = tmp[c];
+      for (size_t i = b0; i < b1; ++i) {
+        const NodeIn& nd = w.nodes[i];
+        t.zmax = std::max(t.zmax, nd.z);
+        t.terms_end = std::max<uint64_t>(t.terms_end, uint64_t(nd.term_off) + nd.z);
+        if (nd.flags & kNodeHist) {
+          const uint32_t chunks = (nd.n + cap - 1) / cap;
+          t.hist++;
+          if (chunks > 1) t.multi++;
+          t.work += uint64_t(groups) * chunks;
+        } else if (nd.n > uint32_t(kExactSmemMax)) {
+          t.too_big = true;
+          t.big_n = nd.n;
+        } else {
+          t.exact[exact_bucket(nd.n)]++;
+        }
+        t.tiles += (nd.n + kTileElems - 1) / kTileElems;
+        t.g += uint64_t(nd.z) * nd.n;
+        t.items += csp_items(nd.n, nd.z);
+      }
+    });
+    cc.assign(tmp.begin(), tmp.begin() + (cb.size() - 1));
   }
-  tile_first[size_t(N)] = uint32_t(tiles.size());
-  if (w.given_csr) total_terms = w.given_terms.size();
+  const size_t C = cc.size();
+  Cnt tot;
+  std::vector<Cnt> off(C);
+  uint64_t exact_total = 0;
+  for (size_t c = 0; c < C; ++c) {
+    if (cc[c].too_big)
+      throw std::invalid_argument("exact split of a node with " + std::to_string(cc[c].big_n) +
+                                  " samples exceeds the GPU exact splitter (" +
+                                  std::to_string(kExactSmemMax) + "); use a breakeven <= " +
+                                  std::to_string(kExactSmemMax));
+    off[c].hist = tot.hist;
+    off[c].multi = tot.multi;
+    off[c].work = tot.work;
+    off[c].tiles = tot.tiles;
+    off[c].g = tot.g;
+    tot.hist += cc[c].hist;
+    tot.multi += cc[c].multi;
+    tot.work += cc[c].work;
+    tot.tiles += cc[c].tiles;
+    tot.g += cc[c].g;
+    tot.items += cc[c].items;
+    tot.zmax = std::max(tot.zmax, cc[c].zmax);
+    tot.terms_end = std::max(tot.terms_end, cc[c].terms_end);
+  }
+  uint64_t bucket_base[8] = {0};
+  for (int bk = 0; bk < 7; ++bk) {
+    uint64_t acc = 0;
+    for (size_t c = 0; c < C; ++c) acc += cc[c].exact[bk];
+    bucket_base[bk + 1] = bucket_base[bk] + acc;
+  }
+  exact_total = bucket_base[7];
+  for (int bk = 0; bk < 7; ++bk) {
+    uint64_t run = bucket_base[bk];
+    for (size_t c = 0; c < C; ++c) {
+      off[c].exact[bk] = run;
+      run += cc[c].exact[bk];
+    }
+  }
+  const uint32_t zmax = tot.zmax, n_multi = uint32_t(tot.multi);
+  const uint64_t g_total = tot.g, n_items = tot.items;
+  uint64_t total_terms = w.given_csr ? w.given_terms.size() : tot.terms_end;
+  const size_t nh = size_t(tot.hist);
+  const size_t n_tiles = size_t(tot.tiles), n_work = size_t(tot.work);
 
   // ---- pack inputs -----------------------------------------------------------------------
   Packer pk;
   const size_t o_nodes = pk.add(sizeof(NodeIn) * N);
-  const size_t o_hist = pk.add(4 * hist.size());
-  for (auto& v : exact_b) exact.insert(exact.end(), v.begin(), v.end());
-  const size_t o_exact = pk.add(4 * exact.size());
+  const size_t o_hist = pk.add(4 * nh);
+  const size_t o_exact = pk.add(4 * exact_total);
   const size_t o_gbase = pk.add(8 * size_t(N));
   const size_t o_hslot = pk.add(4 * size_t(N));
   const size_t o_mslot = pk.add(4 * size_t(N));
-  const size_t o_work = pk.add(sizeof(HistWork) * work.size());
-  const size_t o_tiles = pk.add(sizeof(Tile) * tiles.size());
-  const size_t o_tfirst = pk.add(4 * tile_first.size());
+  const size_t o_work = pk.add(sizeof(HistWork) * n_work);
+  const size_t o_tiles = pk.add(sizeof(Tile) * n_tiles);
+  const size_t o_tfirst = pk.add(4 * (size_t(N) + 1));
   size_t o_gterms = 0, o_grp = 0, o_gpos = 0;
   if (w.given_csr) {
     o_gterms = pk.add(4 * w.given_terms.size());
@@ -122,26 +183,58 @@ void WaveRunner::submit(const WaveSpec& w) {
     o_gpos = pk.add(4 * w.given_pos.size());
   }
   unsigned char* hb = h_in_.ensure(pk.total);
-  auto put = [&](size_t off, const void* src, size_t bytes) {
-    if (bytes) std::memcpy(hb + off, src, bytes);
+  NodeIn* p_nodes = reinterpret_cast<NodeIn*>(hb + o_nodes);
+  uint32_t* p_hist = reinterpret_cast<uint32_t*>(hb + o_hist);
+  uint32_t* p_exact = reinterpret_cast<uint32_t*>(hb + o_exact);
+  uint64_t* p_gbase = reinterpret_cast<uint64_t*>(hb + o_gbase);
+  uint32_t* p_hslot = reinterpret_cast<uint32_t*>(hb + o_hslot);
+  uint32_t* p_mslot = reinterpret_cast<uint32_t*>(hb + o_mslot);
+  HistWork* p_work = reinterpret_cast<HistWork*>(hb + o_work);
+  Tile* p_tiles = reinterpret_cast<Tile*>(hb + o_tiles);
+  uint32_t* p_tfirst = reinterpret_cast<uint32_t*>(hb + o_tfirst);
+  // pass 2: fills, same chunk boundaries
+  auto fill = [&](size_t c, size_t b0, size_t b1) {
+    Cnt o = off[c];
+    for (size_t i = b0; i < b1; ++i) {
+      const NodeIn& nd = w.nodes[i];
+      p_nodes[i] = nd;
+      p_gbase[i] = o.g;
+      o.g += uint64_t(nd.z) * nd.n;
+      p_tfirst[i] = uint32_t(o.tiles);
+      for (uint32_t s0 = 0, t = 0; s0 < nd.n; s0 += kTileElems, ++t)
+        p_tiles[o.tiles++] = {uint32_t(i), s0, std::min(nd.n - s0, uint32_t(kTileElems)), t};
+      p_mslot[i] = ~0u;
+      p_hslot[i] = ~0u;
+      if (nd.flags & kNodeHist) {
+        p_hslot[i] = uint32_t(o.hist);
+        p_hist[o.hist++] = uint32_t(i);
+        const uint32_t chunks = (nd.n + cap - 1) / cap;
+        if (chunks > 1) p_mslot[i] = uint32_t(o.multi++);
+        for (uint32_t g = 0; g < groups; ++g)
+          for (uint32_t ch = 0; ch < chunks; ++ch) {
+            const uint32_t s0 = ch * cap;
+            p_work[o.work++] = {uint32_t(i), g * kHistRowsPerCta, s0, std::min(nd.n - s0, cap), ch,
+                                chunks};
+          }
+      } else {
+        p_exact[o.exact[exact_bucket(nd.n)]++] = uint32_t(i);
+      }
+    }
   };
-  put(o_nodes, w.nodes.data(), sizeof(NodeIn) * N);
-  put(o_hist, hist.data(), 4 * hist.size());
-  put(o_exact, exact.data(), 4 * exact.size());
-  put(o_gbase, gbase.data(), 8 * size_t(N));
-  put(o_hslot, hist_slot.data(), 4 * size_t(N));
-  put(o_mslot, multi_slot.data(), 4 * size_t(N));
-  put(o_work, work.data(), sizeof(HistWork) * work.size());
-  put(o_tiles, tiles.data(), sizeof(Tile) * tiles.size());
-  put(o_tfirst, tile_first.data(), 4 * tile_first.size());
+  if (cb.size() > 2) {
+    pool->parallel_for(cb.size() - 1, [&](size_t c) { fill(c, cb[c], cb[c + 1]); });
+  } else {
+    fill(0, 0, size_t(N));
+  }
+  p_tfirst[N] = uint32_t(n_tiles);
   if (w.given_csr) {
-    put(o_gterms, w.given_terms.data(), 4 * w.given_terms.size());
-    put(o_grp, w.given_row_ptr.data(), 4 * w.given_row_ptr.size());
-    put(o_gpos, w.given_pos.data(), 4 * w.given_pos.size());
+    std::memcpy(hb + o_gterms, w.given_terms.data(), 4 * w.given_terms.size());
+    std::memcpy(hb + o_grp, w.given_row_ptr.data(), 4 * w.given_row_ptr.size());
+    std::memcpy(hb + o_gpos, w.given_pos.data(), 4 * w.given_pos.size());
   }
   unsigned char* db = d_in_.ensure(pk.total);
   cuda_check(cudaMemcpyAsync(db, hb, pk.total, cudaMemcpyHostToDevice, st_), "H2D wave");
-  auto dp = [&](size_t off) { return db + off; };
+  auto dp = [&](size_t off2) { return db + off2; };
   const NodeIn* d_nodes = reinterpret_cast<const NodeIn*>(dp(o_nodes));
   const uint32_t* d_hist = reinterpret_cast<const uint32_t*>(dp(o_hist));
   const uint32_t* d_exact = reinterpret_cast<const uint32_t*>(dp(o_exact));
@@ -151,6 +244,8 @@ void WaveRunner::submit(const WaveSpec& w) {
   const HistWork* d_work = reinterpret_cast<const HistWork*>(dp(o_work));
   const Tile* d_tiles = reinterpret_cast<const Tile*>(dp(o_tiles));
   const uint32_t* d_tfirst = reinterpret_cast<const uint32_t*>(dp(o_tfirst));
+  std::vector<size_t> exact_b_count(7);
+  for (int bk = 0; bk < 7; ++bk) exact_b_count[size_t(bk)] = size_t(bucket_base[bk + 1] - bucket_base[bk]);
 
   // ---- scratch ---------------------------------------------------------------------------
   uint32_t* d_terms;
@@ -168,7 +263,6 @@ void WaveRunner::submit(const WaveSpec& w) {
   last_terms_ = d_terms;
   last_rp_ = d_rp;
   uint32_t* d_pos_split = pos_split_.ensure(size_t(N));
-  const size_t nh = hist.size();
   uint32_t* d_draws = draws_.ensure(std::max<size_t>(1, nh * R * bins));
   float* d_bnd = bnd_.ensure(std::max<size_t>(1, nh * R * (bins - 1)));
   uint32_t* d_nb = nb_.ensure(std::max<size_t>(1, nh * R));
@@ -179,8 +273,8 @@ void WaveRunner::submit(const WaveSpec& w) {
   float* d_G = G_.ensure(std::max<uint64_t>(1, g_total));
   uint64_t* d_items = items_.ensure(std::max<uint64_t>(1, n_items));
   uint32_t* d_fcnt = fcnt_.ensure(w.d);
-  uint32_t* d_flags = flags_.ensure(std::max<size_t>(1, tiles.size() * 32));
-  uint32_t* d_tleft = tile_left_.ensure(std::max<size_t>(1, tiles.size()));
+  uint32_t* d_flags = flags_.ensure(std::max<size_t>(1, n_tiles * 32));
+  uint32_t* d_tleft = tile_left_.ensure(std::max<size_t>(1, n_tiles));
 
   cuda_check(cudaMemsetAsync(d_res, 0, sizeof(NodeRes) * N, st_), "memset res");
   if (n_multi) {
@@ -190,35 +284,44 @@ void WaveRunner::submit(const WaveSpec& w) {
 
   const bool timing = collect_stats;
   if (sector_accounting)
-    cuda_check(launch_sector_count(d_nodes, d_tiles, int(tiles.size()), w.idx_in, d_res, st_),
+    cuda_check(launch_sector_count(d_nodes, d_tiles, int(n_tiles), w.idx_in, d_res, st_),
                "sector_count");
-  if (timing) cudaEventRecord(ev_[0], st_);
+  if (timing) {
+    cudaEventRecord(ev_[0], st_);
+    cudaEventRecord(mk_[0], st_);
+  }
+  n_marks_ = 0;
   int launches = 0;
   if (!w.given_csr) {
     cuda_check(launch_sample_projection(d_nodes, N, w.d, R, zmax, d_terms, d_rp, d_pos_proj, st_),
                "sample_projection");
     ++launches;
+    mark("sample_projection");
   }
   cuda_check(launch_csp(d_nodes, N, d_gbase, d_terms, w.d, n_items, d_fcnt, d_items, w.idx_in,
                         D.X.p, D.ld, d_G, st_),
              "column_sweep_gather");
   launches += 4;
+  mark("column_sweep_gather");
   if (timing) cudaEventRecord(ev_[1], st_);
   if (nh) {
     cuda_check(launch_hist_draws(d_nodes, d_hist, int(nh), R, bins, d_pos_proj, d_draws,
                                  d_pos_split, st_),
                "hist_draws");
+    mark("hist_draws");
     cuda_check(launch_hist_boundaries(d_nodes, d_hist, int(nh), R, bins, d_draws, d_terms, d_rp,
                                       d_gbase, d_G, d_bnd, d_nb, st_),
                "hist_boundaries");
     launches += 2;
+    mark("hist_boundaries");
   }
   if (timing) cudaEventRecord(ev_[2], st_);
   if (nh) {
-    cuda_check(launch_hist_count(d_nodes, d_hslot, d_work, int(work.size()), d_mslot, R, bins, k,
+    cuda_check(launch_hist_count(d_nodes, d_hslot, d_work, int(n_work), d_mslot, R, bins, k,
                                  w.chunk_cap, d_terms, d_rp, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
                                  D.xl.p, d_gcnt, d_done, d_rowres, st_),
                "hist_count");
+    mark("hist_count");
     cuda_check(launch_hist_select(d_hist, int(nh), R, d_rowres, d_res, st_), "hist_select");
     launches += 2;
   }
@@ -226,21 +329,26 @@ void WaveRunner::submit(const WaveSpec& w) {
   {
     size_t off = 0;
     for (int b = 0; b < 7; ++b) {
-      const size_t m = exact_b[b].size();
+      const size_t m = exact_b_count[size_t(b)];
       if (!m) continue;
       cuda_check(launch_exact_bucket(b, d_nodes, d_exact + off, int(m), R, k, d_terms, d_rp,
                                      w.lab_in, d_gbase, d_G, D.xl.p, d_res, st_),
                  "exact_bucket");
       off += m;
       ++launches;
+      static const char* kBucketName[7] = {"exact_n<=32", "exact_n<=64", "exact_n<=128",
+                                           "exact_n<=256", "exact_n<=512", "exact_n<=1024",
+                                           "exact_n<=2048"};
+      mark(kBucketName[b]);
     }
   }
   if (timing) cudaEventRecord(ev_[4], st_);
-  cuda_check(launch_partition(d_nodes, N, d_tiles, int(tiles.size()), d_tfirst, R, k, d_terms,
+  cuda_check(launch_partition(d_nodes, N, d_tiles, int(n_tiles), d_tfirst, R, k, d_terms,
                               d_rp, d_pos_proj, d_pos_split, w.idx_in, w.lab_in, w.idx_out,
                               w.lab_out, d_gbase, d_G, d_res, d_flags, d_tleft, st_),
              "partition");
   launches += 3;
+  mark("partition");
   if (timing) cudaEventRecord(ev_[5], st_);
 
   NodeRes* hr = h_res_.ensure(size_t(N));
@@ -249,7 +357,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   pend_dres_ = d_res;
   pend_launches_ = launches;
   pend_hist_ = nh;
-  pend_exact_ = exact.size();
+  pend_exact_ = size_t(exact_total);
 }
 
 void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
@@ -279,6 +387,11 @@ void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
     float tt;
     cudaEventElapsedTime(&tt, ev_[0], ev_[5]);
     stats.ms_total += tt;
+    for (int i = 0; i < n_marks_; ++i) {
+      float dt;
+      cudaEventElapsedTime(&dt, mk_[i], mk_[i + 1]);
+      stats.add_kernel(mk_name_[i], dt);
+    }
     for (int i = 0; i < N; ++i) {
       const NodeIn& nd = w.nodes[size_t(i)];
       const double strict = 4.0 * double(nd.n) * double(nd.z);

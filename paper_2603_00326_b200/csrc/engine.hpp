@@ -11,6 +11,8 @@
 
 namespace sofg {
 
+class ThreadPool;
+
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -100,6 +102,12 @@ struct WaveSpec {
   uint8_t* lab_out = nullptr;
 };
 
+struct KernelTime {
+  const char* name;
+  double ms;
+  uint64_t launches;
+};
+
 struct WaveStats {
   double ms_sample = 0, ms_hist_rng = 0, ms_hist_count = 0, ms_exact = 0, ms_partition = 0;
   double ms_total = 0;
@@ -109,6 +117,16 @@ struct WaveStats {
   double hist_strict_bytes = 0, hist_sector_bytes = 0, exact_strict_bytes = 0,
          exact_sector_bytes = 0;
   uint64_t hist_count_launches = 0, exact_launches = 0;
+  std::vector<KernelTime> per_kernel;  // CUDA-event time per launch site (stats mode)
+  void add_kernel(const char* name, double ms) {
+    for (auto& k : per_kernel)
+      if (k.name == name) {
+        k.ms += ms;
+        k.launches++;
+        return;
+      }
+    per_kernel.push_back({name, ms, 1});
+  }
 };
 
 class WaveRunner {
@@ -138,14 +156,23 @@ class WaveRunner {
   // kWinTermsMax terms NodeRes carries inline).
   std::vector<uint32_t> fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row);
 
+  void set_pool(ThreadPool* p) { pool_ = p; }
+
   WaveStats stats;
   bool collect_stats = false;   // CUDA-event timing per phase + sector accounting
   bool sector_accounting = false;
 
  private:
   int device_;
+  ThreadPool* pool_ = nullptr;
   cudaStream_t st_ = nullptr;
   cudaEvent_t ev_[6]{};
+  // fine-grained per-launch timing (stats mode)
+  static constexpr int kMaxMarks = 32;
+  cudaEvent_t mk_[kMaxMarks + 1]{};
+  const char* mk_name_[kMaxMarks]{};
+  int n_marks_ = 0;
+  void mark(const char* name);
   DeviceData data_;
 
   // packed host->device inputs

@@ -61,6 +61,8 @@ struct Best {
   float thr;
   uint32_t nl;
   int row;
+  double xmin;   // impurity sum of the best row (monotone proxy for its gain)
+  double inv_n;  // 1/n (window bound only; every compared gain uses the exact division)
 };
 
 // Search one sorted row (keys in blocked layout). Updates `b` when this row's best gain is
@@ -137,14 +139,17 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   });
   xmin = warp_min_f64(xmin);
   if (!(xmin < inf)) return;
+  // gain = parent - X / n is monotone non-increasing in X: a row whose minimum impurity is not
+  // below the best row's cannot have a strictly larger gain (split.hpp:260 keeps earlier rows).
+  if (b.row >= 0 && !(xmin < b.xmin)) return;
   const double g = gain_from_x(parent, xmin, dn);
   if (!(g > 0.0)) return;
   if (b.row >= 0 && !(g > b.gain)) return;
-  const double win = x_window(parent, xmin, dn);
+  const double win = x_window_fast(parent, xmin, dn, b.inv_n);
   uint32_t first = 0xffffffffu;
   float fa = 0.f, fb = 0.f;
   eval([&](double X, uint32_t p, float a, float bb) {
-    if (X <= win && gain_from_x(parent, X, dn) == g) {
+    if (X == xmin || (X <= win && gain_from_x(parent, X, dn) == g)) {
       first = p;
       fa = a;
       fb = bb;
@@ -156,6 +161,7 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   const int src = __ffs(__ballot_sync(0xffffffffu, first == fp)) - 1;
   fa = __shfl_sync(0xffffffffu, fa, src);
   fb = __shfl_sync(0xffffffffu, fb, src);
+  b.xmin = xmin;
   b.row = row;
   b.gain = g;
   b.thr = midpoint_down(fa, fb);
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(128) k_exact_reg(
 
   const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
   const uint32_t* nterms = terms + nd.term_off;
-  Best best{0.0, 0.f, 0, -1};
+  Best best{0.0, 0.f, 0, -1, 0.0, 1.0 / double(n)};
 
   for (uint32_t r0 = uint32_t(wr * GR); r0 < R; r0 += uint32_t(WPN * GR)) {
     uint32_t tb[GR];
@@ -246,15 +252,25 @@ __global__ void __launch_bounds__(128) k_exact_reg(
         }
       }
     }
-#pragma unroll
+    // One copy of the sort/scan code for all GR rows (instruction-cache footprint): the row's
+    // values are picked out of the unrolled accumulator registers with selects.
+#pragma unroll 1
     for (int g = 0; g < GR; ++g) {
       const uint32_t r = r0 + uint32_t(g);
-      if (r >= R || nt[g] == 0) continue;  // empty rows are skipped in exact mode (split.hpp:308)
+      int ntg = 0;
+#pragma unroll
+      for (int gg = 0; gg < GR; ++gg)
+        if (gg == g) ntg = nt[gg];
+      if (r >= R || ntg == 0) continue;  // empty rows are skipped in exact mode (split.hpp:308)
       uint64_t key[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
+        double a = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < GR; ++gg)
+          if (gg == g) a = acc[gg][e];
         if (uint32_t(lane * E + e) < n) {
-          const float v = __double2float_rn(acc[g][e]);
+          const float v = __double2float_rn(a);
           key[e] = (uint64_t(order_key(v)) << 32) | uint64_t(__ldg(lab + nd.begin + lane * E + e));
         } else {
           key[e] = ~0ull;
@@ -278,7 +294,7 @@ __global__ void __launch_bounds__(128) k_exact_reg(
   if (lane == 0) s_best[w] = best;
   __syncthreads();
   if (threadIdx.x == 0) {
-    Best bb{0.0, 0.f, 0, -1};
+    Best bb{0.0, 0.f, 0, -1, 0.0, 0.0};
     for (int i = 0; i < WPN; ++i) {
       const Best& c = s_best[i];
       if (c.row < 0) continue;
@@ -308,31 +324,41 @@ __device__ __forceinline__ void team_sync(int team) {
 }
 
 template <int W, int KC>
-__global__ void __launch_bounds__(256) k_exact_team(
+__global__ void __launch_bounds__(256, 3) k_exact_team(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
     const float* __restrict__ G, const double* __restrict__ xl, NodeRes* __restrict__ res) {
   constexpr int E = 8;
   constexpr int TEAMS = 8 / W;
-  constexpr int P = 32 * E * W;
-  __shared__ uint64_t s_keys[8 * 32 * E];   // TEAMS * P == 2048 keys
+  constexpr int P = 32 * E * W;  // positions per team
+  // per team: ping-pong key/label arrays for the radix passes + per-warp digit histograms
+  __shared__ uint32_t s_key[2][8 * 256];
+  __shared__ uint8_t s_lab[2][8 * 256];
+  __shared__ uint32_t s_hist[8][256];
   __shared__ uint32_t s_cnt[8][KC];
   __shared__ uint64_t s_first[8];
   __shared__ double s_xmin[8];
   __shared__ uint32_t s_pos[8];
+  __shared__ uint32_t s_scan[8];
   __shared__ Best s_best[TEAMS];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int team = w / W;
   const int wt = w % W;
-  uint64_t* buf = s_keys + team * P;
+  const int tt = wt * 32 + lane;  // thread index inside the team
+  uint32_t* keyA = s_key[0] + team * P;
+  uint32_t* keyB = s_key[1] + team * P;
+  uint8_t* labA = s_lab[0] + team * P;
+  uint8_t* labB = s_lab[1] + team * P;
   const uint32_t node = list[blockIdx.x];
   const NodeIn nd = nodes[node];
   const uint32_t n = nd.n;
-  const int p0 = (wt * 32 + lane) * E;  // first position held by this lane
-
   const float* Gn = G + gbase[node];
+  const int p0 = tt * E;  // blocked layout used by the scan phase
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  // node class totals (every team holds the full node)
   uint32_t cnt[KC];
 #pragma unroll
   for (int c = 0; c < KC; ++c) cnt[c] = 0;
@@ -345,7 +371,6 @@ __global__ void __launch_bounds__(256) k_exact_team(
       for (int c = 0; c < KC; ++c) cnt[c] += (c == yy);
     }
   }
-  // node class totals (whole CTA: every team holds the full node)
 #pragma unroll
   for (int c = 0; c < KC; ++c) {
     uint32_t x = cnt[c];
@@ -365,7 +390,7 @@ __global__ void __launch_bounds__(256) k_exact_team(
 
   const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
   const uint32_t* nterms = terms + nd.term_off;
-  Best best{0.0, 0.f, 0, -1};
+  Best best{0.0, 0.f, 0, -1, 0.0, 1.0 / double(n)};
   const double dn = double(n);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
 
@@ -373,75 +398,99 @@ __global__ void __launch_bounds__(256) k_exact_team(
     const uint32_t tb = rp[r];
     const int nt = int(rp[r + 1] - tb);
     if (nt == 0) continue;  // uniform per team; split.hpp:308
+    // ---- projected values (terms combined in ascending feature order) -> radix layout
+    //      position q = wt*256 + e*32 + lane (warp-blocked, round-striped)
     double acc[E];
     for (int t = 0; t < nt; ++t) {
       const uint32_t tm = __ldg(nterms + tb + t);
       const float* gq = Gn + uint64_t(tb + uint32_t(t)) * n;
       float xv[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) xv[e] = uint32_t(p0 + e) < n ? gq[p0 + e] : 0.f;
+      for (int e = 0; e < E; ++e) {
+        const uint32_t q = uint32_t(wt * 256 + e * 32 + lane);
+        xv[e] = q < n ? gq[q] : 0.f;
+      }
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const double dx = (tm & 1u) ? -double(xv[e]) : double(xv[e]);
         acc[e] = t == 0 ? dx : __dadd_rn(acc[e], dx);
       }
     }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t q = uint32_t(wt * 256 + e * 32 + lane);
+      keyA[q] = q < n ? order_key(__double2float_rn(acc[e])) : 0xffffffffu;
+      labA[q] = q < n ? __ldg(lab + nd.begin + q) : uint8_t(0);
+    }
+    team_sync<W>(team);
+    // ---- LSD radix sort, 8-bit digits, stable (match.any ranking per 32-key round)
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = pass * 8;
+      uint32_t* src_k = (pass & 1) ? keyB : keyA;
+      uint8_t* src_l = (pass & 1) ? labB : labA;
+      uint32_t* dst_k = (pass & 1) ? keyA : keyB;
+      uint8_t* dst_l = (pass & 1) ? labA : labB;
+      uint32_t* hist = s_hist[w];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) hist[i * 32 + lane] = 0;
+      __syncwarp();
+      uint32_t kk[E], rk[E];
+      uint8_t ll[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int q = wt * 256 + e * 32 + lane;
+        kk[e] = src_k[q];
+        ll[e] = src_l[q];
+        const uint32_t dg = (kk[e] >> shift) & 0xffu;
+        const unsigned m = __match_any_sync(0xffffffffu, dg);
+        const uint32_t before = hist[dg];
+        rk[e] = before + __popc(m & lt_mask);
+        __syncwarp();
+        if ((m & lt_mask) == 0) hist[dg] = before + __popc(m);
+        __syncwarp();
+      }
+      team_sync<W>(team);
+      // exclusive scan over (digit, warp) in digit-major order: 256*W counters, 8 per thread
+      {
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int idx = tt * 8 + i;  // digit-major index
+          v[i] = s_hist[team * W + (idx % W)][idx / W];
+          sum += v[i];
+        }
+        uint32_t wtot;
+        uint32_t ex = warp_excl_scan_u32(sum, lane, &wtot);
+        if constexpr (W > 1) {
+          if (lane == 0) s_scan[w] = wtot;
+          team_sync<W>(team);
+          for (int i = 0; i < wt; ++i) ex += s_scan[team * W + i];
+        }
+        team_sync<W>(team);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int idx = tt * 8 + i;
+          s_hist[team * W + (idx % W)][idx / W] = ex;
+          ex += v[i];
+        }
+      }
+      team_sync<W>(team);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t dg = (kk[e] >> shift) & 0xffu;
+        const uint32_t pos = s_hist[w][dg] + rk[e];
+        dst_k[pos] = kk[e];
+        dst_l[pos] = ll[e];
+      }
+      team_sync<W>(team);
+    }
+    // sorted keys back in keyA/labA; blocked layout for the scan
     uint64_t key[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      if (uint32_t(p0 + e) < n) {
-        const float v = __double2float_rn(acc[e]);
-        key[e] = (uint64_t(order_key(v)) << 32) | uint64_t(__ldg(lab + nd.begin + p0 + e));
-      } else {
-        key[e] = ~0ull;
-      }
-    }
-    // ---- bitonic sort over the team's P positions
-#pragma unroll
-    for (int kk = 2; kk <= P; kk <<= 1) {
-#pragma unroll
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        if (j >= 32 * E) {  // across warps, through shared memory
-#pragma unroll
-          for (int e = 0; e < E; ++e) buf[p0 + e] = key[e];
-          team_sync<W>(team);
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int i = p0 + e;
-            const uint64_t o = buf[i ^ j];
-            const bool up = (i & kk) == 0;
-            const bool lower = (i & j) == 0;
-            const uint64_t mn = o < key[e] ? o : key[e];
-            const uint64_t mx = o < key[e] ? key[e] : o;
-            key[e] = (lower == up) ? mn : mx;
-          }
-          team_sync<W>(team);
-        } else if (j >= E) {
-          const int lm = j / E;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const uint64_t o = __shfl_xor_sync(0xffffffffu, key[e], lm);
-            const int i = p0 + e;
-            const bool up = (i & kk) == 0;
-            const bool lower = (lane & lm) == 0;
-            const uint64_t mn = o < key[e] ? o : key[e];
-            const uint64_t mx = o < key[e] ? key[e] : o;
-            key[e] = (lower == up) ? mn : mx;
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            if ((e & j) == 0) {
-              const int i = p0 + e;
-              const bool up = (i & kk) == 0;
-              const uint64_t a = key[e], b = key[e | j];
-              const bool sw = (a > b) == up;
-              key[e] = sw ? b : a;
-              key[e | j] = sw ? a : b;
-            }
-          }
-        }
-      }
+      const int q = p0 + e;
+      key[e] = (uint64_t(keyA[q]) << 32) | uint64_t(labA[q]);
     }
     // ---- class prefix across the team
     uint32_t loc[KC], pre[KC];
@@ -470,12 +519,14 @@ __global__ void __launch_bounds__(256) k_exact_team(
     if (lane == 31) next_first = (wt + 1 < W) ? s_first[w + 1] : ~0ull;
     team_sync<W>(team);
 
-    auto eval = [&](auto&& visit) {
+    double Xs[E];
+    {
       uint32_t left[KC];
 #pragma unroll
       for (int c = 0; c < KC; ++c) left[c] = pre[c];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
+        Xs[e] = inf;
         const uint32_t p = uint32_t(p0 + e);
         if (p + 1 < n) {
           const int c = int(key[e] & 0xffu);
@@ -486,12 +537,11 @@ __global__ void __launch_bounds__(256) k_exact_team(
           const float bb = order_key_inv(uint32_t(kb >> 32));
           if (a < bb) {
             const uint32_t nl = p + 1;
-            double Xv;
             if constexpr (KC == 2) {
               const uint32_t l1 = left[1], l0 = nl - l1;
               const double sl = __dadd_rn(__ldg(xl + l0), __ldg(xl + l1));
               const double sr = __dadd_rn(__ldg(xl + tot[0] - l0), __ldg(xl + tot[1] - l1));
-              Xv = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+              Xs[e] = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
             } else {
               double sl = 0.0, sr = 0.0;
 #pragma unroll
@@ -500,65 +550,53 @@ __global__ void __launch_bounds__(256) k_exact_team(
                   sl = __dadd_rn(sl, __ldg(xl + left[cc]));
                   sr = __dadd_rn(sr, __ldg(xl + tot[cc] - left[cc]));
                 }
-              Xv = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+              Xs[e] = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
             }
-            if (visit(Xv, p, a, bb)) return;
           }
         }
       }
-    };
+    }
     double xmin = inf;
-    eval([&](double Xv, uint32_t, float, float) {
-      xmin = fmin(xmin, Xv);
-      return false;
-    });
+#pragma unroll
+    for (int e = 0; e < E; ++e) xmin = fmin(xmin, Xs[e]);
     xmin = warp_min_f64(xmin);
     if (lane == 0) s_xmin[w] = xmin;
     team_sync<W>(team);
     for (int i = 0; i < W; ++i) xmin = fmin(xmin, s_xmin[team * W + i]);
     team_sync<W>(team);
     if (!(xmin < inf)) continue;
+    if (best.row >= 0 && !(xmin < best.xmin)) continue;  // cannot beat an earlier row
     const double g = gain_from_x(nd.parent, xmin, dn);
     if (!(g > 0.0)) continue;
     if (best.row >= 0 && !(g > best.gain)) continue;
-    const double win = x_window(nd.parent, xmin, dn);
+    const double win = x_window_fast(nd.parent, xmin, dn, best.inv_n);
     uint32_t first = 0xffffffffu;
-    eval([&](double Xv, uint32_t p, float, float) {
-      if (Xv <= win && gain_from_x(nd.parent, Xv, dn) == g) {
-        first = p;
-        return true;
-      }
-      return false;
-    });
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double X = Xs[e];
+      if (first == 0xffffffffu && X <= win &&
+          (X == xmin || gain_from_x(nd.parent, X, dn) == g))
+        first = uint32_t(p0 + e);
+    }
     first = warp_min_u32(first);
     if (lane == 0) s_pos[w] = first;
     team_sync<W>(team);
     uint32_t fp = first;
     for (int i = 0; i < W; ++i) fp = min(fp, s_pos[team * W + i]);
-    // the two keys around the winning gap: positions fp, fp+1
-    if (uint32_t(p0) <= fp && fp < uint32_t(p0 + E)) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (uint32_t(p0 + e) == fp) s_first[team * W] = key[e];
-    }
-    if (uint32_t(p0) <= fp + 1 && fp + 1 < uint32_t(p0 + E)) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (uint32_t(p0 + e) == fp + 1) s_keys[team * P + 0] = key[e];
-    }
-    team_sync<W>(team);
-    const float a = order_key_inv(uint32_t(s_first[team * W] >> 32));
-    const float b = order_key_inv(uint32_t(s_keys[team * P + 0] >> 32));
+    // the two keys around the winning gap: sorted positions fp, fp+1 (still in keyA)
+    const float a = order_key_inv(keyA[fp]);
+    const float b = order_key_inv(keyA[fp + 1]);
     team_sync<W>(team);
     best.row = int(r);
     best.gain = g;
+    best.xmin = xmin;
     best.thr = midpoint_down(a, b);
     best.nl = fp + 1;
   }
   if (wt == 0 && lane == 0) s_best[team] = best;
   __syncthreads();
   if (threadIdx.x == 0) {
-    Best bb{0.0, 0.f, 0, -1};
+    Best bb{0.0, 0.f, 0, -1, 0.0, 0.0};
     for (int i = 0; i < TEAMS; ++i) {
       const Best& c = s_best[i];
       if (c.row < 0) continue;

@@ -37,8 +37,11 @@ void ThreadPool::worker() {
       n = job_n_;
       ++active_;
     }
-    if (job)
-      for (size_t i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) (*job)(i);
+    if (job) {
+      const size_t g = std::max<size_t>(1, n / (size_t(workers_.size() + 1) * 16));
+      for (size_t i0 = next_.fetch_add(g); i0 < n; i0 = next_.fetch_add(g))
+        for (size_t i = i0; i < std::min(n, i0 + g); ++i) (*job)(i);
+    }
     {
       std::lock_guard<std::mutex> g(mu_);
       if (--active_ == 0) done_cv_.notify_all();
@@ -60,10 +63,23 @@ void ThreadPool::parallel_for(size_t n, const std::function<void(size_t)>& f) {
     ++gen_;
   }
   cv_.notify_all();
-  for (size_t i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) f(i);
+  {
+    const size_t g = std::max<size_t>(1, n / (size_t(workers_.size() + 1) * 16));
+    for (size_t i0 = next_.fetch_add(g); i0 < n; i0 = next_.fetch_add(g))
+      for (size_t i = i0; i < std::min(n, i0 + g); ++i) f(i);
+  }
   std::unique_lock<std::mutex> lk(mu_);
   done_cv_.wait(lk, [&] { return active_ == 0 && next_.load() >= n; });
   job_ = nullptr;
+}
+
+std::vector<size_t> ThreadPool::chunks(size_t n, size_t grain,
+                                       const std::function<void(size_t, size_t, size_t)>& f) {
+  size_t c = std::max<size_t>(1, std::min<size_t>(size_t(size()) * 4, (n + grain - 1) / std::max<size_t>(grain, 1)));
+  std::vector<size_t> b(c + 1);
+  for (size_t i = 0; i <= c; ++i) b[i] = n * i / c;
+  parallel_for(c, [&](size_t i) { f(i, b[i], b[i + 1]); });
+  return b;
 }
 
 // ------------------------------------------------------------------------------ scheduler
@@ -140,80 +156,98 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
 
   std::vector<std::vector<BNode>> trees(B);
   std::vector<std::vector<uint32_t>> pools(B);
-  std::vector<Open> frontier(B);
-  pool.parallel_for(B, [&](size_t b) {
-    trees[b].reserve(1024);
-    trees[b].emplace_back();
-    Open o{};
-    o.tree = uint32_t(b);
-    o.bnode = 0;
-    o.begin = uint32_t(off[b]);
-    o.n = uint32_t(roots[b].size());
-    o.depth = root_depth;
-    o.seed = root_seeds[b];
-    for (uint32_t s : roots[b]) o.counts[D.labels_host[s]]++;
-    frontier[b] = o;
+  // The frontier is kept in P parts; part p owns trees [B*p/P, B*(p+1)/P), so parts are processed
+  // in parallel without sharing a tree and never need to be concatenated.
+  const size_t NP = std::max<size_t>(1, std::min<size_t>(B, size_t(pool.size()) * 4));
+  std::vector<std::vector<Open>> fr(NP), sp(NP), nx(NP), rt(NP);
+  pool.parallel_for(NP, [&](size_t p) {
+    for (size_t b = B * p / NP; b < B * (p + 1) / NP; ++b) {
+      trees[b].reserve(1024);
+      trees[b].emplace_back();
+      Open o{};
+      o.tree = uint32_t(b);
+      o.bnode = 0;
+      o.begin = uint32_t(off[b]);
+      o.n = uint32_t(roots[b].size());
+      o.depth = root_depth;
+      o.seed = root_seeds[b];
+      for (uint32_t s0 : roots[b]) o.counts[D.labels_host[s0]]++;
+      fr[p].push_back(o);
+    }
   });
   times.ms_roots += ms_since(t0);
 
   int cur = 0;
-  std::vector<Open> split_list, retry, next;
   std::vector<uint32_t> spec_z, spec_pos;
+  std::vector<size_t> poff(NP + 1);
   std::vector<NodeRes> res;
   WaveSpec w;
   w.R = P.R;
   w.d = uint32_t(D.d);
   w.bins = uint32_t(P.bins);
   w.k = k;
+  eng.set_pool(&pool);
 
-  while (!frontier.empty()) {
+  auto count_open = [](const std::vector<std::vector<Open>>& v) {
+    size_t t = 0;
+    for (const auto& x : v) t += x.size();
+    return t;
+  };
+
+  while (count_open(fr) > 0) {
     times.levels++;
     t0 = Clock::now();
-    split_list.clear();
-    next.clear();
-    for (const Open& o : frontier) {
-      uint32_t top = 0;
-      for (int c = 0; c < k; ++c) top = std::max(top, o.counts[c]);
-      const bool can = top < o.n && o.n >= P.min_samples_split && o.n >= 2 &&
-                       (!P.max_depth || o.depth < *P.max_depth);  // forest.hpp:178-179
-      if (can)
-        split_list.push_back(o);
-      else
-        trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
-    }
+    pool.parallel_for(NP, [&](size_t p) {
+      std::vector<Open>& out = sp[p];
+      out.clear();
+      for (const Open& o : fr[p]) {
+        uint32_t top = 0;
+        for (int cc = 0; cc < k; ++cc) top = std::max(top, o.counts[cc]);
+        const bool can = top < o.n && o.n >= P.min_samples_split && o.n >= 2 &&
+                         (!P.max_depth || o.depth < *P.max_depth);  // forest.hpp:178-179
+        if (can)
+          out.push_back(o);
+        else
+          trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
+      }
+      nx[p].clear();
+    });
     times.ms_prep += ms_since(t0);
-    while (!split_list.empty()) {
+    while (count_open(sp) > 0) {
       t0 = Clock::now();
-      const size_t N = split_list.size();
+      poff[0] = 0;
+      for (size_t p = 0; p < NP; ++p) poff[p + 1] = poff[p] + sp[p].size();
+      const size_t N = poff[NP];
       w.nodes.resize(N);
-      // binomial draws not done speculatively (roots, retries) + parent entropies
+      // binomial draws not done speculatively (roots, retries), parent entropies, node records
       const auto tb = Clock::now();
-      pool.parallel_for(N, [&](size_t i) {
-        Open& o = split_list[i];
-        if (!o.has_z) {
-          uint64_t used;
-          o.z = uint32_t(binom(o.seed, o.pos, &used));
-          o.zpos = uint32_t(used);
-          o.has_z = 1;
+      pool.parallel_for(NP, [&](size_t p) {
+        for (size_t j = 0; j < sp[p].size(); ++j) {
+          Open& o = sp[p][j];
+          if (!o.has_z) {
+            uint64_t used;
+            o.z = uint32_t(binom(o.seed, o.pos, &used));
+            o.zpos = uint32_t(used);
+            o.has_z = 1;
+          }
+          NodeIn& nd = w.nodes[poff[p] + j];
+          nd.parent = host::entropy(o.counts, k);
+          nd.seed = o.seed;
+          nd.begin = o.begin;
+          nd.n = o.n;
+          nd.z = o.z;
+          nd.pos = o.zpos;
+          const bool hist = P.mode == 1 || (P.mode == 2 && o.n > P.breakeven);  // split.hpp:46-48
+          nd.flags = hist ? kNodeHist : 0u;
+          nd.hist_slot = 0;
+          nd.tree = o.tree;
         }
-        w.nodes[i].parent = host::entropy(o.counts, k);
       });
       times.ms_binomial += ms_since(tb);
       uint64_t term_off = 0;
       for (size_t i = 0; i < N; ++i) {
-        const Open& o = split_list[i];
-        NodeIn& nd = w.nodes[i];
-        nd.seed = o.seed;
-        nd.begin = o.begin;
-        nd.n = o.n;
-        nd.z = o.z;
-        nd.pos = o.zpos;
-        const bool hist = P.mode == 1 || (P.mode == 2 && o.n > P.breakeven);  // split.hpp:46-48
-        nd.flags = hist ? kNodeHist : 0u;
-        nd.term_off = uint32_t(term_off);
-        nd.hist_slot = 0;
-        nd.tree = o.tree;
-        term_off += o.z;
+        w.nodes[i].term_off = uint32_t(term_off);
+        term_off += w.nodes[i].z;
       }
       if (term_off >= (1ull << 32)) throw std::runtime_error("wave term count overflow");
       w.idx_in = idx[cur].p;
@@ -230,12 +264,15 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       t0 = Clock::now();
       spec_z.resize(2 * N);
       spec_pos.resize(2 * N);
-      pool.parallel_for(N, [&](size_t i) {
-        const Open& o = split_list[i];
-        for (int c = 0; c < 2; ++c) {
-          uint64_t used;
-          spec_z[2 * i + c] = uint32_t(binom(host::derive_seed(o.seed, uint64_t(c + 1)), 0, &used));
-          spec_pos[2 * i + c] = uint32_t(used);
+      pool.parallel_for(NP, [&](size_t p) {
+        for (size_t j = 0; j < sp[p].size(); ++j) {
+          const size_t i = poff[p] + j;
+          const uint64_t seed = sp[p][j].seed;
+          for (int c = 0; c < 2; ++c) {
+            uint64_t used;
+            spec_z[2 * i + c] = uint32_t(binom(host::derive_seed(seed, uint64_t(c + 1)), 0, &used));
+            spec_pos[2 * i + c] = uint32_t(used);
+          }
         }
       });
       times.ms_spec += ms_since(t0);
@@ -244,66 +281,69 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       times.ms_wait += ms_since(t0);
 
       t0 = Clock::now();
-      retry.clear();
-      for (size_t i = 0; i < N; ++i) {
-        Open& o = split_list[i];
-        const NodeRes& r = res[i];
-        if (r.row >= 0 && r.n_left > 0 && r.n_left < o.n) {
-          std::vector<BNode>& tr = trees[o.tree];
-          std::vector<uint32_t>& tp = pools[o.tree];
-          const int32_t L = int32_t(tr.size());
-          {
-            BNode& p = tr[size_t(o.bnode)];
-            p.thr = r.threshold;
-            p.left = L;
-            p.right = L + 1;
-            p.term_off = uint32_t(tp.size());
-            p.term_len = r.n_terms;
-            if (r.n_terms <= uint32_t(kWinTermsMax)) {
-              tp.insert(tp.end(), r.terms, r.terms + r.n_terms);
-            } else {
-              const std::vector<uint32_t> t = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
-              tp.insert(tp.end(), t.begin(), t.end());
+      pool.parallel_for(NP, [&](size_t p) {
+        rt[p].clear();
+        for (size_t j = 0; j < sp[p].size(); ++j) {
+          const size_t i = poff[p] + j;
+          Open& o = sp[p][j];
+          const NodeRes& r = res[i];
+          if (r.row >= 0 && r.n_left > 0 && r.n_left < o.n) {
+            std::vector<BNode>& tr = trees[o.tree];
+            std::vector<uint32_t>& tp = pools[o.tree];
+            const int32_t L = int32_t(tr.size());
+            {
+              BNode& pn = tr[size_t(o.bnode)];
+              pn.thr = r.threshold;
+              pn.left = L;
+              pn.right = L + 1;
+              pn.term_off = uint32_t(tp.size());
+              pn.term_len = r.n_terms;
+              if (r.n_terms <= uint32_t(kWinTermsMax)) {
+                tp.insert(tp.end(), r.terms, r.terms + r.n_terms);
+              } else {
+                const std::vector<uint32_t> t = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
+                tp.insert(tp.end(), t.begin(), t.end());
+              }
             }
+            tr.emplace_back();
+            tr.emplace_back();
+            Open l{}, rr{};
+            l.tree = rr.tree = o.tree;
+            l.bnode = L;
+            rr.bnode = L + 1;
+            l.depth = rr.depth = o.depth + 1;
+            l.begin = o.begin;
+            l.n = r.n_left;
+            rr.begin = o.begin + r.n_left;
+            rr.n = o.n - r.n_left;
+            l.seed = host::derive_seed(o.seed, 1);  // forest.hpp:226-228
+            rr.seed = host::derive_seed(o.seed, 2);
+            l.z = spec_z[2 * i];
+            l.zpos = spec_pos[2 * i];
+            rr.z = spec_z[2 * i + 1];
+            rr.zpos = spec_pos[2 * i + 1];
+            l.has_z = rr.has_z = 1;
+            for (int c = 0; c < k; ++c) {
+              l.counts[c] = r.left_counts[c];
+              rr.counts[c] = o.counts[c] - r.left_counts[c];
+            }
+            nx[p].push_back(l);
+            nx[p].push_back(rr);
+          } else if (o.attempt < P.max_split_retries) {  // forest.hpp:187,211: next attempt
+            o.attempt++;
+            o.pos = r.pos_after;
+            o.has_z = 0;
+            rt[p].push_back(o);
+          } else {
+            trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
           }
-          tr.emplace_back();
-          tr.emplace_back();
-          Open l{}, rr{};
-          l.tree = rr.tree = o.tree;
-          l.bnode = L;
-          rr.bnode = L + 1;
-          l.depth = rr.depth = o.depth + 1;
-          l.begin = o.begin;
-          l.n = r.n_left;
-          rr.begin = o.begin + r.n_left;
-          rr.n = o.n - r.n_left;
-          l.seed = host::derive_seed(o.seed, 1);  // forest.hpp:226-228
-          rr.seed = host::derive_seed(o.seed, 2);
-          l.z = spec_z[2 * i];
-          l.zpos = spec_pos[2 * i];
-          rr.z = spec_z[2 * i + 1];
-          rr.zpos = spec_pos[2 * i + 1];
-          l.has_z = rr.has_z = 1;
-          for (int c = 0; c < k; ++c) {
-            l.counts[c] = r.left_counts[c];
-            rr.counts[c] = o.counts[c] - r.left_counts[c];
-          }
-          next.push_back(l);
-          next.push_back(rr);
-        } else if (o.attempt < P.max_split_retries) {  // forest.hpp:187,211: next attempt
-          o.attempt++;
-          o.pos = r.pos_after;
-          o.has_z = 0;
-          retry.push_back(o);
-        } else {
-          trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
         }
-      }
-      split_list.swap(retry);
+        sp[p].swap(rt[p]);
+      });
       times.ms_post += ms_since(t0);
     }
     cur ^= 1;
-    frontier.swap(next);
+    fr.swap(nx);
   }
 
   // ---- reference node order: ids assigned at split time in depth-first order (H4) ------------

@@ -52,6 +52,10 @@ class ThreadPool {
   int size() const { return int(workers_.size()) + 1; }
   // f(i) for i in [0, n), caller participates.
   void parallel_for(size_t n, const std::function<void(size_t)>& f);
+  // Splits [0, n) into contiguous chunks (at least `grain` items each) and runs
+  // f(chunk, begin, end) in parallel; returns the chunk boundaries (size chunks + 1).
+  std::vector<size_t> chunks(size_t n, size_t grain,
+                             const std::function<void(size_t, size_t, size_t)>& f);
 
  private:
   void worker();
