@@ -1,0 +1,10 @@
+# ncu --set full captures of the top kernels at a mid-tree level (20-tree batch, 1M x 4096)
+K="k_csp_gather:12 k_hist_count:8 k_exact_reg<1:12 k_exact_reg<4:8 k_exact_team<1:8 k_exact_team<4:6"
+for kv in $K; do
+  name=${kv%%:*}; skip=${kv##*:}
+  tag=$(echo $name | tr -c 'a-z0-9_' '_')
+  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:${name}" -s $skip -c 1 \
+     -o gpurun_out/prof_${tag} python scratch/prof_run.py 20 > gpurun_out/prof_${tag}.log 2>&1
+  tail -2 gpurun_out/prof_${tag}.log
+done
+ls -la gpurun_out
