@@ -1,5 +1,6 @@
 // C ABI (include/sofg.h) and C++ API (include/sofg/soforest_gpu.hpp) over the level-wise trainer.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -92,6 +93,15 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   D.ld = (n + 31) / 32 * 32;
   D.X.exact(D.ld * d);
   copy_X(D.X.p, D.ld);
+  // Row-major copy for the sample-major projection sweep (sweep.cu); rows padded to 128 B.
+  D.XR.release();
+  D.ldr = (d + 1 + 31) / 32 * 32;  // >= one zero pad column (the sweep's empty-row term)
+  if (!std::getenv("SOFG_NO_ROW_TABLE")) {
+    D.XR.exact(n * D.ldr);
+    cuda_check(sofg::launch_transpose_rows(D.X.p, D.ld, n, d, D.XR.p, D.ldr, c->eng->stream()),
+               "transpose_rows");
+    cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync transpose");
+  }
   D.labels_host.assign(labels, labels + n);
   std::vector<uint8_t> l8(n);
   for (uint64_t i = 0; i < n; ++i) l8[i] = uint8_t(labels[i]);

@@ -85,6 +85,10 @@ struct Tile {
   uint32_t tile_in_node;
 };
 
+// Row pitch of the wave's projected-value block V (sample j of node i at V[vbase[i] + j*Rp]):
+// R rounded up to 8 rows so 8 consecutive rows of a sample are one aligned 32-byte sector.
+SOFG_HD inline uint32_t vpitch(uint32_t R) { return (R + 7u) & ~7u; }
+
 // Term encoding: feature index in the high 31 bits, sign in bit 0 (1 = weight -1).
 SOFG_HD inline uint32_t encode_term(uint32_t feature, bool negative) {
   return (feature << 1) | (negative ? 1u : 0u);

@@ -20,6 +20,7 @@ WaveRunner::WaveRunner(int device) : device_(device) {
     cudaGetLastError();
   }
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device);
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   for (auto& e : mk_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
 }
@@ -115,8 +116,8 @@ void WaveRunner::submit(const WaveSpec& w) {
           t.exact[exact_bucket(nd.n)]++;
         }
         t.tiles += (nd.n + kTileElems - 1) / kTileElems;
-        t.g += uint64_t(nd.z) * nd.n;
-        t.items += csp_items(nd.n, nd.z);
+        t.g += uint64_t(vpitch(R)) * nd.n;
+        t.items += uint64_t(nd.z) * nd.n;
       }
     });
     cc.assign(tmp.begin(), tmp.begin() + (cb.size() - 1));
@@ -160,7 +161,7 @@ void WaveRunner::submit(const WaveSpec& w) {
     }
   }
   const uint32_t zmax = tot.zmax, n_multi = uint32_t(tot.multi);
-  const uint64_t g_total = tot.g, n_items = tot.items;
+  const uint64_t g_total = tot.g, sum_nz = tot.items;
   uint64_t total_terms = w.given_csr ? w.given_terms.size() : tot.terms_end;
   const size_t nh = size_t(tot.hist);
   const size_t n_tiles = size_t(tot.tiles), n_work = size_t(tot.work);
@@ -199,7 +200,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       const NodeIn& nd = w.nodes[i];
       p_nodes[i] = nd;
       p_gbase[i] = o.g;
-      o.g += uint64_t(nd.z) * nd.n;
+      o.g += uint64_t(vpitch(R)) * nd.n;
       p_tfirst[i] = uint32_t(o.tiles);
       for (uint32_t s0 = 0, t = 0; s0 < nd.n; s0 += kTileElems, ++t)
         p_tiles[o.tiles++] = {uint32_t(i), s0, std::min(nd.n - s0, uint32_t(kTileElems)), t};
@@ -270,9 +271,15 @@ void WaveRunner::submit(const WaveSpec& w) {
   uint32_t* d_gcnt = gcnt_.ensure(std::max<size_t>(1, size_t(n_multi) * R * bpad * k));
   uint32_t* d_done = done_.ensure(std::max<size_t>(1, size_t(n_multi) * groups));
   NodeRes* d_res = res_.ensure(size_t(N));
-  float* d_G = G_.ensure(std::max<uint64_t>(1, g_total));
-  uint64_t* d_items = items_.ensure(std::max<uint64_t>(1, n_items));
-  uint32_t* d_fcnt = fcnt_.ensure(w.d);
+  float* d_G = V_.ensure(std::max<uint64_t>(1, g_total));
+  // Projection stage: sweep the row-major table when the wave's gathers would touch a sizeable
+  // part of it (a full sweep streams n*d*4 bytes; gathers cost one 32 B sector per term value).
+  bool sweep = w.inv && D.XR.p && w.B > 0 &&
+               row_sweep_smem(D.ldr, w.B, R) <= size_t(227) * 1024 &&
+               double(sum_nz) >= 0.25 * double(D.n) * double(D.d);
+  if (w.force_mode == 0) sweep = false;
+  if (w.force_mode == 1 && w.inv && D.XR.p) sweep = true;
+  uint32_t* d_pos_node = sweep ? pos_node_.ensure(std::max<uint64_t>(1, w.total)) : nullptr;
   uint32_t* d_flags = flags_.ensure(std::max<size_t>(1, n_tiles * 32));
   uint32_t* d_tleft = tile_left_.ensure(std::max<size_t>(1, n_tiles));
 
@@ -298,11 +305,24 @@ void WaveRunner::submit(const WaveSpec& w) {
     ++launches;
     mark("sample_projection");
   }
-  cuda_check(launch_csp(d_nodes, N, d_gbase, d_terms, w.d, n_items, d_fcnt, d_items, w.idx_in,
-                        D.X.p, D.ld, d_G, st_),
-             "column_sweep_gather");
-  launches += 4;
-  mark("column_sweep_gather");
+  if (sweep) {
+    cuda_check(launch_pos_fill(d_nodes, d_tiles, int(n_tiles), w.total, d_pos_node, st_), "pos_fill");
+    void* d_aug = aug_.ensure(aug_bytes(total_terms, uint32_t(N), R, w.d));
+    uint4* d_qoff = qoff_.ensure(size_t(N));
+    cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, d_qoff, st_), "aug_build");
+    cuda_check(launch_row_sweep(D.XR.p, D.ldr, uint32_t(D.n), w.inv, w.B, d_pos_node, d_nodes,
+                                d_gbase, d_aug, d_qoff, R, w.d, d_G, n_sm_, st_),
+               "row_sweep");
+    launches += 3;
+    mark("row_sweep");
+  } else {
+    cuda_check(launch_project_gather(d_nodes, d_tiles, int(n_tiles), d_gbase, d_terms, d_rp, R,
+                                     zmax, w.idx_in, D.X.p, D.ld, d_G, st_),
+               "project_gather");
+    launches += 1;
+    mark("project_gather");
+  }
+  pend_sweep_ = sweep;
   if (timing) cudaEventRecord(ev_[1], st_);
   if (nh) {
     cuda_check(launch_hist_draws(d_nodes, d_hist, int(nh), R, bins, d_pos_proj, d_draws,
@@ -345,7 +365,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   if (timing) cudaEventRecord(ev_[4], st_);
   cuda_check(launch_partition(d_nodes, N, d_tiles, int(n_tiles), d_tfirst, R, k, d_terms,
                               d_rp, d_pos_proj, d_pos_split, w.idx_in, w.lab_in, w.idx_out,
-                              w.lab_out, d_gbase, d_G, d_res, d_flags, d_tleft, st_),
+                              w.lab_out, d_gbase, d_G, d_res, d_flags, d_tleft, w.inv, w.B, st_),
              "partition");
   launches += 3;
   mark("partition");
@@ -375,6 +395,7 @@ void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
   stats.exact_nodes += pend_exact_;
   stats.launches += uint64_t(launches);
   if (nh) stats.hist_count_launches++;
+  (pend_sweep_ ? stats.sweep_waves : stats.gather_waves)++;
   if (pend_exact_) stats.exact_launches++;
   if (timing) {
     float t[5];

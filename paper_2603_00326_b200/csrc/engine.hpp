@@ -76,6 +76,8 @@ struct PinnedBuf {
 // u8 labels, and the reference's xlogx table up to n.
 struct DeviceData {
   DevBuf<float> X;
+  DevBuf<float> XR;  // row-major copy [n][ldr] for the sample-major projection sweep (sweep.cu)
+  uint64_t ldr = 0;
   DevBuf<uint8_t> lab;
   DevBuf<double> xl;
   uint64_t n = 0, d = 0, ld = 0;
@@ -100,6 +102,12 @@ struct WaveSpec {
   const uint8_t* lab_in = nullptr;
   uint32_t* idx_out = nullptr;
   uint8_t* lab_out = nullptr;
+  // inverse map of the batch (sweep.cu): inv[s*B + tree] = level position of sample s in tree,
+  // maintained by the partition. nullptr: the projection stage gathers instead of sweeping.
+  uint32_t* inv = nullptr;
+  uint32_t B = 0;
+  uint64_t total = 0;  // level buffer length (positions)
+  int force_mode = -1;  // -1 auto, 0 gather, 1 sweep (tests / experiments)
 };
 
 struct KernelTime {
@@ -117,6 +125,7 @@ struct WaveStats {
   double hist_strict_bytes = 0, hist_sector_bytes = 0, exact_strict_bytes = 0,
          exact_sector_bytes = 0;
   uint64_t hist_count_launches = 0, exact_launches = 0;
+  uint64_t sweep_waves = 0, gather_waves = 0;
   std::vector<KernelTime> per_kernel;  // CUDA-event time per launch site (stats mode)
   void add_kernel(const char* name, double ms) {
     for (auto& k : per_kernel)
@@ -185,15 +194,18 @@ class WaveRunner {
   DevBuf<float> bnd_;
   DevBuf<RowRes> rowres_;
   DevBuf<NodeRes> res_;
-  DevBuf<float> G_;        // gathered term values of the wave (csp.cu)
-  DevBuf<uint64_t> items_; // feature-sorted gather items
-  DevBuf<uint32_t> fcnt_;  // per-feature item counts / cursors
+  DevBuf<float> V_;          // projected rows of the wave (sweep.cu)
+  DevBuf<uint32_t> pos_node_;  // level position -> wave node (sweep mode)
+  DevBuf<unsigned char> aug_;  // augmented term lists (sweep mode)
+  DevBuf<uint4> qoff_;         // per-node sub-list offsets (sweep mode)
+  int n_sm_ = 148;
   const uint32_t* last_terms_ = nullptr;
   const uint32_t* last_rp_ = nullptr;
   // submit -> collect state
   NodeRes* pend_dres_ = nullptr;
   int pend_n_ = 0, pend_launches_ = 0;
   size_t pend_hist_ = 0, pend_exact_ = 0;
+  bool pend_sweep_ = false;
 };
 
 }  // namespace sofg

@@ -208,52 +208,41 @@ __global__ void __launch_bounds__(128) k_exact_reg(
   }
 
   const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
-  const uint32_t* nterms = terms + nd.term_off;
+  const uint32_t Rp = vpitch(R);
   Best best{0.0, 0.f, 0, -1, 0.0, 1.0 / double(n)};
 
   for (uint32_t r0 = uint32_t(wr * GR); r0 < R; r0 += uint32_t(WPN * GR)) {
-    uint32_t tb[GR];
     int nt[GR];
-    int ntmax = 0;
 #pragma unroll
     for (int g = 0; g < GR; ++g) {
       const uint32_t r = r0 + uint32_t(g);
-      if (r < R) {
-        tb[g] = rp[r];
-        nt[g] = int(rp[r + 1] - tb[g]);
-      } else {
-        tb[g] = 0;
-        nt[g] = 0;
-      }
-      ntmax = max(ntmax, nt[g]);
+      nt[g] = r < R ? int(__ldg(rp + r + 1) - __ldg(rp + r)) : 0;
     }
-    double acc[GR][E];
-    for (int t = 0; t < ntmax; ++t) {
-      float xv[GR][E];
-      uint32_t tm[GR];
+    // Rows r0..r0+GR-1 of this lane's samples: one aligned vector load each (GR divides the
+    // 8-row pitch, so the group never crosses a sample's sector).
+    float val[GR][E];
 #pragma unroll
-      for (int g = 0; g < GR; ++g) tm[g] = t < nt[g] ? __ldg(nterms + tb[g] + t) : 0u;
+    for (int e = 0; e < E; ++e) {
+      const uint32_t j = uint32_t(lane * E + e);
+      const float* src = Gn + uint64_t(j < n ? j : 0u) * Rp + r0;
+      if constexpr (GR == 8) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(src) + 1);
+        val[0][e] = a.x; val[1][e] = a.y; val[2][e] = a.z; val[3][e] = a.w;
+        val[4][e] = b.x; val[5][e] = b.y; val[6][e] = b.z; val[7][e] = b.w;
+      } else if constexpr (GR == 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+        val[0][e] = a.x; val[1][e] = a.y; val[2][e] = a.z; val[3][e] = a.w;
+      } else if constexpr (GR == 2) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(src));
+        val[0][e] = a.x; val[1][e] = a.y;
+      } else {
 #pragma unroll
-      for (int g = 0; g < GR; ++g) {
-        const float* gq = Gn + uint64_t(tb[g] + uint32_t(t)) * n;
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-          xv[g][e] = (t < nt[g] && uint32_t(lane * E + e) < n) ? gq[lane * E + e] : 0.f;
-      }
-#pragma unroll
-      for (int g = 0; g < GR; ++g) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const double dx = (tm[g] & 1u) ? -double(xv[g][e]) : double(xv[g][e]);
-          if (t == 0)
-            acc[g][e] = dx;
-          else if (t < nt[g])
-            acc[g][e] = __dadd_rn(acc[g][e], dx);
-        }
+        for (int g = 0; g < GR; ++g) val[g][e] = __ldg(src + g);
       }
     }
     // One copy of the sort/scan code for all GR rows (instruction-cache footprint): the row's
-    // values are picked out of the unrolled accumulator registers with selects.
+    // values are picked out of the unrolled registers with selects.
 #pragma unroll 1
     for (int g = 0; g < GR; ++g) {
       const uint32_t r = r0 + uint32_t(g);
@@ -265,12 +254,11 @@ __global__ void __launch_bounds__(128) k_exact_reg(
       uint64_t key[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        double a = 0.0;
+        float v = 0.f;
 #pragma unroll
         for (int gg = 0; gg < GR; ++gg)
-          if (gg == g) a = acc[gg][e];
+          if (gg == g) v = val[gg][e];
         if (uint32_t(lane * E + e) < n) {
-          const float v = __double2float_rn(a);
           key[e] = (uint64_t(order_key(v)) << 32) | uint64_t(__ldg(lab + nd.begin + lane * E + e));
         } else {
           key[e] = ~0ull;
@@ -389,7 +377,7 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
   __syncthreads();
 
   const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
-  const uint32_t* nterms = terms + nd.term_off;
+  const uint32_t Rp = vpitch(R);
   Best best{0.0, 0.f, 0, -1, 0.0, 1.0 / double(n)};
   const double dn = double(n);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -398,28 +386,12 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
     const uint32_t tb = rp[r];
     const int nt = int(rp[r + 1] - tb);
     if (nt == 0) continue;  // uniform per team; split.hpp:308
-    // ---- projected values (terms combined in ascending feature order) -> radix layout
+    // ---- projected values of row r (V block, sample-major) -> radix layout
     //      position q = wt*256 + e*32 + lane (warp-blocked, round-striped)
-    double acc[E];
-    for (int t = 0; t < nt; ++t) {
-      const uint32_t tm = __ldg(nterms + tb + t);
-      const float* gq = Gn + uint64_t(tb + uint32_t(t)) * n;
-      float xv[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const uint32_t q = uint32_t(wt * 256 + e * 32 + lane);
-        xv[e] = q < n ? gq[q] : 0.f;
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const double dx = (tm & 1u) ? -double(xv[e]) : double(xv[e]);
-        acc[e] = t == 0 ? dx : __dadd_rn(acc[e], dx);
-      }
-    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t q = uint32_t(wt * 256 + e * 32 + lane);
-      keyA[q] = q < n ? order_key(__double2float_rn(acc[e])) : 0xffffffffu;
+      keyA[q] = q < n ? order_key(__ldg(Gn + uint64_t(q) * Rp + r)) : 0xffffffffu;
       labA[q] = q < n ? __ldg(lab + nd.begin + q) : uint8_t(0);
     }
     team_sync<W>(team);

@@ -33,12 +33,28 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
                               uint32_t* done, RowRes* rowres, cudaStream_t st);
 cudaError_t launch_hist_select(const uint32_t* hist_nodes, int n_hist, uint32_t R,
                                const RowRes* rowres, NodeRes* res, cudaStream_t st);
-// csp.cu — column-sweep gather into G (per node: z x n raw values, term-major)
-uint64_t csp_items(uint32_t n, uint32_t z);
-cudaError_t launch_csp(const NodeIn* nodes, int n_nodes, const uint64_t* gbase,
-                       const uint32_t* terms, uint32_t d, uint64_t n_items, uint32_t* cnt,
-                       uint64_t* items, const uint32_t* idx, const float* X, uint64_t ld, float* G,
-                       cudaStream_t st);
+// sweep.cu — projection stage: node rows into V (per node n x Rp floats, sample-major)
+cudaError_t launch_transpose_rows(const float* X, uint64_t ld, uint64_t n, uint64_t d, float* XR,
+                                  uint64_t ldr, cudaStream_t st);
+cudaError_t launch_inv_init(const uint32_t* idx, const uint64_t* off, uint32_t B,
+                            uint64_t n_samples, uint64_t max_per_tree, uint32_t* inv,
+                            cudaStream_t st);
+cudaError_t launch_pos_fill(const NodeIn* nodes, const Tile* tiles, int n_tiles, uint64_t total,
+                            uint32_t* pos_node, cudaStream_t st);
+size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d);
+cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
+                             const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
+                             uint4* qoff, cudaStream_t st);
+size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R);
+cudaError_t launch_row_sweep(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
+                             uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
+                             const uint64_t* vbase, const void* aug, const uint4* qoff,
+                             uint32_t R, uint32_t d, float* V, int n_sm, cudaStream_t st);
+cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_tiles,
+                                  const uint64_t* vbase, const uint32_t* terms,
+                                  const uint32_t* row_ptr, uint32_t R, uint32_t zmax,
+                                  const uint32_t* idx, const float* X, uint64_t ld, float* V,
+                                  cudaStream_t st);
 
 // exact.cu — register-resident exact splitter, bucketed by node size (<= 2048 samples)
 int exact_bucket(uint32_t n);
@@ -54,7 +70,7 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint32_t* pos_split, const uint32_t* idx_in,
                              const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
                              const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
-                             uint32_t* tile_left, cudaStream_t st);
+                             uint32_t* tile_left, uint32_t* inv, uint32_t B, cudaStream_t st);
 
 cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_tiles,
                                 const uint32_t* idx, NodeRes* res, cudaStream_t st);

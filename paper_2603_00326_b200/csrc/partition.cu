@@ -32,11 +32,8 @@ __global__ void __launch_bounds__(256) k_part_flags(
   if (threadIdx.x < kMaxClasses) s_cls[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_left = 0;
   __syncthreads();
-  const uint32_t* rp = row_ptr + size_t(tl.node) * (R + 1);
-  const uint32_t q0 = rp[row];
-  const uint32_t* rt = terms + nd.term_off + q0;
-  const int nt = int(rp[row + 1] - q0);
-  const float* Gn = G + gbase[tl.node];
+  const uint32_t Rp = vpitch(R);
+  const float* Vn = G + gbase[tl.node] + row;  // winning row of the node's V block (sweep.cu)
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   uint32_t my_left = 0;
@@ -49,7 +46,7 @@ __global__ void __launch_bounds__(256) k_part_flags(
   for (int e = 0; e < 4; ++e) {
     const uint32_t l = uint32_t(e * 256 + threadIdx.x);
     if (l < tl.len) {
-      v[e] = combine_g(Gn, nd.n, rt, nt, q0, tl.start + l);
+      v[e] = __ldg(Vn + uint64_t(tl.start + l) * Rp);
       y[e] = lab[nd.begin + tl.start + l];
     }
   }
@@ -122,7 +119,7 @@ __global__ void __launch_bounds__(256) k_part_scatter(
     const NodeRes* __restrict__ res, const uint32_t* __restrict__ flags,
     const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ idx_in,
     const uint8_t* __restrict__ lab_in, uint32_t* __restrict__ idx_out,
-    uint8_t* __restrict__ lab_out) {
+    uint8_t* __restrict__ lab_out, uint32_t* __restrict__ inv, uint32_t B) {
   __shared__ uint32_t s_wpre[32];
   const Tile tl = tiles[blockIdx.x];
   if (res[tl.node].row < 0) return;
@@ -149,8 +146,10 @@ __global__ void __launch_bounds__(256) k_part_scatter(
     const bool left = (m >> lane) & 1u;
     const uint32_t dst = left ? L : n_left + (p - L);
     const uint32_t src = nd.begin + p;
-    idx_out[nd.begin + dst] = idx_in[src];
+    const uint32_t smp = idx_in[src];
+    idx_out[nd.begin + dst] = smp;
     lab_out[nd.begin + dst] = lab_in[src];
+    if (inv) inv[uint64_t(smp) * B + nd.tree] = nd.begin + dst;  // sweep.cu inverse map
   }
 }
 
@@ -189,7 +188,7 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint32_t* pos_split, const uint32_t* idx_in,
                              const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
                              const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
-                             uint32_t* tile_left, cudaStream_t st) {
+                             uint32_t* tile_left, uint32_t* inv, uint32_t B, cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
   if (n_tiles > 0)
     dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, lab_in, gbase,
@@ -198,7 +197,7 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                                                       row_ptr, pos_proj, pos_split, tile_left, res);
   if (n_tiles > 0)
     dev::k_part_scatter<<<n_tiles, 256, 0, st>>>(nodes, tiles, res, flags, tile_left, idx_in,
-                                                 lab_in, idx_out, lab_out);
+                                                 lab_in, idx_out, lab_out, inv, B);
   return cudaGetLastError();
 }
 

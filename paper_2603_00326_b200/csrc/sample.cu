@@ -234,11 +234,8 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
   }
   const uint32_t m = min(bins, n);
   const uint32_t J0 = n - m;
-  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
-  const uint32_t q0 = rp[r];
-  const uint32_t* rt = terms + nd.term_off + q0;
-  const int nt = int(rp[r + 1] - q0);
-  const float* Gn = G + gbase[node];
+  const uint32_t Rp = vpitch(R);
+  const float* Vn = G + gbase[node] + r;  // row r of the node's V block (sweep.cu)
 
   if (m < n) {
     const uint32_t* t = draws + size_t(h) * R * bins + size_t(r) * m;
@@ -273,13 +270,13 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
       uint32_t key = 0xffffffffu;
       if (i < int(m)) {
         const uint32_t p = col[i] ? J0 + uint32_t(i) : t[i];
-        key = order_key(combine_g(Gn, n, rt, nt, q0, p));
+        key = order_key(__ldg(Vn + uint64_t(p) * Rp));
       }
       vk[i] = key;
     }
   } else {
     for (int i = lane; i < mpad; i += 32)
-      vk[i] = i < int(m) ? order_key(combine_g(Gn, n, rt, nt, q0, uint32_t(i))) : 0xffffffffu;
+      vk[i] = i < int(m) ? order_key(__ldg(Vn + uint64_t(i) * Rp)) : 0xffffffffu;
   }
   __syncwarp();
   warp_bitonic_sort(vk, mpad, lane);

@@ -157,11 +157,8 @@ __global__ void __launch_bounds__(256) k_hist_count(
   __syncthreads();
 
   if (nb > 0) {
-    const uint32_t* rp = row_ptr + size_t(wk.node) * (R + 1);
-    const uint32_t q0 = rp[r];
-    const uint32_t* rt = terms + nd.term_off + q0;
-    const int nt = int(rp[r + 1] - q0);
-    const float* Gn = G + gbase[wk.node];
+    const uint32_t Rp = vpitch(R);
+    const float* Vn = G + gbase[wk.node] + r;  // row r of the node's V block (sweep.cu)
     for (uint32_t j0 = 0; j0 < wk.len; j0 += 128) {
       float v[4];
       uint8_t y[4];
@@ -169,7 +166,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
       for (int u = 0; u < 4; ++u) {
         const uint32_t j = j0 + uint32_t(u * 32 + lane);
         if (j < wk.len) {
-          v[u] = combine_g(Gn, nd.n, rt, nt, q0, wk.start + j);
+          v[u] = __ldg(Vn + uint64_t(wk.start + j) * Rp);
           y[u] = lab_s[j];
         }
       }

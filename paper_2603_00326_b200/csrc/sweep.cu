@@ -1,0 +1,518 @@
+// Projection stage of a wave: every open node's projected rows (reference apply_projection,
+// projection.hpp:86-108, called per row by find_node_split, split.hpp:247-250) written to the
+// wave's value block V. Node i owns V[vbase[i] .. + n_i * Rp): sample j of the node (its j-th
+// active sample) has its R projected values contiguous at V[vbase[i] + j*Rp + r] (Rp = R rounded
+// up to 8, one 32-byte sector per 8 rows). Downstream kernels read rows with vector loads.
+//
+// Two producers write the same V:
+//
+//  k_row_sweep       sample-major sweep over the row-major copy of the table (XR). Each CTA takes
+//                    one sample s at a time: it looks up, through the batch's inverse map
+//                    inv[s][tree] (position of s in the tree's level buffer) and pos_node, every
+//                    open node of the wave that contains s, streams the sample's 16 KB row into
+//                    shared memory once, and computes all R rows of every such node from shared
+//                    memory. One coalesced read of the table row serves the ~60 trees that hold the
+//                    sample, instead of ~60 x 192 scattered 4-byte gathers from the column-major
+//                    table (each a 32-byte L2 sector); V is written with coalesced 128-byte stores.
+//  k_project_gather  node-major gathers from the column-major table (used for waves that cover
+//                    few samples — retries, deep levels — and for primitive entry points whose
+//                    active sets need not be distinct).
+//
+// Terms of a row are combined exactly as the reference does: ascending feature order, the first
+// term assigns, later terms add, all in double, one rounding to float; an empty row is 0.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.hpp"
+#include "dev_util.cuh"
+#include "kernels.hpp"
+
+namespace sofg {
+namespace dev {
+
+// Column-major X[f*ld + s] -> row-major XR[s*ldr + f] (32x32 smem tiles).
+__global__ void __launch_bounds__(256) k_transpose_rows(const float* __restrict__ X, uint64_t ld,
+                                                        uint64_t n, uint64_t d,
+                                                        float* __restrict__ XR, uint64_t ldr) {
+  __shared__ float tile[32][33];
+  const uint64_t s0 = uint64_t(blockIdx.x) * 32, f0 = uint64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8) {
+    const uint64_t f = f0 + i, s = s0 + tx;
+    tile[i][tx] = (f < d && s < n) ? X[f * ld + s] : 0.f;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const uint64_t s = s0 + i, f = f0 + tx;
+    if (s < n && f < ldr) XR[s * ldr + f] = tile[tx][i];
+  }
+}
+
+// inv[s*B + tree(p)] = p for every position p of the root level buffer (tree b owns
+// [off[b], off[b+1])). inv is pre-filled with ~0.
+__global__ void k_inv_init(const uint32_t* __restrict__ idx, const uint64_t* __restrict__ off,
+                           uint32_t B, uint32_t* __restrict__ inv) {
+  const uint32_t b = blockIdx.y;
+  const uint64_t p0 = off[b], p1 = off[b + 1];
+  for (uint64_t p = p0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < p1;
+       p += uint64_t(gridDim.x) * blockDim.x)
+    inv[uint64_t(idx[p]) * B + b] = uint32_t(p);
+}
+
+// pos_node[p] = wave node owning level position p (pre-filled with ~0 for closed nodes).
+__global__ void __launch_bounds__(256) k_pos_fill(const NodeIn* __restrict__ nodes,
+                                                  const Tile* __restrict__ tiles,
+                                                  uint32_t* __restrict__ pos_node) {
+  const Tile tl = tiles[blockIdx.x];
+  const uint32_t begin = nodes[tl.node].begin + tl.start;
+  for (uint32_t l = threadIdx.x; l < tl.len; l += blockDim.x) pos_node[begin + l] = tl.node;
+}
+
+// +-x of term t (bit 0 = negative weight) as a double; negation is exact, so this equals the
+// reference's weight * double(x) for weights +-1.
+__device__ __forceinline__ double signed_term(const float* xs, uint32_t t) {
+  return double(__uint_as_float(__float_as_uint(xs[t >> 1]) ^ (t << 31)));
+}
+
+// Combine the terms [q0, q1) of one row for a sample whose features are in `xs` (shared memory).
+__device__ __forceinline__ float project_from(const float* xs, const uint32_t* tm, uint32_t q0,
+                                              uint32_t q1) {
+  if (q1 <= q0) return 0.f;
+  double acc = signed_term(xs, tm[q0]);
+  for (uint32_t q = q0 + 1; q < q1; ++q) acc = __dadd_rn(acc, signed_term(xs, tm[q]));
+  return __double2float_rn(acc);
+}
+
+// ------------------------------------------------------------------------------------------
+// Augmented term lists for the sweep. A node's R rows are split into kQ contiguous row ranges
+// ("quarters"); each range gets its own list: the CSR terms of its rows in order, each entry
+// feature << 2 | last << 1 | negative (so entry & ~3 is the feature's byte offset in a row of XR),
+// with one dummy entry (feature d: the zero pad column of XR) for every empty row, so walking a
+// list completes its rows in order. Each list starts 16-byte aligned and is followed by neutral
+// pad entries (zero column, no row end). Entries are u16 when d < 8192, else u32.
+// Node i's block starts at aug_off(i); sub-list offsets (entries, relative) are in qoff[i].
+// ------------------------------------------------------------------------------------------
+constexpr int kQ = 4;
+
+template <typename E>
+__device__ __forceinline__ uint64_t aug_off(uint32_t term_off, uint32_t i, uint32_t R) {
+  constexpr uint64_t A = 16 / sizeof(E);
+  return (uint64_t(term_off) + uint64_t(i) * (R + 3 * kQ * A) + A - 1) & ~(A - 1);
+}
+__host__ __device__ __forceinline__ uint32_t q_row(uint32_t R, uint32_t c) { return R * c / kQ; }
+
+template <typename E>
+__global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ nodes, int n_nodes,
+                                                   const uint32_t* __restrict__ terms,
+                                                   const uint32_t* __restrict__ row_ptr, uint32_t R,
+                                                   uint32_t d, E* __restrict__ aug,
+                                                   uint4* __restrict__ qoff) {
+  constexpr uint32_t A = 16 / sizeof(E);
+  extern __shared__ uint32_t s_empty_pre[];  // [4 warps][R + 1]: empty rows before row r
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int node = int(blockIdx.x) * 4 + w;
+  if (node >= n_nodes) return;
+  uint32_t* epre = s_empty_pre + size_t(w) * (R + 1);
+  const NodeIn nd = nodes[node];
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  const uint32_t* tm = terms + nd.term_off;
+  E* out = aug + aug_off<E>(nd.term_off, uint32_t(node), R);
+  uint32_t carry = 0;
+  for (uint32_t r0 = 0; r0 < R; r0 += 32) {
+    const uint32_t r = r0 + uint32_t(lane);
+    const bool empty = r < R && __ldg(rp + r + 1) == __ldg(rp + r);
+    const unsigned m = __ballot_sync(0xffffffffu, empty);
+    if (r < R) epre[r] = carry + __popc(m & ((1u << lane) - 1u));
+    carry += __popc(m);
+  }
+  if (lane == 0) epre[R] = carry;
+  __syncwarp();
+  // sub-list offsets: aligned, each followed by A neutral pads
+  uint32_t off[kQ + 1];
+  off[0] = 0;
+#pragma unroll
+  for (int c = 0; c < kQ; ++c) {
+    const uint32_t ra = q_row(R, uint32_t(c)), rb = q_row(R, uint32_t(c + 1));
+    const uint32_t len = (__ldg(rp + rb) - __ldg(rp + ra)) + (epre[rb] - epre[ra]);
+    off[c + 1] = (off[c] + len + A + A - 1) & ~(A - 1);
+  }
+  if (lane == 0) qoff[node] = make_uint4(off[0], off[1], off[2], off[3]);
+  for (uint32_t r = uint32_t(lane); r < R; r += 32) {
+    const uint32_t c = r * kQ / R;  // quarter of row r: largest c with R*c/kQ <= r
+    uint32_t cc = 0;
+#pragma unroll
+    for (int k = 1; k < kQ; ++k)
+      if (q_row(R, uint32_t(k)) <= r) cc = uint32_t(k);
+    (void)c;
+    const uint32_t ra = q_row(R, cc);
+    uint32_t base = 0;
+#pragma unroll
+    for (int k = 0; k < kQ; ++k)
+      if (uint32_t(k) == cc) base = off[k];
+    const uint32_t q0 = __ldg(rp + r), q1 = __ldg(rp + r + 1);
+    const uint32_t pos = base + (q0 - __ldg(rp + ra)) + (epre[r] - epre[ra]);
+    if (q1 == q0) {
+      out[pos] = E((d << 2) | 2u);
+    } else {
+      for (uint32_t q = q0; q < q1; ++q) {
+        const uint32_t t = __ldg(tm + q);
+        out[pos + (q - q0)] = E(((t >> 1) << 2) | (q + 1 == q1 ? 2u : 0u) | (t & 1u));
+      }
+    }
+  }
+  // neutral pads after each sub-list
+#pragma unroll
+  for (int c = 0; c < kQ; ++c) {
+    const uint32_t ra = q_row(R, uint32_t(c)), rb = q_row(R, uint32_t(c + 1));
+    const uint32_t len = (__ldg(rp + rb) - __ldg(rp + ra)) + (epre[rb] - epre[ra]);
+    for (uint32_t i = uint32_t(lane); i < A; i += 32) out[off[c] + len + i] = E(d << 2);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Sample-major sweep. A CTA takes K consecutive samples at a time: their rows stream into shared
+// memory (cp.async; one coalesced read of each row per level) and the inverse map lists every
+// open node of the wave that holds one of them. Then kQ lanes per (node, sample) pair each walk
+// one sub-list in order — 16-byte loads with four in flight, the entries' feature reads as
+// independent shared-memory loads, one double accumulator per row — and park their rows in a
+// per-lane staging slot, written to V at the end with vector stores.
+// ------------------------------------------------------------------------------------------
+constexpr int kSweepThreads = 512;
+
+struct Pair {
+  uint32_t node, j, k, pad;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = uint32_t(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+template <typename E>
+__device__ __forceinline__ void unpack16(const uint4& v, uint32_t (&e)[16 / sizeof(E)]) {
+  if constexpr (sizeof(E) == 2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      e[2 * i] = w[i] & 0xffffu;
+      e[2 * i + 1] = w[i] >> 16;
+    }
+  } else {
+    e[0] = v.x;
+    e[1] = v.y;
+    e[2] = v.z;
+    e[3] = v.w;
+  }
+}
+
+__host__ __device__ __forceinline__ uint32_t sweep_out_pitch(uint32_t R) {
+  return ((R + kQ - 1) / kQ + 3u) / 4u * 4u + 4u;  // floats per lane (16B multiple, bank shift)
+}
+
+// smem: xs[K][ldr] | pairs[K*B] | out[kSweepThreads][pitch]
+template <typename E>
+__global__ void __launch_bounds__(kSweepThreads) k_row_sweep(
+    const float* __restrict__ XR, uint64_t ldr, uint32_t N, uint32_t K,
+    const uint32_t* __restrict__ inv, uint32_t B, const uint32_t* __restrict__ pos_node,
+    const NodeIn* __restrict__ nodes, const uint64_t* __restrict__ vbase,
+    const E* __restrict__ aug, const uint4* __restrict__ qoff, uint32_t R,
+    float* __restrict__ V) {
+  constexpr int EPV = 16 / sizeof(E);  // entries per 16-byte load
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* xs = reinterpret_cast<float*>(smem_raw);
+  Pair* pairs = reinterpret_cast<Pair*>(smem_raw + size_t(K) * ldr * 4);
+  const uint32_t pitch = sweep_out_pitch(R);
+  float* sout = reinterpret_cast<float*>(pairs + size_t(K) * B) + size_t(threadIdx.x) * pitch;
+  __shared__ uint32_t s_cnt;
+  const int lane = threadIdx.x & 31;
+  const uint32_t Rp = vpitch(R);
+  const uint32_t nvec = uint32_t(ldr / 4);
+  const uint32_t KB = K * B;
+  const uint32_t c = threadIdx.x % kQ;  // my sub-list
+  const uint32_t ra = q_row(R, c), rb = q_row(R, c + 1);
+  constexpr uint32_t kPairsPerRound = kSweepThreads / kQ;
+
+  for (uint32_t s0 = blockIdx.x * K; s0 < N; s0 += gridDim.x * K) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    // ---- rows of the K samples -> shared memory (asynchronous)
+    const uint32_t ks = min(K, N - s0);
+    {
+      const float4* src = reinterpret_cast<const float4*>(XR + uint64_t(s0) * ldr);
+      float4* dst = reinterpret_cast<float4*>(xs);
+      for (uint32_t v = threadIdx.x; v < ks * nvec; v += kSweepThreads) cp_async16(dst + v, src + v);
+    }
+    // ---- (node, j) pairs of the K samples: inv -> level position -> wave node
+    for (uint32_t e0 = 0; e0 < KB; e0 += kSweepThreads) {
+      const uint32_t e = e0 + threadIdx.x;
+      const uint32_t k = e / B;
+      uint32_t node = ~0u, p = ~0u;
+      if (e < KB && k < ks) {
+        p = __ldcs(inv + uint64_t(s0) * B + e);
+        if (p != ~0u) node = __ldg(pos_node + p);
+      }
+      const bool act = node != ~0u;
+      const unsigned m = __ballot_sync(0xffffffffu, act);
+      uint32_t base = 0;
+      if (lane == 0 && m) base = atomicAdd(&s_cnt, uint32_t(__popc(m)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (act) pairs[base + __popc(m & ((1u << lane) - 1u))] = Pair{node, p - __ldg(&nodes[node].begin), k, 0u};
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const uint32_t cnt = s_cnt;
+    const uint32_t rounds = (cnt + kPairsPerRound - 1) / kPairsPerRound;  // uniform
+    for (uint32_t rd = 0; rd < rounds; ++rd) {
+      const uint32_t pi = rd * kPairsPerRound + threadIdx.x / kQ;
+      uint32_t r = rb;  // rows done (this lane's range [ra, rb))
+      const uint4* a4 = reinterpret_cast<const uint4*>(aug);
+      const char* xb = reinterpret_cast<const char*>(xs);
+      float* vout = V;
+      if (pi < cnt) {
+        const Pair pr = pairs[pi];
+        const uint4 qo = __ldg(qoff + pr.node);
+        const uint32_t so = c == 0 ? qo.x : c == 1 ? qo.y : c == 2 ? qo.z : qo.w;
+        a4 = reinterpret_cast<const uint4*>(aug + aug_off<E>(__ldg(&nodes[pr.node].term_off), pr.node, R) + so);
+        xb = reinterpret_cast<const char*>(xs + size_t(pr.k) * ldr);
+        vout = V + __ldg(vbase + pr.node) + uint64_t(pr.j) * Rp;
+        r = ra;
+      }
+      const uint32_t out_base = uint32_t(__cvta_generic_to_shared(sout)) - ra * 4u;
+      double acc = 0.0;
+      bool first = true;
+      // four 16-byte loads in flight (sub-lists are followed by >= 64 readable bytes)
+      uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0, q2 = q0, q3 = q0;
+      if (r < rb) {
+        q0 = __ldg(a4);
+        q1 = __ldg(a4 + 1);
+        q2 = __ldg(a4 + 2);
+        q3 = __ldg(a4 + 3);
+      }
+      for (uint32_t it = 0; __any_sync(0xffffffffu, r < rb); ++it) {
+        if (r < rb) {
+          uint32_t e[EPV];
+          unpack16<E>(q0, e);
+          q0 = q1;
+          q1 = q2;
+          q2 = q3;
+          q3 = __ldg(a4 + it + 4);
+          uint32_t xv[EPV];
+#pragma unroll
+          for (int u = 0; u < EPV; ++u) xv[u] = *reinterpret_cast<const uint32_t*>(xb + (e[u] & ~3u));
+          // no per-entry guard: entries past the sub-list are neutral pads (no row end)
+#pragma unroll
+          for (int u = 0; u < EPV; ++u) {
+            const double dx = double(__uint_as_float(xv[u] ^ (e[u] << 31)));
+            const double sum = __dadd_rn(acc, dx);
+            acc = first ? dx : sum;
+            first = (e[u] & 2u) != 0u;
+            if (first) {
+              const float v = __double2float_rn(acc);
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(out_base + r * 4u), "f"(v) : "memory");
+              ++r;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (pi < cnt) {  // rows [ra, rb) of the pair -> V
+        if (((ra | Rp) & 3u) == 0u) {
+          const uint32_t n4 = (rb - ra) / 4;
+          for (uint32_t i = 0; i < n4; ++i)
+            reinterpret_cast<float4*>(vout + ra)[i] = reinterpret_cast<const float4*>(sout)[i];
+          for (uint32_t rr = ra + 4 * n4; rr < rb; ++rr) vout[rr] = sout[rr - ra];
+        } else {
+          for (uint32_t rr = ra; rr < rb; ++rr) vout[rr] = sout[rr - ra];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Gather producer: a CTA takes one partition tile (<= kTileElems samples of one node); each warp
+// handles 32 samples at a time, lane = sample. The node's CSR is staged in shared memory; each
+// lane walks the terms in order with 8 independent gathers in flight and closes rows at their
+// row_ptr boundaries (uniform across the warp). Rows are staged per warp as [32][Rp] and written
+// out with coalesced stores.
+constexpr int kGatherWarps = 8;
+__global__ void __launch_bounds__(256) k_project_gather(
+    const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles,
+    const uint64_t* __restrict__ vbase, const uint32_t* __restrict__ terms,
+    const uint32_t* __restrict__ row_ptr, uint32_t R, const uint32_t* __restrict__ idx,
+    const float* __restrict__ X, uint64_t ld, float* __restrict__ V) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t Rp = vpitch(R);
+  const Tile tl = tiles[blockIdx.x];
+  const NodeIn nd = nodes[tl.node];
+  const uint32_t* rpg = row_ptr + size_t(tl.node) * (R + 1);
+  const uint32_t z = __ldg(rpg + R) - __ldg(rpg);
+  float* stg = reinterpret_cast<float*>(smem_raw) + size_t(w) * 32 * Rp;
+  uint32_t* s_rp = reinterpret_cast<uint32_t*>(smem_raw + size_t(kGatherWarps) * 32 * Rp * 4);
+  uint32_t* s_tm = s_rp + R + 1;
+  for (uint32_t r = threadIdx.x; r <= R; r += blockDim.x) s_rp[r] = __ldg(rpg + r);
+  for (uint32_t q = threadIdx.x; q < z; q += blockDim.x) s_tm[q] = __ldg(terms + nd.term_off + q);
+  __syncthreads();
+  float* Vn = V + vbase[tl.node];
+  for (uint32_t c0 = uint32_t(w) * 32; c0 < tl.len; c0 += 32 * kGatherWarps) {
+    const uint32_t jl = c0 + uint32_t(lane);
+    const bool ok = jl < tl.len;
+    const float* xcol = X + (ok ? idx[nd.begin + tl.start + jl] : idx[nd.begin + tl.start]);
+    uint32_t r = 0;
+    while (r < R && s_rp[r + 1] == s_rp[r]) stg[size_t(lane) * Rp + r++] = 0.f;  // leading empty rows
+    uint32_t rend = r < R ? s_rp[r + 1] : ~0u;
+    double acc = 0.0;
+    bool first = true;
+    for (uint32_t q0 = 0; q0 < z; q0 += 8) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t q = q0 + uint32_t(u);
+        x[u] = q < z ? gather(xcol + uint64_t(s_tm[q] >> 1) * ld) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t q = q0 + uint32_t(u);
+        if (q < z) {
+          const double dx = double(__uint_as_float(__float_as_uint(x[u]) ^ (s_tm[q] << 31)));
+          acc = first ? dx : __dadd_rn(acc, dx);
+          first = false;
+          if (q + 1 == rend) {  // row r complete; following empty rows are zero
+            stg[size_t(lane) * Rp + r] = __double2float_rn(acc);
+            first = true;
+            ++r;
+            while (r < R && s_rp[r + 1] == s_rp[r]) stg[size_t(lane) * Rp + r++] = 0.f;
+            rend = r < R ? s_rp[r + 1] : ~0u;
+          }
+        }
+      }
+    }
+    for (; r < R; ++r) stg[size_t(lane) * Rp + r] = 0.f;  // (only when z == 0)
+    __syncwarp();
+    const uint32_t cnt = min(32u, tl.len - c0);
+    float* dstv = Vn + uint64_t(tl.start + c0) * Rp;
+    for (uint32_t i = uint32_t(lane); i < cnt * Rp; i += 32) dstv[i] = stg[i];
+    __syncwarp();
+  }
+}
+
+}  // namespace dev
+
+cudaError_t launch_transpose_rows(const float* X, uint64_t ld, uint64_t n, uint64_t d, float* XR,
+                                  uint64_t ldr, cudaStream_t st) {
+  const uint64_t gx = (n + 31) / 32, gy = (ldr + 31) / 32;
+  if (gy > 65535) return cudaErrorInvalidValue;
+  for (uint64_t x0 = 0; x0 < gx; x0 += 1u << 30) {
+    const unsigned bx = unsigned(std::min<uint64_t>(gx - x0, 1u << 30));
+    dev::k_transpose_rows<<<dim3(bx, unsigned(gy)), 256, 0, st>>>(X + x0 * 32, ld, n - x0 * 32, d,
+                                                                   XR + x0 * 32 * ldr, ldr);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_inv_init(const uint32_t* idx, const uint64_t* off, uint32_t B, uint64_t n_samples,
+                            uint64_t max_per_tree, uint32_t* inv, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(inv, 0xff, 4 * n_samples * B, st);
+  if (e != cudaSuccess || B == 0) return e;
+  const unsigned gx = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((max_per_tree + 255) / 256, 1024)));
+  dev::k_inv_init<<<dim3(gx, B), 256, 0, st>>>(idx, off, B, inv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pos_fill(const NodeIn* nodes, const Tile* tiles, int n_tiles, uint64_t total,
+                            uint32_t* pos_node, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(pos_node, 0xff, 4 * total, st);
+  if (e != cudaSuccess || n_tiles == 0) return e;
+  dev::k_pos_fill<<<n_tiles, 256, 0, st>>>(nodes, tiles, pos_node);
+  return cudaGetLastError();
+}
+
+bool aug_narrow(uint32_t d) { return d < 8192; }
+
+size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d) {
+  const size_t es = aug_narrow(d) ? 2 : 4;
+  return (size_t(total_terms) + size_t(n_nodes) * (R + 3 * dev::kQ * (16 / es)) + 256) * es;
+}
+
+cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
+                             const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
+                             uint4* qoff, cudaStream_t st) {
+  if (n_nodes == 0) return cudaSuccess;
+  const size_t smem = size_t(4) * (R + 1) * 4;
+  if (aug_narrow(d))
+    dev::k_aug_build<uint16_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint16_t*>(aug), qoff);
+  else
+    dev::k_aug_build<uint32_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint32_t*>(aug), qoff);
+  return cudaGetLastError();
+}
+
+static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
+  return size_t(K) * ldr * 4 + size_t(K) * B * sizeof(dev::Pair) +
+         size_t(dev::kSweepThreads) * dev::sweep_out_pitch(R) * 4;
+}
+
+// Samples per CTA iteration: enough (node, sample) pairs to fill the CTA's lanes (a sample sits
+// in ~63% of the batch's trees), within shared memory.
+static uint32_t sweep_k(uint64_t ldr, uint32_t B, uint32_t R) {
+  const uint32_t want = std::max<uint32_t>(1, (dev::kSweepThreads / dev::kQ + (B * 5 / 8) - 1) / std::max<uint32_t>(1, B * 5 / 8));
+  uint32_t K = std::min<uint32_t>(want, 8);
+  while (K > 1 && sweep_smem_k(ldr, B, R, K) > 110 * 1024) --K;
+  return K;
+}
+
+size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R) {
+  return sweep_smem_k(ldr, B, R, sweep_k(ldr, B, R));
+}
+
+template <typename E>
+static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
+                                  uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
+                                  const uint64_t* vbase, const void* aug, const uint4* qoff,
+                                  uint32_t R, float* V, int n_sm, cudaStream_t st) {
+  const uint32_t K = sweep_k(ldr, B, R);
+  const size_t smem = sweep_smem_k(ldr, B, R, K);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(dev::k_row_sweep<E>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_row_sweep<E>, dev::kSweepThreads, smem);
+  const uint32_t groups = (N + K - 1) / K;
+  const unsigned grid = unsigned(std::max(1, std::min<int>(int(groups), n_sm * std::max(per_sm, 1))));
+  dev::k_row_sweep<E><<<grid, dev::kSweepThreads, smem, st>>>(
+      XR, ldr, N, K, inv, B, pos_node, nodes, vbase, static_cast<const E*>(aug), qoff, R, V);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_sweep(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
+                             uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
+                             const uint64_t* vbase, const void* aug, const uint4* qoff, uint32_t R,
+                             uint32_t d, float* V, int n_sm, cudaStream_t st) {
+  return aug_narrow(d) ? launch_sweep_t<uint16_t>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st)
+                       : launch_sweep_t<uint32_t>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st);
+}
+
+cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_tiles,
+                                  const uint64_t* vbase, const uint32_t* terms,
+                                  const uint32_t* row_ptr, uint32_t R, uint32_t zmax,
+                                  const uint32_t* idx, const float* X, uint64_t ld, float* V,
+                                  cudaStream_t st) {
+  if (n_tiles == 0) return cudaSuccess;
+  const size_t smem = size_t(dev::kGatherWarps) * 32 * vpitch(R) * 4 + size_t(R + 1 + zmax) * 4;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(dev::k_project_gather,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  dev::k_project_gather<<<n_tiles, 256, smem, st>>>(nodes, tiles, vbase, terms, row_ptr, R, idx, X,
+                                                   ld, V);
+  return cudaGetLastError();
+}
+
+}  // namespace sofg

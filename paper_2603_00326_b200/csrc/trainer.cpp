@@ -2,9 +2,11 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "host_rng.hpp"
+#include "kernels.hpp"
 
 namespace sofg {
 
@@ -153,6 +155,31 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     cuda_check(cudaMemcpyAsync(idx[0].p, hi, 4 * total, cudaMemcpyHostToDevice, eng.stream()), "H2D idx");
     cuda_check(cudaMemcpyAsync(lab[0].p, hl, total, cudaMemcpyHostToDevice, eng.stream()), "H2D lab");
   }
+  // Inverse map for the projection sweep (sweep.cu): needs each tree's samples to be distinct
+  // (bootstrap_sample returns a sorted set; explicit active sets are checked).
+  DevBuf<uint32_t> inv;
+  DevBuf<uint64_t> d_off;
+  bool use_inv = D.XR.p != nullptr;
+  for (size_t b = 0; b < B && use_inv; ++b) {
+    const std::vector<uint32_t>& r = roots[b];
+    bool inc = true;
+    for (size_t j = 1; j < r.size() && inc; ++j) inc = r[j - 1] < r[j];
+    if (!inc) {
+      std::vector<uint32_t> c(r);
+      std::sort(c.begin(), c.end());
+      use_inv = std::adjacent_find(c.begin(), c.end()) == c.end();
+    }
+  }
+  if (use_inv) {
+    uint64_t maxn = 0;
+    for (size_t b = 0; b < B; ++b) maxn = std::max<uint64_t>(maxn, roots[b].size());
+    d_off.exact(B + 1);
+    cuda_check(cudaMemcpyAsync(d_off.p, off.data(), 8 * (B + 1), cudaMemcpyHostToDevice, eng.stream()),
+               "H2D off");
+    inv.exact(D.n * B);
+    cuda_check(launch_inv_init(idx[0].p, d_off.p, uint32_t(B), D.n, maxn, inv.p, eng.stream()),
+               "inv_init");
+  }
 
   std::vector<std::vector<BNode>> trees(B);
   std::vector<std::vector<uint32_t>> pools(B);
@@ -186,6 +213,10 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   w.d = uint32_t(D.d);
   w.bins = uint32_t(P.bins);
   w.k = k;
+  w.inv = use_inv ? inv.p : nullptr;
+  w.B = uint32_t(B);
+  w.total = total;
+  if (const char* e = std::getenv("SOFG_PROJECT_MODE")) w.force_mode = std::atoi(e);
   eng.set_pool(&pool);
 
   auto count_open = [](const std::vector<std::vector<Open>>& v) {

@@ -1,0 +1,14 @@
+set -x
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+SOFG_PROJECT_MODE=1 timeout 600 python -m pytest tests -m gpu -x -q -k "forest or tree or golden" 2>&1 | tail -3
+SOFG_PROJECT_MODE=0 timeout 600 python -m pytest tests -m gpu -x -q -k "forest or tree or golden" 2>&1 | tail -3
+timeout 600 python bench.py --trees 20 --warmup 1 --steps 1 --no-cpu-baseline --no-e2e 2>&1 | tail -1 > gpurun_out/b20s.json
+timeout 900 python bench.py --trees 100 --warmup 1 --steps 1 --no-cpu-baseline --no-e2e 2>&1 | tail -1 > gpurun_out/b100s.json
+python - <<'PY'
+import json
+for f in ("gpurun_out/b20s.json","gpurun_out/b100s.json"):
+    try:
+        d=json.load(open(f)); r=d["roofline"]
+        print(f, round(d["value"],2), "ms/step", round(d["ms_per_step"]), r["phase_ms"], r["kernel_ms"])
+    except Exception as e: print(f, "ERR", e, open(f).read()[-2000:])
+PY
