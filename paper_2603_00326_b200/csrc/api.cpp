@@ -2,6 +2,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <thread>
 #include <memory>
 #include <string>
 
@@ -18,6 +20,12 @@ struct sofg_ctx {
   int pool_threads = 0;
   sofg::HostTimes times;
   int stats_mode = 0;
+  // second tree group in flight on the same GPU (own stream and host threads, shared table):
+  // while one group's host thread prepares a level, the other group's kernels run.
+  std::unique_ptr<sofg::WaveRunner> eng2;
+  std::unique_ptr<sofg::ThreadPool> pool1, pool2;
+  int pool1_threads = 0, pool2_threads = 0;
+  sofg::HostTimes times2;
 };
 
 struct sofg_forest {
@@ -72,6 +80,36 @@ sofg::ThreadPool& pool_for(sofg_ctx* c, uint64_t n_workers) {
   }
   c->eng->set_pool(c->pool.get());
   return *c->pool;
+}
+
+sofg::WaveRunner& runner2(sofg_ctx* c) {
+  if (!c->eng2) {
+    c->eng2.reset(new sofg::WaveRunner(c->eng->device(), c->eng->shared_data()));
+    c->eng2->collect_stats = c->eng->collect_stats;
+    c->eng2->sector_accounting = c->eng->sector_accounting;
+  }
+  return *c->eng2;
+}
+
+sofg::ThreadPool& pool_n(std::unique_ptr<sofg::ThreadPool>& p, int& have, int want) {
+  want = std::max(1, want);
+  if (!p || have != want) {
+    p.reset(new sofg::ThreadPool(want));
+    have = want;
+  }
+  return *p;
+}
+
+void append_forest(sofg::FlatForest& dst, const sofg::FlatForest& src) {
+  const int64_t nb = int64_t(dst.left.size()), qb = int64_t(dst.feat.size());
+  dst.left.insert(dst.left.end(), src.left.begin(), src.left.end());
+  dst.right.insert(dst.right.end(), src.right.begin(), src.right.end());
+  dst.pred.insert(dst.pred.end(), src.pred.begin(), src.pred.end());
+  dst.thr.insert(dst.thr.end(), src.thr.begin(), src.thr.end());
+  dst.feat.insert(dst.feat.end(), src.feat.begin(), src.feat.end());
+  dst.weight.insert(dst.weight.end(), src.weight.begin(), src.weight.end());
+  for (size_t i = 1; i < src.tree_off.size(); ++i) dst.tree_off.push_back(src.tree_off[i] + nb);
+  for (size_t i = 1; i < src.term_off.size(); ++i) dst.term_off.push_back(src.term_off[i] + qb);
 }
 
 // Dataset staging into HBM: ld = n rounded up to 32 samples (128 B column alignment).
@@ -294,7 +332,44 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
       });
       c->times.ms_bootstrap +=
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tbs).count();
-      sofg::grow_trees(*c->eng, P, pool, roots, seeds, 0, res->f, c->times);
+      // Two tree groups in flight (SOFG_GROUPS=1 disables): group 2 runs on its own stream and
+      // host threads so each group's host-side level work overlaps the other's kernels.
+      const char* ge = std::getenv("SOFG_GROUPS");
+      const int groups = ge ? std::max(1, std::atoi(ge)) : 2;
+      if (groups >= 2 && B >= 16 && pool.size() >= 2) {
+        const size_t h = B / 2;
+        std::vector<std::vector<uint32_t>> r1(std::make_move_iterator(roots.begin()),
+                                              std::make_move_iterator(roots.begin() + long(h)));
+        std::vector<std::vector<uint32_t>> r2(std::make_move_iterator(roots.begin() + long(h)),
+                                              std::make_move_iterator(roots.end()));
+        std::vector<uint64_t> s1(seeds.begin(), seeds.begin() + long(h)), s2(seeds.begin() + long(h), seeds.end());
+        const int t1n = std::max(1, pool.size() / 2);
+        sofg::WaveRunner& e2 = runner2(c);
+        sofg::ThreadPool& p1 = pool_n(c->pool1, c->pool1_threads, t1n);
+        sofg::ThreadPool& p2 = pool_n(c->pool2, c->pool2_threads, std::max(1, pool.size() - t1n));
+        sofg::FlatForest f1, f2;
+        std::exception_ptr err2;
+        std::thread th([&] {
+          try {
+            sofg::grow_trees(e2, P, p2, r2, s2, 0, f2, c->times2);
+          } catch (...) {
+            err2 = std::current_exception();
+          }
+        });
+        try {
+          sofg::grow_trees(*c->eng, P, p1, r1, s1, 0, f1, c->times);
+        } catch (...) {
+          th.join();
+          throw;
+        }
+        th.join();
+        if (err2) std::rethrow_exception(err2);
+        append_forest(res->f, f1);
+        append_forest(res->f, f2);
+        c->eng->set_pool(&pool);
+      } else {
+        sofg::grow_trees(*c->eng, P, pool, roots, seeds, 0, res->f, c->times);
+      }
     }
     *out = guard_res.release();
   });
@@ -594,8 +669,11 @@ int sofg_set_stats(sofg_ctx* c, int enable) {
   return guard([&] {
     require_ctx(c);
     c->stats_mode = enable;
-    c->eng->collect_stats = enable != 0;
-    c->eng->sector_accounting = enable >= 2;
+    for (sofg::WaveRunner* e : {c->eng.get(), c->eng2.get()}) {
+      if (!e) continue;
+      e->collect_stats = enable != 0;
+      e->sector_accounting = enable >= 2;
+    }
   });
 }
 
@@ -603,7 +681,8 @@ int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
   return guard([&] {
     require_ctx(c);
     std::memset(o, 0, sizeof(*o));
-    const sofg::WaveStats& s = c->eng->stats;
+    sofg::WaveStats s = c->eng->stats;  // both tree groups (kernel times of concurrent streams add)
+    if (c->eng2) s.merge(c->eng2->stats);
     o->ms_sample = s.ms_sample;
     o->ms_hist_rng = s.ms_hist_rng;
     o->ms_hist_count = s.ms_hist_count;
@@ -635,12 +714,21 @@ int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
   });
 }
 
-int sofg_stats_kernels(sofg_ctx* c) { return c && c->eng ? int(c->eng->stats.per_kernel.size()) : 0; }
+namespace {
+thread_local sofg::WaveStats g_merged;
+const sofg::WaveStats& merged_stats(sofg_ctx* c) {
+  g_merged = c->eng->stats;
+  if (c->eng2) g_merged.merge(c->eng2->stats);
+  return g_merged;
+}
+}  // namespace
+
+int sofg_stats_kernels(sofg_ctx* c) { return c && c->eng ? int(merged_stats(c).per_kernel.size()) : 0; }
 
 int sofg_stats_kernel(sofg_ctx* c, int i, const char** name, double* ms, uint64_t* launches) {
   return guard([&] {
     require_ctx(c);
-    const auto& v = c->eng->stats.per_kernel;
+    const auto& v = merged_stats(c).per_kernel;
     if (i < 0 || size_t(i) >= v.size()) throw std::out_of_range("kernel stat index");
     *name = v[size_t(i)].name;
     *ms = v[size_t(i)].ms;
@@ -652,7 +740,9 @@ int sofg_reset_stats(sofg_ctx* c) {
   return guard([&] {
     require_ctx(c);
     c->eng->stats = sofg::WaveStats{};
+    if (c->eng2) c->eng2->stats = sofg::WaveStats{};
     c->times = sofg::HostTimes{};
+    c->times2 = sofg::HostTimes{};
   });
 }
 

@@ -9,7 +9,8 @@
 
 namespace sofg {
 
-WaveRunner::WaveRunner(int device) : device_(device) {
+WaveRunner::WaveRunner(int device, std::shared_ptr<DeviceData> data)
+    : device_(device), data_(data ? std::move(data) : std::make_shared<DeviceData>()) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   // The split search is a scattered 4-byte gather: ask L2 to fetch single 32-byte sectors from
   // HBM instead of larger granules (override with SOFG_L2_FETCH=0..128 for experiments).
@@ -62,7 +63,7 @@ int pow2_at_least(int x, int lo) {
 
 void WaveRunner::submit(const WaveSpec& w) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-  const DeviceData& D = data_;
+  const DeviceData& D = *data_;
   const int N = int(w.nodes.size());
   pend_n_ = N;
   if (N == 0) return;

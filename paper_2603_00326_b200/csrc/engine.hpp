@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -127,6 +128,25 @@ struct WaveStats {
   uint64_t hist_count_launches = 0, exact_launches = 0;
   uint64_t sweep_waves = 0, gather_waves = 0;
   std::vector<KernelTime> per_kernel;  // CUDA-event time per launch site (stats mode)
+  void merge(const WaveStats& o) {
+    ms_sample += o.ms_sample; ms_hist_rng += o.ms_hist_rng; ms_hist_count += o.ms_hist_count;
+    ms_exact += o.ms_exact; ms_partition += o.ms_partition; ms_total += o.ms_total;
+    waves += o.waves; nodes += o.nodes; hist_nodes += o.hist_nodes; exact_nodes += o.exact_nodes;
+    launches += o.launches; hist_strict_bytes += o.hist_strict_bytes;
+    hist_sector_bytes += o.hist_sector_bytes; exact_strict_bytes += o.exact_strict_bytes;
+    exact_sector_bytes += o.exact_sector_bytes; hist_count_launches += o.hist_count_launches;
+    exact_launches += o.exact_launches; sweep_waves += o.sweep_waves; gather_waves += o.gather_waves;
+    for (const auto& k : o.per_kernel) {
+      bool found = false;
+      for (auto& m : per_kernel)
+        if (m.name == k.name) {
+          m.ms += k.ms;
+          m.launches += k.launches;
+          found = true;
+        }
+      if (!found) per_kernel.push_back(k);
+    }
+  }
   void add_kernel(const char* name, double ms) {
     for (auto& k : per_kernel)
       if (k.name == name) {
@@ -140,15 +160,18 @@ struct WaveStats {
 
 class WaveRunner {
  public:
-  explicit WaveRunner(int device);
+  // Runners created with a shared DeviceData train on the same resident table on their own stream
+  // (several tree groups in flight on one GPU).
+  explicit WaveRunner(int device, std::shared_ptr<DeviceData> data = nullptr);
   ~WaveRunner();
   WaveRunner(const WaveRunner&) = delete;
   WaveRunner& operator=(const WaveRunner&) = delete;
 
   cudaStream_t stream() const { return st_; }
   int device() const { return device_; }
-  DeviceData& data() { return data_; }
-  const DeviceData& data() const { return data_; }
+  DeviceData& data() { return *data_; }
+  const DeviceData& data() const { return *data_; }
+  std::shared_ptr<DeviceData> shared_data() const { return data_; }
 
   // Searches and partitions every node of `w`; res[i] receives node i's result.
   void run(const WaveSpec& w, std::vector<NodeRes>& res) {
@@ -171,6 +194,12 @@ class WaveRunner {
   bool collect_stats = false;   // CUDA-event timing per phase + sector accounting
   bool sector_accounting = false;
 
+  // Level state of grow_trees (kept across calls so no allocation synchronizes the device).
+  DevBuf<uint32_t> lvl_idx[2];
+  DevBuf<uint8_t> lvl_lab[2];
+  DevBuf<uint32_t> inv;
+  DevBuf<uint64_t> tree_off;
+
  private:
   int device_;
   ThreadPool* pool_ = nullptr;
@@ -182,7 +211,7 @@ class WaveRunner {
   const char* mk_name_[kMaxMarks]{};
   int n_marks_ = 0;
   void mark(const char* name);
-  DeviceData data_;
+  std::shared_ptr<DeviceData> data_;
 
   // packed host->device inputs
   PinnedBuf<unsigned char> h_in_;

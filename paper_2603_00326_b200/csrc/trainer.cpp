@@ -124,6 +124,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
                 const std::vector<uint64_t>& root_seeds, uint32_t root_depth, FlatForest& out,
                 HostTimes& times) {
   const auto t_start = Clock::now();
+  cuda_check(cudaSetDevice(eng.device()), "cudaSetDevice");
   DeviceData& D = eng.data();
   const int k = D.k;
   const size_t B = roots.size();
@@ -138,11 +139,11 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   for (size_t b = 0; b < B; ++b) off[b + 1] = off[b] + roots[b].size();
   const uint64_t total = off[B];
   if (total >= (1ull << 32)) throw std::invalid_argument("batch exceeds 2^32 samples");
-  DevBuf<uint32_t> idx[2];
-  DevBuf<uint8_t> lab[2];
+  DevBuf<uint32_t>* idx = eng.lvl_idx;
+  DevBuf<uint8_t>* lab = eng.lvl_lab;
   for (int i = 0; i < 2; ++i) {
-    idx[i].exact(total);
-    lab[i].exact(total);
+    idx[i].ensure(total);
+    lab[i].ensure(total);
   }
   {
     unsigned char* stg = eng.staging.ensure(5 * total);
@@ -157,8 +158,8 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   }
   // Inverse map for the projection sweep (sweep.cu): needs each tree's samples to be distinct
   // (bootstrap_sample returns a sorted set; explicit active sets are checked).
-  DevBuf<uint32_t> inv;
-  DevBuf<uint64_t> d_off;
+  DevBuf<uint32_t>& inv = eng.inv;
+  DevBuf<uint64_t>& d_off = eng.tree_off;
   bool use_inv = D.XR.p != nullptr;
   for (size_t b = 0; b < B && use_inv; ++b) {
     const std::vector<uint32_t>& r = roots[b];
@@ -173,10 +174,10 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   if (use_inv) {
     uint64_t maxn = 0;
     for (size_t b = 0; b < B; ++b) maxn = std::max<uint64_t>(maxn, roots[b].size());
-    d_off.exact(B + 1);
+    d_off.ensure(B + 1);
     cuda_check(cudaMemcpyAsync(d_off.p, off.data(), 8 * (B + 1), cudaMemcpyHostToDevice, eng.stream()),
                "H2D off");
-    inv.exact(D.n * B);
+    inv.ensure(D.n * B);
     cuda_check(launch_inv_init(idx[0].p, d_off.p, uint32_t(B), D.n, maxn, inv.p, eng.stream()),
                "inv_init");
   }

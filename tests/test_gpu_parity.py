@@ -220,3 +220,32 @@ def test_predict_matches_oracle(gpu_ctx, oracle):
     lab, votes = gpu_ctx.predict(g, Xt.T.copy())
     assert np.array_equal(lab, olab)
     assert np.array_equal(votes, ovotes)
+
+
+@pytest.mark.parametrize("batch", [0, 7])
+def test_train_forest_two_groups_and_batches(gpu_ctx, oracle, batch):
+    """>= 16 trees per batch runs two tree groups concurrently (own streams, shared table);
+    batch_trees splits the forest into several batches. Trees must not depend on either."""
+    X, y = oracle.generate_trunk(4000, 24, 9)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=21, mode="dynamic", breakeven=256, seed=3, n_workers=4, batch_trees=batch)
+    g = gpu_ctx.train_forest(gc)
+    o = oracle.train_forest(X, y, 2, oc)
+    assert g.n_trees == 21
+    assert _forest_equal(g, o) == []
+
+
+def test_tree_range_shards_concatenate(gpu_ctx, oracle):
+    """tree_begin/tree_end blocks (the multi-GPU shards) reproduce the whole forest."""
+    from paper_2603_00326_b200.shard import concat_forests, shard_range
+
+    X, y = oracle.generate_trunk(3000, 16, 4)
+    gpu_ctx.upload(X, y, 2)
+    parts = []
+    for r in range(3):
+        b, e = shard_range(11, r, 3)
+        gc, _ = _cfg(n_trees=11, mode="dynamic", breakeven=300, seed=8, tree_begin=b, tree_end=e)
+        parts.append(gpu_ctx.train_forest(gc))
+    g = concat_forests(parts)
+    _, oc = _cfg(n_trees=11, mode="dynamic", breakeven=300, seed=8)
+    assert _forest_equal(g, oracle.train_forest(X, y, 2, oc)) == []
