@@ -2,9 +2,9 @@
 //
 //  k_hist_count   histogram splitter (reference build_histogram + best_split_histogram,
 //                 histogram.hpp:180-206, split.hpp:84-120). One CTA = 8 rows (one warp each) x
-//                 one chunk of the node's samples. Projected values are computed on the fly from
-//                 the column-major table (projection.hpp:86-108), binned by an upper_bound over
-//                 the row's boundaries in shared memory, and counted with warp-private shared
+//                 one chunk of the node's samples. Each lane reads a sample's 8 projected rows
+//                 (one 32-byte sector of V), bins each by an upper_bound over that row's
+//                 boundaries (implicit search tree in shared memory) and counts with shared
 //                 atomics. Single-chunk nodes scan in place; multi-chunk nodes merge into global
 //                 counters and the last CTA of the (node, row group) scans.
 //  k_hist_select  best row of a histogram node (split.hpp:259-263: strict '>', lowest row wins).
@@ -115,7 +115,7 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
   const uint32_t nl = __shfl_sync(0xffffffffu, first_nl, src);
   res.valid = 1;
   res.gain = gbest;
-  res.threshold = bnd[fb];
+  res.threshold = __ldg(bnd + fb);  // sorted boundaries (global)
   res.n_left = nl;
   return res;
 }
@@ -142,51 +142,66 @@ __global__ void __launch_bounds__(256) k_hist_count(
   uint8_t* lab_s = reinterpret_cast<uint8_t*>(bnd_s + size_t(8) * bpad);     // [chunk_cap]
   __shared__ int s_last;
 
-  const uint32_t r = wk.row0 + uint32_t(w);
+  const uint32_t r = wk.row0 + uint32_t(w);  // the row this warp scans at the end
   const bool row_ok = r < R;
   const uint32_t nb = row_ok ? nb_g[size_t(h) * R + r] : 0;
   uint32_t* my_cnt = cnt_s + size_t(w) * bpad * k;
-  float* my_bnd = bnd_s + size_t(w) * bpad;
-  for (int i = lane; i < bpad * k; i += 32) my_cnt[i] = 0;
   const float inf = __int_as_float(0x7f800000);
   const float* gb = bnd_g + (size_t(h) * R + (row_ok ? r : 0)) * (bins - 1);
-  for (int i = lane; i < bpad; i += 32) my_bnd[i] = i < int(nb) ? gb[i] : inf;
+  // Boundaries of the 8 rows as implicit search trees (Eytzinger order: node t >= 1 holds the
+  // sorted boundary ((2(t - 2^l) + 1) << (L-1-l)) - 1 at level l), padded with +inf. A search
+  // step at level l touches one of 2^l consecutive words, so the 32 lanes' probes spread over
+  // the banks instead of piling onto one (sorted-order probes are power-of-two strided).
+  int L = 0;
+  while ((1 << L) < bpad) ++L;
+  for (int i = threadIdx.x; i < 8 * bpad; i += blockDim.x) {
+    const int g = i / bpad, t = i % bpad;
+    float v = inf;
+    const uint32_t rg = wk.row0 + uint32_t(g);
+    if (t > 0 && rg < R) {
+      const int l = 31 - __clz(t);
+      const int sidx = ((2 * (t - (1 << l)) + 1) << (L - 1 - l)) - 1;
+      const uint32_t nbg = nb_g[size_t(h) * R + rg];
+      if (uint32_t(sidx) < nbg) v = bnd_g[(size_t(h) * R + rg) * (bins - 1) + sidx];
+    }
+    bnd_s[i] = v;
+  }
+  for (int i = threadIdx.x; i < 8 * bpad * k; i += blockDim.x) cnt_s[i] = 0;
   // stage the chunk's labels
   const uint8_t* lseg = lab + nd.begin + wk.start;
   for (uint32_t j = threadIdx.x; j < wk.len; j += blockDim.x) lab_s[j] = lseg[j];
   __syncthreads();
 
-  if (nb > 0) {
+  {
+    // Each lane takes one sample at a time and bins its 8 rows (one aligned 32-byte load).
     const uint32_t Rp = vpitch(R);
-    const float* Vn = G + gbase[wk.node] + r;  // row r of the node's V block (sweep.cu)
-    for (uint32_t j0 = 0; j0 < wk.len; j0 += 128) {
-      float v[4];
-      uint8_t y[4];
+    const float* Vn = G + gbase[wk.node] + wk.row0;  // rows row0.. of the node's V block
+    uint32_t live = 0;  // rows of this group with boundaries
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t j = j0 + uint32_t(u * 32 + lane);
-        if (j < wk.len) {
-          v[u] = __ldg(Vn + uint64_t(wk.start + j) * Rp);
-          y[u] = lab_s[j];
-        }
-      }
+    for (int g = 0; g < 8; ++g) {
+      const uint32_t rg = wk.row0 + uint32_t(g);
+      if (rg < R && nb_g[size_t(h) * R + rg] > 0) live |= 1u << g;
+    }
+    for (uint32_t j = uint32_t(threadIdx.x); j < wk.len; j += blockDim.x) {
+      const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(wk.start + j) * Rp);
+      const float4 a = __ldg(src), b = __ldg(src + 1);
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      const uint32_t y = lab_s[j];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t j = j0 + uint32_t(u * 32 + lane);
-        if (j < wk.len) {
-          int pos = 0;
-          for (int step = bpad >> 1; step > 0; step >>= 1)
-            if (my_bnd[pos + step - 1] <= v[u]) pos += step;
-          atomicAdd(&my_cnt[pos * k + y[u]], 1u);
-        }
+      for (int g = 0; g < 8; ++g) {
+        if (!(live & (1u << g))) continue;  // uniform
+        const float* tr = bnd_s + g * bpad;
+        int t = 1;
+        for (int l = 0; l < L; ++l) t = 2 * t + (tr[t] <= v[g] ? 1 : 0);
+        atomicAdd(&cnt_s[(size_t(g) * bpad + size_t(t - bpad)) * k + y], 1u);
       }
     }
   }
-  __syncwarp();
+  __syncthreads();
 
   if (wk.n_chunks == 1) {
     if (nb > 0) {
-      const RowRes rr = hist_row_scan(my_cnt, my_bnd, nb, k, bpad, nd.parent, xl, lane);
+      const RowRes rr = hist_row_scan(my_cnt, gb, nb, k, bpad, nd.parent, xl, lane);
       if (lane == 0) rowres[size_t(h) * R + r] = rr;
     } else if (row_ok && lane == 0) {
       RowRes z{};
@@ -216,7 +231,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
     const uint32_t* g = gcnt + (size_t(ms) * R + r) * size_t(bpad) * k;
     for (int i = lane; i < int(nb + 1) * k; i += 32) my_cnt[i] = __ldcg(g + i);
     __syncwarp();
-    const RowRes rr = hist_row_scan(my_cnt, my_bnd, nb, k, bpad, nd.parent, xl, lane);
+    const RowRes rr = hist_row_scan(my_cnt, gb, nb, k, bpad, nd.parent, xl, lane);
     if (lane == 0) rowres[size_t(h) * R + r] = rr;
   } else if (row_ok && lane == 0) {
     RowRes z{};
