@@ -10,8 +10,11 @@ the data path); rank r trains its own slice of the forest each step.
 value  device-timed trees/s over all ranks (CUDA events on the trainer's stream, max over ranks)
 e2e    the same through the C ABI with host buffers: every step uploads the 16.4 GB table from
        page-locked memory (sofg_upload_dataset), trains, and reads the forest back.
-roofline  the histogram counting kernel (the dominant one), sector-model gather bytes / its
-       event-timed duration, against MEASURED_PEAKS.json's HBM copy bandwidth.
+roofline  the dominant kernel, k_row_sweep (projection sweep): algorithmic bytes per launch (table
+       rows streamed + projected rows written + term lists read) over its CUDA-event time, against
+       MEASURED_PEAKS.json's HBM copy bandwidth, measured in one extra untimed profile step; traffic =
+       DRAM bytes per launch from the committed ncu launch list (profiles/). Also the SURVEY 8(d)
+       sector-model rate of the whole split finder.
 cpu_baseline  the reference itself (oracle/_ref, compiled from the reference headers) training
        trees of the same forest on this host's cores; those trees are also compared bit-for-bit
        with the GPU's.
@@ -52,6 +55,7 @@ def parse():
     p.add_argument("--cpu-trees", type=int, default=0, help="CPU baseline sample (0 = one per core)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-profile", action="store_true", help="skip the untimed per-kernel profile step")
     return p.parse_args()
 
 
@@ -114,6 +118,56 @@ def measured_peak():
             return float(json.load(fh)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def committed_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu launch list of this bench command
+    (profiles/r*_launches_bench_summary.json, written by scratch/launch_summary.py)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_launches_bench_summary.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as fh:
+            d = json.load(fh)
+        for k, v in d.items():
+            if k.startswith(kernel):
+                return v["dram_bytes_per_launch"], os.path.basename(files[-1])
+    except Exception:
+        pass
+    return None, None
+
+
+def roofline_block(st, args):
+    """Dominant kernel k_row_sweep: algorithmic bytes (table rows streamed + projected rows written +
+    term lists read, engine accounting) per launch over its CUDA-event time per launch."""
+    peak, peak_kind = measured_peak()
+    kern = st.get("kernels", {})
+    rs = kern.get("row_sweep", {"ms": 0.0, "launches": 0})
+    launches = max(1, int(st["sweep_waves"]))
+    avg_ms = rs["ms"] / launches if rs["launches"] else 0.0
+    alg = st["sweep_alg_bytes"] / launches
+    achieved = alg / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
+    traffic, src = committed_traffic("k_row_sweep")
+    split_ms = st["ms_waves_total"]
+    sector = st["hist_sector_bytes"] + st["exact_sector_bytes"]
+    strict = st["hist_strict_bytes"] + st["exact_strict_bytes"]
+    return {"bound": "hbm", "kernel": "k_row_sweep (projection: sample-major sweep of the row-major table)",
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "peak_kind": peak_kind, "traffic": traffic, "traffic_source": src,
+            "algorithmic_bytes_per_launch": alg, "avg_launch_ms": round(avg_ms, 3), "launches": launches,
+            "algorithmic_bytes_definition": "XR rows streamed (n*ldr*4) + V written (sum n_i*Rp*4) + "
+                                            "augmented term lists read, per sweep launch",
+            "split_finder": {"ms_per_step": round(split_ms, 2),
+                             "sector_model_GBps": round(sector / (split_ms / 1e3) / 1e9, 1) if split_ms else 0.0,
+                             "sector_model_frac": round(sector / (split_ms / 1e3) / 1e9 / peak, 4) if split_ms else 0.0,
+                             "strict_GBps": round(strict / (split_ms / 1e3) / 1e9, 1) if split_ms else 0.0,
+                             "note": "SURVEY 8(d) sector model: 32 B per gathered value of a per-node gather "
+                                     "implementation, over the whole split finder's device time"},
+            "phase_ms": {k: round(st[k], 2) for k in ("ms_sample", "ms_hist_rng", "ms_hist_count", "ms_exact",
+                                                      "ms_partition", "ms_waves_total", "ms_train_total")},
+            "kernel_ms": kern, "profile_step": "one extra untimed step, one tree group, CUDA events per launch site"}
 
 
 def cpu_reference_sample(X, y, n_trees, args, threads):
@@ -203,7 +257,7 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     T = args.trees
     per_step = T * world
-    total_trees = (args.warmup + args.steps + args.e2e_steps) * per_step
+    total_trees = (args.warmup + args.steps + args.e2e_steps + 1) * per_step
 
     def cfg_for(step):
         b = step * per_step + rank * T
@@ -227,8 +281,8 @@ def main():
         f = ctx.train_forest(cfg_for(s))
         if s == 0:
             first = f
-    # ---- timed region ------------------------------------------------------------------------
-    ctx.set_stats(2)
+    # ---- timed region (no per-kernel events, no accounting kernels) ---------------------------
+    ctx.set_stats(0)
     ctx.reset_stats()
     nodes = 0
     barrier()
@@ -244,29 +298,21 @@ def main():
     barrier()
     ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms)
-    st = ctx.stats()
-    ctx.set_stats(0)
+    gpu_launches = int(ctx.stats()["kernel_launches"])
     value = world * T * args.steps / (ms_max / 1000.0)
 
-    peak, peak_kind = measured_peak()
-    hist_ms = st["ms_hist_count"]
-    exact_ms = st["ms_exact"]
-    hist_launches = max(1, st["hist_count_launches"])
-    achieved = st["hist_sector_bytes"] / (hist_ms / 1000.0) / 1e9 if hist_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "kernel": "k_hist_count (projection + histogram, sector-model gathers)",
-                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "peak_kind": peak_kind, "traffic": None,
-                "algorithmic_bytes_per_launch": st["hist_sector_bytes"] / hist_launches,
-                "avg_launch_ms": hist_ms / hist_launches,
-                "strict_gbs": round(st["hist_strict_bytes"] / (hist_ms / 1000.0) / 1e9, 1) if hist_ms else 0.0,
-                "exact_kernel_gbs": round(st["exact_sector_bytes"] / (exact_ms / 1000.0) / 1e9, 1) if exact_ms else 0.0,
-                "phase_ms": {k: round(st[k], 2) for k in ("ms_sample", "ms_hist_rng", "ms_hist_count", "ms_exact",
-                                                          "ms_partition", "ms_waves_total", "ms_host_binomial",
-                                                          "ms_host_bootstrap", "ms_train_total", "ms_host_roots",
-                                                          "ms_host_prep", "ms_host_submit", "ms_host_spec",
-                                                          "ms_host_wait", "ms_host_post", "ms_host_final")},
-                "kernel_ms": st.get("kernels", {})}
-    gpu_launches = int(st["kernel_launches"])
+    # ---- profile step (untimed): one more step with CUDA events per launch site, one tree group
+    #      on one stream (so a kernel's event time is its own), and sector accounting ---------------
+    roofline = None
+    if not args.no_profile:
+        os.environ["SOFG_GROUPS"] = "1"
+        ctx.set_stats(2)
+        ctx.reset_stats()
+        ctx.train_forest(cfg_for(args.warmup + args.steps + args.e2e_steps))
+        st = ctx.stats()
+        ctx.set_stats(0)
+        os.environ.pop("SOFG_GROUPS", None)
+        roofline = roofline_block(st, args)
 
     # ---- end to end through the C ABI with host buffers ---------------------------------------
     e2e = None

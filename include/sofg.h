@@ -148,6 +148,10 @@ typedef struct sofg_stats {
   /* host-side phases of the level loop (ms) */
   double ms_host_roots, ms_host_prep, ms_host_submit, ms_host_spec, ms_host_wait, ms_host_post,
       ms_host_final;
+  /* projection stage: waves swept over the row-major table vs gathered, and the sweep's
+     algorithmic bytes (table rows streamed + projected rows written + term lists read) */
+  uint64_t sweep_waves, gather_waves;
+  double sweep_alg_bytes;
 } sofg_stats;
 /* enable: 1 = CUDA-event timing per phase (+ sector accounting when 2); 0 = off */
 int sofg_set_stats(sofg_ctx* ctx, int enable);

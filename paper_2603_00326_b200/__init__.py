@@ -54,7 +54,8 @@ class _Stats(C.Structure):
                                            "levels", "hist_count_launches", "exact_launches")] + \
                [(n, C.c_double) for n in ("hist_strict_bytes", "exact_strict_bytes", "hist_sector_bytes",
                                           "exact_sector_bytes", "ms_host_roots", "ms_host_prep", "ms_host_submit",
-                                          "ms_host_spec", "ms_host_wait", "ms_host_post", "ms_host_final")]
+                                          "ms_host_spec", "ms_host_wait", "ms_host_post", "ms_host_final")] + \
+               [(n, C.c_uint64) for n in ("sweep_waves", "gather_waves")] + [("sweep_alg_bytes", C.c_double)]
 
 
 _MODES = {"exact": 0, "histogram": 1, "dynamic": 2}

@@ -711,6 +711,9 @@ int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
     o->ms_host_wait = c->times.ms_wait;
     o->ms_host_post = c->times.ms_post;
     o->ms_host_final = c->times.ms_final;
+    o->sweep_waves = s.sweep_waves;
+    o->gather_waves = s.gather_waves;
+    o->sweep_alg_bytes = s.sweep_alg_bytes;
   });
 }
 

@@ -308,9 +308,12 @@ void WaveRunner::submit(const WaveSpec& w) {
   }
   if (sweep) {
     cuda_check(launch_pos_fill(d_nodes, d_tiles, int(n_tiles), w.total, d_pos_node, st_), "pos_fill");
-    void* d_aug = aug_.ensure(aug_bytes(total_terms, uint32_t(N), R, w.d));
+    const size_t abytes = aug_bytes(total_terms, uint32_t(N), R, w.d);
+    void* d_aug = aug_.ensure(abytes);
+    pend_sweep_bytes_ = double(D.n) * double(D.ldr) * 4.0 + double(g_total) * 4.0 + double(abytes);
     uint4* d_qoff = qoff_.ensure(size_t(N));
     cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, d_qoff, st_), "aug_build");
+    mark("sweep_prep");
     cuda_check(launch_row_sweep(D.XR.p, D.ldr, uint32_t(D.n), w.inv, w.B, d_pos_node, d_nodes,
                                 d_gbase, d_aug, d_qoff, R, w.d, d_G, n_sm_, st_),
                "row_sweep");
@@ -397,6 +400,7 @@ void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
   stats.launches += uint64_t(launches);
   if (nh) stats.hist_count_launches++;
   (pend_sweep_ ? stats.sweep_waves : stats.gather_waves)++;
+  if (pend_sweep_) stats.sweep_alg_bytes += pend_sweep_bytes_;
   if (pend_exact_) stats.exact_launches++;
   if (timing) {
     float t[5];

@@ -127,6 +127,7 @@ struct WaveStats {
          exact_sector_bytes = 0;
   uint64_t hist_count_launches = 0, exact_launches = 0;
   uint64_t sweep_waves = 0, gather_waves = 0;
+  double sweep_alg_bytes = 0;  // table rows streamed + V written + term lists read (sweep waves)
   std::vector<KernelTime> per_kernel;  // CUDA-event time per launch site (stats mode)
   void merge(const WaveStats& o) {
     ms_sample += o.ms_sample; ms_hist_rng += o.ms_hist_rng; ms_hist_count += o.ms_hist_count;
@@ -136,6 +137,7 @@ struct WaveStats {
     hist_sector_bytes += o.hist_sector_bytes; exact_strict_bytes += o.exact_strict_bytes;
     exact_sector_bytes += o.exact_sector_bytes; hist_count_launches += o.hist_count_launches;
     exact_launches += o.exact_launches; sweep_waves += o.sweep_waves; gather_waves += o.gather_waves;
+    sweep_alg_bytes += o.sweep_alg_bytes;
     for (const auto& k : o.per_kernel) {
       bool found = false;
       for (auto& m : per_kernel)
@@ -235,6 +237,7 @@ class WaveRunner {
   int pend_n_ = 0, pend_launches_ = 0;
   size_t pend_hist_ = 0, pend_exact_ = 0;
   bool pend_sweep_ = false;
+  double pend_sweep_bytes_ = 0;
 };
 
 }  // namespace sofg

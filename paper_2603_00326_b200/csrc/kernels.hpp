@@ -9,6 +9,10 @@
 
 namespace sofg {
 
+// Dynamic shared-memory opt-in, always set to the sm_100 maximum: the attribute is per kernel and
+// process-wide, so per-launch values would race between the host threads of concurrent tree groups.
+constexpr int kSmemOptin = 227 * 1024;
+
 // sample.cu
 cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t d, uint32_t R,
                                      uint32_t zmax, uint32_t* terms, uint32_t* row_ptr,

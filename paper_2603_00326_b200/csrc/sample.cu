@@ -318,7 +318,7 @@ cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t 
   const size_t smem = per_warp * warps;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(dev::k_sample_projection, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
+                         kSmemOptin);
   const int grid = (n_nodes + warps - 1) / warps;
   dev::k_sample_projection<<<grid, warps * 32, smem, st>>>(nodes, n_nodes, d, R, zpad, terms,
                                                            row_ptr, pos_after);
@@ -347,7 +347,7 @@ cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nod
   const size_t smem = per_warp * warps;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(dev::k_hist_boundaries, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
+                         kSmemOptin);
   const uint64_t items = uint64_t(n_hist) * R;
   const unsigned grid = unsigned((items + warps - 1) / warps);
   dev::k_hist_boundaries<<<grid, warps * 32, smem, st>>>(nodes, hist_nodes, n_hist, R, bins, mpad,

@@ -288,7 +288,7 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
   if (n_work == 0) return cudaSuccess;
   const int bpad = pow2_at_least(int(bins), 32);
   const size_t smem = hist_count_smem(bins, k, chunk_cap);
-  cudaFuncSetAttribute(dev::k_hist_count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaFuncSetAttribute(dev::k_hist_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   dev::k_hist_count<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins,
                                                bpad, k, chunk_cap, terms, row_ptr, lab, gbase, G,
                                                bnd, nb, xl, gcnt, done, rowres);

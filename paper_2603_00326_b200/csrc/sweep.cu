@@ -480,7 +480,7 @@ static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, con
   const size_t smem = sweep_smem_k(ldr, B, R, K);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(dev::k_row_sweep<E>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_row_sweep<E>, dev::kSweepThreads, smem);
@@ -508,7 +508,7 @@ cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_
   const size_t smem = size_t(dev::kGatherWarps) * 32 * vpitch(R) * 4 + size_t(R + 1 + zmax) * 4;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(dev::k_project_gather,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   if (e != cudaSuccess) return e;
   dev::k_project_gather<<<n_tiles, 256, smem, st>>>(nodes, tiles, vbase, terms, row_ptr, R, idx, X,
                                                    ld, V);
