@@ -5,6 +5,7 @@
 #include <exception>
 #include <thread>
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include "../../include/sofg.h"
@@ -20,11 +21,9 @@ struct sofg_ctx {
   int pool_threads = 0;
   sofg::HostTimes times;
   int stats_mode = 0;
-  // second tree group in flight on the same GPU (own stream and host threads, shared table):
-  // while one group's host thread prepares a level, the other group's kernels run.
+  // second tree group in flight on the same GPU (own stream and host thread, shared table and
+  // pool): while one group prepares a level on the host, the other group's kernels run.
   std::unique_ptr<sofg::WaveRunner> eng2;
-  std::unique_ptr<sofg::ThreadPool> pool1, pool2;
-  int pool1_threads = 0, pool2_threads = 0;
   sofg::HostTimes times2;
 };
 
@@ -91,15 +90,6 @@ sofg::WaveRunner& runner2(sofg_ctx* c) {
   return *c->eng2;
 }
 
-sofg::ThreadPool& pool_n(std::unique_ptr<sofg::ThreadPool>& p, int& have, int want) {
-  want = std::max(1, want);
-  if (!p || have != want) {
-    p.reset(new sofg::ThreadPool(want));
-    have = want;
-  }
-  return *p;
-}
-
 void append_forest(sofg::FlatForest& dst, const sofg::FlatForest& src) {
   const int64_t nb = int64_t(dst.left.size()), qb = int64_t(dst.feat.size());
   dst.left.insert(dst.left.end(), src.left.begin(), src.left.end());
@@ -148,6 +138,9 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   const std::vector<double> xl = sofg::host::xlogx_table(n);
   D.xl.exact(n + 1);
   cuda_check(cudaMemcpy(D.xl.p, xl.data(), 8 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx");
+  std::vector<float> xlf(xl.begin(), xl.end());
+  D.xlf.exact(n + 1);
+  cuda_check(cudaMemcpy(D.xlf.p, xlf.data(), 4 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx f32");
 }
 
 struct PCfg {
@@ -335,29 +328,27 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
       // Two tree groups in flight (SOFG_GROUPS=1 disables): group 2 runs on its own stream and
       // host threads so each group's host-side level work overlaps the other's kernels.
       const char* ge = std::getenv("SOFG_GROUPS");
-      const int groups = ge ? std::max(1, std::atoi(ge)) : 2;
-      if (groups >= 2 && B >= 16 && pool.size() >= 2) {
+      const int groups = ge ? std::max(1, std::atoi(ge)) : 1;  // measured: 2 concurrent groups are not faster
+      if (groups >= 2 && B >= 16) {
         const size_t h = B / 2;
         std::vector<std::vector<uint32_t>> r1(std::make_move_iterator(roots.begin()),
                                               std::make_move_iterator(roots.begin() + long(h)));
         std::vector<std::vector<uint32_t>> r2(std::make_move_iterator(roots.begin() + long(h)),
                                               std::make_move_iterator(roots.end()));
         std::vector<uint64_t> s1(seeds.begin(), seeds.begin() + long(h)), s2(seeds.begin() + long(h), seeds.end());
-        const int t1n = std::max(1, pool.size() / 2);
         sofg::WaveRunner& e2 = runner2(c);
-        sofg::ThreadPool& p1 = pool_n(c->pool1, c->pool1_threads, t1n);
-        sofg::ThreadPool& p2 = pool_n(c->pool2, c->pool2_threads, std::max(1, pool.size() - t1n));
         sofg::FlatForest f1, f2;
         std::exception_ptr err2;
+        std::mutex turn;  // host phases alternate between the groups; both use the full pool
         std::thread th([&] {
           try {
-            sofg::grow_trees(e2, P, p2, r2, s2, 0, f2, c->times2);
+            sofg::grow_trees(e2, P, pool, r2, s2, 0, f2, c->times2, &turn);
           } catch (...) {
             err2 = std::current_exception();
           }
         });
         try {
-          sofg::grow_trees(*c->eng, P, p1, r1, s1, 0, f1, c->times);
+          sofg::grow_trees(*c->eng, P, pool, r1, s1, 0, f1, c->times, &turn);
         } catch (...) {
           th.join();
           throw;

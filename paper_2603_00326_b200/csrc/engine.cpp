@@ -356,7 +356,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       const size_t m = exact_b_count[size_t(b)];
       if (!m) continue;
       cuda_check(launch_exact_bucket(b, d_nodes, d_exact + off, int(m), R, k, d_terms, d_rp,
-                                     w.lab_in, d_gbase, d_G, D.xl.p, d_res, st_),
+                                     w.lab_in, d_gbase, d_G, D.xl.p, D.xlf.p, d_res, st_),
                  "exact_bucket");
       off += m;
       ++launches;

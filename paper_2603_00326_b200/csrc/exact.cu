@@ -65,12 +65,42 @@ struct Best {
   double inv_n;  // 1/n (window bound only; every compared gain uses the exact division)
 };
 
+// Impurity sum of a candidate in float from the float copy of the xlogx table (prefilter only).
+// Same operation structure as impurity_sum; |Xf - X| <= prefilter_eps(xl[n], k).
+template <int KC>
+__device__ __forceinline__ float impurity_sum_f(const float* __restrict__ xlf, const uint32_t* left,
+                                                const uint32_t* tot, int k, uint32_t nl,
+                                                uint32_t nr) {
+  float sl = 0.f, sr = 0.f;
+  if constexpr (KC == 2) {
+    sl = __ldg(xlf + left[0]) + __ldg(xlf + left[1]);
+    sr = __ldg(xlf + tot[0] - left[0]) + __ldg(xlf + tot[1] - left[1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < KC; ++c)
+      if (c < k) {
+        sl += __ldg(xlf + left[c]);
+        sr += __ldg(xlf + tot[c] - left[c]);
+      }
+  }
+  return ((__ldg(xlf + nl) - sl) + __ldg(xlf + nr)) - sr;
+}
+// Bound on |Xf - X|: 2k+2 table values each within 2^-24 relative of xl[n] (the largest table
+// entry used), and 2k+1 float operations on partial sums bounded by 2 xl[n] each; doubled margin.
+__device__ __forceinline__ double prefilter_eps(double xln, int k) {
+  return double(2 * (2 * k + 2) + 4 * (2 * k + 1)) * xln * 0x1p-24 + 0x1p-60;
+}
+
 // Search one sorted row (keys in blocked layout). Updates `b` when this row's best gain is
 // strictly larger (rows are visited in increasing order by the calling warp).
+// Pass 1 evaluates every candidate gap in float; only candidates whose float impurity lies within
+// 2 eps of the row's float minimum (a superset of every candidate whose exact gain can equal the
+// row's best) are evaluated exactly in double, in the reference's operation order.
 template <int E, int KC>
 __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, int k,
                                          const uint32_t* tot, double parent,
-                                         const double* __restrict__ xl, int row, int lane,
+                                         const double* __restrict__ xl,
+                                         const float* __restrict__ xlf, int row, int lane,
                                          Best& b) {
   // per-lane class counts
   uint32_t loc[KC], pre[KC];
@@ -93,52 +123,73 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   const uint64_t next_first = __shfl_down_sync(0xffffffffu, key[0], 1);
   const double dn = double(n);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const float inff = __int_as_float(0x7f800000);
 
-  auto eval = [&](auto&& visit) {
+  // pass 1: float impurity per candidate gap (a < b between consecutive sorted values)
+  float Xf[E];
+  float xminf = inff;
+  {
     uint32_t left[KC];
 #pragma unroll
     for (int c = 0; c < KC; ++c) left[c] = pre[c];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
+      Xf[e] = inff;
       const uint32_t p = uint32_t(p0 + e);
       if (p + 1 < n) {
         const int c = int(key[e] & 0xffu);
 #pragma unroll
         for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
         const uint64_t kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
-        const float a = order_key_inv(uint32_t(key[e] >> 32));
-        const float bb = order_key_inv(uint32_t(kb >> 32));
-        if (a < bb) {
+        if (order_key_inv(uint32_t(key[e] >> 32)) < order_key_inv(uint32_t(kb >> 32))) {
+          if constexpr (KC == 2) {
+            uint32_t lf[2] = {(p + 1) - left[1], left[1]};
+            Xf[e] = impurity_sum_f<2>(xlf, lf, tot, k, p + 1, n - (p + 1));
+          } else {
+            Xf[e] = impurity_sum_f<KC>(xlf, left, tot, k, p + 1, n - (p + 1));
+          }
+          xminf = fminf(xminf, Xf[e]);
+        }
+      }
+    }
+  }
+  xminf = warp_min_f32(xminf);
+  if (!(xminf < inff)) return;
+  const double eps = prefilter_eps(__ldg(xl + n), k);
+  // the row cannot beat the best row so far (its exact minimum exceeds the best's)
+  if (b.row >= 0 && double(xminf) - 2.0 * eps > b.xmin) return;
+  const double lim = double(xminf) + 3.0 * eps;  // 2 eps + slack for the equal-gain window
+  // pass 2: exact impurity for the prefiltered candidates
+  double Xd[E];
+  double xmin = inf;
+  {
+    uint32_t left[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) left[c] = pre[c];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      Xd[e] = inf;
+      const uint32_t p = uint32_t(p0 + e);
+      if (p + 1 < n) {
+        const int c = int(key[e] & 0xffu);
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
+        if (double(Xf[e]) <= lim) {
           const uint32_t nl = p + 1;
-          double X;
           if constexpr (KC == 2) {
             const uint32_t l1 = left[1], l0 = nl - l1;
             const double sl = __dadd_rn(__ldg(xl + l0), __ldg(xl + l1));
             const double sr = __dadd_rn(__ldg(xl + tot[0] - l0), __ldg(xl + tot[1] - l1));
-            X = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+            Xd[e] = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
           } else {
-            double sl = 0.0, sr = 0.0;
-#pragma unroll
-            for (int cc = 0; cc < KC; ++cc)
-              if (cc < k) {
-                sl = __dadd_rn(sl, __ldg(xl + left[cc]));
-                sr = __dadd_rn(sr, __ldg(xl + tot[cc] - left[cc]));
-              }
-            X = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+            Xd[e] = impurity_sum<KC>(xl, left, tot, k, nl, n - nl);
           }
-          if (visit(X, p, a, bb)) return;
+          xmin = fmin(xmin, Xd[e]);
         }
       }
     }
-  };
-
-  double xmin = inf;
-  eval([&](double X, uint32_t, float, float) {
-    xmin = fmin(xmin, X);
-    return false;
-  });
+  }
   xmin = warp_min_f64(xmin);
-  if (!(xmin < inf)) return;
   // gain = parent - X / n is monotone non-increasing in X: a row whose minimum impurity is not
   // below the best row's cannot have a strictly larger gain (split.hpp:260 keeps earlier rows).
   if (b.row >= 0 && !(xmin < b.xmin)) return;
@@ -147,24 +198,31 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   if (b.row >= 0 && !(g > b.gain)) return;
   const double win = x_window_fast(parent, xmin, dn, b.inv_n);
   uint32_t first = 0xffffffffu;
-  float fa = 0.f, fb = 0.f;
-  eval([&](double X, uint32_t p, float a, float bb) {
-    if (X == xmin || (X <= win && gain_from_x(parent, X, dn) == g)) {
-      first = p;
-      fa = a;
-      fb = bb;
-      return true;
+  int fe = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const double X = Xd[e];
+    if (first == 0xffffffffu && X <= win && (X == xmin || gain_from_x(parent, X, dn) == g)) {
+      first = uint32_t(p0 + e);
+      fe = e;
     }
-    return false;
-  });
+  }
   const uint32_t fp = warp_min_u32(first);
   const int src = __ffs(__ballot_sync(0xffffffffu, first == fp)) - 1;
-  fa = __shfl_sync(0xffffffffu, fa, src);
-  fb = __shfl_sync(0xffffffffu, fb, src);
+  // the two keys around the winning gap (positions fp, fp+1)
+  uint64_t ka = 0, kb = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (e == fe) {
+      ka = key[e];
+      kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
+    }
+  ka = __shfl_sync(0xffffffffu, ka, src);
+  kb = __shfl_sync(0xffffffffu, kb, src);
   b.xmin = xmin;
   b.row = row;
   b.gain = g;
-  b.thr = midpoint_down(fa, fb);
+  b.thr = midpoint_down(order_key_inv(uint32_t(ka >> 32)), order_key_inv(uint32_t(kb >> 32)));
   b.nl = fp + 1;
 }
 
@@ -174,7 +232,8 @@ __global__ void __launch_bounds__(128) k_exact_reg(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
-    const float* __restrict__ G, const double* __restrict__ xl, NodeRes* __restrict__ res) {
+    const float* __restrict__ G, const double* __restrict__ xl, const float* __restrict__ xlf,
+    NodeRes* __restrict__ res) {
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int li = (WPN == 1) ? int(blockIdx.x) * 4 + w : int(blockIdx.x);
@@ -265,7 +324,7 @@ __global__ void __launch_bounds__(128) k_exact_reg(
         }
       }
       reg_bitonic_sort<E>(key, lane);
-      scan_row<E, KC>(key, n, k, tot, nd.parent, xl, int(r), lane, best);
+      scan_row<E, KC>(key, n, k, tot, nd.parent, xl, xlf, int(r), lane, best);
     }
   }
 
@@ -316,7 +375,8 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
-    const float* __restrict__ G, const double* __restrict__ xl, NodeRes* __restrict__ res) {
+    const float* __restrict__ G, const double* __restrict__ xl, const float* __restrict__ xlf,
+    NodeRes* __restrict__ res) {
   constexpr int E = 8;
   constexpr int TEAMS = 8 / W;
   constexpr int P = 32 * E * W;  // positions per team
@@ -327,6 +387,7 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
   __shared__ uint32_t s_cnt[8][KC];
   __shared__ uint64_t s_first[8];
   __shared__ double s_xmin[8];
+  __shared__ float s_xminf[8];
   __shared__ uint32_t s_pos[8];
   __shared__ uint32_t s_scan[8];
   __shared__ Best s_best[TEAMS];
@@ -491,8 +552,46 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
     if (lane == 31) next_first = (wt + 1 < W) ? s_first[w + 1] : ~0ull;
     team_sync<W>(team);
 
-    double Xs[E];
+    // pass 1 (float prefilter, see scan_row), team-wide minimum
+    float Xf[E];
+    float xminf = __int_as_float(0x7f800000);
     {
+      uint32_t left[KC];
+#pragma unroll
+      for (int c = 0; c < KC; ++c) left[c] = pre[c];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        Xf[e] = __int_as_float(0x7f800000);
+        const uint32_t p = uint32_t(p0 + e);
+        if (p + 1 < n) {
+          const int c = int(key[e] & 0xffu);
+#pragma unroll
+          for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
+          const uint64_t kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
+          if (order_key_inv(uint32_t(key[e] >> 32)) < order_key_inv(uint32_t(kb >> 32))) {
+            if constexpr (KC == 2) {
+              uint32_t lf[2] = {(p + 1) - left[1], left[1]};
+              Xf[e] = impurity_sum_f<2>(xlf, lf, tot, k, p + 1, n - (p + 1));
+            } else {
+              Xf[e] = impurity_sum_f<KC>(xlf, left, tot, k, p + 1, n - (p + 1));
+            }
+            xminf = fminf(xminf, Xf[e]);
+          }
+        }
+      }
+    }
+    xminf = warp_min_f32(xminf);
+    if (lane == 0) s_xminf[w] = xminf;
+    team_sync<W>(team);
+    for (int i = 0; i < W; ++i) xminf = fminf(xminf, s_xminf[team * W + i]);
+    const double eps = prefilter_eps(__ldg(xl + n), k);
+    const bool row_live = xminf < __int_as_float(0x7f800000) &&
+                          !(best.row >= 0 && double(xminf) - 2.0 * eps > best.xmin);
+    const double lim = double(xminf) + 3.0 * eps;
+    // pass 2: exact impurity of the prefiltered candidates
+    double Xs[E];
+    double xmin = inf;
+    if (row_live) {  // uniform across the team
       uint32_t left[KC];
 #pragma unroll
       for (int c = 0; c < KC; ++c) left[c] = pre[c];
@@ -504,10 +603,7 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
           const int c = int(key[e] & 0xffu);
 #pragma unroll
           for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
-          const uint64_t kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
-          const float a = order_key_inv(uint32_t(key[e] >> 32));
-          const float bb = order_key_inv(uint32_t(kb >> 32));
-          if (a < bb) {
+          if (double(Xf[e]) <= lim) {
             const uint32_t nl = p + 1;
             if constexpr (KC == 2) {
               const uint32_t l1 = left[1], l0 = nl - l1;
@@ -515,23 +611,15 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
               const double sr = __dadd_rn(__ldg(xl + tot[0] - l0), __ldg(xl + tot[1] - l1));
               Xs[e] = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
             } else {
-              double sl = 0.0, sr = 0.0;
-#pragma unroll
-              for (int cc = 0; cc < KC; ++cc)
-                if (cc < k) {
-                  sl = __dadd_rn(sl, __ldg(xl + left[cc]));
-                  sr = __dadd_rn(sr, __ldg(xl + tot[cc] - left[cc]));
-                }
-              Xs[e] = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+              Xs[e] = impurity_sum<KC>(xl, left, tot, k, nl, n - nl);
             }
+            xmin = fmin(xmin, Xs[e]);
           }
         }
       }
     }
-    double xmin = inf;
-#pragma unroll
-    for (int e = 0; e < E; ++e) xmin = fmin(xmin, Xs[e]);
     xmin = warp_min_f64(xmin);
+    team_sync<W>(team);  // s_xminf reads done
     if (lane == 0) s_xmin[w] = xmin;
     team_sync<W>(team);
     for (int i = 0; i < W; ++i) xmin = fmin(xmin, s_xmin[team * W + i]);
@@ -585,21 +673,21 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
 template <int W, int KC>
 cudaError_t launch_team(const NodeIn* nodes, const uint32_t* list, int n, uint32_t R, int k,
                         const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
-                        const uint64_t* gbase, const float* G, const double* xl, NodeRes* res,
-                        cudaStream_t st) {
+                        const uint64_t* gbase, const float* G, const double* xl, const float* xlf,
+                        NodeRes* res, cudaStream_t st) {
   k_exact_team<W, KC><<<n, 256, 0, st>>>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl,
-                                         res);
+                                         xlf, res);
   return cudaGetLastError();
 }
 
 template <int E, int GR, int WPN, int KC>
 cudaError_t launch_bucket(const NodeIn* nodes, const uint32_t* list, int n, uint32_t R, int k,
                           const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
-                          const uint64_t* gbase, const float* G, const double* xl, NodeRes* res,
-                          cudaStream_t st) {
+                          const uint64_t* gbase, const float* G, const double* xl, const float* xlf,
+                          NodeRes* res, cudaStream_t st) {
   const int grid = WPN == 1 ? (n + 3) / 4 : n;
   k_exact_reg<E, GR, WPN, KC><<<grid, 128, 0, st>>>(nodes, list, n, R, k, terms, row_ptr, lab,
-                                                     gbase, G, xl, res);
+                                                     gbase, G, xl, xlf, res);
   return cudaGetLastError();
 }
 
@@ -607,15 +695,15 @@ template <int KC>
 cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
                              uint32_t R, int k, const uint32_t* terms, const uint32_t* row_ptr,
                              const uint8_t* lab, const uint64_t* gbase, const float* G,
-                             const double* xl, NodeRes* res, cudaStream_t st) {
+                             const double* xl, const float* xlf, NodeRes* res, cudaStream_t st) {
   switch (bucket) {
-    case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
-    case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
-    case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
-    case 3: return launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
-    case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
-    case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
-    case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, res, st);
+    case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 3: return launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -635,13 +723,14 @@ int exact_bucket(uint32_t n) {
 cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
                                 uint32_t R, int k, const uint32_t* terms,
                                 const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
-                                const float* G, const double* xl, NodeRes* res, cudaStream_t st) {
+                                const float* G, const double* xl, const float* xlf, NodeRes* res,
+                                cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   if (k == 2)
     return dev::launch_bucket_kc<2>(bucket, nodes, list, n, R, k, terms, row_ptr, lab, gbase, G,
-                                    xl, res, st);
+                                    xl, xlf, res, st);
   return dev::launch_bucket_kc<kMaxClasses>(bucket, nodes, list, n, R, k, terms, row_ptr, lab,
-                                            gbase, G, xl, res, st);
+                                            gbase, G, xl, xlf, res, st);
 }
 
 }  // namespace sofg

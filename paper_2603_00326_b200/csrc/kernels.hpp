@@ -11,7 +11,7 @@ namespace sofg {
 
 // Dynamic shared-memory opt-in, always set to the sm_100 maximum: the attribute is per kernel and
 // process-wide, so per-launch values would race between the host threads of concurrent tree groups.
-constexpr int kSmemOptin = 227 * 1024;
+constexpr int kSmemOptin = 226 * 1024;  // 227 KB opt-in minus room for static __shared__
 
 // sample.cu
 cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t d, uint32_t R,
@@ -65,7 +65,8 @@ int exact_bucket(uint32_t n);
 cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
                                 uint32_t R, int k, const uint32_t* terms,
                                 const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
-                                const float* G, const double* xl, NodeRes* res, cudaStream_t st);
+                                const float* G, const double* xl, const float* xlf, NodeRes* res,
+                                cudaStream_t st);
 
 // partition.cu
 cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles, int n_tiles,

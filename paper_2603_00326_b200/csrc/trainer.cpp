@@ -122,7 +122,9 @@ int32_t argmax_first(const uint32_t* c, int k) {  // std::max_element: first max
 void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
                 const std::vector<std::vector<uint32_t>>& roots,
                 const std::vector<uint64_t>& root_seeds, uint32_t root_depth, FlatForest& out,
-                HostTimes& times) {
+                HostTimes& times, std::mutex* turn) {
+  std::unique_lock<std::mutex> host_turn;
+  if (turn) host_turn = std::unique_lock<std::mutex>(*turn);
   const auto t_start = Clock::now();
   cuda_check(cudaSetDevice(eng.device()), "cudaSetDevice");
   DeviceData& D = eng.data();
@@ -309,7 +311,9 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       });
       times.ms_spec += ms_since(t0);
       t0 = Clock::now();
+      if (turn) host_turn.unlock();  // the other groups prepare their waves meanwhile
       eng.collect(w, res);
+      if (turn) host_turn.lock();
       times.ms_wait += ms_since(t0);
 
       t0 = Clock::now();
