@@ -192,8 +192,8 @@ class Forest:
 def _export(h) -> Forest:
     L = load()
     T, N, Q = L.sofg_forest_num_trees(h), L.sofg_forest_num_nodes(h), L.sofg_forest_num_terms(h)
-    f = Forest(np.zeros(T + 1, np.int64), np.zeros(N, np.int32), np.zeros(N, np.int32), np.zeros(N, np.int32),
-               np.zeros(N, np.float32), np.zeros(N + 1, np.int64), np.zeros(Q, np.uint32), np.zeros(Q, np.float32),
+    f = Forest(np.empty(T + 1, np.int64), np.empty(N, np.int32), np.empty(N, np.int32), np.empty(N, np.int32),
+               np.empty(N, np.float32), np.empty(N + 1, np.int64), np.empty(Q, np.uint32), np.empty(Q, np.float32),
                int(L.sofg_forest_breakeven(h)))
     L.sofg_forest_export(h, *(a.ctypes.data for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off,
                                                        f.feat, f.weight)))

@@ -400,14 +400,35 @@ void sofg_forest_export(const sofg_forest* fo, int64_t* tree_off, int32_t* left,
                         int32_t* pred, float* thr, int64_t* term_off, uint32_t* feat,
                         float* weight) {
   const sofg::FlatForest& f = fo->f;
-  std::memcpy(tree_off, f.tree_off.data(), 8 * f.tree_off.size());
-  std::memcpy(left, f.left.data(), 4 * f.left.size());
-  std::memcpy(right, f.right.data(), 4 * f.right.size());
-  std::memcpy(pred, f.pred.data(), 4 * f.pred.size());
-  std::memcpy(thr, f.thr.data(), 4 * f.thr.size());
-  std::memcpy(term_off, f.term_off.data(), 8 * f.term_off.size());
-  std::memcpy(feat, f.feat.data(), 4 * f.feat.size());
-  std::memcpy(weight, f.weight.data(), 4 * f.weight.size());
+  // parallel copies (hundreds of MB for a 100-tree forest at 1M x 4096)
+  struct Part {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  const Part parts[] = {{tree_off, f.tree_off.data(), 8 * f.tree_off.size()},
+                        {left, f.left.data(), 4 * f.left.size()},
+                        {right, f.right.data(), 4 * f.right.size()},
+                        {pred, f.pred.data(), 4 * f.pred.size()},
+                        {thr, f.thr.data(), 4 * f.thr.size()},
+                        {term_off, f.term_off.data(), 8 * f.term_off.size()},
+                        {feat, f.feat.data(), 4 * f.feat.size()},
+                        {weight, f.weight.data(), 4 * f.weight.size()}};
+  size_t total = 0;
+  for (const Part& p : parts) total += p.bytes;
+  const int nt = total > (size_t(64) << 20) ? std::max(1, std::min(8, hw_threads())) : 1;
+  auto run = [&](int t) {
+    for (const Part& p : parts) {
+      if (!p.dst || !p.bytes) continue;
+      const size_t b0 = p.bytes * size_t(t) / size_t(nt) & ~size_t(63);
+      const size_t b1 = t + 1 == nt ? p.bytes : (p.bytes * size_t(t + 1) / size_t(nt) & ~size_t(63));
+      if (b1 > b0) std::memcpy(static_cast<char*>(p.dst) + b0, static_cast<const char*>(p.src) + b0, b1 - b0);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(run, t);
+  run(0);
+  for (auto& x : th) x.join();
 }
 
 int sofg_forest_import(uint64_t n_trees, uint64_t n_features, int32_t k, const int64_t* tree_off,

@@ -9,6 +9,8 @@
 #include <condition_variable>
 #include <cstdint>
 #include <functional>
+#include <memory>
+#include <type_traits>
 #include <mutex>
 #include <optional>
 #include <thread>
@@ -18,13 +20,34 @@
 
 namespace sofg {
 
+// std::vector whose resize() leaves trivially-constructible elements uninitialized (the forest
+// arrays are written in parallel right after sizing; zero-filling them first is a serial pass).
+template <class T, class A = std::allocator<T>>
+struct default_init_allocator : A {
+  using A::A;
+  template <class U>
+  struct rebind {
+    using other = default_init_allocator<U, typename std::allocator_traits<A>::template rebind_alloc<U>>;
+  };
+  template <class U>
+  void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    std::allocator_traits<A>::construct(static_cast<A&>(*this), p, std::forward<Args>(args)...);
+  }
+};
+template <class T>
+using pod_vector = std::vector<T, default_init_allocator<T>>;
+
 struct FlatForest {
-  std::vector<int64_t> tree_off{0};
-  std::vector<int32_t> left, right, pred;
-  std::vector<float> thr;
-  std::vector<int64_t> term_off{0};
-  std::vector<uint32_t> feat;
-  std::vector<float> weight;
+  pod_vector<int64_t> tree_off{0};
+  pod_vector<int32_t> left, right, pred;
+  pod_vector<float> thr;
+  pod_vector<int64_t> term_off{0};
+  pod_vector<uint32_t> feat;
+  pod_vector<float> weight;
   uint64_t breakeven = 0;
   int32_t class_count = 0;
   uint64_t n_features = 0;

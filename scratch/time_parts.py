@@ -6,7 +6,7 @@ from paper_2603_00326_b200 import _export
 ctx = sofg.Context(0)
 ctx.generate_trunk(1_000_000, 4096, 2, seed=1)
 NT = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-for groups in ("2", "1"):
+for groups in ("1",):
     os.environ["SOFG_GROUPS"] = groups
     for it in range(3):
         cfg = sofg.TrainConfig(n_trees=1000, mode="dynamic", breakeven=1024, seed=7, tree_begin=NT * it, tree_end=NT * it + NT)
