@@ -13,6 +13,8 @@
 // round-robin, reduced in shared memory (lowest row wins ties, as split.hpp:259-263).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.hpp"
 #include "dev_util.cuh"
 #include "kernels.hpp"
@@ -700,7 +702,7 @@ cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* li
     case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
-    case 3: return launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 3: return std::getenv("SOFG_TEAM256") ? launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st) : launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
