@@ -193,10 +193,15 @@ sofg::TrainParams params_for(const sofg_train_config* cfg, const sofg::DeviceDat
   return P;
 }
 
-uint64_t auto_batch(uint64_t n_root, uint64_t n_trees) {
-  // level buffers: 2 x (4 B id + 1 B label) per root sample; keep them under ~6 GB
-  const uint64_t per_tree = 10 * std::max<uint64_t>(n_root, 1);
-  const uint64_t cap = std::max<uint64_t>(1, (6ull << 30) / per_tree);
+uint64_t auto_batch(uint64_t n_root, uint64_t n_trees, const sofg::TrainParams& P, uint64_t d) {
+  const uint64_t n0 = std::max<uint64_t>(n_root, 1);
+  // level buffers: 2 x (4 B id + 1 B label) per root sample + the inverse map; keep under ~8 GB
+  uint64_t cap = std::max<uint64_t>(1, (8ull << 30) / (14 * n0));
+  // projected rows of the widest (root) level: n0 x Rp floats per tree; keep under ~40 GB
+  cap = std::min<uint64_t>(cap, std::max<uint64_t>(1, (40ull << 30) / (n0 * sofg::vpitch(P.R) * 4)));
+  // terms per wave stay < 2^31: the widest level has far fewer than n0/32 open nodes per tree
+  const double ez = std::max(1.0, double(P.R) * double(d) * P.density);
+  cap = std::min<uint64_t>(cap, std::max<uint64_t>(1, uint64_t(2147483648.0 / (std::max(1.0, n0 / 32.0) * ez))));
   return std::min(n_trees, cap);
 }
 
@@ -310,7 +315,7 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
     res->f.breakeven = cfg->mode == 2 ? P.breakeven : 0;
     uint64_t k0 = uint64_t(std::llround(cfg->bootstrap_fraction * double(D.n)));
     k0 = std::clamp<uint64_t>(k0, 1, D.n);
-    const uint64_t batch = P.batch_trees ? P.batch_trees : auto_batch(k0, te - tb);
+    const uint64_t batch = P.batch_trees ? P.batch_trees : auto_batch(k0, te - tb, P, D.d);
     for (uint64_t t0 = tb; t0 < te; t0 += batch) {
       const uint64_t t1 = std::min(te, t0 + batch);
       const size_t B = size_t(t1 - t0);

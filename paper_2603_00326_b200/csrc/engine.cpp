@@ -264,6 +264,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   }
   last_terms_ = d_terms;
   last_rp_ = d_rp;
+  last_nodes_ = d_nodes;
   uint32_t* d_pos_split = pos_split_.ensure(size_t(N));
   uint32_t* d_draws = draws_.ensure(std::max<size_t>(1, nh * R * bins));
   float* d_bnd = bnd_.ensure(std::max<size_t>(1, nh * R * (bins - 1)));
@@ -390,6 +391,33 @@ void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
   if (N == 0) return;
   cuda_check(cudaStreamSynchronize(st_), "wave sync");
   std::memcpy(res.data(), h_res_.p, sizeof(NodeRes) * N);
+  // winning rows longer than NodeRes carries inline: one gather + one D2H for the whole wave
+  long_off_.assign(1, 0u);
+  std::vector<uint32_t> list;
+  for (int i = 0; i < N; ++i)
+    if (res[size_t(i)].row >= 0 && res[size_t(i)].n_terms > uint32_t(kWinTermsMax)) {
+      list.push_back(uint32_t(i));
+      long_off_.push_back(long_off_.back() + res[size_t(i)].n_terms);
+    }
+  if (!list.empty()) {
+    long_pos_.assign(size_t(N), ~0u);
+    for (size_t k = 0; k < list.size(); ++k) long_pos_[list[k]] = uint32_t(k);
+    const size_t L = list.size(), T = long_off_.back();
+    uint32_t* hb = h_long_.ensure(2 * L + 1 + T);
+    std::memcpy(hb, list.data(), 4 * L);
+    std::memcpy(hb + L, long_off_.data(), 4 * (L + 1));
+    uint32_t* db = d_long_.ensure(2 * L + 1 + T);
+    cuda_check(cudaMemcpyAsync(db, hb, 4 * (2 * L + 1), cudaMemcpyHostToDevice, st_), "H2D long rows");
+    cuda_check(launch_win_terms(last_nodes_, pend_dres_, last_rp_, last_terms_, w.R, db, int(L),
+                                db + L, db + 2 * L + 1, st_),
+               "win_terms");
+    cuda_check(cudaMemcpyAsync(hb + 2 * L + 1, db + 2 * L + 1, 4 * T, cudaMemcpyDeviceToHost, st_),
+               "D2H long rows");
+    cuda_check(cudaStreamSynchronize(st_), "long rows sync");
+    long_terms_.assign(hb + 2 * L + 1, hb + 2 * L + 1 + T);
+  } else {
+    long_pos_.clear();
+  }
   const size_t nh = pend_hist_;
   const int launches = pend_launches_;
   const bool timing = collect_stats;
@@ -433,17 +461,14 @@ void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
   }
 }
 
-std::vector<uint32_t> WaveRunner::fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row) {
-  const uint32_t R = w.R;
-  uint32_t rp[2];
-  cuda_check(cudaMemcpy(rp, last_rp_ + size_t(node) * (R + 1) + row, 8, cudaMemcpyDeviceToHost),
-             "fetch row_ptr");
-  std::vector<uint32_t> out(rp[1] - rp[0]);
-  if (!out.empty())
-    cuda_check(cudaMemcpy(out.data(), last_terms_ + w.nodes[node].term_off + rp[0], 4 * out.size(),
-                          cudaMemcpyDeviceToHost),
-               "fetch terms");
-  return out;
+std::vector<uint32_t> WaveRunner::fetch_row_terms(const WaveSpec& w, uint32_t node,
+                                                  uint32_t row) const {
+  (void)w;
+  (void)row;
+  if (node >= long_pos_.size() || long_pos_[node] == ~0u)
+    throw std::logic_error("winning row terms were not fetched");
+  const uint32_t k = long_pos_[node];
+  return std::vector<uint32_t>(long_terms_.begin() + long_off_[k], long_terms_.begin() + long_off_[k + 1]);
 }
 
 }  // namespace sofg

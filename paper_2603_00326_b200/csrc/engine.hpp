@@ -187,9 +187,9 @@ class WaveRunner {
   void collect(const WaveSpec& w, std::vector<NodeRes>& res);
   // Page-locked staging reused across calls (root segments).
   PinnedBuf<unsigned char> staging;
-  // Terms of projection row `row` of node `node` of the last wave (for rows longer than the
-  // kWinTermsMax terms NodeRes carries inline).
-  std::vector<uint32_t> fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row);
+  // Terms of node `node`'s winning row in the last collected wave, for rows longer than the
+  // kWinTermsMax terms NodeRes carries inline (fetched in one batch by collect()).
+  std::vector<uint32_t> fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row) const;
 
   void set_pool(ThreadPool* p) { pool_ = p; }
 
@@ -232,6 +232,11 @@ class WaveRunner {
   DevBuf<uint4> qoff_;         // per-node sub-list offsets (sweep mode)
   int n_sm_ = 148;
   const uint32_t* last_terms_ = nullptr;
+  const NodeIn* last_nodes_ = nullptr;
+  // long winning rows of the last wave (host copies): node -> [long_off_[k], long_off_[k+1])
+  std::vector<uint32_t> long_pos_, long_off_, long_terms_;
+  PinnedBuf<uint32_t> h_long_;
+  DevBuf<uint32_t> d_long_;
   const uint32_t* last_rp_ = nullptr;
   // submit -> collect state
   NodeRes* pend_dres_ = nullptr;

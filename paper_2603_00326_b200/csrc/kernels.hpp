@@ -77,6 +77,9 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
                              uint32_t* tile_left, uint32_t* inv, uint32_t B, cudaStream_t st);
 
+cudaError_t launch_win_terms(const NodeIn* nodes, const NodeRes* res, const uint32_t* row_ptr,
+                             const uint32_t* terms, uint32_t R, const uint32_t* list, int n_list,
+                             const uint32_t* off, uint32_t* out, cudaStream_t st);
 cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_tiles,
                                 const uint32_t* idx, NodeRes* res, cudaStream_t st);
 

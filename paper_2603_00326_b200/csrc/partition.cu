@@ -173,7 +173,33 @@ __global__ void __launch_bounds__(256) k_sector_count(const NodeIn* __restrict__
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&res[tl.node].sectors, c);
 }
 
+// Winning-row terms of nodes whose row is longer than NodeRes carries inline (dense projection
+// matrices): one warp per listed node copies its row into a compact buffer for one D2H copy.
+__global__ void k_win_terms(const NodeIn* __restrict__ nodes, const NodeRes* __restrict__ res,
+                            const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ terms,
+                            uint32_t R, const uint32_t* __restrict__ list, int n_list,
+                            const uint32_t* __restrict__ off, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int li = int(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (li >= n_list) return;
+  const uint32_t node = list[li];
+  const int row = res[node].row;
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  const uint32_t q0 = rp[row], q1 = rp[row + 1];
+  const uint32_t* src = terms + nodes[node].term_off + q0;
+  for (uint32_t q = uint32_t(lane); q < q1 - q0; q += 32) out[off[li] + q] = src[q];
+}
+
 }  // namespace dev
+
+cudaError_t launch_win_terms(const NodeIn* nodes, const NodeRes* res, const uint32_t* row_ptr,
+                             const uint32_t* terms, uint32_t R, const uint32_t* list, int n_list,
+                             const uint32_t* off, uint32_t* out, cudaStream_t st) {
+  if (n_list == 0) return cudaSuccess;
+  dev::k_win_terms<<<(n_list + 3) / 4, 128, 0, st>>>(nodes, res, row_ptr, terms, R, list, n_list, off,
+                                                     out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_tiles,
                                 const uint32_t* idx, NodeRes* res, cudaStream_t st) {

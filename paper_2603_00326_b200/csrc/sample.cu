@@ -25,16 +25,19 @@ namespace dev {
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_sample_projection(
     const NodeIn* __restrict__ nodes, int n_nodes, uint32_t d, uint32_t R, int zpad,
-    uint32_t* __restrict__ terms, uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ pos_after) {
+    uint32_t* __restrict__ terms, uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ pos_after,
+    uint32_t* __restrict__ gkeys) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int node = blockIdx.x * (blockDim.x >> 5) + wib;
   if (node >= n_nodes) return;
-  const size_t per_warp = size_t(2 * kMtN) * 8 + size_t(2 * zpad) * 4;
+  // dense matrices (large z): the cell sets live in global scratch instead of shared memory
+  const size_t per_warp = size_t(2 * kMtN) * 8 + (gkeys ? 0 : size_t(2 * zpad) * 4);
   unsigned char* base = smem_raw + per_warp * wib;
   uint64_t* blk = reinterpret_cast<uint64_t*>(base);
-  uint32_t* keys = reinterpret_cast<uint32_t*>(base + size_t(2 * kMtN) * 8);
+  uint32_t* keys = gkeys ? gkeys + size_t(node) * 2 * zpad
+                         : reinterpret_cast<uint32_t*>(base + size_t(2 * kMtN) * 8);
   uint32_t* draws = keys + zpad;
 
   const NodeIn nd = nodes[node];
@@ -312,17 +315,26 @@ cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t 
                                      uint32_t* pos_after, cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
   const int zpad = next_pow2(int(zmax));
-  const size_t per_warp = size_t(2 * dev::kMtN) * 8 + size_t(2 * zpad) * 4;
+  const bool global_sets = size_t(2 * dev::kMtN) * 8 + size_t(2 * zpad) * 4 > 96 * 1024;
+  const size_t per_warp = size_t(2 * dev::kMtN) * 8 + (global_sets ? 0 : size_t(2 * zpad) * 4);
   int warps = 4;
   while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
   const size_t smem = per_warp * warps;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(dev::k_sample_projection, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemOptin);
+  uint32_t* gkeys = nullptr;
+  if (global_sets) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&gkeys),
+                                    size_t(n_nodes) * 2 * size_t(zpad) * 4, st);
+    if (e != cudaSuccess) return e;
+  }
   const int grid = (n_nodes + warps - 1) / warps;
   dev::k_sample_projection<<<grid, warps * 32, smem, st>>>(nodes, n_nodes, d, R, zpad, terms,
-                                                           row_ptr, pos_after);
-  return cudaGetLastError();
+                                                           row_ptr, pos_after, gkeys);
+  cudaError_t e = cudaGetLastError();
+  if (gkeys) cudaFreeAsync(gkeys, st);
+  return e;
 }
 
 cudaError_t launch_hist_draws(const NodeIn* nodes, const uint32_t* hist_nodes, int n_hist,

@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(256) k_project_gather(
     const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles,
     const uint64_t* __restrict__ vbase, const uint32_t* __restrict__ terms,
     const uint32_t* __restrict__ row_ptr, uint32_t R, const uint32_t* __restrict__ idx,
-    const float* __restrict__ X, uint64_t ld, float* __restrict__ V) {
+    const float* __restrict__ X, uint64_t ld, float* __restrict__ V, bool stage_terms) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t Rp = vpitch(R);
@@ -354,9 +354,15 @@ __global__ void __launch_bounds__(256) k_project_gather(
   const uint32_t z = __ldg(rpg + R) - __ldg(rpg);
   float* stg = reinterpret_cast<float*>(smem_raw) + size_t(w) * 32 * Rp;
   uint32_t* s_rp = reinterpret_cast<uint32_t*>(smem_raw + size_t(kGatherWarps) * 32 * Rp * 4);
-  uint32_t* s_tm = s_rp + R + 1;
+  const uint32_t* s_tm;  // the node's terms: shared memory, or global (L1) for dense matrices
+  if (stage_terms) {
+    uint32_t* st_tm = s_rp + R + 1;
+    for (uint32_t q = threadIdx.x; q < z; q += blockDim.x) st_tm[q] = __ldg(terms + nd.term_off + q);
+    s_tm = st_tm;
+  } else {
+    s_tm = terms + nd.term_off;
+  }
   for (uint32_t r = threadIdx.x; r <= R; r += blockDim.x) s_rp[r] = __ldg(rpg + r);
-  for (uint32_t q = threadIdx.x; q < z; q += blockDim.x) s_tm[q] = __ldg(terms + nd.term_off + q);
   __syncthreads();
   float* Vn = V + vbase[tl.node];
   for (uint32_t c0 = uint32_t(w) * 32; c0 < tl.len; c0 += 32 * kGatherWarps) {
@@ -505,13 +511,15 @@ cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_
                                   const uint32_t* idx, const float* X, uint64_t ld, float* V,
                                   cudaStream_t st) {
   if (n_tiles == 0) return cudaSuccess;
-  const size_t smem = size_t(dev::kGatherWarps) * 32 * vpitch(R) * 4 + size_t(R + 1 + zmax) * 4;
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  size_t smem = size_t(dev::kGatherWarps) * 32 * vpitch(R) * 4 + size_t(R + 1 + zmax) * 4;
+  const bool stage_terms = smem <= size_t(kSmemOptin);
+  if (!stage_terms) smem = size_t(dev::kGatherWarps) * 32 * vpitch(R) * 4 + size_t(R + 1) * 4;
+  if (smem > size_t(kSmemOptin)) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(dev::k_project_gather,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   if (e != cudaSuccess) return e;
   dev::k_project_gather<<<n_tiles, 256, smem, st>>>(nodes, tiles, vbase, terms, row_ptr, R, idx, X,
-                                                   ld, V);
+                                                   ld, V, stage_terms);
   return cudaGetLastError();
 }
 

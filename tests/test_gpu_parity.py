@@ -249,3 +249,37 @@ def test_tree_range_shards_concatenate(gpu_ctx, oracle):
     g = concat_forests(parts)
     _, oc = _cfg(n_trees=11, mode="dynamic", breakeven=300, seed=8)
     assert _forest_equal(g, oracle.train_forest(X, y, 2, oc)) == []
+
+
+@pytest.mark.parametrize("density,d", [(0.05, 256), (0.6, 64)])
+def test_dense_multiclass_forest_config5_style(gpu_ctx, oracle, density, d):
+    """BASELINE config 5 in miniature: 4 classes, dense projections (the SURVEY D3 density knob),
+    so rows carry many terms (winning rows longer than NodeRes holds inline) and z is large."""
+    rng = np.random.default_rng(5)
+    n, k = 3000, 4
+    y = (np.arange(n) % k).astype(np.int32)
+    X = (rng.standard_normal((d, n)) + 0.5 * (y[None, :] == (np.arange(d) % k)[:, None])).astype(np.float32)
+    gpu_ctx.upload(X, y, k)
+    gc, oc = _cfg(n_trees=3, mode="dynamic", breakeven=400, seed=13, cell_density=density)
+    assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, k, oc)) == []
+
+
+def test_wide_table_sweep_u32_terms(gpu_ctx, oracle):
+    """d >= 8192 switches the sweep's term lists to 32-bit entries (feature index > 13 bits)."""
+    X, y = oracle.generate_trunk(600, 9000, 3)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=2, mode="dynamic", breakeven=128, seed=4)
+    assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, 2, oc)) == []
+
+
+def test_sample_projection_very_dense_global_scratch(gpu_ctx, oracle):
+    """z ~ 20K cells per matrix: the Floyd cell sets no longer fit in shared memory."""
+    d, R, dens = 4096, 96, 0.05
+    seeds = np.array([3, 77, 1234], dtype=np.uint64)
+    rp, feat, w, used = gpu_ctx.sample_projection(d, R, dens, seeds, cap=24000)
+    for i in range(len(seeds)):
+        orp, ofeat, ow, oused = oracle.sample_projection(d, R, dens, int(seeds[i]), 0, cap=1 << 16)
+        z = int(orp[-1])
+        assert z > 16000
+        assert np.array_equal(rp[i], orp) and np.array_equal(feat[i, :z], ofeat)
+        assert np.array_equal(_bits(w[i, :z]), _bits(ow)) and int(used[i]) == oused
