@@ -49,7 +49,9 @@ def parse():
     p.add_argument("--n", type=int, default=1_000_000)
     p.add_argument("--d", type=int, default=4096)
     p.add_argument("--trees", type=int, default=100, help="trees per GPU per step")
-    p.add_argument("--breakeven", type=int, default=1024)
+    p.add_argument("--breakeven", type=int, default=768,
+                   help="dynamic-switch threshold; 768 = B200 calibration (DESIGN.md 3, calibrate.py)")
+    p.add_argument("--mode", default="dynamic", choices=["dynamic", "exact", "histogram"])
     p.add_argument("--seed", type=int, default=7)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-trees", type=int, default=0, help="CPU baseline sample (0 = one per core)")
@@ -177,7 +179,7 @@ def cpu_reference_sample(X, y, n_trees, args, threads):
 
     orc = oracle_lib.get("reference") if oracle_lib.have_reference() else oracle_lib.get("port")
     ds = orc.dataset(X, y, 2)
-    cfg = oracle_lib.make_config(n_trees=n_trees, mode="dynamic", breakeven=args.breakeven, seed=args.seed,
+    cfg = oracle_lib.make_config(n_trees=n_trees, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
                                  n_workers=threads)
     t0 = time.perf_counter()
     forest = orc.train_forest_ds(ds, cfg)
@@ -222,7 +224,7 @@ def run_reference(args, rank, world):
             "data": "synthetic trunk model (numpy, host)", "impl": "reference",
             "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, trees to purity (BASELINE config 3)",
                        "n_samples": args.n, "n_features": args.d, "trees_per_step": n_trees,
-                       "breakeven": args.breakeven, "mode": "dynamic", "seed": args.seed},
+                       "breakeven": args.breakeven, "mode": args.mode, "seed": args.seed},
             "cpu_baseline": {"value": v, "unit": "trees/s", "cores": threads, "kind": kind,
                              "sample": f"{n_trees} full trees of the 1M x 4096 forest on {threads} threads "
                                        f"per step; {steps} step(s), no warm-up (each step ~{times[0]:.0f} s)"},
@@ -261,7 +263,7 @@ def main():
 
     def cfg_for(step):
         b = step * per_step + rank * T
-        return sofg.TrainConfig(n_trees=total_trees, mode="dynamic", breakeven=args.breakeven, seed=args.seed,
+        return sofg.TrainConfig(n_trees=total_trees, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
                                 n_workers=0, tree_begin=b, tree_end=b + T)
 
     def barrier():
@@ -369,7 +371,7 @@ def main():
             "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, {T} trees per GPU to purity "
                                    f"(BASELINE config 3)",
                        "n_samples": args.n, "n_features": args.d, "trees_per_gpu_per_step": T,
-                       "mode": "dynamic", "breakeven": args.breakeven, "bin_count": 256, "seed": args.seed,
+                       "mode": args.mode, "breakeven": args.breakeven, "bin_count": 256, "seed": args.seed,
                        "parallelism": f"tree-sharded x{world}", "l2": "inputs 16.4 GB > 126 MB L2",
                        "nodes_per_step": nodes / args.steps, "datagen_s": round(gen_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,

@@ -82,8 +82,7 @@ void WaveRunner::submit(const WaveSpec& w) {
     uint64_t exact[7] = {0, 0, 0, 0, 0, 0, 0};
     uint32_t zmax = 32;
     uint64_t terms_end = 0;
-    bool too_big = false;
-    uint32_t big_n = 0;
+    uint64_t big = 0;
   };
   ThreadPool* pool = pool_;
   std::vector<Cnt> cc;
@@ -111,8 +110,7 @@ void WaveRunner::submit(const WaveSpec& w) {
           if (chunks > 1) t.multi++;
           t.work += uint64_t(groups) * chunks;
         } else if (nd.n > uint32_t(kExactSmemMax)) {
-          t.too_big = true;
-          t.big_n = nd.n;
+          t.big++;  // device-wide segmented sort path (exact_big.cu)
         } else {
           t.exact[exact_bucket(nd.n)]++;
         }
@@ -128,11 +126,6 @@ void WaveRunner::submit(const WaveSpec& w) {
   std::vector<Cnt> off(C);
   uint64_t exact_total = 0;
   for (size_t c = 0; c < C; ++c) {
-    if (cc[c].too_big)
-      throw std::invalid_argument("exact split of a node with " + std::to_string(cc[c].big_n) +
-                                  " samples exceeds the GPU exact splitter (" +
-                                  std::to_string(kExactSmemMax) + "); use a breakeven <= " +
-                                  std::to_string(kExactSmemMax));
     off[c].hist = tot.hist;
     off[c].multi = tot.multi;
     off[c].work = tot.work;
@@ -144,6 +137,7 @@ void WaveRunner::submit(const WaveSpec& w) {
     tot.tiles += cc[c].tiles;
     tot.g += cc[c].g;
     tot.items += cc[c].items;
+    tot.big += cc[c].big;
     tot.zmax = std::max(tot.zmax, cc[c].zmax);
     tot.terms_end = std::max(tot.terms_end, cc[c].terms_end);
   }
@@ -218,7 +212,7 @@ void WaveRunner::submit(const WaveSpec& w) {
             p_work[o.work++] = {uint32_t(i), g * kHistRowsPerCta, s0, std::min(nd.n - s0, cap), ch,
                                 chunks};
           }
-      } else {
+      } else if (nd.n <= uint32_t(kExactSmemMax)) {
         p_exact[o.exact[exact_bucket(nd.n)]++] = uint32_t(i);
       }
     }
@@ -366,6 +360,18 @@ void WaveRunner::submit(const WaveSpec& w) {
                                            "exact_n<=2048"};
       mark(kBucketName[b]);
     }
+  }
+  if (tot.big) {
+    std::vector<uint32_t> big;
+    big.reserve(size_t(tot.big));
+    for (int i = 0; i < N; ++i)
+      if (!(w.nodes[size_t(i)].flags & kNodeHist) && w.nodes[size_t(i)].n > uint32_t(kExactSmemMax))
+        big.push_back(uint32_t(i));
+    cuda_check(launch_exact_big(d_nodes, w.nodes.data(), big.data(), int(big.size()), R, k, d_rp,
+                                w.lab_in, d_gbase, d_G, D.xl.p, d_res, st_),
+               "exact_big");
+    launches += 4;
+    mark("exact_big");
   }
   if (timing) cudaEventRecord(ev_[4], st_);
   cuda_check(launch_partition(d_nodes, N, d_tiles, int(n_tiles), d_tfirst, R, k, d_terms,

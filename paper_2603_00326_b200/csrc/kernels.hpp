@@ -68,6 +68,12 @@ cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t*
                                 const float* G, const double* xl, const float* xlf, NodeRes* res,
                                 cudaStream_t st);
 
+// exact_big.cu — exact splits of nodes above kExactSmemMax (device-wide segmented sort)
+cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const uint32_t* h_list,
+                             int n, uint32_t R, int k, const uint32_t* row_ptr, const uint8_t* lab,
+                             const uint64_t* vbase, const float* V, const double* xl, NodeRes* res,
+                             cudaStream_t st);
+
 // partition.cu
 cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles, int n_tiles,
                              const uint32_t* tile_first, uint32_t R, int k, const uint32_t* terms,

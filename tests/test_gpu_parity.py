@@ -283,3 +283,15 @@ def test_sample_projection_very_dense_global_scratch(gpu_ctx, oracle):
         assert z > 16000
         assert np.array_equal(rp[i], orp) and np.array_equal(feat[i, :z], ofeat)
         assert np.array_equal(_bits(w[i, :z]), _bits(ow)) and int(used[i]) == oused
+
+
+@pytest.mark.parametrize("mode,breakeven", [("exact", None), ("dynamic", 5000)])
+def test_exact_large_nodes_segmented_sort(gpu_ctx, oracle, mode, breakeven):
+    """Exact splits of nodes above the shared-memory splitter (n > 2048): ExactOnly mode (the
+    'sort' arm of BASELINE config 2) and a breakeven above 2048 use the device-wide segmented sort."""
+    X, y = oracle.generate_trunk(9000, 20, 6)
+    Xq = np.round(X * 8) / 8  # plus heavy ties
+    for data in (X, Xq):
+        gpu_ctx.upload(data, y, 2)
+        gc, oc = _cfg(n_trees=3, mode=mode, breakeven=breakeven, seed=21)
+        assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(data, y, 2, oc)) == []
