@@ -226,7 +226,7 @@ def run_reference(args, rank, world):
                        "n_samples": args.n, "n_features": args.d, "trees_per_step": n_trees,
                        "breakeven": args.breakeven, "mode": args.mode, "seed": args.seed},
             "cpu_baseline": {"value": v, "unit": "trees/s", "cores": threads, "kind": kind,
-                             "sample": f"{n_trees} full trees of the 1M x 4096 forest on {threads} threads "
+                             "sample": f"{n_trees} full trees of the {args.n} x {args.d} forest on {threads} threads "
                                        f"per step; {steps} step(s), no warm-up (each step ~{times[0]:.0f} s)"},
             "e2e": {"value": v, "unit": "trees/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -361,8 +361,8 @@ def main():
                                    first.feat, first.weight)
         same = sum(ff.tree_equal(forest, t) for t in range(n_cpu))
         cpu = {"value": n_cpu / dt, "unit": "trees/s", "cores": threads, "kind": kind,
-               "sample": f"trees 0..{n_cpu - 1} of the bench forest (full 1M x 4096 trees, one per thread), "
-                         f"{dt:.1f} s", "bitexact_trees": f"{same}/{n_cpu}"}
+               "sample": f"trees 0..{n_cpu - 1} of the bench forest (full {args.n} x {args.d} trees, "
+                         f"{threads} threads), {dt:.1f} s", "bitexact_trees": f"{same}/{n_cpu}"}
 
     line = {"metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
