@@ -284,39 +284,60 @@ __global__ void __launch_bounds__(kSweepThreads) k_row_sweep(
       const uint32_t out_base = uint32_t(__cvta_generic_to_shared(sout)) - ra * 4u;
       double acc = 0.0;
       bool first = true;
-      // four 16-byte loads in flight (sub-lists are followed by >= 64 readable bytes)
-      uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0, q2 = q0, q3 = q0;
-      if (r < rb) {
-        q0 = __ldg(a4);
-        q1 = __ldg(a4 + 1);
-        q2 = __ldg(a4 + 2);
-        q3 = __ldg(a4 + 3);
-      }
-      for (uint32_t it = 0; __any_sync(0xffffffffu, r < rb); ++it) {
-        if (r < rb) {
-          uint32_t e[EPV];
-          unpack16<E>(q0, e);
-          q0 = q1;
-          q1 = q2;
-          q2 = q3;
-          q3 = __ldg(a4 + it + 4);
-          uint32_t xv[EPV];
+      // Term entries in 16-byte vectors; two register sets of four vectors ping-pong so the next
+      // four loads are in flight while the current four are consumed (sub-lists are followed by
+      // >= 128 readable bytes). A vector is consumed only while the lane still has rows to close:
+      // entries past its sub-list are either neutral pads or another list's.
+      auto consume = [&](const uint4& q) {
+        if (r >= rb) return;
+        uint32_t e[EPV];
+        unpack16<E>(q, e);
+        uint32_t xv[EPV];
 #pragma unroll
-          for (int u = 0; u < EPV; ++u) xv[u] = *reinterpret_cast<const uint32_t*>(xb + (e[u] & ~3u));
-          // no per-entry guard: entries past the sub-list are neutral pads (no row end)
+        for (int u = 0; u < EPV; ++u) xv[u] = *reinterpret_cast<const uint32_t*>(xb + (e[u] & ~3u));
 #pragma unroll
-          for (int u = 0; u < EPV; ++u) {
-            const double dx = double(__uint_as_float(xv[u] ^ (e[u] << 31)));
-            const double sum = __dadd_rn(acc, dx);
-            acc = first ? dx : sum;
-            first = (e[u] & 2u) != 0u;
-            if (first) {
-              const float v = __double2float_rn(acc);
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(out_base + r * 4u), "f"(v) : "memory");
-              ++r;
-            }
+        for (int u = 0; u < EPV; ++u) {
+          const double dx = double(__uint_as_float(xv[u] ^ (e[u] << 31)));
+          const double sum = __dadd_rn(acc, dx);
+          acc = first ? dx : sum;
+          first = (e[u] & 2u) != 0u;
+          if (first) {
+            const float v = __double2float_rn(acc);
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(out_base + r * 4u), "f"(v) : "memory");
+            ++r;
           }
         }
+      };
+      uint4 A0 = make_uint4(0, 0, 0, 0), A1 = A0, A2 = A0, A3 = A0, B0 = A0, B1 = A0, B2 = A0, B3 = A0;
+      if (r < rb) {
+        A0 = __ldg(a4);
+        A1 = __ldg(a4 + 1);
+        A2 = __ldg(a4 + 2);
+        A3 = __ldg(a4 + 3);
+      }
+      for (uint32_t it = 4;; it += 8) {
+        if (!__any_sync(0xffffffffu, r < rb)) break;
+        if (r < rb) {
+          B0 = __ldg(a4 + it);
+          B1 = __ldg(a4 + it + 1);
+          B2 = __ldg(a4 + it + 2);
+          B3 = __ldg(a4 + it + 3);
+        }
+        consume(A0);
+        consume(A1);
+        consume(A2);
+        consume(A3);
+        if (!__any_sync(0xffffffffu, r < rb)) break;
+        if (r < rb) {
+          A0 = __ldg(a4 + it + 4);
+          A1 = __ldg(a4 + it + 5);
+          A2 = __ldg(a4 + it + 6);
+          A3 = __ldg(a4 + it + 7);
+        }
+        consume(B0);
+        consume(B1);
+        consume(B2);
+        consume(B3);
       }
       __syncwarp();
       if (pi < cnt) {  // rows [ra, rb) of the pair -> V
@@ -442,7 +463,7 @@ bool aug_narrow(uint32_t d) { return d < 8192; }
 
 size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d) {
   const size_t es = aug_narrow(d) ? 2 : 4;
-  return (size_t(total_terms) + size_t(n_nodes) * (R + 3 * dev::kQ * (16 / es)) + 256) * es;
+  return (size_t(total_terms) + size_t(n_nodes) * (R + 3 * dev::kQ * (16 / es)) + 512) * es;
 }
 
 cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
@@ -469,7 +490,7 @@ static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
 static uint32_t sweep_k(uint64_t ldr, uint32_t B, uint32_t R) {
   const uint32_t want = std::max<uint32_t>(1, (dev::kSweepThreads / dev::kQ + (B * 5 / 8) - 1) / std::max<uint32_t>(1, B * 5 / 8));
   uint32_t K = std::min<uint32_t>(want, 8);
-  while (K > 1 && sweep_smem_k(ldr, B, R, K) > 110 * 1024) --K;
+  while (K > 1 && sweep_smem_k(ldr, B, R, K) > 112 * 1024) --K;
   return K;
 }
 
