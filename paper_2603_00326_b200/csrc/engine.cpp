@@ -392,19 +392,37 @@ void WaveRunner::submit(const WaveSpec& w) {
 }
 
 void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
+  const NodeRes* r = collect_view(w);
+  res.assign(r, r + pend_n_);
+}
+
+const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
   const int N = pend_n_;
-  res.assign(size_t(N), NodeRes{});
-  if (N == 0) return;
+  if (N == 0) return h_res_.p;
   cuda_check(cudaStreamSynchronize(st_), "wave sync");
-  std::memcpy(res.data(), h_res_.p, sizeof(NodeRes) * N);
+  const NodeRes* res = h_res_.p;
   // winning rows longer than NodeRes carries inline: one gather + one D2H for the whole wave
   long_off_.assign(1, 0u);
   std::vector<uint32_t> list;
-  for (int i = 0; i < N; ++i)
-    if (res[size_t(i)].row >= 0 && res[size_t(i)].n_terms > uint32_t(kWinTermsMax)) {
-      list.push_back(uint32_t(i));
-      long_off_.push_back(long_off_.back() + res[size_t(i)].n_terms);
+  {
+    auto is_long = [&](size_t i) { return res[i].row >= 0 && res[i].n_terms > uint32_t(kWinTermsMax); };
+    bool any = false;
+    if (pool_ && N >= 65536) {  // the scan reads one line per result: split it over the host pool
+      std::vector<unsigned char> hit(size_t(pool_->size()) * 4 + 1, 0);
+      pool_->chunks(size_t(N), 16384, [&](size_t c, size_t b0, size_t b1) {
+        for (size_t i = b0; i < b1 && !hit[c]; ++i) hit[c] = is_long(i);
+      });
+      for (unsigned char h : hit) any |= h != 0;
+    } else {
+      any = true;
     }
+    if (any)
+      for (int i = 0; i < N; ++i)
+        if (is_long(size_t(i))) {
+          list.push_back(uint32_t(i));
+          long_off_.push_back(long_off_.back() + res[size_t(i)].n_terms);
+        }
+  }
   if (!list.empty()) {
     long_pos_.assign(size_t(N), ~0u);
     for (size_t k = 0; k < list.size(); ++k) long_pos_[list[k]] = uint32_t(k);
@@ -465,6 +483,7 @@ void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
       }
     }
   }
+  return res;
 }
 
 std::vector<uint32_t> WaveRunner::fetch_row_terms(const WaveSpec& w, uint32_t node,

@@ -185,6 +185,8 @@ class WaveRunner {
   // collect() waits for them and copies the node results out. `w` must stay alive in between.
   void submit(const WaveSpec& w);
   void collect(const WaveSpec& w, std::vector<NodeRes>& res);
+  // Same wait, no copy: the node results in page-locked memory, valid until the next submit().
+  const NodeRes* collect_view(const WaveSpec& w);
   // Page-locked staging reused across calls (root segments).
   PinnedBuf<unsigned char> staging;
   // Terms of node `node`'s winning row in the last collected wave, for rows longer than the

@@ -210,7 +210,6 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   int cur = 0;
   std::vector<uint32_t> spec_z, spec_pos;
   std::vector<size_t> poff(NP + 1);
-  std::vector<NodeRes> res;
   WaveSpec w;
   w.R = P.R;
   w.d = uint32_t(D.d);
@@ -312,7 +311,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       times.ms_spec += ms_since(t0);
       t0 = Clock::now();
       if (turn) host_turn.unlock();  // the other groups prepare their waves meanwhile
-      eng.collect(w, res);
+      const NodeRes* res = eng.collect_view(w);
       if (turn) host_turn.lock();
       times.ms_wait += ms_since(t0);
 
