@@ -204,6 +204,7 @@ class WaveRunner {
   DevBuf<uint8_t> lvl_lab[2];
   DevBuf<uint32_t> inv;
   DevBuf<uint64_t> tree_off;
+  DevBuf<uint32_t> root_counts;
 
  private:
   int device_;

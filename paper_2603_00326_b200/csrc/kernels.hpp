@@ -90,6 +90,9 @@ cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_ti
                                 const uint32_t* idx, NodeRes* res, cudaStream_t st);
 
 // misc.cu
+cudaError_t launch_root_labels(const uint32_t* idx, const uint64_t* off, uint32_t B,
+                               uint64_t max_per_tree, const uint8_t* labels, uint8_t* lab_out,
+                               uint32_t* counts, cudaStream_t st);
 cudaError_t launch_generate_trunk(float* X, uint64_t ld, uint8_t* labels, uint64_t n, uint64_t d,
                                   int k, uint64_t seed, cudaStream_t st);
 cudaError_t launch_apply_projection(const float* X, uint64_t ld, const uint32_t* terms, int nt,

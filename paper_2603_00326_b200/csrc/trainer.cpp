@@ -147,38 +147,50 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     idx[i].ensure(total);
     lab[i].ensure(total);
   }
+  // Root segments: sample ids to the device; labels and class counts gathered there.
+  uint64_t maxn = 0;
+  for (size_t b = 0; b < B; ++b) maxn = std::max<uint64_t>(maxn, roots[b].size());
+  DevBuf<uint64_t>& d_off = eng.tree_off;
+  d_off.ensure(B + 1);
+  std::vector<uint32_t> root_counts(B * kMaxClasses);
   {
-    unsigned char* stg = eng.staging.ensure(5 * total);
+    unsigned char* stg = eng.staging.ensure(4 * total + 8 * (B + 1) + 4 * kMaxClasses * B);
     uint32_t* hi = reinterpret_cast<uint32_t*>(stg);
-    uint8_t* hl = stg + 4 * total;
-    pool.parallel_for(B, [&](size_t b) {
-      std::memcpy(hi + off[b], roots[b].data(), 4 * roots[b].size());
-      for (size_t j = 0; j < roots[b].size(); ++j) hl[off[b] + j] = uint8_t(D.labels_host[roots[b][j]]);
-    });
+    uint64_t* ho = reinterpret_cast<uint64_t*>(stg + 4 * total);
+    uint32_t* hc = reinterpret_cast<uint32_t*>(stg + 4 * total + 8 * (B + 1));
+    pool.parallel_for(B, [&](size_t b) { std::memcpy(hi + off[b], roots[b].data(), 4 * roots[b].size()); });
+    std::memcpy(ho, off.data(), 8 * (B + 1));
+    DevBuf<uint32_t>& d_cnt = eng.root_counts;
+    d_cnt.ensure(kMaxClasses * B);
     cuda_check(cudaMemcpyAsync(idx[0].p, hi, 4 * total, cudaMemcpyHostToDevice, eng.stream()), "H2D idx");
-    cuda_check(cudaMemcpyAsync(lab[0].p, hl, total, cudaMemcpyHostToDevice, eng.stream()), "H2D lab");
+    cuda_check(cudaMemcpyAsync(d_off.p, ho, 8 * (B + 1), cudaMemcpyHostToDevice, eng.stream()), "H2D off");
+    cuda_check(launch_root_labels(idx[0].p, d_off.p, uint32_t(B), maxn, D.lab.p, lab[0].p, d_cnt.p,
+                                  eng.stream()),
+               "root_labels");
+    cuda_check(cudaMemcpyAsync(hc, d_cnt.p, 4 * kMaxClasses * B, cudaMemcpyDeviceToHost, eng.stream()),
+               "D2H root counts");
+    cuda_check(cudaStreamSynchronize(eng.stream()), "root sync");
+    std::memcpy(root_counts.data(), hc, 4 * kMaxClasses * B);
   }
   // Inverse map for the projection sweep (sweep.cu): needs each tree's samples to be distinct
   // (bootstrap_sample returns a sorted set; explicit active sets are checked).
   DevBuf<uint32_t>& inv = eng.inv;
-  DevBuf<uint64_t>& d_off = eng.tree_off;
   bool use_inv = D.XR.p != nullptr;
-  for (size_t b = 0; b < B && use_inv; ++b) {
-    const std::vector<uint32_t>& r = roots[b];
-    bool inc = true;
-    for (size_t j = 1; j < r.size() && inc; ++j) inc = r[j - 1] < r[j];
-    if (!inc) {
-      std::vector<uint32_t> c(r);
-      std::sort(c.begin(), c.end());
-      use_inv = std::adjacent_find(c.begin(), c.end()) == c.end();
-    }
+  if (use_inv) {
+    std::vector<unsigned char> distinct(B, 1);
+    pool.parallel_for(B, [&](size_t b) {
+      const std::vector<uint32_t>& r = roots[b];
+      bool inc = true;
+      for (size_t j = 1; j < r.size() && inc; ++j) inc = r[j - 1] < r[j];
+      if (!inc) {
+        std::vector<uint32_t> c(r);
+        std::sort(c.begin(), c.end());
+        distinct[b] = std::adjacent_find(c.begin(), c.end()) == c.end();
+      }
+    });
+    for (unsigned char x : distinct) use_inv = use_inv && x;
   }
   if (use_inv) {
-    uint64_t maxn = 0;
-    for (size_t b = 0; b < B; ++b) maxn = std::max<uint64_t>(maxn, roots[b].size());
-    d_off.ensure(B + 1);
-    cuda_check(cudaMemcpyAsync(d_off.p, off.data(), 8 * (B + 1), cudaMemcpyHostToDevice, eng.stream()),
-               "H2D off");
     inv.ensure(D.n * B);
     cuda_check(launch_inv_init(idx[0].p, d_off.p, uint32_t(B), D.n, maxn, inv.p, eng.stream()),
                "inv_init");
@@ -201,7 +213,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       o.n = uint32_t(roots[b].size());
       o.depth = root_depth;
       o.seed = root_seeds[b];
-      for (uint32_t s0 : roots[b]) o.counts[D.labels_host[s0]]++;
+      for (int c = 0; c < k; ++c) o.counts[c] = root_counts[b * kMaxClasses + size_t(c)];
       fr[p].push_back(o);
     }
   });
