@@ -239,22 +239,32 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     return t;
   };
 
+  // forest.hpp:178-179: a node is split iff it is impure, large enough and above max_depth
+  auto can_split = [&](const Open& o) {
+    uint32_t top = 0;
+    for (int cc = 0; cc < k; ++cc) top = std::max(top, o.counts[cc]);
+    return top < o.n && o.n >= P.min_samples_split && o.n >= 2 &&
+           (!P.max_depth || o.depth < *P.max_depth);
+  };
+  // The roots are filtered here; children are filtered when they are created (post below), so
+  // every later level's frontier is already the list of nodes to split.
+  pool.parallel_for(NP, [&](size_t p) {
+    std::vector<Open> keep;
+    for (const Open& o : fr[p]) {
+      if (can_split(o))
+        keep.push_back(o);
+      else
+        trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);  // forest.hpp:233-236
+    }
+    fr[p].swap(keep);
+  });
+
   while (count_open(fr) > 0) {
     times.levels++;
     t0 = Clock::now();
     pool.parallel_for(NP, [&](size_t p) {
-      std::vector<Open>& out = sp[p];
-      out.clear();
-      for (const Open& o : fr[p]) {
-        uint32_t top = 0;
-        for (int cc = 0; cc < k; ++cc) top = std::max(top, o.counts[cc]);
-        const bool can = top < o.n && o.n >= P.min_samples_split && o.n >= 2 &&
-                         (!P.max_depth || o.depth < *P.max_depth);  // forest.hpp:178-179
-        if (can)
-          out.push_back(o);
-        else
-          trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
-      }
+      sp[p].swap(fr[p]);
+      fr[p].clear();
       nx[p].clear();
     });
     times.ms_prep += ms_since(t0);
@@ -289,12 +299,22 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
         }
       });
       times.ms_binomial += ms_since(tb);
-      uint64_t term_off = 0;
-      for (size_t i = 0; i < N; ++i) {
-        w.nodes[i].term_off = uint32_t(term_off);
-        term_off += w.nodes[i].z;
-      }
-      if (term_off >= (1ull << 32)) throw std::runtime_error("wave term count overflow");
+      // term offsets: per-part sums, then a parallel fill
+      std::vector<uint64_t> pz(NP + 1, 0);
+      pool.parallel_for(NP, [&](size_t p) {
+        uint64_t z = 0;
+        for (size_t j = 0; j < sp[p].size(); ++j) z += w.nodes[poff[p] + j].z;
+        pz[p + 1] = z;
+      });
+      for (size_t p = 0; p < NP; ++p) pz[p + 1] += pz[p];
+      if (pz[NP] >= (1ull << 32)) throw std::runtime_error("wave term count overflow");
+      pool.parallel_for(NP, [&](size_t p) {
+        uint64_t t = pz[p];
+        for (size_t j = 0; j < sp[p].size(); ++j) {
+          w.nodes[poff[p] + j].term_off = uint32_t(t);
+          t += w.nodes[poff[p] + j].z;
+        }
+      });
       w.idx_in = idx[cur].p;
       w.lab_in = lab[cur].p;
       w.idx_out = idx[cur ^ 1].p;
@@ -374,8 +394,12 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
               l.counts[c] = r.left_counts[c];
               rr.counts[c] = o.counts[c] - r.left_counts[c];
             }
-            nx[p].push_back(l);
-            nx[p].push_back(rr);
+            for (Open* ch : {&l, &rr}) {
+              if (can_split(*ch))
+                nx[p].push_back(*ch);
+              else
+                trees[o.tree][size_t(ch->bnode)].pred = argmax_first(ch->counts, k);
+            }
           } else if (o.attempt < P.max_split_retries) {  // forest.hpp:187,211: next attempt
             o.attempt++;
             o.pos = r.pos_after;
