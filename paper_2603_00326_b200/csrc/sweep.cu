@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
 // independent shared-memory loads, one double accumulator per row — and park their rows in a
 // per-lane staging slot, written to V at the end with vector stores.
 // ------------------------------------------------------------------------------------------
+#ifndef SOFG_SWEEP_DIRECT
+#define SOFG_SWEEP_DIRECT 0  // 1: rows straight to V with 4-byte stores (measured 2x slower: partial-sector writes)
+#endif
 constexpr int kSweepThreads = 512;
 
 struct Pair {
@@ -303,7 +306,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_row_sweep(
           first = (e[u] & 2u) != 0u;
           if (first) {
             const float v = __double2float_rn(acc);
+#if SOFG_SWEEP_DIRECT
+            vout[r] = v;
+#else
             asm volatile("st.shared.f32 [%0], %1;" ::"r"(out_base + r * 4u), "f"(v) : "memory");
+#endif
             ++r;
           }
         }
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_row_sweep(
         consume(B3);
       }
       __syncwarp();
-      if (pi < cnt) {  // rows [ra, rb) of the pair -> V
+      if (!SOFG_SWEEP_DIRECT && pi < cnt) {  // rows [ra, rb) of the pair -> V
         if (((ra | Rp) & 3u) == 0u) {
           const uint32_t n4 = (rb - ra) / 4;
           for (uint32_t i = 0; i < n4; ++i)
@@ -482,7 +489,7 @@ cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* t
 
 static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
   return size_t(K) * ldr * 4 + size_t(K) * B * sizeof(dev::Pair) +
-         size_t(dev::kSweepThreads) * dev::sweep_out_pitch(R) * 4;
+         (SOFG_SWEEP_DIRECT ? 0 : size_t(dev::kSweepThreads) * dev::sweep_out_pitch(R) * 4);
 }
 
 // Samples per CTA iteration: enough (node, sample) pairs to fill the CTA's lanes (a sample sits
