@@ -2,6 +2,7 @@
 // scalar helpers plus warp-level sorting / scanning primitives.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "common.hpp"
 
@@ -95,6 +96,68 @@ __device__ __forceinline__ void warp_bitonic_sort(K* a, int P, int lane) {
       }
       __syncwarp();
     }
+  }
+}
+
+// Register bitonic sort of 32*E keys held E per lane in blocked layout (lane l holds sorted
+// positions [l*E, (l+1)*E)), ascending: intra-lane compare-exchange for strides < E, shuffles for
+// strides >= E.
+template <int E, class K>
+__device__ __forceinline__ void reg_bitonic_sort_k(K (&key)[E], int lane) {
+  constexpr int P = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lm = j / E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const K o = __shfl_xor_sync(0xffffffffu, key[e], lm);
+          const int i = lane * E + e;
+          const bool up = (i & k) == 0;
+          const bool lower = (lane & lm) == 0;
+          const K mn = o < key[e] ? o : key[e];
+          const K mx = o < key[e] ? key[e] : o;
+          key[e] = (lower == up) ? mn : mx;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & j) == 0) {
+            const int i = lane * E + e;
+            const bool up = (i & k) == 0;
+            const K a = key[e], b = key[e | j];
+            const bool sw = (a > b) == up;
+            key[e] = sw ? b : a;
+            key[e | j] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Sort a[0..P) in (warp-private) shared memory, P a power of two in [32, 256], through registers.
+template <class K>
+__device__ __forceinline__ void warp_sort_via_regs(K* a, int P, int lane) {
+  auto run = [&](auto eval) {
+    constexpr int E = decltype(eval)::value;
+    K k[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) k[e] = a[lane * E + e];
+    reg_bitonic_sort_k<E, K>(k, lane);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[lane * E + e] = k[e];
+    __syncwarp();
+  };
+  switch (P) {
+    case 32: run(std::integral_constant<int, 1>{}); break;
+    case 64: run(std::integral_constant<int, 2>{}); break;
+    case 128: run(std::integral_constant<int, 4>{}); break;
+    case 256: run(std::integral_constant<int, 8>{}); break;
+    default: warp_bitonic_sort(a, P, lane);
   }
 }
 

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128) k_sample_projection(
   // Set = {t_q} unless some t collides (prob ~ z^2 / 2 cells); sort and test neighbours.
   for (int i = lane; i < zpad; i += 32) keys[i] = i < int(z) ? draws[i] : 0xffffffffu;
   __syncwarp();
-  warp_bitonic_sort(keys, zpad, lane);
+  if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
   bool dup = false;
   for (int i = lane + 1; i < int(z); i += 32) dup |= keys[i] == keys[i - 1];
   if (__any_sync(0xffffffffu, dup)) {
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(128) k_sample_projection(
     for (int i = lane; i < zpad; i += 32)
       if (i >= int(z)) keys[i] = 0xffffffffu;
     __syncwarp();
-    warp_bitonic_sort(keys, zpad, lane);
+    if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
   }
 
   // Coins: cell i (ascending) gets the top bit of the next output (uniform_int<int>(0,1)).
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
     for (int i = lane; i < mpad; i += 32)
       keys[i] = i < int(m) ? ((uint64_t(t[i]) << 16) | uint64_t(i)) : ~0ull;
     __syncwarp();
-    warp_bitonic_sort(keys, mpad, lane);
+    warp_sort_via_regs(keys, mpad, lane);
     for (int i = lane; i < int(m); i += 32) {
       const uint32_t me = uint32_t(keys[i] & 0xffffu);
       const bool c1 = i > 0 && (keys[i] >> 16) == (keys[i - 1] >> 16);
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
       vk[i] = i < int(m) ? order_key(__ldg(Vn + uint64_t(i) * Rp)) : 0xffffffffu;
   }
   __syncwarp();
-  warp_bitonic_sort(vk, mpad, lane);
+  warp_sort_via_regs(vk, mpad, lane);
   // midpoints of consecutive distinct values (float comparison: -0 == +0)
   uint32_t base_cnt = 0;
   for (int i0 = 1; i0 < int(m); i0 += 32) {
