@@ -138,7 +138,8 @@ __device__ __forceinline__ void reg_bitonic_sort_k(K (&key)[E], int lane) {
   }
 }
 
-// Sort a[0..P) in (warp-private) shared memory, P a power of two in [32, 256], through registers.
+// Sort a[0..P) in (warp-private) shared memory, P a power of two in [32, 512], through registers
+// (larger P: the shared-memory network).
 template <class K>
 __device__ __forceinline__ void warp_sort_via_regs(K* a, int P, int lane) {
   auto run = [&](auto eval) {
@@ -157,6 +158,7 @@ __device__ __forceinline__ void warp_sort_via_regs(K* a, int P, int lane) {
     case 64: run(std::integral_constant<int, 2>{}); break;
     case 128: run(std::integral_constant<int, 4>{}); break;
     case 256: run(std::integral_constant<int, 8>{}); break;
+    case 512: run(std::integral_constant<int, 16>{}); break;
     default: warp_bitonic_sort(a, P, lane);
   }
 }
