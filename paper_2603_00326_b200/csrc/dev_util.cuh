@@ -102,35 +102,72 @@ __device__ __forceinline__ void warp_bitonic_sort(K* a, int P, int lane) {
 // Register bitonic sort of 32*E keys held E per lane in blocked layout (lane l holds sorted
 // positions [l*E, (l+1)*E)), ascending: intra-lane compare-exchange for strides < E, shuffles for
 // strides >= E.
-template <int E, class K>
+template <int E, class K, bool COMPACT = false>
 __device__ __forceinline__ void reg_bitonic_sort_k(K (&key)[E], int lane) {
   constexpr int P = 32 * E;
-#pragma unroll
-  for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= E) {
+  if constexpr (COMPACT) {
+    // Stage loops as runtime loops (compact code for large kernels, where the fully unrolled
+    // network for E >= 8 overflows the instruction cache); only the register indexing is unrolled.
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+      for (int j = k >> 1; j >= E; j >>= 1) {  // partner in another lane
         const int lm = j / E;
+        const bool lower = (lane & lm) == 0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const K o = __shfl_xor_sync(0xffffffffu, key[e], lm);
-          const int i = lane * E + e;
-          const bool up = (i & k) == 0;
-          const bool lower = (lane & lm) == 0;
+          const bool up = ((lane * E + e) & k) == 0;
           const K mn = o < key[e] ? o : key[e];
           const K mx = o < key[e] ? key[e] : o;
           key[e] = (lower == up) ? mn : mx;
         }
-      } else {
+      }
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          if ((e & j) == 0) {
+      for (int j = (E >> 1); j > 0; j >>= 1) {  // partner in this lane
+        if (j < k) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            if ((e & j) == 0) {
+              const bool up = ((lane * E + e) & k) == 0;
+              const K a = key[e], b = key[e | j];
+              const bool sw = (a > b) == up;
+              key[e] = sw ? b : a;
+              key[e | j] = sw ? a : b;
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // the fully unrolled network (every index and direction a constant)
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j >= E) {
+          const int lm = j / E;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const K o = __shfl_xor_sync(0xffffffffu, key[e], lm);
             const int i = lane * E + e;
             const bool up = (i & k) == 0;
-            const K a = key[e], b = key[e | j];
-            const bool sw = (a > b) == up;
-            key[e] = sw ? b : a;
-            key[e | j] = sw ? a : b;
+            const bool lower = (lane & lm) == 0;
+            const K mn = o < key[e] ? o : key[e];
+            const K mx = o < key[e] ? key[e] : o;
+            key[e] = (lower == up) ? mn : mx;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            if ((e & j) == 0) {
+              const int i = lane * E + e;
+              const bool up = (i & k) == 0;
+              const K a = key[e], b = key[e | j];
+              const bool sw = (a > b) == up;
+              key[e] = sw ? b : a;
+              key[e | j] = sw ? a : b;
+            }
           }
         }
       }

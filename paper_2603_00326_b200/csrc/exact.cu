@@ -24,38 +24,7 @@ namespace dev {
 
 template <int E>
 __device__ __forceinline__ void reg_bitonic_sort(uint64_t (&key)[E], int lane) {
-  constexpr int P = 32 * E;
-#pragma unroll
-  for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= E) {
-        const int lm = j / E;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint64_t o = __shfl_xor_sync(0xffffffffu, key[e], lm);
-          const int i = lane * E + e;
-          const bool up = (i & k) == 0;
-          const bool lower = (lane & lm) == 0;
-          const uint64_t mn = o < key[e] ? o : key[e];
-          const uint64_t mx = o < key[e] ? key[e] : o;
-          key[e] = (lower == up) ? mn : mx;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          if ((e & j) == 0) {
-            const int i = lane * E + e;
-            const bool up = (i & k) == 0;
-            const uint64_t a = key[e], b = key[e | j];
-            const bool sw = (a > b) == up;
-            key[e] = sw ? b : a;
-            key[e | j] = sw ? a : b;
-          }
-        }
-      }
-    }
-  }
+  reg_bitonic_sort_k<E, uint64_t, (E >= 8)>(key, lane);
 }
 
 struct Best {
