@@ -24,7 +24,7 @@ namespace dev {
 
 template <int E>
 __device__ __forceinline__ void reg_bitonic_sort(uint64_t (&key)[E], int lane) {
-  reg_bitonic_sort_k<E, uint64_t, (E >= 8)>(key, lane);
+  reg_bitonic_sort_k<E, uint64_t, (E >= 8)>(key, lane);  // compact stages for E >= 8 (i-cache)
 }
 
 struct Best {
@@ -130,16 +130,14 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   // the row cannot beat the best row so far (its exact minimum exceeds the best's)
   if (b.row >= 0 && double(xminf) - 2.0 * eps > b.xmin) return;
   const double lim = double(xminf) + 3.0 * eps;  // 2 eps + slack for the equal-gain window
-  // pass 2: exact impurity for the prefiltered candidates
-  double Xd[E];
-  double xmin = inf;
-  {
+  // pass 2: exact impurity of the prefiltered candidates (the pass is repeated below to find the
+  // first position; the exact values are not kept, so wide E costs no extra registers)
+  auto exact_pass = [&](auto&& visit) {
     uint32_t left[KC];
 #pragma unroll
     for (int c = 0; c < KC; ++c) left[c] = pre[c];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      Xd[e] = inf;
       const uint32_t p = uint32_t(p0 + e);
       if (p + 1 < n) {
         const int c = int(key[e] & 0xffu);
@@ -147,19 +145,29 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
         for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
         if (double(Xf[e]) <= lim) {
           const uint32_t nl = p + 1;
+          double X;
           if constexpr (KC == 2) {
             const uint32_t l1 = left[1], l0 = nl - l1;
             const double sl = __dadd_rn(__ldg(xl + l0), __ldg(xl + l1));
             const double sr = __dadd_rn(__ldg(xl + tot[0] - l0), __ldg(xl + tot[1] - l1));
-            Xd[e] = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
+            X = __dsub_rn(__dadd_rn(__dsub_rn(__ldg(xl + nl), sl), __ldg(xl + (n - nl))), sr);
           } else {
-            Xd[e] = impurity_sum<KC>(xl, left, tot, k, nl, n - nl);
+            X = impurity_sum<KC>(xl, left, tot, k, nl, n - nl);
           }
-          xmin = fmin(xmin, Xd[e]);
+          visit(e, X);
         }
       }
     }
-  }
+  };
+  constexpr bool kKeep = E < 8;  // small E: keep the exact values; wide E: recompute (registers)
+  double Xd[kKeep ? E : 1];
+#pragma unroll
+  for (int e = 0; e < (kKeep ? E : 1); ++e) Xd[e] = inf;
+  double xmin = inf;
+  exact_pass([&](int e, double X) {
+    xmin = fmin(xmin, X);
+    if constexpr (kKeep) Xd[e] = X;
+  });
   xmin = warp_min_f64(xmin);
   // gain = parent - X / n is monotone non-increasing in X: a row whose minimum impurity is not
   // below the best row's cannot have a strictly larger gain (split.hpp:260 keeps earlier rows).
@@ -170,13 +178,17 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   const double win = x_window_fast(parent, xmin, dn, b.inv_n);
   uint32_t first = 0xffffffffu;
   int fe = 0;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const double X = Xd[e];
+  auto take = [&](int e, double X) {
     if (first == 0xffffffffu && X <= win && (X == xmin || gain_from_x(parent, X, dn) == g)) {
       first = uint32_t(p0 + e);
       fe = e;
     }
+  };
+  if constexpr (kKeep) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) take(e, Xd[e]);
+  } else {
+    exact_pass(take);
   }
   const uint32_t fp = warp_min_u32(first);
   const int src = __ffs(__ballot_sync(0xffffffffu, first == fp)) - 1;
@@ -672,7 +684,7 @@ cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* li
     case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 3: return std::getenv("SOFG_TEAM256") ? launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st) : launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
-    case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 4: return std::getenv("SOFG_REG512") ? launch_bucket<16, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st) : launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);  // register E=16 measured slower
     case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
     default: return cudaErrorInvalidValue;
