@@ -140,6 +140,14 @@ orc_split orc_find_node_split(const float* X, const int32_t* labels, uint64_t n_
                               uint64_t seed, uint64_t skip, uint64_t* consumed,
                               float* winner_values);
 
+/* ---- model I/O (reference build only; model_io.hpp) ---- */
+/* train_forest + save_model(forest, path) with the reference's writer. */
+int orc_train_save_model(const float* X, const int32_t* labels, uint64_t n_samples,
+                         uint64_t n_features, int32_t class_count, const orc_config* cfg,
+                         const char* path);
+/* load_model(path) with the reference's validating loader; totals of the loaded forest. */
+int orc_load_model_summary(const char* path, uint64_t* n_trees, uint64_t* n_nodes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -387,3 +387,24 @@ extern "C" orc_split orc_find_node_split(const float* X, const int32_t* y, uint6
     std::memcpy(winner_values, scratch.values.data() + s->candidate.projection_index * na, na * 4);
   return to_c(s->candidate);
 }
+
+// ---- model I/O (model_io.hpp:124-283): the reference's own writer, for byte-identity tests ----
+#include "soforest/model_io.hpp"
+
+extern "C" int orc_train_save_model(const float* X, const int32_t* y, uint64_t n, uint64_t d,
+                                    int32_t k, const orc_config* c, const char* path) {
+  return orc_guard([&] {
+    const Forest forest = train_forest(make_data(X, y, n, d, k), to_cfg(c));  // forest.hpp:267
+    save_model(forest, path);                                                 // model_io.hpp:124
+  });
+}
+
+extern "C" int orc_load_model_summary(const char* path, uint64_t* n_trees, uint64_t* n_nodes) {
+  return orc_guard([&] {
+    const Forest f = load_model<float>(path);  // model_io.hpp:186 (validating loader)
+    *n_trees = f.trees.size();
+    uint64_t nodes = 0;
+    for (const auto& t : f.trees) nodes += t.nodes.size();
+    *n_nodes = nodes;
+  });
+}

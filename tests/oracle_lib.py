@@ -163,6 +163,9 @@ class Oracle:
         L.orc_best_split_exact.argtypes = [vp, vp, u64, i32]
         L.orc_best_split_histogram.restype = OrcSplit
         L.orc_best_split_histogram.argtypes = [vp, u64, vp, i32]
+        if kind == "reference":
+            L.orc_train_save_model.argtypes = [vp, vp, u64, u64, i32, p(OrcConfig), C.c_char_p]
+            L.orc_load_model_summary.argtypes = [C.c_char_p, p(u64), p(u64)]
         L.orc_find_node_split.restype = OrcSplit
         L.orc_find_node_split.argtypes = [vp, vp, u64, i32, vp, u64, vp, u64, vp, vp, i32, u64, u64, u64,
                                           p(u64), vp]
@@ -243,6 +246,19 @@ class Oracle:
         self._err(self.lib.orc_predict(h, rows.ctypes.data, rows.shape[0], d, out.ctypes.data, votes.ctypes.data),
                   "predict")
         return out, votes
+
+    # -- model I/O (reference build) ---------------------------------------------------------
+    def train_save_model(self, X, y, k, cfg, path: str):
+        X = np.ascontiguousarray(X, np.float32)
+        y = np.ascontiguousarray(y, np.int32)
+        d, n = X.shape
+        self._err(self.lib.orc_train_save_model(X.ctypes.data, y.ctypes.data, n, d, k, C.byref(cfg),
+                                                path.encode()), "train_save_model")
+
+    def load_model_summary(self, path: str):
+        t, nn = C.c_uint64(), C.c_uint64()
+        self._err(self.lib.orc_load_model_summary(path.encode(), C.byref(t), C.byref(nn)), "load_model")
+        return t.value, nn.value
 
     # -- primitives --------------------------------------------------------------------------
     def split_mix64(self, x):
