@@ -49,8 +49,8 @@ def parse():
     p.add_argument("--n", type=int, default=1_000_000)
     p.add_argument("--d", type=int, default=4096)
     p.add_argument("--trees", type=int, default=100, help="trees per GPU per step")
-    p.add_argument("--breakeven", type=int, default=768,
-                   help="dynamic-switch threshold; 768 = B200 calibration (DESIGN.md 3, calibrate.py)")
+    p.add_argument("--breakeven", type=int, default=512,
+                   help="dynamic-switch threshold; 512 = B200 calibration (DESIGN.md 3, calibrate.py)")
     p.add_argument("--mode", default="dynamic", choices=["dynamic", "exact", "histogram"])
     p.add_argument("--seed", type=int, default=7)
     p.add_argument("--e2e-steps", type=int, default=2)

@@ -1,4 +1,4 @@
-for be in 256 512 768 1024 1536 2048; do
+for be in 320 448 512 640 768 1024; do
   timeout 900 python bench.py --trees 100 --warmup 1 --steps 2 --no-cpu-baseline --no-e2e --breakeven $be 2>&1 | tail -1 > gpurun_out/be_$be.json
   python -c "
 import json; d=json.load(open('gpurun_out/be_$be.json')); r=d['roofline']
