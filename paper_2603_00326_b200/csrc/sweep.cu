@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
 #ifndef SOFG_SWEEP_DIRECT
 #define SOFG_SWEEP_DIRECT 0  // 1: rows straight to V with 4-byte stores (measured 2x slower: partial-sector writes)
 #endif
-constexpr int kSweepThreads = 512;
+constexpr int kSweepThreads = 256;
 
 struct Pair {
   uint32_t node, j, k, pad;
@@ -495,7 +495,8 @@ static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
 // Samples per CTA iteration: enough (node, sample) pairs to fill the CTA's lanes (a sample sits
 // in ~63% of the batch's trees), within shared memory.
 static uint32_t sweep_k(uint64_t ldr, uint32_t B, uint32_t R) {
-  const uint32_t want = std::max<uint32_t>(1, (dev::kSweepThreads / dev::kQ + (B * 5 / 8) - 1) / std::max<uint32_t>(1, B * 5 / 8));
+  const uint32_t per = std::max<uint32_t>(1, B * 5 / 8);  // pairs per sample
+  const uint32_t want = std::max<uint32_t>(1, (dev::kSweepThreads / dev::kQ + per / 2) / per);
   uint32_t K = std::min<uint32_t>(want, 8);
   while (K > 1 && sweep_smem_k(ldr, B, R, K) > 112 * 1024) --K;
   return K;
