@@ -265,6 +265,32 @@ __device__ __forceinline__ double impurity_sum(const double* __restrict__ xl, co
   return __dsub_rn(__dadd_rn(__dsub_rn(xl[nl], sl), xl[nr]), sr);
 }
 
+// Impurity sum of a candidate in float from the float copy of the xlogx table (prefilter only).
+// Same operation structure as impurity_sum; |Xf - X| <= prefilter_eps(xl[n], k).
+template <int KC>
+__device__ __forceinline__ float impurity_sum_f(const float* __restrict__ xlf, const uint32_t* left,
+                                                const uint32_t* tot, int k, uint32_t nl,
+                                                uint32_t nr) {
+  float sl = 0.f, sr = 0.f;
+  if constexpr (KC == 2) {
+    sl = __ldg(xlf + left[0]) + __ldg(xlf + left[1]);
+    sr = __ldg(xlf + tot[0] - left[0]) + __ldg(xlf + tot[1] - left[1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < KC; ++c)
+      if (c < k) {
+        sl += __ldg(xlf + left[c]);
+        sr += __ldg(xlf + tot[c] - left[c]);
+      }
+  }
+  return ((__ldg(xlf + nl) - sl) + __ldg(xlf + nr)) - sr;
+}
+// Bound on |Xf - X|: 2k+2 table values each within 2^-24 relative of xl[n] (the largest table
+// entry used), and 2k+1 float operations on partial sums bounded by 2 xl[n] each; doubled margin.
+__device__ __forceinline__ double prefilter_eps(double xln, int k) {
+  return double(2 * (2 * k + 2) + 4 * (2 * k + 1)) * xln * 0x1p-24 + 0x1p-60;
+}
+
 __device__ __forceinline__ double gain_from_x(double parent, double X, double n) {
   return __dsub_rn(parent, __ddiv_rn(X, n));
 }
