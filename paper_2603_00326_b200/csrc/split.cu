@@ -21,6 +21,7 @@ namespace dev {
 
 // Count-vector scan of one histogram row, warp-cooperative. cnt is bin-major [nbins][k] in
 // shared memory, nb boundaries in bnd. Returns the reference's best candidate for this row.
+template <int KC>
 __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t nb, int k,
                                 int bpad, double parent, const double* __restrict__ xl,
                                 int lane) {
@@ -32,20 +33,20 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
   res._pad = 0;
   const int E = bpad / 32;
   const int b0 = lane * E;
-  uint32_t loc[kMaxClasses], pre[kMaxClasses], tot[kMaxClasses];
+  uint32_t loc[KC], pre[KC], tot[KC];
 #pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c) loc[c] = 0;
+  for (int c = 0; c < KC; ++c) loc[c] = 0;
   for (int e = 0; e < E; ++e) {
     const int b = b0 + e;
     if (b <= int(nb)) {
 #pragma unroll
-      for (int c = 0; c < kMaxClasses; ++c)
+      for (int c = 0; c < KC; ++c)
         if (c < k) loc[c] += cnt[b * k + c];
     }
   }
   uint32_t n = 0;
 #pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c) {
+  for (int c = 0; c < KC; ++c) {
     if (c < k) {
       pre[c] = warp_excl_scan_u32(loc[c], lane, &tot[c]);
       n += tot[c];
@@ -60,22 +61,22 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
   // pass 1: min impurity over candidate boundaries b < nb
   double xmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf
   {
-    uint32_t left[kMaxClasses];
+    uint32_t left[KC];
 #pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) left[c] = pre[c];
+    for (int c = 0; c < KC; ++c) left[c] = pre[c];
     for (int e = 0; e < E; ++e) {
       const int b = b0 + e;
       if (b >= int(nb)) break;
       uint32_t nl = 0;
 #pragma unroll
-      for (int c = 0; c < kMaxClasses; ++c)
+      for (int c = 0; c < KC; ++c)
         if (c < k) {
           left[c] += cnt[b * k + c];
           nl += left[c];
         }
       const uint32_t nr = n - nl;
       if (nl == 0 || nr == 0) continue;
-      const double X = impurity_sum<kMaxClasses>(xl, left, tot, k, nl, nr);
+      const double X = impurity_sum<KC>(xl, left, tot, k, nl, nr);
       xmin = fmin(xmin, X);
     }
   }
@@ -87,22 +88,22 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
   // pass 2: first boundary whose gain equals gbest
   uint32_t first = 0xffffffffu, first_nl = 0;
   {
-    uint32_t left[kMaxClasses];
+    uint32_t left[KC];
 #pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) left[c] = pre[c];
+    for (int c = 0; c < KC; ++c) left[c] = pre[c];
     for (int e = 0; e < E; ++e) {
       const int b = b0 + e;
       if (b >= int(nb)) break;
       uint32_t nl = 0;
 #pragma unroll
-      for (int c = 0; c < kMaxClasses; ++c)
+      for (int c = 0; c < KC; ++c)
         if (c < k) {
           left[c] += cnt[b * k + c];
           nl += left[c];
         }
       const uint32_t nr = n - nl;
       if (nl == 0 || nr == 0) continue;
-      const double X = impurity_sum<kMaxClasses>(xl, left, tot, k, nl, nr);
+      const double X = impurity_sum<KC>(xl, left, tot, k, nl, nr);
       if (X <= win && gain_from_x(parent, X, dn) == gbest) {
         first = uint32_t(b);
         first_nl = nl;
@@ -121,6 +122,7 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
 }
 
 // ------------------------------------------------------------------------------------------
+template <int KC>
 __global__ void __launch_bounds__(256) k_hist_count(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ node_hist_slot,
     const HistWork* __restrict__ work, const uint32_t* __restrict__ multi_slot,
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
 
   if (wk.n_chunks == 1) {
     if (nb > 0) {
-      const RowRes rr = hist_row_scan(my_cnt, gb, nb, k, bpad, nd.parent, xl, lane);
+      const RowRes rr = hist_row_scan<KC>(my_cnt, gb, nb, k, bpad, nd.parent, xl, lane);
       if (lane == 0) rowres[size_t(h) * R + r] = rr;
     } else if (row_ok && lane == 0) {
       RowRes z{};
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
     const uint32_t* g = gcnt + (size_t(ms) * R + r) * size_t(bpad) * k;
     for (int i = lane; i < int(nb + 1) * k; i += 32) my_cnt[i] = __ldcg(g + i);
     __syncwarp();
-    const RowRes rr = hist_row_scan(my_cnt, gb, nb, k, bpad, nd.parent, xl, lane);
+    const RowRes rr = hist_row_scan<KC>(my_cnt, gb, nb, k, bpad, nd.parent, xl, lane);
     if (lane == 0) rowres[size_t(h) * R + r] = rr;
   } else if (row_ok && lane == 0) {
     RowRes z{};
@@ -288,10 +290,12 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
   if (n_work == 0) return cudaSuccess;
   const int bpad = pow2_at_least(int(bins), 32);
   const size_t smem = hist_count_smem(bins, k, chunk_cap);
-  cudaFuncSetAttribute(dev::k_hist_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
-  dev::k_hist_count<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins,
-                                               bpad, k, chunk_cap, terms, row_ptr, lab, gbase, G,
-                                               bnd, nb, xl, gcnt, done, rowres);
+  // class-count specialised (k = 2 is the trunk workload; generic up to kMaxClasses)
+  auto kern = k == 2 ? dev::k_hist_count<2> : dev::k_hist_count<kMaxClasses>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
+  kern<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins, bpad, k,
+                                  chunk_cap, terms, row_ptr, lab, gbase, G, bnd, nb, xl, gcnt,
+                                  done, rowres);
   return cudaGetLastError();
 }
 
