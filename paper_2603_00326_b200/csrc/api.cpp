@@ -83,7 +83,9 @@ sofg::ThreadPool& pool_for(sofg_ctx* c, uint64_t n_workers) {
 
 sofg::WaveRunner& runner2(sofg_ctx* c) {
   if (!c->eng2) {
-    c->eng2.reset(new sofg::WaveRunner(c->eng->device(), c->eng->shared_data()));
+    // same stream as the first group: the groups' waves alternate on the GPU (no concurrent
+    // kernels), while each group's host phase overlaps the other group's wave
+    c->eng2.reset(new sofg::WaveRunner(c->eng->device(), c->eng->shared_data(), c->eng->stream()));
     c->eng2->collect_stats = c->eng->collect_stats;
     c->eng2->sector_accounting = c->eng->sector_accounting;
   }
@@ -333,7 +335,7 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
       // Two tree groups in flight (SOFG_GROUPS=1 disables): group 2 runs on its own stream and
       // host threads so each group's host-side level work overlaps the other's kernels.
       const char* ge = std::getenv("SOFG_GROUPS");
-      const int groups = ge ? std::max(1, std::atoi(ge)) : 1;  // measured: 2 concurrent groups are not faster
+      const int groups = ge ? std::max(1, std::atoi(ge)) : 1;  // 2 groups measured slower (half-size waves)
       if (groups >= 2 && B >= 16) {
         const size_t h = B / 2;
         std::vector<std::vector<uint32_t>> r1(std::make_move_iterator(roots.begin()),

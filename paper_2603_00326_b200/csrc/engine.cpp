@@ -9,7 +9,7 @@
 
 namespace sofg {
 
-WaveRunner::WaveRunner(int device, std::shared_ptr<DeviceData> data)
+WaveRunner::WaveRunner(int device, std::shared_ptr<DeviceData> data, cudaStream_t stream)
     : device_(device), data_(data ? std::move(data) : std::make_shared<DeviceData>()) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   // The split search is a scattered 4-byte gather: ask L2 to fetch single 32-byte sectors from
@@ -20,7 +20,13 @@ WaveRunner::WaveRunner(int device, std::shared_ptr<DeviceData> data)
     cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
     cudaGetLastError();
   }
-  cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (stream) {
+    st_ = stream;
+    own_stream_ = false;
+  } else {
+    cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  cuda_check(cudaEventCreateWithFlags(&done_ev_, cudaEventDisableTiming), "cudaEventCreate");
   cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device);
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   for (auto& e : mk_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
@@ -39,7 +45,8 @@ WaveRunner::~WaveRunner() {
     if (e) cudaEventDestroy(e);
   for (auto& e : mk_)
     if (e) cudaEventDestroy(e);
-  if (st_) cudaStreamDestroy(st_);
+  if (done_ev_) cudaEventDestroy(done_ev_);
+  if (st_ && own_stream_) cudaStreamDestroy(st_);
 }
 
 namespace {
@@ -385,6 +392,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   NodeRes* hr = h_res_.ensure(size_t(N));
   cuda_check(cudaMemcpyAsync(hr, d_res, sizeof(NodeRes) * N, cudaMemcpyDeviceToHost, st_),
              "D2H res");
+  cuda_check(cudaEventRecord(done_ev_, st_), "record wave end");
   pend_dres_ = d_res;
   pend_launches_ = launches;
   pend_hist_ = nh;
@@ -396,10 +404,14 @@ void WaveRunner::collect(const WaveSpec& w, std::vector<NodeRes>& res) {
   res.assign(r, r + pend_n_);
 }
 
+void WaveRunner::wait_wave() {
+  if (pend_n_ > 0) cuda_check(cudaEventSynchronize(done_ev_), "wave sync");
+}
+
 const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
   const int N = pend_n_;
   if (N == 0) return h_res_.p;
-  cuda_check(cudaStreamSynchronize(st_), "wave sync");
+  cuda_check(cudaEventSynchronize(done_ev_), "wave sync");
   const NodeRes* res = h_res_.p;
   // winning rows longer than NodeRes carries inline: one gather + one D2H for the whole wave
   long_off_.assign(1, 0u);
@@ -437,7 +449,8 @@ const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
                "win_terms");
     cuda_check(cudaMemcpyAsync(hb + 2 * L + 1, db + 2 * L + 1, 4 * T, cudaMemcpyDeviceToHost, st_),
                "D2H long rows");
-    cuda_check(cudaStreamSynchronize(st_), "long rows sync");
+    cuda_check(cudaEventRecord(done_ev_, st_), "record long rows");
+    cuda_check(cudaEventSynchronize(done_ev_), "long rows sync");
     long_terms_.assign(hb + 2 * L + 1, hb + 2 * L + 1 + T);
   } else {
     long_pos_.clear();

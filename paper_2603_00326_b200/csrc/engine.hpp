@@ -165,7 +165,10 @@ class WaveRunner {
  public:
   // Runners created with a shared DeviceData train on the same resident table on their own stream
   // (several tree groups in flight on one GPU).
-  explicit WaveRunner(int device, std::shared_ptr<DeviceData> data = nullptr);
+  // `stream`, when given, is shared (not owned): runners on one stream execute their waves in
+  // submission order, and collect() waits on this runner's own completion event only.
+  explicit WaveRunner(int device, std::shared_ptr<DeviceData> data = nullptr,
+                      cudaStream_t stream = nullptr);
   ~WaveRunner();
   WaveRunner(const WaveRunner&) = delete;
   WaveRunner& operator=(const WaveRunner&) = delete;
@@ -187,6 +190,9 @@ class WaveRunner {
   void collect(const WaveSpec& w, std::vector<NodeRes>& res);
   // Same wait, no copy: the node results in page-locked memory, valid until the next submit().
   const NodeRes* collect_view(const WaveSpec& w);
+  // Only the wait for the wave (no host pool use): callers sharing a pool wait first, then
+  // take their host turn and call collect_view().
+  void wait_wave();
   // Page-locked staging reused across calls (root segments).
   PinnedBuf<unsigned char> staging;
   // Terms of node `node`'s winning row in the last collected wave, for rows longer than the
@@ -210,6 +216,8 @@ class WaveRunner {
   int device_;
   ThreadPool* pool_ = nullptr;
   cudaStream_t st_ = nullptr;
+  bool own_stream_ = true;
+  cudaEvent_t done_ev_ = nullptr;  // end of this runner's last submitted wave
   cudaEvent_t ev_[6]{};
   // fine-grained per-launch timing (stats mode)
   static constexpr int kMaxMarks = 32;

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
 #ifndef SOFG_SWEEP_DIRECT
 #define SOFG_SWEEP_DIRECT 0  // 1: rows straight to V with 4-byte stores (measured 2x slower: partial-sector writes)
 #endif
-constexpr int kSweepThreads = 256;
+constexpr int kSweepThreadsMax = 256;  // CTA size: 256 for ~60+ trees per wave, 128 below
 
 struct Pair {
   uint32_t node, j, k, pad;
@@ -216,9 +216,9 @@ __host__ __device__ __forceinline__ uint32_t sweep_out_pitch(uint32_t R) {
   return ((R + kQ - 1) / kQ + 3u) / 4u * 4u + 4u;  // floats per lane (16B multiple, bank shift)
 }
 
-// smem: xs[K][ldr] | pairs[K*B] | out[kSweepThreads][pitch]
-template <typename E>
-__global__ void __launch_bounds__(kSweepThreads) k_row_sweep(
+// smem: xs[K][ldr] | pairs[K*B] | out[NT][pitch]
+template <typename E, int NT>
+__global__ void __launch_bounds__(NT) k_row_sweep(
     const float* __restrict__ XR, uint64_t ldr, uint32_t N, uint32_t K,
     const uint32_t* __restrict__ inv, uint32_t B, const uint32_t* __restrict__ pos_node,
     const NodeIn* __restrict__ nodes, const uint64_t* __restrict__ vbase,
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_row_sweep(
   const uint32_t KB = K * B;
   const uint32_t c = threadIdx.x % kQ;  // my sub-list
   const uint32_t ra = q_row(R, c), rb = q_row(R, c + 1);
-  constexpr uint32_t kPairsPerRound = kSweepThreads / kQ;
+  constexpr uint32_t kPairsPerRound = NT / kQ;
 
   for (uint32_t s0 = blockIdx.x * K; s0 < N; s0 += gridDim.x * K) {
     if (threadIdx.x == 0) s_cnt = 0;
@@ -247,10 +247,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_row_sweep(
     {
       const float4* src = reinterpret_cast<const float4*>(XR + uint64_t(s0) * ldr);
       float4* dst = reinterpret_cast<float4*>(xs);
-      for (uint32_t v = threadIdx.x; v < ks * nvec; v += kSweepThreads) cp_async16(dst + v, src + v);
+      for (uint32_t v = threadIdx.x; v < ks * nvec; v += NT) cp_async16(dst + v, src + v);
     }
     // ---- (node, j) pairs of the K samples: inv -> level position -> wave node
-    for (uint32_t e0 = 0; e0 < KB; e0 += kSweepThreads) {
+    for (uint32_t e0 = 0; e0 < KB; e0 += NT) {
       const uint32_t e = e0 + threadIdx.x;
       const uint32_t k = e / B;
       uint32_t node = ~0u, p = ~0u;
@@ -487,16 +487,18 @@ cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* t
   return cudaGetLastError();
 }
 
+static int sweep_threads(uint32_t B) { return B * 5 / 8 > 40 ? 256 : 128; }
+
 static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
   return size_t(K) * ldr * 4 + size_t(K) * B * sizeof(dev::Pair) +
-         (SOFG_SWEEP_DIRECT ? 0 : size_t(dev::kSweepThreads) * dev::sweep_out_pitch(R) * 4);
+         (SOFG_SWEEP_DIRECT ? 0 : size_t(sweep_threads(B)) * dev::sweep_out_pitch(R) * 4);
 }
 
 // Samples per CTA iteration: enough (node, sample) pairs to fill the CTA's lanes (a sample sits
 // in ~63% of the batch's trees), within shared memory.
 static uint32_t sweep_k(uint64_t ldr, uint32_t B, uint32_t R) {
   const uint32_t per = std::max<uint32_t>(1, B * 5 / 8);  // pairs per sample
-  const uint32_t want = std::max<uint32_t>(1, (dev::kSweepThreads / dev::kQ + per / 2) / per);
+  const uint32_t want = std::max<uint32_t>(1, (uint32_t(sweep_threads(B)) / dev::kQ + per / 2) / per);
   uint32_t K = std::min<uint32_t>(want, 8);
   while (K > 1 && sweep_smem_k(ldr, B, R, K) > 112 * 1024) --K;
   return K;
@@ -506,7 +508,7 @@ size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R) {
   return sweep_smem_k(ldr, B, R, sweep_k(ldr, B, R));
 }
 
-template <typename E>
+template <typename E, int NT>
 static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
                                   uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
                                   const uint64_t* vbase, const void* aug, const uint4* qoff,
@@ -514,14 +516,14 @@ static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, con
   const uint32_t K = sweep_k(ldr, B, R);
   const size_t smem = sweep_smem_k(ldr, B, R, K);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(dev::k_row_sweep<E>,
+  cudaError_t e = cudaFuncSetAttribute(dev::k_row_sweep<E, NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_row_sweep<E>, dev::kSweepThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_row_sweep<E, NT>, NT, smem);
   const uint32_t groups = (N + K - 1) / K;
   const unsigned grid = unsigned(std::max(1, std::min<int>(int(groups), n_sm * std::max(per_sm, 1))));
-  dev::k_row_sweep<E><<<grid, dev::kSweepThreads, smem, st>>>(
+  dev::k_row_sweep<E, NT><<<grid, NT, smem, st>>>(
       XR, ldr, N, K, inv, B, pos_node, nodes, vbase, static_cast<const E*>(aug), qoff, R, V);
   return cudaGetLastError();
 }
@@ -530,8 +532,12 @@ cudaError_t launch_row_sweep(const float* XR, uint64_t ldr, uint32_t N, const ui
                              uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
                              const uint64_t* vbase, const void* aug, const uint4* qoff, uint32_t R,
                              uint32_t d, float* V, int n_sm, cudaStream_t st) {
-  return aug_narrow(d) ? launch_sweep_t<uint16_t>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st)
-                       : launch_sweep_t<uint32_t>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st);
+  const bool wide = sweep_threads(B) == 256;
+  if (aug_narrow(d))
+    return wide ? launch_sweep_t<uint16_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st)
+                : launch_sweep_t<uint16_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st);
+  return wide ? launch_sweep_t<uint32_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st)
+              : launch_sweep_t<uint32_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st);
 }
 
 cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_tiles,

@@ -342,9 +342,12 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       });
       times.ms_spec += ms_since(t0);
       t0 = Clock::now();
-      if (turn) host_turn.unlock();  // the other groups prepare their waves meanwhile
+      if (turn) {
+        host_turn.unlock();  // the other groups prepare their waves meanwhile
+        eng.wait_wave();
+        host_turn.lock();
+      }
       const NodeRes* res = eng.collect_view(w);
-      if (turn) host_turn.lock();
       times.ms_wait += ms_since(t0);
 
       t0 = Clock::now();
