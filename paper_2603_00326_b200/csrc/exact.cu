@@ -41,8 +41,47 @@ struct Best {
 // Pass 1 evaluates every candidate gap in float; only candidates whose float impurity lies within
 // 2 eps of the row's float minimum (a superset of every candidate whose exact gain can equal the
 // row's best) are evaluated exactly in double, in the reference's operation order.
-template <int E, int KC>
-__device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, int k,
+// Key policies for scan_row.
+// Packed keys: order_key(v) << 32 | label (the reference's sort key, split.hpp:173-176).
+struct Key64Ops {
+  __device__ int cls(uint64_t k) const { return int(k & 0xffu); }
+  __device__ bool gap(uint64_t a, uint64_t b) const {
+    return order_key_inv(uint32_t(a >> 32)) < order_key_inv(uint32_t(b >> 32));
+  }
+  __device__ void values(uint64_t a, uint64_t b, int, float* fa, float* fb) const {
+    *fa = order_key_inv(uint32_t(a >> 32));
+    *fb = order_key_inv(uint32_t(b >> 32));
+  }
+};
+// Folded 32-bit keys for two classes: (order_key(v) & ~1) | label. Valid only when no two
+// samples of the row share the upper 31 key bits and no value is +-0 or +-denorm_min (checked by
+// the caller): then sorted order equals value order, every neighbouring pair is a gap between
+// distinct values, and the winner's exact values are recovered from the original keys.
+template <int E>
+struct Key32FoldOps {
+  const uint32_t (&orig)[E];  // this lane's unsorted order keys
+  __device__ int cls(uint32_t k) const { return int(k & 1u); }
+  __device__ bool gap(uint32_t, uint32_t) const { return true; }
+  __device__ uint32_t recover(uint32_t folded) const {
+    uint32_t hit = 0;
+    bool found = false;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if ((orig[e] >> 1) == (folded >> 1)) {
+        hit = orig[e];
+        found = true;
+      }
+    const unsigned m = __ballot_sync(0xffffffffu, found);
+    return __shfl_sync(0xffffffffu, hit, __ffs(m) - 1);
+  }
+  __device__ void values(uint32_t a, uint32_t b, int, float* fa, float* fb) const {
+    *fa = order_key_inv(recover(a));
+    *fb = order_key_inv(recover(b));
+  }
+};
+
+template <int E, int KC, class K, class Ops>
+__device__ __forceinline__ void scan_row(const K (&key)[E], const Ops& ops, uint32_t n, int k,
                                          const uint32_t* tot, double parent,
                                          const double* __restrict__ xl,
                                          const float* __restrict__ xlf, int row, int lane,
@@ -55,7 +94,7 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     if (uint32_t(p0 + e) < n) {
-      const int c = int(key[e] & 0xffu);
+      const int c = ops.cls(key[e]);
 #pragma unroll
       for (int cc = 0; cc < KC; ++cc) loc[cc] += (cc == c);
     }
@@ -65,7 +104,7 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
     uint32_t t;
     pre[c] = warp_excl_scan_u32(loc[c], lane, &t);
   }
-  const uint64_t next_first = __shfl_down_sync(0xffffffffu, key[0], 1);
+  const K next_first = __shfl_down_sync(0xffffffffu, key[0], 1);
   const double dn = double(n);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const float inff = __int_as_float(0x7f800000);
@@ -82,11 +121,11 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
       Xf[e] = inff;
       const uint32_t p = uint32_t(p0 + e);
       if (p + 1 < n) {
-        const int c = int(key[e] & 0xffu);
+        const int c = ops.cls(key[e]);
 #pragma unroll
         for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
-        const uint64_t kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
-        if (order_key_inv(uint32_t(key[e] >> 32)) < order_key_inv(uint32_t(kb >> 32))) {
+        const K kb = (e + 1 < E) ? key[(e + 1) % E] : next_first;
+        if (ops.gap(key[e], kb)) {
           if constexpr (KC == 2) {
             uint32_t lf[2] = {(p + 1) - left[1], left[1]};
             Xf[e] = impurity_sum_f<2>(xlf, lf, tot, k, p + 1, n - (p + 1));
@@ -114,7 +153,7 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
     for (int e = 0; e < E; ++e) {
       const uint32_t p = uint32_t(p0 + e);
       if (p + 1 < n) {
-        const int c = int(key[e] & 0xffu);
+        const int c = ops.cls(key[e]);
 #pragma unroll
         for (int cc = 0; cc < KC; ++cc) left[cc] += (cc == c);
         if (double(Xf[e]) <= lim) {
@@ -167,7 +206,7 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   const uint32_t fp = warp_min_u32(first);
   const int src = __ffs(__ballot_sync(0xffffffffu, first == fp)) - 1;
   // the two keys around the winning gap (positions fp, fp+1)
-  uint64_t ka = 0, kb = 0;
+  K ka = 0, kb = 0;
 #pragma unroll
   for (int e = 0; e < E; ++e)
     if (e == fe) {
@@ -179,7 +218,9 @@ __device__ __forceinline__ void scan_row(const uint64_t (&key)[E], uint32_t n, i
   b.xmin = xmin;
   b.row = row;
   b.gain = g;
-  b.thr = midpoint_down(order_key_inv(uint32_t(ka >> 32)), order_key_inv(uint32_t(kb >> 32)));
+  float fa, fb;
+  ops.values(ka, kb, lane, &fa, &fb);
+  b.thr = midpoint_down(fa, fb);
   b.nl = fp + 1;
 }
 
@@ -267,6 +308,43 @@ __global__ void __launch_bounds__(128) k_exact_reg(
       for (int gg = 0; gg < GR; ++gg)
         if (gg == g) ntg = nt[gg];
       if (r >= R || ntg == 0) continue;  // empty rows are skipped in exact mode (split.hpp:308)
+      if constexpr (KC == 2) {
+        // fast path: 32-bit folded keys (half the shuffle/compare work of the packed 64-bit key)
+        uint32_t ok[E], k32[E];
+        bool special = false;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          float v = 0.f;
+#pragma unroll
+          for (int gg = 0; gg < GR; ++gg)
+            if (gg == g) v = val[gg][e];
+          if (uint32_t(lane * E + e) < n) {
+            ok[e] = order_key(v);
+            const uint32_t top = ok[e] >> 1;
+            special |= top == 0x3FFFFFFFu || top == 0x40000000u;  // +-0, +-denorm_min
+            k32[e] = (ok[e] & ~1u) | uint32_t(__ldg(lab + nd.begin + lane * E + e));
+          } else {
+            ok[e] = 0xFFFFFFFFu;
+            k32[e] = 0xFFFFFFFFu;
+          }
+        }
+        if (!__any_sync(0xffffffffu, special)) {
+          reg_bitonic_sort_k<E, uint32_t, (E >= 8)>(k32, lane);
+          // collision: neighbours (among the n real samples) with equal upper 31 bits
+          bool coll = false;
+          const uint32_t nf = __shfl_down_sync(0xffffffffu, k32[0], 1);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const uint32_t p = uint32_t(lane * E + e);
+            const uint32_t nx = (e + 1 < E) ? k32[(e + 1) % E] : nf;
+            coll |= p + 1 < n && (k32[e] >> 1) == (nx >> 1);
+          }
+          if (!__any_sync(0xffffffffu, coll)) {
+            scan_row<E, 2>(k32, Key32FoldOps<E>{ok}, n, k, tot, nd.parent, xl, xlf, int(r), lane, best);
+            continue;
+          }
+        }
+      }
       uint64_t key[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -281,7 +359,7 @@ __global__ void __launch_bounds__(128) k_exact_reg(
         }
       }
       reg_bitonic_sort<E>(key, lane);
-      scan_row<E, KC>(key, n, k, tot, nd.parent, xl, xlf, int(r), lane, best);
+      scan_row<E, KC>(key, Key64Ops{}, n, k, tot, nd.parent, xl, xlf, int(r), lane, best);
     }
   }
 
