@@ -46,8 +46,8 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=1_000_000)
-    p.add_argument("--d", type=int, default=4096)
+    p.add_argument("--samples", "--n", dest="n", type=int, default=1_000_000)
+    p.add_argument("--features", "--d", dest="d", type=int, default=4096)
     p.add_argument("--trees", type=int, default=100, help="trees per GPU per step")
     p.add_argument("--breakeven", type=int, default=512,
                    help="dynamic-switch threshold; 512 = B200 calibration (DESIGN.md 3, calibrate.py)")
@@ -222,7 +222,8 @@ def run_reference(args, rank, world):
             "steps_requested": args.steps, "warmup": 0, "ms_per_step": 1000 * statistics.median(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
             "data": "synthetic trunk model (numpy, host)", "impl": "reference",
-            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, trees to purity (BASELINE config 3)",
+            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, trees to purity"
+                                   + (" (BASELINE config 3)" if (args.n, args.d) == (1_000_000, 4096) else ""),
                        "n_samples": args.n, "n_features": args.d, "trees_per_step": n_trees,
                        "breakeven": args.breakeven, "mode": args.mode, "seed": args.seed},
             "cpu_baseline": {"value": v, "unit": "trees/s", "cores": threads, "kind": kind,
@@ -239,7 +240,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        # SOFG_BENCH_BACKEND / SOFG_BENCH_DEVICE: test hooks to run several ranks on one GPU
+        backend = os.environ.get("SOFG_BENCH_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
+        dist.init_process_group(backend)
     if args.impl == "reference":
         run_reference(args, rank, world)
         if dist:
@@ -251,6 +254,8 @@ def main():
 
     import paper_2603_00326_b200 as sofg
 
+    if os.environ.get("SOFG_BENCH_DEVICE"):
+        local = int(os.environ["SOFG_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     ctx = sofg.Context(local)
     t0 = time.perf_counter()
@@ -263,8 +268,10 @@ def main():
 
     def cfg_for(step):
         b = step * per_step + rank * T
+        # host threads split between the ranks sharing this host (one rank per GPU)
+        workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
         return sofg.TrainConfig(n_trees=total_trees, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
-                                n_workers=0, tree_begin=b, tree_end=b + T)
+                                n_workers=workers, tree_begin=b, tree_end=b + T)
 
     def barrier():
         if dist:
@@ -273,7 +280,8 @@ def main():
     def max_over_ranks(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -368,11 +376,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 values / f64 accumulate+gain",
             "data": "synthetic trunk model generated in HBM (counter-based RNG), inputs > L2",
-            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, {T} trees per GPU to purity "
-                                   f"(BASELINE config 3)",
+            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, {T} trees per GPU to purity"
+                                   + (" (BASELINE config 3)" if (args.n, args.d) == (1_000_000, 4096) else ""),
                        "n_samples": args.n, "n_features": args.d, "trees_per_gpu_per_step": T,
                        "mode": args.mode, "breakeven": args.breakeven, "bin_count": 256, "seed": args.seed,
-                       "parallelism": f"tree-sharded x{world}", "l2": "inputs 16.4 GB > 126 MB L2",
+                       "parallelism": f"tree-sharded x{world}",
+                       "l2": f"inputs {args.n * args.d * 4 / 1e9:.2f} GB table (+ row-major copy) vs 126 MB L2",
                        "nodes_per_step": nodes / args.steps, "datagen_s": round(gen_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
             "clocks": clocks.summary()}
