@@ -353,12 +353,35 @@ void WaveRunner::submit(const WaveSpec& w) {
   }
   if (timing) cudaEventRecord(ev_[3], st_);
   {
+    // Exact nodes above 64 samples (two classes): per-row bounds first, so rows that cannot
+    // hold the node's best split are not sorted (k_exact_prune, exact.cu).
+    const int kPruneFrom = 2;  // bucket of n <= 128
+    size_t prune_off = 0, prune_n = 0;
+    for (int b = 0; b < 7; ++b) {
+      if (b < kPruneFrom) prune_off += exact_b_count[size_t(b)];
+      else prune_n += exact_b_count[size_t(b)];
+    }
+    const bool prune = k == 2 && prune_n > 0 && !(std::getenv("SOFG_PRUNE") && std::atoi(std::getenv("SOFG_PRUNE")) == 0);
+    float* d_rowlb = nullptr;
+    unsigned long long* d_xstar = nullptr;
+    if (prune) {
+      d_rowlb = rowlb_.ensure(prune_n * R);
+      d_xstar = xstar_.ensure(prune_n);
+      cuda_check(launch_exact_prune(d_nodes, d_exact + prune_off, int(prune_n), R, d_rp, w.lab_in,
+                                    d_gbase, d_G, D.xl.p, d_rowlb, d_xstar, st_),
+                 "exact_prune");
+      ++launches;
+      mark("exact_prune");
+    }
     size_t off = 0;
     for (int b = 0; b < 7; ++b) {
       const size_t m = exact_b_count[size_t(b)];
       if (!m) continue;
+      const bool pb = prune && b >= kPruneFrom;
       cuda_check(launch_exact_bucket(b, d_nodes, d_exact + off, int(m), R, k, d_terms, d_rp,
-                                     w.lab_in, d_gbase, d_G, D.xl.p, D.xlf.p, d_res, st_),
+                                     w.lab_in, d_gbase, d_G, D.xl.p, D.xlf.p, d_res,
+                                     pb ? d_rowlb + (off - prune_off) * R : nullptr,
+                                     pb ? d_xstar + (off - prune_off) : nullptr, st_),
                  "exact_bucket");
       off += m;
       ++launches;

@@ -241,6 +241,8 @@ class WaveRunner {
   DevBuf<uint32_t> pos_node_;  // level position -> wave node (sweep mode)
   DevBuf<unsigned char> aug_;  // augmented term lists (sweep mode)
   DevBuf<uint4> qoff_;         // per-node sub-list offsets (sweep mode)
+  DevBuf<float> rowlb_;                // exact branch-and-bound: per (node, row) lower bounds
+  DevBuf<unsigned long long> xstar_;   // and per node the best pivot-candidate impurity
   int n_sm_ = 148;
   const uint32_t* last_terms_ = nullptr;
   const NodeIn* last_nodes_ = nullptr;

@@ -224,6 +224,95 @@ __device__ __forceinline__ void scan_row(const K (&key)[E], const Ops& ops, uint
   b.nl = fp + 1;
 }
 
+// ------------------------------------------------------------------------------------------
+// Row bounds for the exact splitter (branch and bound). For each (node, row): 31 pivots (row
+// values at fixed positions, sorted) split the row into 32 value buckets; one pass counts each
+// bucket's classes. The split "v < pivot" is a real candidate gap, so its exact impurity X is an
+// achievable value: xstar[node] = min over rows of those. Every other gap lies inside one bucket,
+// whose left class counts (l0, l1) range over a box; X = sum over children of n_c * H(child) is
+// concave in (l0, l1), so its minimum over the box is at a corner. rowlb = min(pivot X, bucket
+// corner minima) bounds every candidate of the row from below. A row with rowlb > xstar (+ a
+// margin far above rounding) cannot contain the node's best split nor tie it (gain = parent - X/n
+// is monotone), and the exact kernels skip sorting it.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ double prune_limit(unsigned long long xs_bits) {
+  const double xs = __longlong_as_double((long long)xs_bits);
+  return xs + fabs(xs) * 0x1p-30 + 0x1p-30;
+}
+
+template <int KC>
+__device__ __forceinline__ double x_at(const double* __restrict__ xl, uint32_t l0, uint32_t l1,
+                                       const uint32_t* tot, int k, uint32_t n) {
+  uint32_t left[2] = {l0, l1};
+  return impurity_sum<2>(xl, left, tot, k, l0 + l1, n - (l0 + l1));
+}
+
+__global__ void __launch_bounds__(256) k_exact_prune(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
+    const uint32_t* __restrict__ row_ptr, const uint8_t* __restrict__ lab,
+    const uint64_t* __restrict__ gbase, const float* __restrict__ G,
+    const double* __restrict__ xl, float* __restrict__ rowlb, unsigned long long* __restrict__ xstar) {
+  __shared__ uint32_t s_cnt[8][32][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t gw = uint64_t(blockIdx.x) * 8 + uint64_t(w);
+  if (gw >= uint64_t(n_list) * R) return;
+  const uint32_t li = uint32_t(gw / R), r = uint32_t(gw % R);
+  const uint32_t node = list[li];
+  const NodeIn nd = nodes[node];
+  const uint32_t n = nd.n;
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  float* out = rowlb + size_t(li) * R + r;
+  if (__ldg(rp + r + 1) == __ldg(rp + r)) {  // empty: skipped by the exact kernels anyway
+    if (lane == 0) *out = __int_as_float(0x7f800000);
+    return;
+  }
+  const uint32_t Rp = vpitch(R);
+  const float* Vn = G + gbase[node] + r;
+  // pivots: the values at positions n*(i+1)/32, i < 31, sorted (lane 31: +inf sentinel)
+  uint32_t piv = 0xFFFFFFFFu;
+  if (lane < 31) piv = order_key(__ldg(Vn + uint64_t((uint64_t(n) * uint32_t(lane + 1)) / 32) * Rp));
+  piv = warp_sort32(piv, lane);
+  s_cnt[w][lane][0] = 0;
+  s_cnt[w][lane][1] = 0;
+  __syncwarp();
+  for (uint32_t j0 = 0; j0 < n; j0 += 32) {  // warp-uniform trip count (shuffles below)
+    const uint32_t j = j0 + uint32_t(lane);
+    const bool ok = j < n;
+    const uint32_t key = ok ? order_key(__ldg(Vn + uint64_t(j) * Rp)) : 0u;
+    const uint32_t y = ok ? uint32_t(__ldg(lab + nd.begin + j)) & 1u : 0u;
+    uint32_t lo = 0;
+#pragma unroll
+    for (uint32_t step = 16; step > 0; step >>= 1) {
+      const uint32_t p = __shfl_sync(0xffffffffu, piv, int(lo + step - 1));
+      if (p <= key) lo += step;
+    }
+    if (ok) atomicAdd(&s_cnt[w][lo][y], 1u);
+  }
+  __syncwarp();
+  const uint32_t c0 = s_cnt[w][lane][0], c1 = s_cnt[w][lane][1];
+  uint32_t t0, t1;
+  const uint32_t a0 = warp_excl_scan_u32(c0, lane, &t0);
+  const uint32_t a1 = warp_excl_scan_u32(c1, lane, &t1);
+  const uint32_t tot[2] = {t0, t1};
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  // pivot candidate: split after bucket `lane` ("v < pivot_lane"), a real gap when 0 < nl < n
+  const uint32_t L0 = a0 + c0, L1 = a1 + c1;
+  double xp = inf;
+  if (lane < 31 && L0 + L1 > 0 && L0 + L1 < n) xp = x_at<2>(xl, L0, L1, tot, 2, n);
+  // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
+  double lb = xp;
+  if (c0 + c1 >= 2) {
+    lb = fmin(lb, fmin(fmin(x_at<2>(xl, a0, a1, tot, 2, n), x_at<2>(xl, a0, a1 + c1, tot, 2, n)),
+                       fmin(x_at<2>(xl, a0 + c0, a1, tot, 2, n), x_at<2>(xl, a0 + c0, a1 + c1, tot, 2, n))));
+  }
+  lb = warp_min_f64(lb);
+  xp = warp_min_f64(xp);
+  if (lane == 0) {
+    *out = __double2float_rd(lb);  // rounded down: a conservative bound
+    if (xp < inf) atomicMin(xstar + li, (unsigned long long)__double_as_longlong(xp));
+  }
+}
+
 // E keys per lane, G rows in flight per warp, WPN warps per node, KC class-count registers.
 template <int E, int GR, int WPN, int KC>
 __global__ void __launch_bounds__(128) k_exact_reg(
@@ -231,7 +320,8 @@ __global__ void __launch_bounds__(128) k_exact_reg(
     int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
     const float* __restrict__ G, const double* __restrict__ xl, const float* __restrict__ xlf,
-    NodeRes* __restrict__ res) {
+    NodeRes* __restrict__ res, const float* __restrict__ rowlb,
+    const unsigned long long* __restrict__ xstar) {
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int li = (WPN == 1) ? int(blockIdx.x) * 4 + w : int(blockIdx.x);
@@ -308,6 +398,7 @@ __global__ void __launch_bounds__(128) k_exact_reg(
       for (int gg = 0; gg < GR; ++gg)
         if (gg == g) ntg = nt[gg];
       if (r >= R || ntg == 0) continue;  // empty rows are skipped in exact mode (split.hpp:308)
+      if (rowlb && double(rowlb[size_t(li) * R + r]) > prune_limit(xstar[li])) continue;  // bound
       if constexpr (KC == 2) {
         // fast path: 32-bit folded keys (half the shuffle/compare work of the packed 64-bit key)
         uint32_t ok[E], k32[E];
@@ -411,7 +502,8 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
     int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
     const float* __restrict__ G, const double* __restrict__ xl, const float* __restrict__ xlf,
-    NodeRes* __restrict__ res) {
+    NodeRes* __restrict__ res, const float* __restrict__ rowlb,
+    const unsigned long long* __restrict__ xstar) {
   constexpr int E = 8;
   constexpr int TEAMS = 8 / W;
   constexpr int P = 32 * E * W;  // positions per team
@@ -482,6 +574,7 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
     const uint32_t tb = rp[r];
     const int nt = int(rp[r + 1] - tb);
     if (nt == 0) continue;  // uniform per team; split.hpp:308
+    if (rowlb && double(rowlb[size_t(blockIdx.x) * R + r]) > prune_limit(xstar[blockIdx.x])) continue;
     // ---- projected values of row r (V block, sample-major) -> radix layout
     //      position q = wt*256 + e*32 + lane (warp-blocked, round-striped)
 #pragma unroll
@@ -709,9 +802,10 @@ template <int W, int KC>
 cudaError_t launch_team(const NodeIn* nodes, const uint32_t* list, int n, uint32_t R, int k,
                         const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
                         const uint64_t* gbase, const float* G, const double* xl, const float* xlf,
-                        NodeRes* res, cudaStream_t st) {
+                        NodeRes* res, const float* rowlb, const unsigned long long* xstar,
+                        cudaStream_t st) {
   k_exact_team<W, KC><<<n, 256, 0, st>>>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl,
-                                         xlf, res);
+                                         xlf, res, rowlb, xstar);
   return cudaGetLastError();
 }
 
@@ -719,10 +813,11 @@ template <int E, int GR, int WPN, int KC>
 cudaError_t launch_bucket(const NodeIn* nodes, const uint32_t* list, int n, uint32_t R, int k,
                           const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
                           const uint64_t* gbase, const float* G, const double* xl, const float* xlf,
-                          NodeRes* res, cudaStream_t st) {
+                          NodeRes* res, const float* rowlb, const unsigned long long* xstar,
+                          cudaStream_t st) {
   const int grid = WPN == 1 ? (n + 3) / 4 : n;
   k_exact_reg<E, GR, WPN, KC><<<grid, 128, 0, st>>>(nodes, list, n, R, k, terms, row_ptr, lab,
-                                                     gbase, G, xl, xlf, res);
+                                                     gbase, G, xl, xlf, res, rowlb, xstar);
   return cudaGetLastError();
 }
 
@@ -730,20 +825,34 @@ template <int KC>
 cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
                              uint32_t R, int k, const uint32_t* terms, const uint32_t* row_ptr,
                              const uint8_t* lab, const uint64_t* gbase, const float* G,
-                             const double* xl, const float* xlf, NodeRes* res, cudaStream_t st) {
+                             const double* xl, const float* xlf, NodeRes* res, const float* rowlb,
+                             const unsigned long long* xstar, cudaStream_t st) {
   switch (bucket) {
-    case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
-    case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
-    case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
-    case 3: return std::getenv("SOFG_TEAM256") ? launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st) : launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
-    case 4: return std::getenv("SOFG_REG512") ? launch_bucket<16, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st) : launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);  // register E=16 measured slower
-    case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
-    case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, st);
+    case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 3: return std::getenv("SOFG_TEAM256") ? launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st) : launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 4: return std::getenv("SOFG_REG512") ? launch_bucket<16, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st) : launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);  // register E=16 measured slower
+    case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 }  // namespace dev
+
+cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_list, uint32_t R,
+                               const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
+                               const float* G, const double* xl, float* rowlb,
+                               unsigned long long* xstar, cudaStream_t st) {
+  if (n_list == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(xstar, 0x7f, sizeof(unsigned long long) * n_list, st);  // ~ +huge
+  if (e != cudaSuccess) return e;
+  const uint64_t warps = uint64_t(n_list) * R;
+  dev::k_exact_prune<<<unsigned((warps + 7) / 8), 256, 0, st>>>(nodes, list, n_list, R, row_ptr, lab,
+                                                                gbase, G, xl, rowlb, xstar);
+  return cudaGetLastError();
+}
 
 int exact_bucket(uint32_t n) {
   int b = 0;
@@ -759,13 +868,14 @@ cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t*
                                 uint32_t R, int k, const uint32_t* terms,
                                 const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
                                 const float* G, const double* xl, const float* xlf, NodeRes* res,
+                                const float* rowlb, const unsigned long long* xstar,
                                 cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   if (k == 2)
     return dev::launch_bucket_kc<2>(bucket, nodes, list, n, R, k, terms, row_ptr, lab, gbase, G,
-                                    xl, xlf, res, st);
+                                    xl, xlf, res, rowlb, xstar, st);
   return dev::launch_bucket_kc<kMaxClasses>(bucket, nodes, list, n, R, k, terms, row_ptr, lab,
-                                            gbase, G, xl, xlf, res, st);
+                                            gbase, G, xl, xlf, res, rowlb, xstar, st);
 }
 
 }  // namespace sofg
