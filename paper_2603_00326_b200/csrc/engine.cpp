@@ -355,7 +355,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   {
     // Exact nodes above 64 samples (two classes): per-row bounds first, so rows that cannot
     // hold the node's best split are not sorted (k_exact_prune, exact.cu).
-    const int kPruneFrom = 2;  // bucket of n <= 128
+    static const int kPruneFrom = std::getenv("SOFG_PRUNE_FROM") ? std::atoi(std::getenv("SOFG_PRUNE_FROM")) : 2;  // bucket of n <= 128
     size_t prune_off = 0, prune_n = 0;
     for (int b = 0; b < 7; ++b) {
       if (b < kPruneFrom) prune_off += exact_b_count[size_t(b)];

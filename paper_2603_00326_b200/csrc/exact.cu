@@ -247,70 +247,95 @@ __device__ __forceinline__ double x_at(const double* __restrict__ xl, uint32_t l
   return impurity_sum<2>(xl, left, tot, k, l0 + l1, n - (l0 + l1));
 }
 
+// One warp per (node, group of 8 rows): each sample's 8 projected values of the group are one
+// 32-byte sector of V (the sample-major pitch is a multiple of 8), read with two vector loads.
 __global__ void __launch_bounds__(256) k_exact_prune(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     const uint32_t* __restrict__ row_ptr, const uint8_t* __restrict__ lab,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
     const double* __restrict__ xl, float* __restrict__ rowlb, unsigned long long* __restrict__ xstar) {
-  __shared__ uint32_t s_cnt[8][32][2];
+  constexpr int GR = 8;
+  __shared__ uint32_t s_cnt[8][GR][32][2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t RG = (R + GR - 1) / GR;
   const uint64_t gw = uint64_t(blockIdx.x) * 8 + uint64_t(w);
-  if (gw >= uint64_t(n_list) * R) return;
-  const uint32_t li = uint32_t(gw / R), r = uint32_t(gw % R);
+  if (gw >= uint64_t(n_list) * RG) return;
+  const uint32_t li = uint32_t(gw / RG), r0 = uint32_t(gw % RG) * GR;
   const uint32_t node = list[li];
   const NodeIn nd = nodes[node];
   const uint32_t n = nd.n;
   const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
-  float* out = rowlb + size_t(li) * R + r;
-  if (__ldg(rp + r + 1) == __ldg(rp + r)) {  // empty: skipped by the exact kernels anyway
-    if (lane == 0) *out = __int_as_float(0x7f800000);
-    return;
-  }
   const uint32_t Rp = vpitch(R);
-  const float* Vn = G + gbase[node] + r;
-  // pivots: the values at positions n*(i+1)/32, i < 31, sorted (lane 31: +inf sentinel)
-  uint32_t piv = 0xFFFFFFFFu;
-  if (lane < 31) piv = order_key(__ldg(Vn + uint64_t((uint64_t(n) * uint32_t(lane + 1)) / 32) * Rp));
-  piv = warp_sort32(piv, lane);
-  s_cnt[w][lane][0] = 0;
-  s_cnt[w][lane][1] = 0;
+  const float* Vn = G + gbase[node] + r0;
+  // pivots of each row: the values at positions n*(i+1)/32, i < 31, sorted (lane 31: +inf)
+  uint32_t piv[GR];
+  {
+    float v[GR];
+    const uint32_t pos = uint32_t((uint64_t(n) * uint32_t(lane + 1)) / 32);
+    const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(lane < 31 ? pos : 0u) * Rp);
+    const float4 a = __ldg(src), b = __ldg(src + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+#pragma unroll
+    for (int g = 0; g < GR; ++g) piv[g] = warp_sort32(lane < 31 ? order_key(v[g]) : 0xFFFFFFFFu, lane);
+  }
+#pragma unroll
+  for (int g = 0; g < GR; ++g) {
+    s_cnt[w][g][lane][0] = 0;
+    s_cnt[w][g][lane][1] = 0;
+  }
   __syncwarp();
   for (uint32_t j0 = 0; j0 < n; j0 += 32) {  // warp-uniform trip count (shuffles below)
     const uint32_t j = j0 + uint32_t(lane);
     const bool ok = j < n;
-    const uint32_t key = ok ? order_key(__ldg(Vn + uint64_t(j) * Rp)) : 0u;
+    const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(ok ? j : 0u) * Rp);
+    const float4 a = __ldg(src), b = __ldg(src + 1);
+    const float v[GR] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     const uint32_t y = ok ? uint32_t(__ldg(lab + nd.begin + j)) & 1u : 0u;
-    uint32_t lo = 0;
 #pragma unroll
-    for (uint32_t step = 16; step > 0; step >>= 1) {
-      const uint32_t p = __shfl_sync(0xffffffffu, piv, int(lo + step - 1));
-      if (p <= key) lo += step;
+    for (int g = 0; g < GR; ++g) {
+      const uint32_t key = order_key(v[g]);
+      uint32_t lo = 0;
+#pragma unroll
+      for (uint32_t step = 16; step > 0; step >>= 1) {
+        const uint32_t p = __shfl_sync(0xffffffffu, piv[g], int(lo + step - 1));
+        if (p <= key) lo += step;
+      }
+      if (ok) atomicAdd(&s_cnt[w][g][lo][y], 1u);
     }
-    if (ok) atomicAdd(&s_cnt[w][lo][y], 1u);
   }
   __syncwarp();
-  const uint32_t c0 = s_cnt[w][lane][0], c1 = s_cnt[w][lane][1];
-  uint32_t t0, t1;
-  const uint32_t a0 = warp_excl_scan_u32(c0, lane, &t0);
-  const uint32_t a1 = warp_excl_scan_u32(c1, lane, &t1);
-  const uint32_t tot[2] = {t0, t1};
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  // pivot candidate: split after bucket `lane` ("v < pivot_lane"), a real gap when 0 < nl < n
-  const uint32_t L0 = a0 + c0, L1 = a1 + c1;
-  double xp = inf;
-  if (lane < 31 && L0 + L1 > 0 && L0 + L1 < n) xp = x_at<2>(xl, L0, L1, tot, 2, n);
-  // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
-  double lb = xp;
-  if (c0 + c1 >= 2) {
-    lb = fmin(lb, fmin(fmin(x_at<2>(xl, a0, a1, tot, 2, n), x_at<2>(xl, a0, a1 + c1, tot, 2, n)),
-                       fmin(x_at<2>(xl, a0 + c0, a1, tot, 2, n), x_at<2>(xl, a0 + c0, a1 + c1, tot, 2, n))));
+  double xbest = inf;
+#pragma unroll 1
+  for (int g = 0; g < GR; ++g) {
+    const uint32_t r = r0 + uint32_t(g);
+    if (r >= R) break;
+    float* out = rowlb + size_t(li) * R + r;
+    if (__ldg(rp + r + 1) == __ldg(rp + r)) {  // empty: skipped by the exact kernels anyway
+      if (lane == 0) *out = __int_as_float(0x7f800000);
+      continue;
+    }
+    const uint32_t c0 = s_cnt[w][g][lane][0], c1 = s_cnt[w][g][lane][1];
+    uint32_t t0, t1;
+    const uint32_t a0 = warp_excl_scan_u32(c0, lane, &t0);
+    const uint32_t a1 = warp_excl_scan_u32(c1, lane, &t1);
+    const uint32_t tot[2] = {t0, t1};
+    // pivot candidate: split after bucket `lane` ("v < pivot_lane"), a real gap when 0 < nl < n
+    const uint32_t L0 = a0 + c0, L1 = a1 + c1;
+    double xp = inf;
+    if (lane < 31 && L0 + L1 > 0 && L0 + L1 < n) xp = x_at<2>(xl, L0, L1, tot, 2, n);
+    // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
+    double lb = xp;
+    if (c0 + c1 >= 2) {
+      lb = fmin(lb, fmin(fmin(x_at<2>(xl, a0, a1, tot, 2, n), x_at<2>(xl, a0, a1 + c1, tot, 2, n)),
+                         fmin(x_at<2>(xl, a0 + c0, a1, tot, 2, n), x_at<2>(xl, a0 + c0, a1 + c1, tot, 2, n))));
+    }
+    lb = warp_min_f64(lb);
+    xbest = fmin(xbest, xp);
+    if (lane == 0) *out = __double2float_rd(lb);  // rounded down: a conservative bound
   }
-  lb = warp_min_f64(lb);
-  xp = warp_min_f64(xp);
-  if (lane == 0) {
-    *out = __double2float_rd(lb);  // rounded down: a conservative bound
-    if (xp < inf) atomicMin(xstar + li, (unsigned long long)__double_as_longlong(xp));
-  }
+  xbest = warp_min_f64(xbest);
+  if (lane == 0 && xbest < inf) atomicMin(xstar + li, (unsigned long long)__double_as_longlong(xbest));
 }
 
 // E keys per lane, G rows in flight per warp, WPN warps per node, KC class-count registers.
@@ -848,7 +873,7 @@ cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_
   if (n_list == 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(xstar, 0x7f, sizeof(unsigned long long) * n_list, st);  // ~ +huge
   if (e != cudaSuccess) return e;
-  const uint64_t warps = uint64_t(n_list) * R;
+  const uint64_t warps = uint64_t(n_list) * ((R + 7) / 8);
   dev::k_exact_prune<<<unsigned((warps + 7) / 8), 256, 0, st>>>(nodes, list, n_list, R, row_ptr, lab,
                                                                 gbase, G, xl, rowlb, xstar);
   return cudaGetLastError();

@@ -205,15 +205,22 @@ __global__ void __launch_bounds__(256) k_hist_draws(
 }
 
 // ------------------------------------------------------------------------------------------
-// Boundaries: one warp per (histogram node, row). smem per warp: mpad u64 + mpad floats(u32)
-// + mpad bytes.
+// Boundaries (reference sample_boundaries, histogram.hpp:42-80): one warp per (histogram node,
+// row), EPL = mpad/32 draws per lane held in registers (blocked layout: lane l owns draw indices
+// [l*EPL, (l+1)*EPL)). smem per warp: a 2*mpad-slot hash table (u64) + mpad collision flags.
+//   1. C1_i: draw t_i equals an earlier draw (hash table of (t << 16 | smallest i)).
+//   2. D_i = C1_i or (t_i - J0 < i and D_{t_i - J0}) (Floyd's replacement J0 + i is itself picked
+//      later): monotone fixpoint over the flags.
+//   3. gather the picked values (EPL independent loads per lane), register bitonic sort,
+//      midpoints of consecutive distinct values, compacted in order.
 // ------------------------------------------------------------------------------------------
+template <int EPL>
 __global__ void __launch_bounds__(128) k_hist_boundaries(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist,
-    uint32_t R, uint32_t bins, int mpad, const uint32_t* __restrict__ draws,
-    const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
+    uint32_t R, uint32_t bins, const uint32_t* __restrict__ draws,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
     float* __restrict__ bnd, uint32_t* __restrict__ nb_out) {
+  constexpr int MP = 32 * EPL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -221,11 +228,9 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
   if (item >= uint64_t(n_hist) * R) return;
   const uint32_t h = uint32_t(item / R);
   const uint32_t r = uint32_t(item % R);
-  const size_t per_warp = size_t(mpad) * 8 + size_t(mpad) * 4 + size_t(mpad);
-  unsigned char* base = smem_raw + per_warp * wib;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(base);
-  uint32_t* vk = reinterpret_cast<uint32_t*>(base + size_t(mpad) * 8);
-  uint8_t* col = reinterpret_cast<uint8_t*>(base + size_t(mpad) * 12);
+  unsigned char* base = smem_raw + size_t(MP) * 17 * wib;
+  uint64_t* ht = reinterpret_cast<uint64_t*>(base);                   // [2*MP]
+  uint8_t* col = reinterpret_cast<uint8_t*>(base + size_t(MP) * 16);  // [MP]
 
   const uint32_t node = hist_nodes[h];
   const NodeIn nd = nodes[node];
@@ -239,66 +244,101 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
   const uint32_t J0 = n - m;
   const uint32_t Rp = vpitch(R);
   const float* Vn = G + gbase[node] + r;  // row r of the node's V block (sweep.cu)
+  const uint32_t i0 = uint32_t(lane * EPL);
+  uint32_t key[EPL];
 
   if (m < n) {
     const uint32_t* t = draws + size_t(h) * R * bins + size_t(r) * m;
-    // C1: t_i equals an earlier t (sort (t, i) pairs; later duplicates collide).
-    for (int i = lane; i < mpad; i += 32)
-      keys[i] = i < int(m) ? ((uint64_t(t[i]) << 16) | uint64_t(i)) : ~0ull;
+    uint32_t tv[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) tv[e] = i0 + e < m ? __ldg(t + i0 + e) : 0u;
+    constexpr uint32_t TS = 2u * MP;  // load <= 1/2
+    constexpr int TB = 31 - __builtin_clz(TS);
+#pragma unroll
+    for (int e = 0; e < 2 * EPL; ++e) ht[e * 32 + lane] = ~0ull;
     __syncwarp();
-    warp_sort_via_regs(keys, mpad, lane);
-    for (int i = lane; i < int(m); i += 32) {
-      const uint32_t me = uint32_t(keys[i] & 0xffffu);
-      const bool c1 = i > 0 && (keys[i] >> 16) == (keys[i - 1] >> 16);
-      col[me] = c1 ? 1 : 0;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const uint32_t i = i0 + uint32_t(e);
+      if (i < m) {
+        const unsigned long long kk = ((unsigned long long)tv[e] << 16) | i;
+        uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
+        for (;;) {
+          const unsigned long long old =
+              atomicCAS(reinterpret_cast<unsigned long long*>(ht + sl), ~0ull, kk);
+          if (old == ~0ull) break;
+          if ((old >> 16) == tv[e]) {
+            atomicMin(reinterpret_cast<unsigned long long*>(ht + sl), kk);
+            break;
+          }
+          sl = (sl + 1) & (TS - 1);
+        }
+      }
     }
     __syncwarp();
-    // D_i = C1_i or (t_i - J0 < i and D_{t_i - J0}); monotone fixpoint over draw order.
-    bool changed = true;
-    while (changed) {
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const uint32_t i = i0 + uint32_t(e);
+      uint8_t c1 = 0;
+      if (i < m) {
+        uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
+        uint64_t en;
+        while (((en = ht[sl]) >> 16) != tv[e]) sl = (sl + 1) & (TS - 1);
+        c1 = uint32_t(en & 0xffffu) != i ? 1 : 0;
+      }
+      col[i] = c1;
+    }
+    __syncwarp();
+    uint32_t done = 0;  // bit e: flag of draw i0+e known set
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) done |= uint32_t(col[i0 + e]) << e;
+    for (;;) {
       bool ch = false;
-      for (int i = lane; i < int(m); i += 32) {
-        if (col[i]) continue;
-        const uint32_t ti = t[i];
-        if (ti >= J0 && ti - J0 < uint32_t(i) && col[ti - J0]) {
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const uint32_t i = i0 + uint32_t(e);
+        if (!(done >> e & 1u) && i < m && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) {
           col[i] = 1;
+          done |= 1u << e;
           ch = true;
         }
       }
       __syncwarp();
-      changed = __any_sync(0xffffffffu, ch);
+      if (!__any_sync(0xffffffffu, ch)) break;
     }
-    // gather the picked values (positions in the node's active order)
-    for (int i = lane; i < mpad; i += 32) {
-      uint32_t key = 0xffffffffu;
-      if (i < int(m)) {
-        const uint32_t p = col[i] ? J0 + uint32_t(i) : t[i];
-        key = order_key(__ldg(Vn + uint64_t(p) * Rp));
-      }
-      vk[i] = key;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const uint32_t i = i0 + uint32_t(e);
+      const uint32_t pidx = (done >> e & 1u) ? J0 + i : tv[e];
+      key[e] = i < m ? order_key(__ldg(Vn + uint64_t(pidx) * Rp)) : 0xffffffffu;
     }
   } else {
-    for (int i = lane; i < mpad; i += 32)
-      vk[i] = i < int(m) ? order_key(__ldg(Vn + uint64_t(i) * Rp)) : 0xffffffffu;
-  }
-  __syncwarp();
-  warp_sort_via_regs(vk, mpad, lane);
-  // midpoints of consecutive distinct values (float comparison: -0 == +0)
-  uint32_t base_cnt = 0;
-  for (int i0 = 1; i0 < int(m); i0 += 32) {
-    const int i = i0 + lane;
-    bool emit = false;
-    float a = 0.f, b = 0.f;
-    if (i < int(m)) {
-      a = order_key_inv(vk[i - 1]);
-      b = order_key_inv(vk[i]);
-      emit = a < b;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const uint32_t i = i0 + uint32_t(e);
+      key[e] = i < m ? order_key(__ldg(Vn + uint64_t(i) * Rp)) : 0xffffffffu;
     }
-    const unsigned mask = __ballot_sync(0xffffffffu, emit);
-    if (emit) out[base_cnt + __popc(mask & ((1u << lane) - 1))] = midpoint_down(a, b);
-    base_cnt += __popc(mask);
   }
-  if (lane == 0) nb_out[size_t(h) * R + r] = base_cnt;
+  reg_bitonic_sort_k<EPL, uint32_t, (EPL >= 16)>(key, lane);
+  // midpoints of consecutive distinct values (float comparison: -0 == +0), in order
+  const uint32_t prev_last = __shfl_up_sync(0xffffffffu, key[EPL - 1], 1);
+  uint32_t emit = 0;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const uint32_t i = i0 + uint32_t(e);
+    const uint32_t pk = e == 0 ? prev_last : key[e > 0 ? e - 1 : 0];
+    if (i >= 1 && i < m && order_key_inv(pk) < order_key_inv(key[e])) emit |= 1u << e;
+  }
+  uint32_t total;
+  uint32_t pos = warp_excl_scan_u32(uint32_t(__popc(emit)), lane, &total);
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    if (emit >> e & 1u) {
+      const uint32_t pk = e == 0 ? prev_last : key[e > 0 ? e - 1 : 0];
+      out[pos++] = midpoint_down(order_key_inv(pk), order_key_inv(key[e]));
+    }
+  }
+  if (lane == 0) nb_out[size_t(h) * R + r] = total;
 }
 
 }  // namespace dev
@@ -351,21 +391,28 @@ cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nod
                                    const uint32_t* terms, const uint32_t* row_ptr,
                                    const uint64_t* gbase, const float* G, float* bnd,
                                    uint32_t* nb, cudaStream_t st) {
+  (void)terms;
+  (void)row_ptr;
   if (n_hist == 0) return cudaSuccess;
   const int mpad = next_pow2(int(bins));
-  const size_t per_warp = size_t(mpad) * 13;
-  int warps = 4;
-  while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
-  const size_t smem = per_warp * warps;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(dev::k_hist_boundaries, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemOptin);
+  const size_t smem = size_t(mpad) * 17 * 4;  // 4 warps
   const uint64_t items = uint64_t(n_hist) * R;
-  const unsigned grid = unsigned((items + warps - 1) / warps);
-  dev::k_hist_boundaries<<<grid, warps * 32, smem, st>>>(nodes, hist_nodes, n_hist, R, bins, mpad,
-                                                         draws, terms, row_ptr, gbase, G, bnd,
-                                                         nb);
-  return cudaGetLastError();
+  const unsigned grid = unsigned((items + 3) / 4);
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
+    kern<<<grid, 128, smem, st>>>(nodes, hist_nodes, n_hist, R, bins, draws, gbase, G, bnd, nb);
+    return cudaGetLastError();
+  };
+  switch (mpad) {
+    case 32: return go(dev::k_hist_boundaries<1>);
+    case 64: return go(dev::k_hist_boundaries<2>);
+    case 128: return go(dev::k_hist_boundaries<4>);
+    case 256: return go(dev::k_hist_boundaries<8>);
+    case 512: return go(dev::k_hist_boundaries<16>);
+    case 1024: return go(dev::k_hist_boundaries<32>);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace sofg

@@ -122,7 +122,8 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
 }
 
 // ------------------------------------------------------------------------------------------
-template <int KC>
+// LT > 0: compile-time search depth (bpad == 1 << LT); the 8 rows' searches interleave.
+template <int KC, int LT>
 __global__ void __launch_bounds__(256) k_hist_count(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ node_hist_slot,
     const HistWork* __restrict__ work, const uint32_t* __restrict__ multi_slot,
@@ -189,13 +190,30 @@ __global__ void __launch_bounds__(256) k_hist_count(
       const float4 a = __ldg(src), b = __ldg(src + 1);
       const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
       const uint32_t y = lab_s[j];
+      if constexpr (LT > 0) {
+        // all 8 searches advance one level per step: 8 independent shared loads in flight
+        constexpr int BP = 1 << LT;
+        int t[8];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        if (!(live & (1u << g))) continue;  // uniform
-        const float* tr = bnd_s + g * bpad;
-        int t = 1;
-        for (int l = 0; l < L; ++l) t = 2 * t + (tr[t] <= v[g] ? 1 : 0);
-        atomicAdd(&cnt_s[(size_t(g) * bpad + size_t(t - bpad)) * k + y], 1u);
+        for (int g = 0; g < 8; ++g) t[g] = 1;
+#pragma unroll
+        for (int l = 0; l < LT; ++l) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g) t[g] = 2 * t[g] + (bnd_s[g * BP + t[g]] <= v[g] ? 1 : 0);
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          if (live & (1u << g))  // uniform
+            atomicAdd(&cnt_s[(size_t(g) * BP + size_t(t[g] - BP)) * k + y], 1u);
+      } else {
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          if (!(live & (1u << g))) continue;  // uniform
+          const float* tr = bnd_s + g * bpad;
+          int t = 1;
+          for (int l = 0; l < L; ++l) t = 2 * t + (tr[t] <= v[g] ? 1 : 0);
+          atomicAdd(&cnt_s[(size_t(g) * bpad + size_t(t - bpad)) * k + y], 1u);
+        }
       }
     }
   }
@@ -291,7 +309,12 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
   const int bpad = pow2_at_least(int(bins), 32);
   const size_t smem = hist_count_smem(bins, k, chunk_cap);
   // class-count specialised (k = 2 is the trunk workload; generic up to kMaxClasses)
-  auto kern = k == 2 ? dev::k_hist_count<2> : dev::k_hist_count<kMaxClasses>;
+  auto kern = k == 2 ? (bpad == 256   ? dev::k_hist_count<2, 8>
+                        : bpad == 128 ? dev::k_hist_count<2, 7>
+                        : bpad == 64  ? dev::k_hist_count<2, 6>
+                        : bpad == 32  ? dev::k_hist_count<2, 5>
+                                      : dev::k_hist_count<2, 0>)
+                     : (bpad == 256 ? dev::k_hist_count<kMaxClasses, 8> : dev::k_hist_count<kMaxClasses, 0>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   kern<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins, bpad, k,
                                   chunk_cap, terms, row_ptr, lab, gbase, G, bnd, nb, xl, gcnt,

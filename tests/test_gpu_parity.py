@@ -103,7 +103,10 @@ def test_find_node_split_trunk400(gpu_ctx, oracle, method, bins):
                                            (512, "exact", 256), (700, "exact", 256), (1024, "exact", 256),
                                            (1025, "exact", 256), (2048, "exact", 256),
                                            (300, "histogram", 256), (5000, "histogram", 256),
-                                           (20000, "histogram", 256), (9000, "histogram", 32)])
+                                           (20000, "histogram", 256), (9000, "histogram", 32),
+                                           (257, "histogram", 256), (3000, "histogram", 1024),
+                                           (1500, "histogram", 512), (40, "histogram", 64),
+                                           (200, "histogram", 128), (129, "histogram", 128)])
 def test_find_node_split_subsets(gpu_ctx, oracle, n, method, bins):
     X, y = oracle.generate_trunk(30000, 16, 5)
     gpu_ctx.upload(X, y, 2)
