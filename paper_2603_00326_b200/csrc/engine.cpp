@@ -86,7 +86,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   const uint32_t cap = uint32_t(w.chunk_cap);
   struct Cnt {
     uint64_t hist = 0, multi = 0, work = 0, tiles = 0, g = 0, items = 0;
-    uint64_t exact[7] = {0, 0, 0, 0, 0, 0, 0};
+    uint64_t exact[kExactBuckets] = {};
     uint32_t zmax = 32;
     uint64_t terms_end = 0;
     uint64_t big = 0;
@@ -148,14 +148,14 @@ void WaveRunner::submit(const WaveSpec& w) {
     tot.zmax = std::max(tot.zmax, cc[c].zmax);
     tot.terms_end = std::max(tot.terms_end, cc[c].terms_end);
   }
-  uint64_t bucket_base[8] = {0};
-  for (int bk = 0; bk < 7; ++bk) {
+  uint64_t bucket_base[kExactBuckets + 1] = {0};
+  for (int bk = 0; bk < kExactBuckets; ++bk) {
     uint64_t acc = 0;
     for (size_t c = 0; c < C; ++c) acc += cc[c].exact[bk];
     bucket_base[bk + 1] = bucket_base[bk] + acc;
   }
-  exact_total = bucket_base[7];
-  for (int bk = 0; bk < 7; ++bk) {
+  exact_total = bucket_base[kExactBuckets];
+  for (int bk = 0; bk < kExactBuckets; ++bk) {
     uint64_t run = bucket_base[bk];
     for (size_t c = 0; c < C; ++c) {
       off[c].exact[bk] = run;
@@ -247,8 +247,8 @@ void WaveRunner::submit(const WaveSpec& w) {
   const HistWork* d_work = reinterpret_cast<const HistWork*>(dp(o_work));
   const Tile* d_tiles = reinterpret_cast<const Tile*>(dp(o_tiles));
   const uint32_t* d_tfirst = reinterpret_cast<const uint32_t*>(dp(o_tfirst));
-  std::vector<size_t> exact_b_count(7);
-  for (int bk = 0; bk < 7; ++bk) exact_b_count[size_t(bk)] = size_t(bucket_base[bk + 1] - bucket_base[bk]);
+  std::vector<size_t> exact_b_count(kExactBuckets);
+  for (int bk = 0; bk < kExactBuckets; ++bk) exact_b_count[size_t(bk)] = size_t(bucket_base[bk + 1] - bucket_base[bk]);
 
   // ---- scratch ---------------------------------------------------------------------------
   uint32_t* d_terms;
@@ -355,9 +355,9 @@ void WaveRunner::submit(const WaveSpec& w) {
   {
     // Exact nodes above 64 samples (two classes): per-row bounds first, so rows that cannot
     // hold the node's best split are not sorted (k_exact_prune, exact.cu).
-    static const int kPruneFrom = std::getenv("SOFG_PRUNE_FROM") ? std::atoi(std::getenv("SOFG_PRUNE_FROM")) : 2;  // bucket of n <= 128
+    static const int kPruneFrom = std::getenv("SOFG_PRUNE_FROM") ? std::atoi(std::getenv("SOFG_PRUNE_FROM")) : 4;  // bucket of n <= 128
     size_t prune_off = 0, prune_n = 0;
-    for (int b = 0; b < 7; ++b) {
+    for (int b = 0; b < kExactBuckets; ++b) {
       if (b < kPruneFrom) prune_off += exact_b_count[size_t(b)];
       else prune_n += exact_b_count[size_t(b)];
     }
@@ -374,7 +374,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       mark("exact_prune");
     }
     size_t off = 0;
-    for (int b = 0; b < 7; ++b) {
+    for (int b = 0; b < kExactBuckets; ++b) {
       const size_t m = exact_b_count[size_t(b)];
       if (!m) continue;
       const bool pb = prune && b >= kPruneFrom;
@@ -385,7 +385,7 @@ void WaveRunner::submit(const WaveSpec& w) {
                  "exact_bucket");
       off += m;
       ++launches;
-      static const char* kBucketName[7] = {"exact_n<=32", "exact_n<=64", "exact_n<=128",
+      static const char* kBucketName[kExactBuckets] = {"exact_n<=8", "exact_n<=16", "exact_n<=32", "exact_n<=64", "exact_n<=128",
                                            "exact_n<=256", "exact_n<=512", "exact_n<=1024",
                                            "exact_n<=2048"};
       mark(kBucketName[b]);

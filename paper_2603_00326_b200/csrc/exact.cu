@@ -507,6 +507,125 @@ __global__ void __launch_bounds__(128) k_exact_reg(
 }
 
 // ------------------------------------------------------------------------------------------
+// Segmented variant for nodes of <= S samples (S = 8, 16): the warp splits into 32/S segments of
+// S lanes, each segment searches its own row (lane = sorted position), so one pass covers 32/S
+// rows. Keys are the packed 64-bit sort keys; every candidate is evaluated exactly (one per
+// lane). Each segment keeps its rows' best (rows in increasing order, strict '>'), and the
+// segments' bests are reduced with the reference's rule (higher gain, then lower row).
+// ------------------------------------------------------------------------------------------
+template <int S, int KC>
+__global__ void __launch_bounds__(128) k_exact_seg(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
+    int k, const uint32_t* __restrict__ row_ptr, const uint8_t* __restrict__ lab,
+    const uint64_t* __restrict__ gbase, const float* __restrict__ G,
+    const double* __restrict__ xl, NodeRes* __restrict__ res) {
+  constexpr int NSEG = 32 / S;
+  const int lane = threadIdx.x & 31;
+  const int li = int(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (li >= n_list) return;  // whole warp
+  const int sl = lane & (S - 1), seg = lane / S;
+  const uint32_t node = list[li];
+  const NodeIn nd = nodes[node];
+  const uint32_t n = nd.n;
+  const int y = uint32_t(sl) < n ? int(__ldg(lab + nd.begin + sl)) : -1;
+  uint32_t tot[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) {
+    uint32_t x = y == c ? 1u : 0u;
+#pragma unroll
+    for (int o = 1; o < S; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    tot[c] = x;
+  }
+  const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
+  const uint32_t Rp = vpitch(R);
+  const float* Gn = G + gbase[node];
+  const double dn = double(n);
+  const double inv_n = 1.0 / dn;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  Best best{0.0, 0.f, 0, -1, 0.0, inv_n};
+  for (uint32_t r0 = 0; r0 < R; r0 += NSEG) {
+    const uint32_t r = r0 + uint32_t(seg);
+    const bool act = r < R && __ldg(rp + r + 1) != __ldg(rp + r);  // split.hpp:308
+    uint64_t key = ~0ull;
+    if (act && uint32_t(sl) < n)
+      key = (uint64_t(order_key(__ldg(Gn + uint64_t(sl) * Rp + r))) << 32) | uint64_t(uint32_t(y));
+    // bitonic sort within the segment, ascending by sl
+#pragma unroll
+    for (int kk = 2; kk <= S; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
+        const bool up = (sl & kk) == 0;
+        const bool lower = (sl & j) == 0;
+        const uint64_t mn = o < key ? o : key, mx = o < key ? key : o;
+        key = (lower == up) ? mn : mx;
+      }
+    }
+    // class counts of positions <= sl
+    const int c = int(key & 0xffu);
+    uint32_t left[KC];
+#pragma unroll
+    for (int cc = 0; cc < KC; ++cc) {
+      uint32_t x = (uint32_t(sl) < n && c == cc) ? 1u : 0u;
+#pragma unroll
+      for (int o = 1; o < S; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o, S);
+        if (sl >= o) x += t;
+      }
+      left[cc] = x;
+    }
+    const uint64_t nxt = __shfl_down_sync(0xffffffffu, key, 1, S);
+    const uint32_t p = uint32_t(sl);
+    const bool cand = act && p + 1 < n &&
+                      order_key_inv(uint32_t(key >> 32)) < order_key_inv(uint32_t(nxt >> 32));
+    double X = inf;
+    if (cand) X = impurity_sum<KC>(xl, left, tot, k, p + 1, n - (p + 1));
+    double xmin = X;
+#pragma unroll
+    for (int o = 1; o < S; o <<= 1) xmin = fmin(xmin, __shfl_xor_sync(0xffffffffu, xmin, o));
+    const double g = gain_from_x(nd.parent, xmin, dn);
+    const bool upd = xmin < inf && !(best.row >= 0 && !(xmin < best.xmin)) && g > 0.0 &&
+                     !(best.row >= 0 && !(g > best.gain));
+    const double win = x_window_fast(nd.parent, xmin, dn, inv_n);
+    uint32_t first = (cand && X <= win && (X == xmin || gain_from_x(nd.parent, X, dn) == g)) ? p : 0xffffffffu;
+#pragma unroll
+    for (int o = 1; o < S; o <<= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    const uint32_t fp = upd ? first : 0u;
+    const int src = seg * S + int(min(fp, uint32_t(S - 2)));
+    const uint64_t ka = __shfl_sync(0xffffffffu, key, src);
+    const uint64_t kb = __shfl_sync(0xffffffffu, key, src + 1);
+    if (upd) {
+      best.xmin = xmin;
+      best.row = int(r);
+      best.gain = g;
+      best.thr = midpoint_down(order_key_inv(uint32_t(ka >> 32)), order_key_inv(uint32_t(kb >> 32)));
+      best.nl = fp + 1;
+    }
+  }
+  // segments' bests -> lane 0 (higher gain, then lower row)
+#pragma unroll
+  for (int o = S; o < 32; o <<= 1) {
+    const int orow = __shfl_xor_sync(0xffffffffu, best.row, o);
+    const double og = __shfl_xor_sync(0xffffffffu, best.gain, o);
+    const float ot = __shfl_xor_sync(0xffffffffu, best.thr, o);
+    const uint32_t onl = __shfl_xor_sync(0xffffffffu, best.nl, o);
+    if (orow >= 0 && (best.row < 0 || og > best.gain || (og == best.gain && orow < best.row))) {
+      best.row = orow;
+      best.gain = og;
+      best.thr = ot;
+      best.nl = onl;
+    }
+  }
+  if (lane == 0) {
+    NodeRes& out = res[node];
+    out.row = best.row;
+    out.gain = best.gain;
+    out.threshold = best.thr;
+    out.n_left_search = best.nl;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Team variant for nodes of 257..2048 samples: a team of W warps (E = 8 keys per lane) sorts one
 // row together. Strides < 8 are intra-lane, < 256 shuffles, >= 256 go through shared memory
 // between the team's warps (named barrier per team). CTA = 8 warps = 8/W teams; teams take rows
@@ -846,13 +965,23 @@ cudaError_t launch_bucket(const NodeIn* nodes, const uint32_t* list, int n, uint
   return cudaGetLastError();
 }
 
+template <int S, int KC>
+cudaError_t launch_seg(const NodeIn* nodes, const uint32_t* list, int n, uint32_t R, int k,
+                       const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
+                       const float* G, const double* xl, NodeRes* res, cudaStream_t st) {
+  k_exact_seg<S, KC><<<(n + 3) / 4, 128, 0, st>>>(nodes, list, n, R, k, row_ptr, lab, gbase, G, xl, res);
+  return cudaGetLastError();
+}
+
 template <int KC>
 cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
                              uint32_t R, int k, const uint32_t* terms, const uint32_t* row_ptr,
                              const uint8_t* lab, const uint64_t* gbase, const float* G,
                              const double* xl, const float* xlf, NodeRes* res, const float* rowlb,
                              const unsigned long long* xstar, cudaStream_t st) {
-  switch (bucket) {
+  switch (bucket - 2) {
+    case -2: return launch_seg<8, KC>(nodes, list, n, R, k, row_ptr, lab, gbase, G, xl, res, st);
+    case -1: return launch_seg<16, KC>(nodes, list, n, R, k, row_ptr, lab, gbase, G, xl, res, st);
     case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
@@ -881,12 +1010,12 @@ cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_
 
 int exact_bucket(uint32_t n) {
   int b = 0;
-  uint32_t cap = 32;
+  uint32_t cap = 8;
   while (cap < n) {
     cap <<= 1;
     ++b;
   }
-  return b;  // 0..6 for n <= 2048
+  return b;  // 0..8 for n <= 2048: 8, 16 (segmented), 32 .. 2048
 }
 
 cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t* list, int n,

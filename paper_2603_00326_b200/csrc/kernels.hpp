@@ -61,6 +61,7 @@ cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_
                                   cudaStream_t st);
 
 // exact.cu — register-resident exact splitter, bucketed by node size (<= 2048 samples)
+constexpr int kExactBuckets = 9;  // n <= 8, 16, 32, ..., 2048
 int exact_bucket(uint32_t n);
 cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t* list, int n,
                                 uint32_t R, int k, const uint32_t* terms,
