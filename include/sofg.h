@@ -104,6 +104,10 @@ int sofg_predict(sofg_ctx* ctx, const sofg_forest* f, const float* rows, uint64_
                  uint64_t n_features, int32_t* labels, double* votes);
 
 /* ---- per-function entry points (kernel-level parity with the reference) -------------------- */
+/* bootstrap_sample (dataset.hpp:332-349): round(fraction * n) distinct sorted row indices drawn
+ * with make_rng(seed) (the caller passes the tree's derive_seed(tree_seed, 0)). Host-only (no
+ * device needed); out has room for n entries; *count = entries written. */
+int sofg_bootstrap_sample(uint64_t n, double fraction, uint64_t seed, uint32_t* out, uint64_t* count);
 /* apply_projection (projection.hpp:86-108) on the resident table. */
 int sofg_apply_projection(sofg_ctx* ctx, const uint32_t* feat, const float* weight,
                           uint64_t n_terms, const uint32_t* active, uint64_t n_active,

@@ -94,6 +94,7 @@ def load():
     L.sofg_predict.argtypes = [vp, vp, vp, u64, u64, vp, vp]
     L.sofg_apply_projection.argtypes = [vp, vp, vp, u64, vp, u64, vp]
     L.sofg_sample_projection.argtypes = [vp, u64, u64, f64, vp, vp, u64, vp, vp, vp, u64, vp]
+    L.sofg_bootstrap_sample.argtypes = [u64, f64, u64, vp, P(u64)]
     L.sofg_find_node_split.argtypes = [vp, vp, u64, vp, u64, vp, vp, i32, u64, u64, u64, P(_Split)]
     L.sofg_stream.restype = vp
     L.sofg_stream.argtypes = [vp]
@@ -349,6 +350,16 @@ class Context:
             kern[nm.value.decode()] = {"ms": round(ms.value, 2), "launches": la.value}
         out["kernels"] = kern
         return out
+
+
+def bootstrap_sample(n: int, fraction: float, seed: int) -> np.ndarray:
+    """soforest::bootstrap_sample (dataset.hpp:332-349) -> sorted uint32 row indices. Host-side."""
+    L = load()
+    out = np.empty(max(int(n), 1), np.uint32)
+    cnt = C.c_uint64()
+    _check(L.sofg_bootstrap_sample(int(n), float(fraction), int(seed) % 2**64, out.ctypes.data, C.byref(cnt)),
+           "bootstrap_sample")
+    return out[:cnt.value].copy()
 
 
 def train_forest(X, y, class_count, cfg: TrainConfig, device: int = 0) -> Forest:

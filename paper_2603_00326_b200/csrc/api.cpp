@@ -549,6 +549,19 @@ int sofg_apply_projection(sofg_ctx* c, const uint32_t* feat, const float* weight
   });
 }
 
+int sofg_bootstrap_sample(uint64_t n, double fraction, uint64_t seed, uint32_t* out, uint64_t* count) {
+  return guard([&] {
+    if (!out || !count) throw std::invalid_argument("null output");
+    if (n == 0) throw std::invalid_argument("empty dataset");
+    if (!(fraction > 0.0) || fraction > 1.0)
+      throw std::invalid_argument("bootstrap fraction must be in (0, 1]");  // dataset.hpp:335-336
+    if (n > 0xFFFFFFFFull) throw std::invalid_argument("n_samples exceeds 2^32");
+    const std::vector<uint32_t> v = sofg::host::bootstrap_indices(n, fraction, seed);
+    std::memcpy(out, v.data(), 4 * v.size());
+    *count = v.size();
+  });
+}
+
 int sofg_sample_projection(sofg_ctx* c, uint64_t d, uint64_t R, double density,
                            const uint64_t* seeds, const uint64_t* skip, uint64_t n_nodes,
                            uint32_t* row_ptr, uint32_t* feat, float* weight, uint64_t cap,

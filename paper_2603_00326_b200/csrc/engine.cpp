@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "kernels.hpp"
@@ -441,22 +442,18 @@ const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
   std::vector<uint32_t> list;
   {
     auto is_long = [&](size_t i) { return res[i].row >= 0 && res[i].n_terms > uint32_t(kWinTermsMax); };
-    bool any = false;
     if (pool_ && N >= 65536) {  // the scan reads one line per result: split it over the host pool
-      std::vector<unsigned char> hit(size_t(pool_->size()) * 4 + 1, 0);
-      pool_->chunks(size_t(N), 16384, [&](size_t c, size_t b0, size_t b1) {
-        for (size_t i = b0; i < b1 && !hit[c]; ++i) hit[c] = is_long(i);
+      std::vector<std::vector<uint32_t>> part(size_t(pool_->size()) * 4 + 1);
+      const std::vector<size_t> cb = pool_->chunks(size_t(N), 16384, [&](size_t c, size_t b0, size_t b1) {
+        for (size_t i = b0; i < b1; ++i)
+          if (is_long(i)) part[c].push_back(uint32_t(i));
       });
-      for (unsigned char h : hit) any |= h != 0;
+      for (size_t c = 0; c + 1 < cb.size(); ++c) list.insert(list.end(), part[c].begin(), part[c].end());
     } else {
-      any = true;
-    }
-    if (any)
       for (int i = 0; i < N; ++i)
-        if (is_long(size_t(i))) {
-          list.push_back(uint32_t(i));
-          long_off_.push_back(long_off_.back() + res[size_t(i)].n_terms);
-        }
+        if (is_long(size_t(i))) list.push_back(uint32_t(i));
+    }
+    for (const uint32_t i : list) long_off_.push_back(long_off_.back() + res[i].n_terms);
   }
   if (!list.empty()) {
     long_pos_.assign(size_t(N), ~0u);
@@ -501,11 +498,15 @@ const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
     float tt;
     cudaEventElapsedTime(&tt, ev_[0], ev_[5]);
     stats.ms_total += tt;
+    last_wave_ms_ = tt;
+    static const bool wave_log = std::getenv("SOFG_LEVEL_LOG") != nullptr;
     for (int i = 0; i < n_marks_; ++i) {
       float dt;
       cudaEventElapsedTime(&dt, mk_[i], mk_[i + 1]);
       stats.add_kernel(mk_name_[i], dt);
+      if (wave_log) std::fprintf(stderr, "%s%s %.2f", i ? ", " : "  [wave] ", mk_name_[i], double(dt));
     }
+    if (wave_log && n_marks_) std::fprintf(stderr, "\n");
     for (int i = 0; i < N; ++i) {
       const NodeIn& nd = w.nodes[size_t(i)];
       const double strict = 4.0 * double(nd.n) * double(nd.z);

@@ -192,6 +192,7 @@ class WaveRunner {
   const NodeRes* collect_view(const WaveSpec& w);
   // Only the wait for the wave (no host pool use): callers sharing a pool wait first, then
   // take their host turn and call collect_view().
+  float last_wave_ms() const { return last_wave_ms_; }  // device time of the last collected wave (stats on)
   void wait_wave();
   // Page-locked staging reused across calls (root segments).
   PinnedBuf<unsigned char> staging;
@@ -254,6 +255,7 @@ class WaveRunner {
   // submit -> collect state
   NodeRes* pend_dres_ = nullptr;
   int pend_n_ = 0, pend_launches_ = 0;
+  float last_wave_ms_ = 0.f;
   size_t pend_hist_ = 0, pend_exact_ = 0;
   bool pend_sweep_ = false;
   double pend_sweep_bytes_ = 0;

@@ -11,7 +11,9 @@
 // on seed words i, i+1 and i+156, so the handful of outputs a binomial draw consumes costs ~160
 // recurrence steps instead of 312 + a full twist.
 #pragma once
+#include <algorithm>
 #include <cstdint>
+#include <new>
 #include <random>
 #include <vector>
 
@@ -63,6 +65,24 @@ class LazyMt64 {
 
   uint64_t consumed() const { return count_; }
 
+  // Advance the seeding recurrence of M engines to word `upto` in lockstep: the chains are
+  // independent, so the multiplies overlap (the recurrence is one dependent chain per engine).
+  template <int M>
+  static void prime(LazyMt64* g, int upto) {
+    int from = g[0].seeded_;
+    for (int j = 1; j < M; ++j) from = std::min(from, g[j].seeded_);
+    uint64_t p[M];
+    for (int j = 0; j < M; ++j) p[j] = g[j].s_[from - 1];
+    for (int i = from; i <= upto; ++i) {
+#pragma GCC unroll 8
+      for (int j = 0; j < M; ++j) {
+        p[j] = 6364136223846793005ull * (p[j] ^ (p[j] >> 62)) + uint64_t(i);
+        g[j].s_[i] = p[j];
+      }
+    }
+    for (int j = 0; j < M; ++j) g[j].seeded_ = upto + 1;
+  }
+
  private:
   static constexpr int kN = 312, kM = 156;
   static uint64_t mix(uint64_t cur, uint64_t nxt, uint64_t far) {
@@ -100,6 +120,24 @@ class LazyMt64 {
 struct BinomialDraw {
   std::binomial_distribution<long long>::param_type param;
   BinomialDraw(uint64_t cells, double density) : param((long long)cells, density) {}
+
+  // Draws for m fresh engines make_rng(seeds[i]) (no skipped outputs), eight at a time with
+  // their seeding recurrences primed together (a draw typically reads outputs 0..6).
+  void batch(const uint64_t* seeds, size_t m, uint32_t* z, uint32_t* used) const {
+    constexpr int M = 8;
+    for (size_t i0 = 0; i0 < m; i0 += M) {
+      const int c = int(std::min<size_t>(M, m - i0));
+      alignas(64) unsigned char mem[M * sizeof(LazyMt64)];
+      LazyMt64* g = reinterpret_cast<LazyMt64*>(mem);
+      for (int j = 0; j < M; ++j) new (g + j) LazyMt64(seeds[i0 + size_t(j < c ? j : 0)]);
+      LazyMt64::prime<M>(g, 156 + 8);
+      for (int j = 0; j < c; ++j) {
+        std::binomial_distribution<long long> dist(param);
+        z[i0 + size_t(j)] = uint32_t(dist(g[j]));
+        used[i0 + size_t(j)] = uint32_t(g[j].consumed());
+      }
+    }
+  }
 
   // Draw for engine make_rng(seed) after `skip` outputs. Returns z; *used = skip + consumed.
   uint64_t operator()(uint64_t seed, uint64_t skip, uint64_t* used) const {

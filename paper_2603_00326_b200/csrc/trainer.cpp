@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "host_rng.hpp"
@@ -110,6 +111,16 @@ struct Open {
   uint32_t counts[kMaxClasses];
 };
 
+// Host structures of grow_trees kept across calls (per calling thread): their capacity is
+// reused, so a training step does not fault in hundreds of MB of fresh pages.
+struct GrowScratch {
+  std::vector<std::vector<BNode>> trees;
+  std::vector<std::vector<uint32_t>> pools;
+  std::vector<std::vector<Open>> fr, sp, nx, rt;
+  std::vector<uint32_t> spec_z, spec_pos;
+  std::vector<NodeIn> nodes;
+};
+
 int32_t argmax_first(const uint32_t* c, int k) {  // std::max_element: first maximum
   int32_t b = 0;
   for (int i = 1; i < k; ++i)
@@ -196,14 +207,25 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
                "inv_init");
   }
 
-  std::vector<std::vector<BNode>> trees(B);
-  std::vector<std::vector<uint32_t>> pools(B);
+  static thread_local GrowScratch S;
+  std::vector<std::vector<BNode>>& trees = S.trees;
+  std::vector<std::vector<uint32_t>>& pools = S.pools;
+  if (trees.size() < B) {
+    trees.resize(B);
+    pools.resize(B);
+  }
   // The frontier is kept in P parts; part p owns trees [B*p/P, B*(p+1)/P), so parts are processed
   // in parallel without sharing a tree and never need to be concatenated.
   const size_t NP = std::max<size_t>(1, std::min<size_t>(B, size_t(pool.size()) * 4));
-  std::vector<std::vector<Open>> fr(NP), sp(NP), nx(NP), rt(NP);
+  std::vector<std::vector<Open>>&fr = S.fr, &sp = S.sp, &nx = S.nx, &rt = S.rt;
+  for (auto* v : {&fr, &sp, &nx, &rt}) {
+    if (v->size() < NP) v->resize(NP);
+    for (size_t p = 0; p < NP; ++p) (*v)[p].clear();
+  }
   pool.parallel_for(NP, [&](size_t p) {
     for (size_t b = B * p / NP; b < B * (p + 1) / NP; ++b) {
+      trees[b].clear();
+      pools[b].clear();
       trees[b].reserve(1024);
       trees[b].emplace_back();
       Open o{};
@@ -220,9 +242,11 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   times.ms_roots += ms_since(t0);
 
   int cur = 0;
-  std::vector<uint32_t> spec_z, spec_pos;
+  static const bool level_log = std::getenv("SOFG_LEVEL_LOG") != nullptr;
+  std::vector<uint32_t>&spec_z = S.spec_z, &spec_pos = S.spec_pos;
   std::vector<size_t> poff(NP + 1);
   WaveSpec w;
+  w.nodes.swap(S.nodes);  // returned below: the node array's capacity persists
   w.R = P.R;
   w.d = uint32_t(D.d);
   w.bins = uint32_t(P.bins);
@@ -319,10 +343,12 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       w.lab_in = lab[cur].p;
       w.idx_out = idx[cur ^ 1].p;
       w.lab_out = lab[cur ^ 1].p;
-      times.ms_prep += ms_since(t0);
+      const double lv_prep = ms_since(t0);
+      times.ms_prep += lv_prep;
       t0 = Clock::now();
       eng.submit(w);
-      times.ms_submit += ms_since(t0);
+      const double lv_submit = ms_since(t0);
+      times.ms_submit += lv_submit;
 
       // While the GPU searches this wave: draw the children's attempt-0 binomials. They depend
       // only on the child seeds derive_seed(seed, 1|2) (forest.hpp:226-228), known already.
@@ -330,25 +356,31 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       spec_z.resize(2 * N);
       spec_pos.resize(2 * N);
       pool.parallel_for(NP, [&](size_t p) {
-        for (size_t j = 0; j < sp[p].size(); ++j) {
-          const size_t i = poff[p] + j;
+        const size_t m = sp[p].size();
+        std::vector<uint64_t> seeds(2 * m);
+        for (size_t j = 0; j < m; ++j) {
           const uint64_t seed = sp[p][j].seed;
-          for (int c = 0; c < 2; ++c) {
-            uint64_t used;
-            spec_z[2 * i + c] = uint32_t(binom(host::derive_seed(seed, uint64_t(c + 1)), 0, &used));
-            spec_pos[2 * i + c] = uint32_t(used);
-          }
+          seeds[2 * j] = host::derive_seed(seed, 1);
+          seeds[2 * j + 1] = host::derive_seed(seed, 2);
         }
+        binom.batch(seeds.data(), 2 * m, spec_z.data() + 2 * poff[p], spec_pos.data() + 2 * poff[p]);
       });
-      times.ms_spec += ms_since(t0);
+      const double lv_spec = ms_since(t0);
+      times.ms_spec += lv_spec;
       t0 = Clock::now();
       if (turn) {
         host_turn.unlock();  // the other groups prepare their waves meanwhile
         eng.wait_wave();
         host_turn.lock();
       }
+      double lv_sync = 0.0;
+      if (level_log) {
+        eng.wait_wave();
+        lv_sync = ms_since(t0);
+      }
       const NodeRes* res = eng.collect_view(w);
-      times.ms_wait += ms_since(t0);
+      const double lv_wait = ms_since(t0);
+      times.ms_wait += lv_wait;
 
       t0 = Clock::now();
       pool.parallel_for(NP, [&](size_t p) {
@@ -415,10 +447,17 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
         sp[p].swap(rt[p]);
       });
       times.ms_post += ms_since(t0);
+      if (level_log) {
+        std::fprintf(stderr, "[level %llu] nodes %zu gpu %.2f prep %.2f submit %.2f spec %.2f sync %.2f collect %.2f post %.2f ms\n",
+                     (unsigned long long)times.levels, N, double(eng.last_wave_ms()), lv_prep, lv_submit, lv_spec,
+                     lv_sync, lv_wait - lv_sync, ms_since(t0));
+      }
     }
     cur ^= 1;
     fr.swap(nx);
   }
+
+  S.nodes.swap(w.nodes);
 
   // ---- reference node order: ids assigned at split time in depth-first order (H4) ------------
   t0 = Clock::now();
