@@ -149,17 +149,19 @@ __global__ void __launch_bounds__(256) k_hist_count(
   const bool row_ok = r < R;
   const uint32_t nb = row_ok ? nb_g[size_t(h) * R + r] : 0;
   uint32_t* my_cnt = cnt_s + size_t(w) * bpad * k;
-  const float inf = __int_as_float(0x7f800000);
+  const float pad = __int_as_float(0x7fc00000);  // NaN
   const float* gb = bnd_g + (size_t(h) * R + (row_ok ? r : 0)) * (bins - 1);
   // Boundaries of the 8 rows as implicit search trees (Eytzinger order: node t >= 1 holds the
-  // sorted boundary ((2(t - 2^l) + 1) << (L-1-l)) - 1 at level l), padded with +inf. A search
+  // sorted boundary ((2(t - 2^l) + 1) << (L-1-l)) - 1 at level l), padded with NaN (pad <= v is false for
+  // every v, so v = +inf lands in bin nb as in the reference; NaN values land in bin 0,
+  // the reference's two-level lookup result, histogram.hpp:117-131). A search
   // step at level l touches one of 2^l consecutive words, so the 32 lanes' probes spread over
   // the banks instead of piling onto one (sorted-order probes are power-of-two strided).
   int L = 0;
   while ((1 << L) < bpad) ++L;
   for (int i = threadIdx.x; i < 8 * bpad; i += blockDim.x) {
     const int g = i / bpad, t = i % bpad;
-    float v = inf;
+    float v = pad;
     const uint32_t rg = wk.row0 + uint32_t(g);
     if (t > 0 && rg < R) {
       const int l = 31 - __clz(t);
