@@ -320,10 +320,15 @@ __global__ void __launch_bounds__(256) k_exact_prune(
     const uint32_t a0 = warp_excl_scan_u32(c0, lane, &t0);
     const uint32_t a1 = warp_excl_scan_u32(c1, lane, &t1);
     const uint32_t tot[2] = {t0, t1};
-    // pivot candidate: split after bucket `lane` ("v < pivot_lane"), a real gap when 0 < nl < n
+    // pivot candidate: split after bucket `lane` ("v < pivot_lane"), a real gap when 0 < nl < n —
+    // except at a +0 pivot, where -0 values (a smaller key, the same float) sit on the left
     const uint32_t L0 = a0 + c0, L1 = a1 + c1;
+    uint32_t pv = 0;  // this lane's pivot (lane i holds the i-th smallest)
+#pragma unroll
+    for (int gg = 0; gg < GR; ++gg)
+      if (gg == g) pv = piv[gg];
     double xp = inf;
-    if (lane < 31 && L0 + L1 > 0 && L0 + L1 < n) xp = x_at<2>(xl, L0, L1, tot, 2, n);
+    if (lane < 31 && L0 + L1 > 0 && L0 + L1 < n && pv != 0x80000000u) xp = x_at<2>(xl, L0, L1, tot, 2, n);
     // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
     double lb = xp;
     if (c0 + c1 >= 2) {

@@ -298,3 +298,24 @@ def test_exact_large_nodes_segmented_sort(gpu_ctx, oracle, mode, breakeven):
         gpu_ctx.upload(data, y, 2)
         gc, oc = _cfg(n_trees=3, mode=mode, breakeven=breakeven, seed=21)
         assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(data, y, 2, oc)) == []
+
+
+@pytest.mark.parametrize("with_inf", [False, True])
+def test_sweep_special_values(gpu_ctx, oracle, with_inf):
+    """Signed zeros and subnormals through the sweep's exact float -> double widening (integer
+    construction + exact scaling); an infinite table value switches the sweep to the conversion
+    unit (upload flags the table as non-finite)."""
+    X, y = oracle.generate_trunk(3000, 24, 8)
+    X = X.copy()
+    rng = np.random.default_rng(8)
+    m = rng.random(X.shape)
+    X[m < 0.05] = 0.0
+    X[(m >= 0.05) & (m < 0.1)] = -0.0
+    X[(m >= 0.1) & (m < 0.15)] *= np.float32(1e-40)  # subnormal
+    X[3, (m[3] > 0.9)] = np.float32(1e-45)  # smallest subnormal
+    if with_inf:
+        X[5, ::97] = np.inf  # one infinite feature: projections are +-inf, never NaN
+    X = X.astype(np.float32)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=3, mode="dynamic", breakeven=300, seed=17)
+    assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, 2, oc)) == []
