@@ -300,8 +300,9 @@ def test_exact_large_nodes_segmented_sort(gpu_ctx, oracle, mode, breakeven):
         assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(data, y, 2, oc)) == []
 
 
-@pytest.mark.parametrize("with_inf", [False, True])
-def test_sweep_special_values(gpu_ctx, oracle, with_inf):
+@pytest.mark.parametrize("with_inf,mode,breakeven", [(False, "dynamic", 300), (True, "dynamic", 300),
+                                                     (False, "exact", None), (True, "histogram", None)])
+def test_sweep_special_values(gpu_ctx, oracle, with_inf, mode, breakeven):
     """Signed zeros and subnormals through the sweep's exact float -> double widening (integer
     construction + exact scaling); an infinite table value switches the sweep to the conversion
     unit (upload flags the table as non-finite)."""
@@ -317,5 +318,5 @@ def test_sweep_special_values(gpu_ctx, oracle, with_inf):
         X[5, ::97] = np.inf  # one infinite feature: projections are +-inf, never NaN
     X = X.astype(np.float32)
     gpu_ctx.upload(X, y, 2)
-    gc, oc = _cfg(n_trees=3, mode="dynamic", breakeven=300, seed=17)
+    gc, oc = _cfg(n_trees=3, mode=mode, breakeven=breakeven, seed=17)
     assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, 2, oc)) == []
