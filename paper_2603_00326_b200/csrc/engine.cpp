@@ -413,7 +413,9 @@ void WaveRunner::submit(const WaveSpec& w) {
   mark("partition");
   if (timing) cudaEventRecord(ev_[5], st_);
 
-  NodeRes* hr = h_res_.ensure(size_t(N));
+  h_res_cur_ ^= 1;
+  NodeRes* hr = h_res_buf_[h_res_cur_].ensure(size_t(N));
+  h_res_p_ = hr;
   cuda_check(cudaMemcpyAsync(hr, d_res, sizeof(NodeRes) * N, cudaMemcpyDeviceToHost, st_),
              "D2H res");
   cuda_check(cudaEventRecord(done_ev_, st_), "record wave end");
@@ -434,9 +436,9 @@ void WaveRunner::wait_wave() {
 
 const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
   const int N = pend_n_;
-  if (N == 0) return h_res_.p;
+  if (N == 0) return h_res_p_;
   cuda_check(cudaEventSynchronize(done_ev_), "wave sync");
-  const NodeRes* res = h_res_.p;
+  const NodeRes* res = h_res_p_;
   // winning rows longer than NodeRes carries inline: one gather + one D2H for the whole wave
   long_off_.assign(1, 0u);
   std::vector<uint32_t> list;

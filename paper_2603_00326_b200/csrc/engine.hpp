@@ -231,7 +231,9 @@ class WaveRunner {
   // packed host->device inputs
   PinnedBuf<unsigned char> h_in_;
   DevBuf<unsigned char> d_in_;
-  PinnedBuf<NodeRes> h_res_;
+  PinnedBuf<NodeRes> h_res_buf_[2];  // alternate per wave: a wave's results stay readable while
+  int h_res_cur_ = 0;                 // the next wave's are copied back
+  NodeRes* h_res_p_ = nullptr;
   // device scratch
   DevBuf<uint32_t> terms_, row_ptr_, pos_proj_, pos_split_, draws_, nb_, flags_, tile_left_,
       gcnt_, done_, sectors_;

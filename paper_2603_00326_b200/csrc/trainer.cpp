@@ -116,7 +116,7 @@ struct Open {
 struct GrowScratch {
   std::vector<std::vector<BNode>> trees;
   std::vector<std::vector<uint32_t>> pools;
-  std::vector<std::vector<Open>> fr, sp, nx, rt;
+  std::vector<std::vector<Open>> fr, sp, nx, rt, dn;
   std::vector<uint32_t> spec_z, spec_pos;
   std::vector<NodeIn> nodes;
 };
@@ -218,7 +218,8 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   // in parallel without sharing a tree and never need to be concatenated.
   const size_t NP = std::max<size_t>(1, std::min<size_t>(B, size_t(pool.size()) * 4));
   std::vector<std::vector<Open>>&fr = S.fr, &sp = S.sp, &nx = S.nx, &rt = S.rt;
-  for (auto* v : {&fr, &sp, &nx, &rt}) {
+  std::vector<std::vector<Open>>& dn = S.dn;  // the last posted wave's nodes (deferred bookkeeping)
+  for (auto* v : {&fr, &sp, &nx, &rt, &dn}) {
     if (v->size() < NP) v->resize(NP);
     for (size_t p = 0; p < NP; ++p) (*v)[p].clear();
   }
@@ -282,6 +283,62 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     }
     fr[p].swap(keep);
   });
+
+  // Tree records of the last posted wave (its nodes in dn, results in dres; the engine keeps a
+  // wave's results and long-row terms readable until the next collect).
+  struct alignas(64) Counter {  // one cache line per tree: parts update their trees concurrently
+    uint32_t v;
+  };
+  std::vector<Counter> tsize(B);
+  for (size_t b = 0; b < B; ++b) tsize[b].v = uint32_t(trees[b].size());
+  const NodeRes* dres = nullptr;
+  std::vector<size_t> dpoff(NP + 1, 0);
+  bool pending = false;
+  auto bookkeep = [&]() {
+    if (!pending) return;
+    pool.parallel_for(NP, [&](size_t p) {
+      for (size_t j = 0; j < dn[p].size(); ++j) {
+        const size_t i = dpoff[p] + j;
+        const Open& o = dn[p][j];
+        const NodeRes& r = dres[i];
+        std::vector<BNode>& tr = trees[o.tree];
+        if (r.row >= 0 && r.n_left > 0 && r.n_left < o.n) {
+          std::vector<uint32_t>& tp = pools[o.tree];
+          const int32_t L = int32_t(tr.size());
+          BNode& pn = tr[size_t(o.bnode)];
+          pn.thr = r.threshold;
+          pn.left = L;
+          pn.right = L + 1;
+          pn.term_off = uint32_t(tp.size());
+          pn.term_len = r.n_terms;
+          if (r.n_terms <= uint32_t(kWinTermsMax)) {
+            tp.insert(tp.end(), r.terms, r.terms + r.n_terms);
+          } else {
+            const std::vector<uint32_t> t = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
+            tp.insert(tp.end(), t.begin(), t.end());
+          }
+          tr.emplace_back();
+          tr.emplace_back();
+          uint32_t lc[kMaxClasses] = {}, rc[kMaxClasses] = {};
+          for (int c = 0; c < k; ++c) {
+            lc[c] = r.left_counts[c];
+            rc[c] = o.counts[c] - r.left_counts[c];
+          }
+          Open l{}, rr{};
+          l.n = r.n_left;
+          rr.n = o.n - r.n_left;
+          l.depth = rr.depth = o.depth + 1;
+          std::memcpy(l.counts, lc, sizeof(lc));
+          std::memcpy(rr.counts, rc, sizeof(rc));
+          if (!can_split(l)) tr[size_t(L)].pred = argmax_first(lc, k);
+          if (!can_split(rr)) tr[size_t(L) + 1].pred = argmax_first(rc, k);
+        } else if (o.attempt >= P.max_split_retries) {
+          tr[size_t(o.bnode)].pred = argmax_first(o.counts, k);
+        }
+      }
+    });
+    pending = false;
+  };
 
   while (count_open(fr) > 0) {
     times.levels++;
@@ -349,6 +406,9 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       eng.submit(w);
       const double lv_submit = ms_since(t0);
       times.ms_submit += lv_submit;
+      t0 = Clock::now();
+      bookkeep();  // the previous wave's tree records, while this wave runs
+      times.ms_book += ms_since(t0);
 
       // While the GPU searches this wave: draw the children's attempt-0 binomials. They depend
       // only on the child seeds derive_seed(seed, 1|2) (forest.hpp:226-228), known already.
@@ -383,32 +443,18 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       times.ms_wait += lv_wait;
 
       t0 = Clock::now();
+      // Critical pass: the children (the next wave's input) and retries. The tree records of this
+      // wave (thresholds, terms, links, leaf predictions) are filled by bookkeep() after the next
+      // wave is submitted, overlapping its kernels.
       pool.parallel_for(NP, [&](size_t p) {
         rt[p].clear();
         for (size_t j = 0; j < sp[p].size(); ++j) {
           const size_t i = poff[p] + j;
-          Open& o = sp[p][j];
+          const Open& o = sp[p][j];
           const NodeRes& r = res[i];
           if (r.row >= 0 && r.n_left > 0 && r.n_left < o.n) {
-            std::vector<BNode>& tr = trees[o.tree];
-            std::vector<uint32_t>& tp = pools[o.tree];
-            const int32_t L = int32_t(tr.size());
-            {
-              BNode& pn = tr[size_t(o.bnode)];
-              pn.thr = r.threshold;
-              pn.left = L;
-              pn.right = L + 1;
-              pn.term_off = uint32_t(tp.size());
-              pn.term_len = r.n_terms;
-              if (r.n_terms <= uint32_t(kWinTermsMax)) {
-                tp.insert(tp.end(), r.terms, r.terms + r.n_terms);
-              } else {
-                const std::vector<uint32_t> t = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
-                tp.insert(tp.end(), t.begin(), t.end());
-              }
-            }
-            tr.emplace_back();
-            tr.emplace_back();
+            const int32_t L = int32_t(tsize[o.tree].v);
+            tsize[o.tree].v += 2;
             Open l{}, rr{};
             l.tree = rr.tree = o.tree;
             l.bnode = L;
@@ -429,23 +475,22 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
               l.counts[c] = r.left_counts[c];
               rr.counts[c] = o.counts[c] - r.left_counts[c];
             }
-            for (Open* ch : {&l, &rr}) {
-              if (can_split(*ch))
-                nx[p].push_back(*ch);
-              else
-                trees[o.tree][size_t(ch->bnode)].pred = argmax_first(ch->counts, k);
-            }
+            if (can_split(l)) nx[p].push_back(l);
+            if (can_split(rr)) nx[p].push_back(rr);
           } else if (o.attempt < P.max_split_retries) {  // forest.hpp:187,211: next attempt
-            o.attempt++;
-            o.pos = r.pos_after;
-            o.has_z = 0;
-            rt[p].push_back(o);
-          } else {
-            trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);
+            Open a = o;
+            a.attempt++;
+            a.pos = r.pos_after;
+            a.has_z = 0;
+            rt[p].push_back(a);
           }
         }
+        dn[p].swap(sp[p]);
         sp[p].swap(rt[p]);
       });
+      dres = res;
+      dpoff = poff;
+      pending = true;
       times.ms_post += ms_since(t0);
       if (level_log) {
         std::fprintf(stderr, "[level %llu] nodes %zu gpu %.2f prep %.2f submit %.2f spec %.2f sync %.2f collect %.2f post %.2f ms\n",
@@ -457,6 +502,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     fr.swap(nx);
   }
 
+  bookkeep();
   S.nodes.swap(w.nodes);
 
   // ---- reference node order: ids assigned at split time in depth-first order (H4) ------------

@@ -96,7 +96,7 @@ class ThreadPool {
 struct HostTimes {
   double ms_binomial = 0, ms_bootstrap = 0, ms_total = 0;
   double ms_roots = 0, ms_prep = 0, ms_submit = 0, ms_spec = 0, ms_wait = 0, ms_post = 0,
-         ms_final = 0;
+         ms_final = 0, ms_book = 0;
   uint64_t levels = 0;
 };
 
