@@ -235,9 +235,15 @@ __device__ __forceinline__ void scan_row(const K (&key)[E], const Ops& ops, uint
 // margin far above rounding) cannot contain the node's best split nor tie it (gain = parent - X/n
 // is monotone), and the exact kernels skip sorting it.
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ double prune_limit(unsigned long long xs_bits) {
-  const double xs = __longlong_as_double((long long)xs_bits);
-  return xs + fabs(xs) * 0x1p-30 + 0x1p-30;
+// Rows whose bound exceeds the limit are skipped. The reference X is the smaller of xstar (an
+// achievable candidate of some row) and the best X found so far by this warp / team (also
+// achievable); the margin is far above rounding and above x_window, so a skipped row can neither
+// beat nor tie the best.
+__device__ __forceinline__ bool pruned(const float* rowlb, size_t at, const unsigned long long* xstar,
+                                       uint32_t li, const Best& b) {
+  double xs = __longlong_as_double((long long)xstar[li]);
+  if (b.row >= 0) xs = fmin(xs, b.xmin);
+  return double(rowlb[at]) > xs + fabs(xs) * 0x1p-30 + 0x1p-30;
 }
 
 template <int KC>
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(128) k_exact_reg(
       for (int gg = 0; gg < GR; ++gg)
         if (gg == g) ntg = nt[gg];
       if (r >= R || ntg == 0) continue;  // empty rows are skipped in exact mode (split.hpp:308)
-      if (rowlb && double(rowlb[size_t(li) * R + r]) > prune_limit(xstar[li])) continue;  // bound
+      if (rowlb && pruned(rowlb, size_t(li) * R + r, xstar, uint32_t(li), best)) continue;  // bound
       if constexpr (KC == 2) {
         // fast path: 32-bit folded keys (half the shuffle/compare work of the packed 64-bit key)
         uint32_t ok[E], k32[E];
@@ -723,7 +729,7 @@ __global__ void __launch_bounds__(256, 3) k_exact_team(
     const uint32_t tb = rp[r];
     const int nt = int(rp[r + 1] - tb);
     if (nt == 0) continue;  // uniform per team; split.hpp:308
-    if (rowlb && double(rowlb[size_t(blockIdx.x) * R + r]) > prune_limit(xstar[blockIdx.x])) continue;
+    if (rowlb && pruned(rowlb, size_t(blockIdx.x) * R + r, xstar, blockIdx.x, best)) continue;
     // ---- projected values of row r (V block, sample-major) -> radix layout
     //      position q = wt*256 + e*32 + lane (warp-blocked, round-striped)
 #pragma unroll
