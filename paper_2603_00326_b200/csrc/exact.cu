@@ -19,6 +19,10 @@
 #include "dev_util.cuh"
 #include "kernels.hpp"
 
+#ifndef SOFG_TEAM_MINB
+#define SOFG_TEAM_MINB 3
+#endif
+
 namespace sofg {
 namespace dev {
 
@@ -652,7 +656,7 @@ __device__ __forceinline__ void team_sync(int team) {
 }
 
 template <int W, int KC>
-__global__ void __launch_bounds__(256, 3) k_exact_team(
+__global__ void __launch_bounds__(256, SOFG_TEAM_MINB) k_exact_team(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
