@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--seed", type=int, default=7)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-trees", type=int, default=0, help="CPU baseline sample (0 = one per core)")
+    p.add_argument("--holdout", type=int, default=20000, help="hold-out rows for the accuracy check")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="skip the untimed per-kernel profile step")
@@ -172,8 +173,9 @@ def roofline_block(st, args):
             "kernel_ms": kern, "profile_step": "one extra untimed step, one tree group, CUDA events per launch site"}
 
 
-def cpu_reference_sample(X, y, n_trees, args, threads):
-    """Reference learner (oracle/_ref) on this host: `n_trees` trees of the bench forest."""
+def cpu_reference_sample(X, y, n_trees, args, threads, predict_rows=None):
+    """Reference learner (oracle/_ref) on this host: `n_trees` trees of the bench forest (timed);
+    optionally the reference's own predict over `predict_rows` (untimed)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib
 
@@ -181,11 +183,15 @@ def cpu_reference_sample(X, y, n_trees, args, threads):
     ds = orc.dataset(X, y, 2)
     cfg = oracle_lib.make_config(n_trees=n_trees, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
                                  n_workers=threads)
-    t0 = time.perf_counter()
-    forest = orc.train_forest_ds(ds, cfg)
-    dt = time.perf_counter() - t0
+    timing = {}
+    pred = None
+    if predict_rows is None:
+        forest = orc.train_forest_ds(ds, cfg, timing=timing)
+    else:  # the reference's predict on the trained handle, outside the timed call
+        forest, (pred, _) = orc.train_forest_ds(ds, cfg, predict_rows=predict_rows, d=X.shape[0], k=2,
+                                                timing=timing)
     orc.dataset_free(ds)
-    return forest, dt, orc.kind
+    return forest, timing["train_s"], orc.kind, pred
 
 
 def host_trunk(n, d, seed=1):
@@ -215,7 +221,7 @@ def run_reference(args, rank, world):
     steps = max(1, min(args.steps, 2))
     times = []
     for _ in range(steps):
-        _, dt, kind = cpu_reference_sample(X, y, n_trees, args, threads)
+        _, dt, kind, _ = cpu_reference_sample(X, y, n_trees, args, threads)
         times.append(dt)
     v = n_trees / statistics.median(times)
     line = {"metric": METRIC, "value": v, "unit": "trees/s", "n_gpus": 0, "steps": steps,
@@ -362,15 +368,30 @@ def main():
             Xh = np.zeros((args.d, args.n), np.float32)
             yh = np.zeros(args.n, np.int32)
             ctx.download(Xh, yh)
-        forest, dt, kind = cpu_reference_sample(Xh, yh, n_cpu, args, threads)
+        # hold-out rows: a second trunk draw, row-major
+        Xt, yt = host_trunk(args.holdout, args.d, seed=2)
+        rows = np.ascontiguousarray(Xt.T)
+        forest, dt, kind, cpu_lab = cpu_reference_sample(Xh, yh, n_cpu, args, threads, predict_rows=rows)
         import oracle_lib
 
         ff = oracle_lib.FlatForest(first.tree_off, first.left, first.right, first.pred, first.thr, first.term_off,
                                    first.feat, first.weight)
         same = sum(ff.tree_equal(forest, t) for t in range(n_cpu))
+        e = int(first.tree_off[n_cpu])
+        q = int(first.term_off[e])
+        head = type(first)(first.tree_off[:n_cpu + 1].copy(), first.left[:e], first.right[:e], first.pred[:e],
+                           first.thr[:e], first.term_off[:e + 1].copy(), first.feat[:q], first.weight[:q],
+                           first.breakeven, first.class_count, first.n_features)
+        gpu_lab_head, _ = ctx.predict(head, rows)
+        gpu_lab_all, _ = ctx.predict(first, rows)
         cpu = {"value": n_cpu / dt, "unit": "trees/s", "cores": threads, "kind": kind,
                "sample": f"trees 0..{n_cpu - 1} of the bench forest (full {args.n} x {args.d} trees, "
-                         f"{threads} threads), {dt:.1f} s", "bitexact_trees": f"{same}/{n_cpu}"}
+                         f"{threads} threads), {dt:.1f} s", "bitexact_trees": f"{same}/{n_cpu}",
+               "holdout": {"rows": int(args.holdout), "data": "trunk model, seed 2",
+                           f"cpu_accuracy_{n_cpu}_trees": round(float((cpu_lab == yt).mean()), 5),
+                           f"gpu_accuracy_{n_cpu}_trees": round(float((gpu_lab_head == yt).mean()), 5),
+                           "identical_labels": bool(np.array_equal(cpu_lab, gpu_lab_head)),
+                           f"gpu_accuracy_{T}_trees": round(float((gpu_lab_all == yt).mean()), 5)}}
 
     line = {"metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

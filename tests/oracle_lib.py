@@ -218,11 +218,19 @@ class Oracle:
     def dataset_free(self, h):
         self.lib.orc_dataset_free(h)
 
-    def train_forest_ds(self, ds, cfg: OrcConfig) -> FlatForest:
+    def train_forest_ds(self, ds, cfg: OrcConfig, predict_rows=None, d=None, k=2, timing=None):
+        import time as _time
+
         h = C.c_void_p()
+        t0 = _time.perf_counter()
         self._err(self.lib.orc_train_forest_ds(ds, C.byref(cfg), C.byref(h)), "train_forest")
+        if timing is not None:
+            timing["train_s"] = _time.perf_counter() - t0
         try:
-            return self._export(h)
+            f = self._export(h)
+            if predict_rows is not None:
+                return f, self._predict(h, predict_rows, d, k)
+            return f
         finally:
             self.lib.orc_forest_free(h)
 
