@@ -257,18 +257,27 @@ __device__ __forceinline__ double x_at(const double* __restrict__ xl, uint32_t l
   return impurity_sum<2>(xl, left, tot, k, l0 + l1, n - (l0 + l1));
 }
 
+#ifndef SOFG_PRUNE_BUCKETS
+#define SOFG_PRUNE_BUCKETS 64
+#endif
+constexpr int kPB = SOFG_PRUNE_BUCKETS;  // value buckets per row (32 or 64)
+constexpr int kPBE = kPB / 32;           // buckets (and pivots) per lane
+
 // One warp per (node, group of 8 rows): each sample's 8 projected values of the group are one
 // 32-byte sector of V (the sample-major pitch is a multiple of 8), read with two vector loads.
-__global__ void __launch_bounds__(256) k_exact_prune(
+// 4 warps per CTA; per warp the sorted pivots and the bucket class counts of its 8 rows live in
+// shared memory.
+__global__ void __launch_bounds__(128) k_exact_prune(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     const uint32_t* __restrict__ row_ptr, const uint8_t* __restrict__ lab,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
     const double* __restrict__ xl, float* __restrict__ rowlb, unsigned long long* __restrict__ xstar) {
   constexpr int GR = 8;
-  __shared__ uint32_t s_cnt[8][GR][32][2];
+  __shared__ uint32_t s_cnt[4][GR][kPB][2];
+  __shared__ uint32_t s_piv[4][GR][kPB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t RG = (R + GR - 1) / GR;
-  const uint64_t gw = uint64_t(blockIdx.x) * 8 + uint64_t(w);
+  const uint64_t gw = uint64_t(blockIdx.x) * 4 + uint64_t(w);
   if (gw >= uint64_t(n_list) * RG) return;
   const uint32_t li = uint32_t(gw / RG), r0 = uint32_t(gw % RG) * GR;
   const uint32_t node = list[li];
@@ -277,41 +286,51 @@ __global__ void __launch_bounds__(256) k_exact_prune(
   const uint32_t* rp = row_ptr + size_t(node) * (R + 1);
   const uint32_t Rp = vpitch(R);
   const float* Vn = G + gbase[node] + r0;
-  // pivots of each row: the values at positions n*(i+1)/32, i < 31, sorted (lane 31: +inf)
-  uint32_t piv[GR];
+  // pivots of each row: the values at positions n*(i+1)/kPB, i < kPB - 1, sorted (last: +inf);
+  // lane l holds sorted positions l*kPBE .. l*kPBE + kPBE - 1
   {
-    float v[GR];
-    const uint32_t pos = uint32_t((uint64_t(n) * uint32_t(lane + 1)) / 32);
-    const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(lane < 31 ? pos : 0u) * Rp);
-    const float4 a = __ldg(src), b = __ldg(src + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    float v[kPBE][GR];
 #pragma unroll
-    for (int g = 0; g < GR; ++g) piv[g] = warp_sort32(lane < 31 ? order_key(v[g]) : 0xFFFFFFFFu, lane);
-  }
-#pragma unroll
-  for (int g = 0; g < GR; ++g) {
-    s_cnt[w][g][lane][0] = 0;
-    s_cnt[w][g][lane][1] = 0;
-  }
-  __syncwarp();
-  for (uint32_t j0 = 0; j0 < n; j0 += 32) {  // warp-uniform trip count (shuffles below)
-    const uint32_t j = j0 + uint32_t(lane);
-    const bool ok = j < n;
-    const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(ok ? j : 0u) * Rp);
-    const float4 a = __ldg(src), b = __ldg(src + 1);
-    const float v[GR] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    const uint32_t y = ok ? uint32_t(__ldg(lab + nd.begin + j)) & 1u : 0u;
+    for (int e = 0; e < kPBE; ++e) {
+      const uint32_t i = uint32_t(lane * kPBE + e);
+      const uint32_t pos = uint32_t((uint64_t(n) * (i + 1)) / kPB);
+      const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(i < kPB - 1 ? pos : 0u) * Rp);
+      const float4 a = __ldg(src), b = __ldg(src + 1);
+      v[e][0] = a.x; v[e][1] = a.y; v[e][2] = a.z; v[e][3] = a.w;
+      v[e][4] = b.x; v[e][5] = b.y; v[e][6] = b.z; v[e][7] = b.w;
+    }
 #pragma unroll
     for (int g = 0; g < GR; ++g) {
-      const uint32_t key = order_key(v[g]);
-      uint32_t lo = 0;
+      uint32_t k[kPBE];
 #pragma unroll
-      for (uint32_t step = 16; step > 0; step >>= 1) {
-        const uint32_t p = __shfl_sync(0xffffffffu, piv[g], int(lo + step - 1));
-        if (p <= key) lo += step;
+      for (int e = 0; e < kPBE; ++e)
+        k[e] = uint32_t(lane * kPBE + e) < uint32_t(kPB - 1) ? order_key(v[e][g]) : 0xFFFFFFFFu;
+      reg_bitonic_sort_k<kPBE, uint32_t>(k, lane);
+#pragma unroll
+      for (int e = 0; e < kPBE; ++e) {
+        s_piv[w][g][lane * kPBE + e] = k[e];
+        s_cnt[w][g][lane * kPBE + e][0] = 0;
+        s_cnt[w][g][lane * kPBE + e][1] = 0;
       }
-      if (ok) atomicAdd(&s_cnt[w][g][lo][y], 1u);
     }
+  }
+  __syncwarp();
+  for (uint32_t j = uint32_t(lane); j < n; j += 32) {
+    const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(j) * Rp);
+    const float4 a = __ldg(src), b = __ldg(src + 1);
+    const float v[GR] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t y = uint32_t(__ldg(lab + nd.begin + j)) & 1u;
+    uint32_t lo[GR];
+#pragma unroll
+    for (int g = 0; g < GR; ++g) lo[g] = 0;
+#pragma unroll
+    for (uint32_t step = kPB / 2; step > 0; step >>= 1) {
+#pragma unroll
+      for (int g = 0; g < GR; ++g)
+        if (s_piv[w][g][lo[g] + step - 1] <= order_key(v[g])) lo[g] += step;
+    }
+#pragma unroll
+    for (int g = 0; g < GR; ++g) atomicAdd(&s_cnt[w][g][lo[g]][y], 1u);
   }
   __syncwarp();
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -325,27 +344,35 @@ __global__ void __launch_bounds__(256) k_exact_prune(
       if (lane == 0) *out = __int_as_float(0x7f800000);
       continue;
     }
-    const uint32_t c0 = s_cnt[w][g][lane][0], c1 = s_cnt[w][g][lane][1];
-    uint32_t t0, t1;
-    const uint32_t a0 = warp_excl_scan_u32(c0, lane, &t0);
-    const uint32_t a1 = warp_excl_scan_u32(c1, lane, &t1);
-    const uint32_t tot[2] = {t0, t1};
-    // pivot candidate: split after bucket `lane` ("v < pivot_lane"), a real gap when 0 < nl < n —
-    // except at a +0 pivot, where -0 values (a smaller key, the same float) sit on the left
-    const uint32_t L0 = a0 + c0, L1 = a1 + c1;
-    uint32_t pv = 0;  // this lane's pivot (lane i holds the i-th smallest)
+    uint32_t c0[kPBE], c1[kPBE], s0 = 0, s1 = 0;
 #pragma unroll
-    for (int gg = 0; gg < GR; ++gg)
-      if (gg == g) pv = piv[gg];
-    double xp = inf;
-    if (lane < 31 && L0 + L1 > 0 && L0 + L1 < n && pv != 0x80000000u) xp = x_at<2>(xl, L0, L1, tot, 2, n);
-    // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
-    double lb = xp;
-    if (c0 + c1 >= 2) {
-      lb = fmin(lb, fmin(fmin(x_at<2>(xl, a0, a1, tot, 2, n), x_at<2>(xl, a0, a1 + c1, tot, 2, n)),
-                         fmin(x_at<2>(xl, a0 + c0, a1, tot, 2, n), x_at<2>(xl, a0 + c0, a1 + c1, tot, 2, n))));
+    for (int e = 0; e < kPBE; ++e) {
+      c0[e] = s_cnt[w][g][lane * kPBE + e][0];
+      c1[e] = s_cnt[w][g][lane * kPBE + e][1];
+      s0 += c0[e];
+      s1 += c1[e];
     }
-    lb = warp_min_f64(lb);
+    uint32_t t0, t1;
+    uint32_t a0 = warp_excl_scan_u32(s0, lane, &t0);
+    uint32_t a1 = warp_excl_scan_u32(s1, lane, &t1);
+    const uint32_t tot[2] = {t0, t1};
+    double xp = inf, lb = inf;
+#pragma unroll
+    for (int e = 0; e < kPBE; ++e) {
+      const uint32_t bk = uint32_t(lane * kPBE + e);
+      // pivot candidate: split after bucket bk ("v < pivot_bk"), a real gap when 0 < nl < n —
+      // except at a +0 pivot, where -0 values (a smaller key, the same float) sit on the left
+      const uint32_t L0 = a0 + c0[e], L1 = a1 + c1[e];
+      if (bk < uint32_t(kPB - 1) && L0 + L1 > 0 && L0 + L1 < n && s_piv[w][g][bk] != 0x80000000u)
+        xp = fmin(xp, x_at<2>(xl, L0, L1, tot, 2, n));
+      // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
+      if (c0[e] + c1[e] >= 2)
+        lb = fmin(lb, fmin(fmin(x_at<2>(xl, a0, a1, tot, 2, n), x_at<2>(xl, a0, L1, tot, 2, n)),
+                           fmin(x_at<2>(xl, L0, a1, tot, 2, n), x_at<2>(xl, L0, L1, tot, 2, n))));
+      a0 = L0;
+      a1 = L1;
+    }
+    lb = warp_min_f64(fmin(lb, xp));
     xbest = fmin(xbest, xp);
     if (lane == 0) *out = __double2float_rd(lb);  // rounded down: a conservative bound
   }
@@ -1018,7 +1045,7 @@ cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_
   cudaError_t e = cudaMemsetAsync(xstar, 0x7f, sizeof(unsigned long long) * n_list, st);  // ~ +huge
   if (e != cudaSuccess) return e;
   const uint64_t warps = uint64_t(n_list) * ((R + 7) / 8);
-  dev::k_exact_prune<<<unsigned((warps + 7) / 8), 256, 0, st>>>(nodes, list, n_list, R, row_ptr, lab,
+  dev::k_exact_prune<<<unsigned((warps + 3) / 4), 128, 0, st>>>(nodes, list, n_list, R, row_ptr, lab,
                                                                 gbase, G, xl, rowlb, xstar);
   return cudaGetLastError();
 }
