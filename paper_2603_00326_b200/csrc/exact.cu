@@ -274,7 +274,11 @@ __global__ void __launch_bounds__(128) k_exact_prune(
     const double* __restrict__ xl, float* __restrict__ rowlb, unsigned long long* __restrict__ xstar) {
   constexpr int GR = 8;
   __shared__ uint32_t s_cnt[4][GR][kPB][2];
-  __shared__ uint32_t s_piv[4][GR][kPB];
+  // pivot i at word i + i/32: positions i and i+32 fall in different banks (a search step's probes
+  // are spread over both halves)
+  constexpr int kPP = kPB + kPB / 32;
+  __shared__ uint32_t s_piv[4][GR][kPP];
+  auto pslot = [](uint32_t i) { return i + (i >> 5); };
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t RG = (R + GR - 1) / GR;
   const uint64_t gw = uint64_t(blockIdx.x) * 4 + uint64_t(w);
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(128) k_exact_prune(
       reg_bitonic_sort_k<kPBE, uint32_t>(k, lane);
 #pragma unroll
       for (int e = 0; e < kPBE; ++e) {
-        s_piv[w][g][lane * kPBE + e] = k[e];
+        s_piv[w][g][pslot(lane * kPBE + e)] = k[e];
         s_cnt[w][g][lane * kPBE + e][0] = 0;
         s_cnt[w][g][lane * kPBE + e][1] = 0;
       }
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(128) k_exact_prune(
     for (uint32_t step = kPB / 2; step > 0; step >>= 1) {
 #pragma unroll
       for (int g = 0; g < GR; ++g)
-        if (s_piv[w][g][lo[g] + step - 1] <= order_key(v[g])) lo[g] += step;
+        if (s_piv[w][g][pslot(lo[g] + step - 1)] <= order_key(v[g])) lo[g] += step;
     }
 #pragma unroll
     for (int g = 0; g < GR; ++g) atomicAdd(&s_cnt[w][g][lo[g]][y], 1u);
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(128) k_exact_prune(
       // pivot candidate: split after bucket bk ("v < pivot_bk"), a real gap when 0 < nl < n —
       // except at a +0 pivot, where -0 values (a smaller key, the same float) sit on the left
       const uint32_t L0 = a0 + c0[e], L1 = a1 + c1[e];
-      if (bk < uint32_t(kPB - 1) && L0 + L1 > 0 && L0 + L1 < n && s_piv[w][g][bk] != 0x80000000u)
+      if (bk < uint32_t(kPB - 1) && L0 + L1 > 0 && L0 + L1 < n && s_piv[w][g][pslot(bk)] != 0x80000000u)
         xp = fmin(xp, x_at<2>(xl, L0, L1, tot, 2, n));
       // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
       if (c0[e] + c1[e] >= 2)
