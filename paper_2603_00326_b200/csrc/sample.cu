@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256) k_hist_draws(
 // Boundaries (reference sample_boundaries, histogram.hpp:42-80): one warp per (histogram node,
 // row), EPL = mpad/32 draws per lane held in registers (blocked layout: lane l owns draw indices
 // [l*EPL, (l+1)*EPL)). smem per warp: a 2*mpad-slot hash table (u64) + mpad collision flags.
-//   1. C1_i: draw t_i equals an earlier draw (hash table of (t << 16 | smallest i)).
+//   1. C1_i: draw t_i equals an earlier draw (hash table of draw values + smallest index).
 //   2. D_i = C1_i or (t_i - J0 < i and D_{t_i - J0}) (Floyd's replacement J0 + i is itself picked
 //      later): monotone fixpoint over the flags.
 //   3. gather the picked values (EPL independent loads per lane), register bitonic sort,
@@ -254,21 +254,23 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
     for (int e = 0; e < EPL; ++e) tv[e] = i0 + e < m ? __ldg(t + i0 + e) : 0u;
     constexpr uint32_t TS = 2u * MP;  // load <= 1/2
     constexpr int TB = 31 - __builtin_clz(TS);
+    uint32_t* hk = reinterpret_cast<uint32_t*>(ht);  // [TS] draw values (~0 = empty)
+    uint32_t* hi = hk + TS;                          // [TS] smallest index holding the value
 #pragma unroll
-    for (int e = 0; e < 2 * EPL; ++e) ht[e * 32 + lane] = ~0ull;
+    for (int e = 0; e < 2 * EPL; ++e) {
+      hk[e * 32 + lane] = ~0u;
+      hi[e * 32 + lane] = ~0u;
+    }
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       const uint32_t i = i0 + uint32_t(e);
       if (i < m) {
-        const unsigned long long kk = ((unsigned long long)tv[e] << 16) | i;
         uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
         for (;;) {
-          const unsigned long long old =
-              atomicCAS(reinterpret_cast<unsigned long long*>(ht + sl), ~0ull, kk);
-          if (old == ~0ull) break;
-          if ((old >> 16) == tv[e]) {
-            atomicMin(reinterpret_cast<unsigned long long*>(ht + sl), kk);
+          const uint32_t old = atomicCAS(hk + sl, ~0u, tv[e]);
+          if (old == ~0u || old == tv[e]) {
+            atomicMin(hi + sl, i);
             break;
           }
           sl = (sl + 1) & (TS - 1);
@@ -282,9 +284,8 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
       uint8_t c1 = 0;
       if (i < m) {
         uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
-        uint64_t en;
-        while (((en = ht[sl]) >> 16) != tv[e]) sl = (sl + 1) & (TS - 1);
-        c1 = uint32_t(en & 0xffffu) != i ? 1 : 0;
+        while (hk[sl] != tv[e]) sl = (sl + 1) & (TS - 1);
+        c1 = hi[sl] != i ? 1 : 0;
       }
       col[i] = c1;
     }
