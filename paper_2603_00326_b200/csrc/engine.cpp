@@ -369,8 +369,15 @@ void WaveRunner::submit(const WaveSpec& w) {
     if (prune) {
       d_rowlb = rowlb_.ensure(prune_n * R);
       d_xstar = xstar_.ensure(prune_n);
-      cuda_check(launch_exact_prune(d_nodes, d_exact + prune_off, int(prune_n), R, d_rp, w.lab_in,
-                                    d_gbase, d_G, D.xl.p, d_rowlb, d_xstar, st_),
+      // 32 value buckets per row for n <= 128 (bounds tight enough, half the cost), 64 above
+      size_t n_small = 0;
+      for (int b = kPruneFrom; b <= 4; ++b) n_small += exact_b_count[size_t(b)];
+      cuda_check(launch_exact_prune(d_nodes, d_exact + prune_off, int(n_small), R, d_rp, w.lab_in,
+                                    d_gbase, d_G, D.xl.p, d_rowlb, d_xstar, 32, st_),
+                 "exact_prune");
+      cuda_check(launch_exact_prune(d_nodes, d_exact + prune_off + n_small, int(prune_n - n_small), R,
+                                    d_rp, w.lab_in, d_gbase, d_G, D.xl.p, d_rowlb + n_small * R,
+                                    d_xstar + n_small, 64, st_),
                  "exact_prune");
       ++launches;
       mark("exact_prune");

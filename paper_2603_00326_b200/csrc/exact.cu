@@ -257,22 +257,20 @@ __device__ __forceinline__ double x_at(const double* __restrict__ xl, uint32_t l
   return impurity_sum<2>(xl, left, tot, k, l0 + l1, n - (l0 + l1));
 }
 
-#ifndef SOFG_PRUNE_BUCKETS
-#define SOFG_PRUNE_BUCKETS 64
-#endif
-constexpr int kPB = SOFG_PRUNE_BUCKETS;  // value buckets per row (32 or 64)
-constexpr int kPBE = kPB / 32;           // buckets (and pivots) per lane
 
 // One warp per (node, group of 8 rows): each sample's 8 projected values of the group are one
 // 32-byte sector of V (the sample-major pitch is a multiple of 8), read with two vector loads.
 // 4 warps per CTA; per warp the sorted pivots and the bucket class counts of its 8 rows live in
 // shared memory.
+// kPB value buckets per row (32 or 64), kPBE per lane.
+template <int kPB>
 __global__ void __launch_bounds__(128) k_exact_prune(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     const uint32_t* __restrict__ row_ptr, const uint8_t* __restrict__ lab,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
     const double* __restrict__ xl, float* __restrict__ rowlb, unsigned long long* __restrict__ xstar) {
   constexpr int GR = 8;
+  constexpr int kPBE = kPB / 32;
   __shared__ uint32_t s_cnt[4][GR][kPB][2];
   // pivot i at word i + i/32: positions i and i+32 fall in different banks (a search step's probes
   // are spread over both halves)
@@ -360,22 +358,31 @@ __global__ void __launch_bounds__(128) k_exact_prune(
     uint32_t a0 = warp_excl_scan_u32(s0, lane, &t0);
     uint32_t a1 = warp_excl_scan_u32(s1, lane, &t1);
     const uint32_t tot[2] = {t0, t1};
+    // X at every bucket's end point (its left counts after the bucket); the pivot candidates are
+    // the valid ones among them, and a bucket's box has corners start, end, (a0, L1), (L0, a1)
+    double xe[kPBE];
     double xp = inf, lb = inf;
 #pragma unroll
     for (int e = 0; e < kPBE; ++e) {
       const uint32_t bk = uint32_t(lane * kPBE + e);
+      const uint32_t L0 = a0 + c0[e], L1 = a1 + c1[e];
+      xe[e] = x_at<2>(xl, L0, L1, tot, 2, n);
       // pivot candidate: split after bucket bk ("v < pivot_bk"), a real gap when 0 < nl < n —
       // except at a +0 pivot, where -0 values (a smaller key, the same float) sit on the left
-      const uint32_t L0 = a0 + c0[e], L1 = a1 + c1[e];
       if (bk < uint32_t(kPB - 1) && L0 + L1 > 0 && L0 + L1 < n && s_piv[w][g][pslot(bk)] != 0x80000000u)
-        xp = fmin(xp, x_at<2>(xl, L0, L1, tot, 2, n));
-      // gaps inside the bucket: the box [a0, a0+c0] x [a1, a1+c1]; concave X -> min at a corner
-      if (c0[e] + c1[e] >= 2)
-        lb = fmin(lb, fmin(fmin(x_at<2>(xl, a0, a1, tot, 2, n), x_at<2>(xl, a0, L1, tot, 2, n)),
-                           fmin(x_at<2>(xl, L0, a1, tot, 2, n), x_at<2>(xl, L0, L1, tot, 2, n))));
+        xp = fmin(xp, xe[e]);
+      // gaps inside the bucket: the box [a0, L0] x [a1, L1]; X is concave, so its minimum is at a
+      // corner (one-class buckets: a segment, minimum at its ends)
+      if (c0[e] > 0 && c1[e] > 0)
+        lb = fmin(lb, fmin(x_at<2>(xl, a0, L1, tot, 2, n), x_at<2>(xl, L0, a1, tot, 2, n)));
+      lb = fmin(lb, xe[e]);
       a0 = L0;
       a1 = L1;
     }
+    // start point of this lane's first bucket = end point of the previous lane's last one
+    double xs0 = __shfl_up_sync(0xffffffffu, xe[kPBE - 1], 1);
+    if (lane == 0) xs0 = x_at<2>(xl, 0u, 0u, tot, 2, n);
+    lb = fmin(lb, xs0);
     lb = warp_min_f64(fmin(lb, xp));
     xbest = fmin(xbest, xp);
     if (lane == 0) *out = __double2float_rd(lb);  // rounded down: a conservative bound
@@ -1044,13 +1051,17 @@ cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* li
 cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_list, uint32_t R,
                                const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
                                const float* G, const double* xl, float* rowlb,
-                               unsigned long long* xstar, cudaStream_t st) {
+                               unsigned long long* xstar, int buckets, cudaStream_t st) {
   if (n_list == 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(xstar, 0x7f, sizeof(unsigned long long) * n_list, st);  // ~ +huge
   if (e != cudaSuccess) return e;
   const uint64_t warps = uint64_t(n_list) * ((R + 7) / 8);
-  dev::k_exact_prune<<<unsigned((warps + 3) / 4), 128, 0, st>>>(nodes, list, n_list, R, row_ptr, lab,
-                                                                gbase, G, xl, rowlb, xstar);
+  if (buckets == 32)
+    dev::k_exact_prune<32><<<unsigned((warps + 3) / 4), 128, 0, st>>>(nodes, list, n_list, R, row_ptr,
+                                                                      lab, gbase, G, xl, rowlb, xstar);
+  else
+    dev::k_exact_prune<64><<<unsigned((warps + 3) / 4), 128, 0, st>>>(nodes, list, n_list, R, row_ptr,
+                                                                      lab, gbase, G, xl, rowlb, xstar);
   return cudaGetLastError();
 }
 
