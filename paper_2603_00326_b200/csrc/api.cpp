@@ -123,10 +123,13 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   D.ld = (n + 31) / 32 * 32;
   D.X.exact(D.ld * d);
   copy_X(D.X.p, D.ld);
-  // Row-major copy for the sample-major projection sweep (sweep.cu); rows padded to 128 B.
-  D.XR.release();
+  // Row-major copy for the sample-major projection sweep (sweep.cu); rows padded to 128 B. The
+  // previous allocation is reused when it is large enough (a 16 GB free + malloc per upload costs
+  // hundreds of ms).
   D.ldr = (d + 1 + 31) / 32 * 32;  // >= one zero pad column (the sweep's empty-row term)
-  if (!std::getenv("SOFG_NO_ROW_TABLE")) {
+  if (std::getenv("SOFG_NO_ROW_TABLE")) {
+    D.XR.release();
+  } else {
     D.XR.exact(n * D.ldr);
     cuda_check(sofg::launch_transpose_rows(D.X.p, D.ld, n, d, D.XR.p, D.ldr, c->eng->stream()),
                "transpose_rows");
@@ -137,12 +140,15 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   for (uint64_t i = 0; i < n; ++i) l8[i] = uint8_t(labels[i]);
   D.lab.exact(n);
   cuda_check(cudaMemcpy(D.lab.p, l8.data(), n, cudaMemcpyHostToDevice), "H2D labels");
-  const std::vector<double> xl = sofg::host::xlogx_table(n);
-  D.xl.exact(n + 1);
-  cuda_check(cudaMemcpy(D.xl.p, xl.data(), 8 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx");
-  std::vector<float> xlf(xl.begin(), xl.end());
-  D.xlf.exact(n + 1);
-  cuda_check(cudaMemcpy(D.xlf.p, xlf.data(), 4 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx f32");
+  if (D.xl_n != n) {  // xlogx tables depend on n only: rebuilt when the sample count changes
+    const std::vector<double> xl = sofg::host::xlogx_table(n);
+    D.xl.exact(n + 1);
+    cuda_check(cudaMemcpy(D.xl.p, xl.data(), 8 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx");
+    std::vector<float> xlf(xl.begin(), xl.end());
+    D.xlf.exact(n + 1);
+    cuda_check(cudaMemcpy(D.xlf.p, xlf.data(), 4 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx f32");
+    D.xl_n = n;
+  }
 }
 
 struct PCfg {

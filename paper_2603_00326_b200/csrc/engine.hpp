@@ -82,6 +82,7 @@ struct DeviceData {
   DevBuf<uint8_t> lab;
   DevBuf<double> xl;
   DevBuf<float> xlf;  // float(xl[i]): prefilter table (exact values are always re-evaluated in double)
+  uint64_t xl_n = 0;  // sample count the xlogx tables were built for
   uint64_t n = 0, d = 0, ld = 0;
   int k = 0;
   std::vector<int32_t> labels_host;  // for root class counts

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.hpp"
 #include "dev_util.cuh"
@@ -487,7 +488,11 @@ cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* t
   return cudaGetLastError();
 }
 
-static int sweep_threads(uint32_t B) { return B * 5 / 8 > 40 ? 256 : 128; }
+static int sweep_threads(uint32_t B) {
+  static const int force = std::getenv("SOFG_SWEEP_NT") ? std::atoi(std::getenv("SOFG_SWEEP_NT")) : 0;
+  if (force) return force;
+  return B * 5 / 8 > 40 ? 256 : 128;
+}
 
 static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
   return size_t(K) * ldr * 4 + size_t(K) * B * sizeof(dev::Pair) +
@@ -499,7 +504,8 @@ static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
 static uint32_t sweep_k(uint64_t ldr, uint32_t B, uint32_t R) {
   const uint32_t per = std::max<uint32_t>(1, B * 5 / 8);  // pairs per sample
   const uint32_t want = std::max<uint32_t>(1, (uint32_t(sweep_threads(B)) / dev::kQ + per / 2) / per);
-  uint32_t K = std::min<uint32_t>(want, 8);
+  static const int force_k = std::getenv("SOFG_SWEEP_K") ? std::atoi(std::getenv("SOFG_SWEEP_K")) : 0;
+  uint32_t K = force_k ? uint32_t(force_k) : std::min<uint32_t>(want, 8);
   while (K > 1 && sweep_smem_k(ldr, B, R, K) > 112 * 1024) --K;
   return K;
 }
