@@ -91,6 +91,9 @@ uint64_t sofg_forest_breakeven(const sofg_forest* f);
 void sofg_forest_export(const sofg_forest* f, int64_t* tree_off, int32_t* left, int32_t* right,
                         int32_t* pred, float* thr, int64_t* term_off, uint32_t* feat,
                         float* weight);
+/* Zero-copy access: pointers to the forest's own arrays (valid until sofg_forest_free), in the
+ * order tree_off, left, right, pred, thr, term_off, feat, weight. */
+void sofg_forest_arrays(const sofg_forest* f, const void** arrays8);
 /* Build a forest from flat arrays (e.g. an oracle forest) for sofg_predict. */
 int sofg_forest_import(uint64_t n_trees, uint64_t n_features, int32_t class_count,
                        const int64_t* tree_off, const int32_t* left, const int32_t* right,

@@ -89,6 +89,7 @@ def load():
         getattr(L, fn).restype = u64
         getattr(L, fn).argtypes = [vp]
     L.sofg_forest_export.argtypes = [vp] * 9
+    L.sofg_forest_arrays.argtypes = [vp, vp]
     L.sofg_forest_import.argtypes = [u64, u64, i32] + [vp] * 8 + [P(vp)]
     L.sofg_forest_free.argtypes = [vp]
     L.sofg_predict.argtypes = [vp, vp, vp, u64, u64, vp, vp]
@@ -191,6 +192,7 @@ class Forest:
 
 
 def _export(h) -> Forest:
+    """Copy of a library forest (the handle stays with the caller)."""
     L = load()
     T, N, Q = L.sofg_forest_num_trees(h), L.sofg_forest_num_nodes(h), L.sofg_forest_num_terms(h)
     f = Forest(np.empty(T + 1, np.int64), np.empty(N, np.int32), np.empty(N, np.int32), np.empty(N, np.int32),
@@ -199,6 +201,53 @@ def _export(h) -> Forest:
     L.sofg_forest_export(h, *(a.ctypes.data for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off,
                                                        f.feat, f.weight)))
     return f
+
+
+class _ForestOwner:
+    """Keeps a library forest alive while numpy views of its arrays exist."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            try:
+                load().sofg_forest_free(self.h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+
+def _adopt(h) -> Forest:
+    """Zero-copy Forest over the library's arrays; the handle is freed with the last view."""
+    L = load()
+    T, N, Q = L.sofg_forest_num_trees(h), L.sofg_forest_num_nodes(h), L.sofg_forest_num_terms(h)
+    ptrs = (C.c_void_p * 8)()
+    L.sofg_forest_arrays(h, ptrs)
+    owner = _ForestOwner(h)
+
+    # numpy arrays cannot carry attributes: a subclass holds the owner reference instead
+    def own(i, count, ctype, dtype):
+        if count == 0 or not ptrs[i]:
+            return np.empty(0, dtype)
+        a = _Owned(np.ctypeslib.as_array((ctype * count).from_address(ptrs[i])).view(dtype))
+        a._owner = owner
+        return a
+
+    f = Forest(own(0, T + 1, C.c_int64, np.int64), own(1, N, C.c_int32, np.int32), own(2, N, C.c_int32, np.int32),
+               own(3, N, C.c_int32, np.int32), own(4, N, C.c_float, np.float32), own(5, N + 1, C.c_int64, np.int64),
+               own(6, Q, C.c_uint32, np.uint32), own(7, Q, C.c_float, np.float32), int(L.sofg_forest_breakeven(h)))
+    return f
+
+
+class _Owned(np.ndarray):
+    """ndarray view that keeps its memory owner alive (attribute `_owner`)."""
+
+    def __new__(cls, a):
+        return np.asarray(a).view(cls)
+
+    def __array_finalize__(self, obj):
+        self._owner = getattr(obj, "_owner", None)
 
 
 class Context:
@@ -251,10 +300,13 @@ class Context:
         c = cfg.to_c()
         h = C.c_void_p()
         _check(self.L.sofg_train_forest(self.h, C.byref(c), C.byref(h)), "train_forest")
-        try:
-            f = _export(h)
-        finally:
-            self.L.sofg_forest_free(h)
+        if os.environ.get("SOFG_COPY_EXPORT"):
+            try:
+                f = _export(h)
+            finally:
+                self.L.sofg_forest_free(h)
+        else:
+            f = _adopt(h)  # zero-copy; the library forest is freed with the arrays
         f.class_count, f.n_features = self.class_count, self.n_features
         return f
 

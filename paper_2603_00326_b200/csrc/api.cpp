@@ -123,6 +123,9 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   D.ld = (n + 31) / 32 * 32;
   D.X.exact(D.ld * d);
   copy_X(D.X.p, D.ld);
+  // Pageable host -> device copies can return before their DMA has landed, and the engine's
+  // stream does not order against the legacy stream: wait for the table before transposing it.
+  cuda_check(cudaDeviceSynchronize(), "upload sync");
   // Row-major copy for the sample-major projection sweep (sweep.cu); rows padded to 128 B. The
   // previous allocation is reused when it is large enough (a 16 GB free + malloc per upload costs
   // hundreds of ms).
@@ -149,6 +152,7 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
     cuda_check(cudaMemcpy(D.xlf.p, xlf.data(), 4 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx f32");
     D.xl_n = n;
   }
+  cuda_check(cudaDeviceSynchronize(), "upload sync");  // labels / tables landed (see above)
 }
 
 struct PCfg {
@@ -408,6 +412,18 @@ uint64_t sofg_forest_num_trees(const sofg_forest* f) { return f->f.n_trees(); }
 uint64_t sofg_forest_num_nodes(const sofg_forest* f) { return f->f.left.size(); }
 uint64_t sofg_forest_num_terms(const sofg_forest* f) { return f->f.feat.size(); }
 uint64_t sofg_forest_breakeven(const sofg_forest* f) { return f->f.breakeven; }
+
+void sofg_forest_arrays(const sofg_forest* fo, const void** a) {
+  const sofg::FlatForest& f = fo->f;
+  a[0] = f.tree_off.data();
+  a[1] = f.left.data();
+  a[2] = f.right.data();
+  a[3] = f.pred.data();
+  a[4] = f.thr.data();
+  a[5] = f.term_off.data();
+  a[6] = f.feat.data();
+  a[7] = f.weight.data();
+}
 
 void sofg_forest_export(const sofg_forest* fo, int64_t* tree_off, int32_t* left, int32_t* right,
                         int32_t* pred, float* thr, int64_t* term_off, uint32_t* feat,

@@ -193,6 +193,7 @@ class WaveRunner {
   const NodeRes* collect_view(const WaveSpec& w);
   // Only the wait for the wave (no host pool use): callers sharing a pool wait first, then
   // take their host turn and call collect_view().
+  bool last_was_sweep() const { return pend_sweep_; }
   float last_wave_ms() const { return last_wave_ms_; }  // device time of the last collected wave (stats on)
   void wait_wave();
   // Page-locked staging reused across calls (root segments).

@@ -218,22 +218,39 @@ cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const u
         off += h_nodes[node].n;
       }
     }
-    dev::BigSeg* d_segs = nullptr;
-    uint64_t *d_k0 = nullptr, *d_k1 = nullptr, *d_b = nullptr, *d_e = nullptr;
-    RowRes* d_rr = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_segs), sizeof(dev::BigSeg) * nseg, st);
-    if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&d_k0), 8 * keys, st);
-    if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&d_k1), 8 * keys, st);
-    if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&d_b), 8 * size_t(nseg), st);
-    if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&d_e), 8 * size_t(nseg), st);
-    if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&d_rr), sizeof(RowRes) * nseg, st);
-    if (!e) e = cudaMemcpyAsync(d_segs, segs.data(), sizeof(dev::BigSeg) * nseg, cudaMemcpyHostToDevice, st);
+    // scratch kept across calls (grow-only, per calling thread)
+    struct Arena {
+      void* p[7] = {};
+      size_t cap[7] = {};
+      void* get(int i, size_t bytes) {
+        if (bytes > cap[i]) {
+          if (p[i]) {
+            cudaDeviceSynchronize();  // earlier chunks may still read it
+            cudaFree(p[i]);
+          }
+          p[i] = nullptr;
+          cap[i] = 0;
+          if (cudaMalloc(&p[i], bytes + bytes / 4) != cudaSuccess) return nullptr;
+          cap[i] = bytes + bytes / 4;
+        }
+        return p[i];
+      }
+    };
+    static thread_local Arena ar;
+    dev::BigSeg* d_segs = static_cast<dev::BigSeg*>(ar.get(0, sizeof(dev::BigSeg) * nseg));
+    uint64_t* d_k0 = static_cast<uint64_t*>(ar.get(1, 8 * keys));
+    uint64_t* d_k1 = static_cast<uint64_t*>(ar.get(2, 8 * keys));
+    uint64_t* d_b = static_cast<uint64_t*>(ar.get(3, 8 * size_t(nseg)));
+    uint64_t* d_e = static_cast<uint64_t*>(ar.get(4, 8 * size_t(nseg)));
+    RowRes* d_rr = static_cast<RowRes*>(ar.get(5, sizeof(RowRes) * nseg));
+    if (!d_segs || !d_k0 || !d_k1 || !d_b || !d_e || !d_rr) return cudaErrorMemoryAllocation;
+    cudaError_t e = cudaMemcpyAsync(d_segs, segs.data(), sizeof(dev::BigSeg) * nseg, cudaMemcpyHostToDevice, st);
     if (e) return e;
     dev::k_big_keys<<<nseg, 256, 0, st>>>(nodes, d_segs, R, lab, vbase, V, d_k0, d_b, d_e);
     size_t tb = 0;
     e = cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tb, d_k0, d_k1, int64_t(keys), nseg, d_b, d_e, 0, 64, st);
-    void* d_tmp = nullptr;
-    if (!e) e = cudaMallocAsync(&d_tmp, tb ? tb : 1, st);
+    void* d_tmp = e ? nullptr : ar.get(6, tb ? tb : 1);
+    if (!e && !d_tmp) e = cudaErrorMemoryAllocation;
     if (!e) e = cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tb, d_k0, d_k1, int64_t(keys), nseg, d_b, d_e, 0, 64, st);
     if (e) return e;
     if (k == 2)
@@ -242,9 +259,6 @@ cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const u
       dev::k_big_scan<kMaxClasses><<<nseg, dev::kBigThreads, 0, st>>>(nodes, d_segs, R, k, row_ptr, d_k1, xl, d_rr);
     dev::k_big_select<<<(nn + 127) / 128, 128, 0, st>>>(d_segs, nn, R, d_rr, res);
     e = cudaGetLastError();
-    for (void* p : {static_cast<void*>(d_segs), static_cast<void*>(d_k0), static_cast<void*>(d_k1),
-                    static_cast<void*>(d_b), static_cast<void*>(d_e), static_cast<void*>(d_rr), d_tmp})
-      cudaFreeAsync(p, st);
     if (e) return e;
     i0 = i1;
   }

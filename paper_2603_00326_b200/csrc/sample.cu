@@ -364,18 +364,30 @@ cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t 
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(dev::k_sample_projection, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemOptin);
+  // global scratch for very dense matrices: grow-only, per calling thread (no stream-ordered
+  // pool allocations on the hot path)
+  static thread_local void* g_scratch = nullptr;
+  static thread_local size_t g_cap = 0;
   uint32_t* gkeys = nullptr;
   if (global_sets) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&gkeys),
-                                    size_t(n_nodes) * 2 * size_t(zpad) * 4, st);
-    if (e != cudaSuccess) return e;
+    const size_t bytes = size_t(n_nodes) * 2 * size_t(zpad) * 4;
+    if (bytes > g_cap) {
+      if (g_scratch) {
+        cudaDeviceSynchronize();
+        cudaFree(g_scratch);
+      }
+      g_scratch = nullptr;
+      g_cap = 0;
+      cudaError_t e = cudaMalloc(&g_scratch, bytes + bytes / 4);
+      if (e != cudaSuccess) return e;
+      g_cap = bytes + bytes / 4;
+    }
+    gkeys = static_cast<uint32_t*>(g_scratch);
   }
   const int grid = (n_nodes + warps - 1) / warps;
   dev::k_sample_projection<<<grid, warps * 32, smem, st>>>(nodes, n_nodes, d, R, zpad, terms,
                                                            row_ptr, pos_after, gkeys);
-  cudaError_t e = cudaGetLastError();
-  if (gkeys) cudaFreeAsync(gkeys, st);
-  return e;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_hist_draws(const NodeIn* nodes, const uint32_t* hist_nodes, int n_hist,

@@ -440,6 +440,30 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       }
       const NodeRes* res = eng.collect_view(w);
       const double lv_wait = ms_since(t0);
+      if (std::getenv("SOFG_WAVE_HASH")) {  // debugging aid: per-wave result digest
+        uint64_t hsh = 1469598103934665603ull;
+        for (size_t i = 0; i < N; ++i) {
+          const uint64_t v = (uint64_t(uint32_t(res[i].row)) << 32) ^ res[i].n_left ^
+                             (uint64_t(__builtin_bit_cast(uint32_t, res[i].threshold)) << 16);
+          hsh = (hsh ^ v) * 1099511628211ull;
+        }
+        std::fprintf(stderr, "[wave] level %llu nodes %zu sweep %d hash %016llx\n",
+                     (unsigned long long)times.levels, N, int(eng.last_was_sweep()),
+                     (unsigned long long)hsh);
+        if (const char* dump = std::getenv("SOFG_WAVE_DUMP")) {  // node records + results
+          if (FILE* fh = std::fopen(dump, "ab")) {
+            const uint64_t nn = N;
+            std::fwrite(&nn, 8, 1, fh);
+            std::fwrite(w.nodes.data(), sizeof(NodeIn), N, fh);
+            for (size_t i = 0; i < N; ++i) {
+              const uint32_t rec[4] = {uint32_t(res[i].row), __builtin_bit_cast(uint32_t, res[i].threshold),
+                                       res[i].n_left, res[i].n_left_search};
+              std::fwrite(rec, 4, 4, fh);
+            }
+            std::fclose(fh);
+          }
+        }
+      }
       times.ms_wait += lv_wait;
 
       t0 = Clock::now();

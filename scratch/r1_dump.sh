@@ -1,0 +1,3 @@
+rm -f gpurun_out/dump_*.bin
+for i in 1 2 3 4 5 6; do SOFG_WAVE_HASH=1 SOFG_WAVE_DUMP=gpurun_out/dump_$i.bin python scratch/dbg_hash.py > gpurun_out/hash_$i.log 2>&1; done
+md5sum gpurun_out/dump_*.bin

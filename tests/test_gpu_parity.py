@@ -320,3 +320,17 @@ def test_sweep_special_values(gpu_ctx, oracle, with_inf, mode, breakeven):
     gpu_ctx.upload(X, y, 2)
     gc, oc = _cfg(n_trees=3, mode=mode, breakeven=breakeven, seed=17)
     assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, 2, oc)) == []
+
+
+def test_reupload_same_shape_alternating(gpu_ctx, oracle):
+    """Back-to-back uploads of different tables of one shape: the row table and label buffers are
+    reused, and each upload must have landed before the next training reads it (pageable copies
+    run on the legacy stream; the engine stream does not order against it)."""
+    X, y = oracle.generate_trunk(6000, 24, 11)
+    variants = [X, np.round(X * 4) / 4, -X, X * np.float32(3.0)]
+    for rep in range(2):
+        for data in variants:
+            data = np.ascontiguousarray(data, np.float32)
+            gpu_ctx.upload(data, y, 2)
+            gc, oc = _cfg(n_trees=3, mode="dynamic", breakeven=400, seed=5 + rep)
+            assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(data, y, 2, oc)) == []
