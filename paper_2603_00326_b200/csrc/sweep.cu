@@ -503,7 +503,10 @@ static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
 // in ~63% of the batch's trees), within shared memory.
 static uint32_t sweep_k(uint64_t ldr, uint32_t B, uint32_t R) {
   const uint32_t per = std::max<uint32_t>(1, B * 5 / 8);  // pairs per sample
-  const uint32_t want = std::max<uint32_t>(1, (uint32_t(sweep_threads(B)) / dev::kQ + per / 2) / per);
+  // about two rounds of pair slots per chunk: one round per sample leaves a mostly empty second
+  // round whenever a sample sits in more trees than there are slots (measured at 100 trees:
+  // K = 1 -> 496 ms, K = 2 -> 470 ms, K = 3 -> 533 ms of sweep per step)
+  const uint32_t want = std::max<uint32_t>(1, (2 * uint32_t(sweep_threads(B)) / dev::kQ + per / 2) / per);
   static const int force_k = std::getenv("SOFG_SWEEP_K") ? std::atoi(std::getenv("SOFG_SWEEP_K")) : 0;
   uint32_t K = force_k ? uint32_t(force_k) : std::min<uint32_t>(want, 8);
   while (K > 1 && sweep_smem_k(ldr, B, R, K) > 112 * 1024) --K;
