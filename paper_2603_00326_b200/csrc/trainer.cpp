@@ -256,6 +256,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   w.B = uint32_t(B);
   w.total = total;
   if (const char* e = std::getenv("SOFG_PROJECT_MODE")) w.force_mode = std::atoi(e);
+  if (const char* e = std::getenv("SOFG_HIST_CHUNK")) w.chunk_cap = std::max(256, std::atoi(e));
   eng.set_pool(&pool);
 
   auto count_open = [](const std::vector<std::vector<Open>>& v) {
