@@ -106,7 +106,7 @@ void append_forest(sofg::FlatForest& dst, const sofg::FlatForest& src) {
 
 // Dataset staging into HBM: ld = n rounded up to 32 samples (128 B column alignment).
 void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t k,
-            const std::function<void(float* dev, uint64_t ld)>& copy_X) {
+            const std::function<bool(float* dev, uint64_t ld)>& copy_X) {
   if (n < 1 || d < 1) throw std::invalid_argument("empty dataset");
   if (n >= (1ull << 31)) throw std::invalid_argument("n_samples must be < 2^31");
   if (k < 1) throw std::invalid_argument("class_count must be positive");
@@ -122,10 +122,12 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   D.k = k;
   D.ld = (n + 31) / 32 * 32;
   D.X.exact(D.ld * d);
-  copy_X(D.X.p, D.ld);
-  // Pageable host -> device copies can return before their DMA has landed, and the engine's
-  // stream does not order against the legacy stream: wait for the table before transposing it.
-  cuda_check(cudaDeviceSynchronize(), "upload sync");
+  // Pageable host -> device copies (legacy stream) can return before their DMA has landed, and
+  // the engine's stream does not order against the legacy stream: wait for those. Copies from
+  // page-locked memory are enqueued on the engine stream instead and left in flight — training
+  // starts with host-side work (bootstrap sampling) that overlaps them.
+  if (!copy_X(D.X.p, D.ld)) cuda_check(cudaDeviceSynchronize(), "upload sync");
+  cudaStream_t st = c->eng->stream();
   // Row-major copy for the sample-major projection sweep (sweep.cu); rows padded to 128 B. The
   // previous allocation is reused when it is large enough (a 16 GB free + malloc per upload costs
   // hundreds of ms).
@@ -134,25 +136,29 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
     D.XR.release();
   } else {
     D.XR.exact(n * D.ldr);
-    cuda_check(sofg::launch_transpose_rows(D.X.p, D.ld, n, d, D.XR.p, D.ldr, c->eng->stream()),
-               "transpose_rows");
-    cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync transpose");
+    cuda_check(sofg::launch_transpose_rows(D.X.p, D.ld, n, d, D.XR.p, D.ldr, st), "transpose_rows");
   }
   D.labels_host.assign(labels, labels + n);
-  std::vector<uint8_t> l8(n);
+  // labels through page-locked staging, on the engine stream (the staging is rewritten only
+  // after its previous copy has completed)
+  if (!D.lab_ev) cuda_check(cudaEventCreateWithFlags(&D.lab_ev, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventSynchronize(D.lab_ev), "label staging");
+  uint8_t* l8 = D.lab_stage.ensure(n);
   for (uint64_t i = 0; i < n; ++i) l8[i] = uint8_t(labels[i]);
   D.lab.exact(n);
-  cuda_check(cudaMemcpy(D.lab.p, l8.data(), n, cudaMemcpyHostToDevice), "H2D labels");
+  cuda_check(cudaMemcpyAsync(D.lab.p, l8, n, cudaMemcpyHostToDevice, st), "H2D labels");
+  cuda_check(cudaEventRecord(D.lab_ev, st), "event");
   if (D.xl_n != n) {  // xlogx tables depend on n only: rebuilt when the sample count changes
     const std::vector<double> xl = sofg::host::xlogx_table(n);
-    D.xl.exact(n + 1);
-    cuda_check(cudaMemcpy(D.xl.p, xl.data(), 8 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx");
     std::vector<float> xlf(xl.begin(), xl.end());
+    D.xl.exact(n + 1);
     D.xlf.exact(n + 1);
-    cuda_check(cudaMemcpy(D.xlf.p, xlf.data(), 4 * (n + 1), cudaMemcpyHostToDevice), "H2D xlogx f32");
+    cuda_check(cudaMemcpyAsync(D.xl.p, xl.data(), 8 * (n + 1), cudaMemcpyHostToDevice, st), "H2D xlogx");
+    cuda_check(cudaMemcpyAsync(D.xlf.p, xlf.data(), 4 * (n + 1), cudaMemcpyHostToDevice, st),
+               "H2D xlogx f32");
+    cuda_check(cudaStreamSynchronize(st), "sync tables");  // the host vectors die here
     D.xl_n = n;
   }
-  cuda_check(cudaDeviceSynchronize(), "upload sync");  // labels / tables landed (see above)
 }
 
 struct PCfg {
@@ -262,8 +268,17 @@ int sofg_upload_dataset(sofg_ctx* c, const float* X, uint64_t n, uint64_t d, con
   return guard([&] {
     require_ctx(c);
     upload(c, n, d, y, k, [&](float* dev, uint64_t ld) {
-      cuda_check(cudaMemcpy2D(dev, ld * 4, X, n * 4, n * 4, d, cudaMemcpyHostToDevice),
-                 "H2D table");
+      cudaPointerAttributes at{};
+      const bool pinned = cudaPointerGetAttributes(&at, X) == cudaSuccess && at.type == cudaMemoryTypeHost;
+      cudaGetLastError();  // clear a failed attribute query (plain pageable memory)
+      if (pinned) {
+        cuda_check(cudaMemcpy2DAsync(dev, ld * 4, X, n * 4, n * 4, d, cudaMemcpyHostToDevice,
+                                     c->eng->stream()),
+                   "H2D table");
+        return true;
+      }
+      cuda_check(cudaMemcpy2D(dev, ld * 4, X, n * 4, n * 4, d, cudaMemcpyHostToDevice), "H2D table");
+      return false;
     });
   });
 }
@@ -278,6 +293,7 @@ int sofg_upload_columns(sofg_ctx* c, const float* const* cols, uint64_t n, uint6
                                    c->eng->stream()),
                    "H2D column");
       cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync columns");
+      return true;
     });
   });
 }
@@ -295,6 +311,7 @@ int sofg_generate_trunk(sofg_ctx* c, uint64_t n, uint64_t d, int32_t k, uint64_t
       cuda_check(launch_generate_trunk(dev, ld, tmp.p, n, d, k, seed, c->eng->stream()),
                  "generate_trunk");
       cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync generate");
+      return true;
     });
   });
 }
@@ -303,6 +320,7 @@ int sofg_download_dataset(sofg_ctx* c, float* X, int32_t* y) {
   return guard([&] {
     require_data(c);
     const sofg::DeviceData& D = c->eng->data();
+    cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync upload");  // an upload may be in flight
     if (X)
       cuda_check(cudaMemcpy2D(X, D.n * 4, D.X.p, D.ld * 4, D.n * 4, D.d, cudaMemcpyDeviceToHost),
                  "D2H table");

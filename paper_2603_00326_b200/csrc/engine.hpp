@@ -83,6 +83,14 @@ struct DeviceData {
   DevBuf<double> xl;
   DevBuf<float> xlf;  // float(xl[i]): prefilter table (exact values are always re-evaluated in double)
   uint64_t xl_n = 0;  // sample count the xlogx tables were built for
+  PinnedBuf<uint8_t> lab_stage;     // page-locked staging of the labels (asynchronous upload)
+  cudaEvent_t lab_ev = nullptr;     // the staging's last copy
+  DeviceData() = default;
+  DeviceData(const DeviceData&) = delete;
+  DeviceData& operator=(const DeviceData&) = delete;
+  ~DeviceData() {
+    if (lab_ev) cudaEventDestroy(lab_ev);
+  }
   uint64_t n = 0, d = 0, ld = 0;
   int k = 0;
   std::vector<int32_t> labels_host;  // for root class counts
