@@ -501,7 +501,11 @@ int sofg_forest_import(uint64_t n_trees, uint64_t n_features, int32_t k, const i
   });
 }
 
-void sofg_forest_free(sofg_forest* f) { delete f; }
+void sofg_forest_free(sofg_forest* f) {
+  if (!f) return;
+  sofg::recycle_forest(std::move(f->f));
+  delete f;
+}
 
 int sofg_predict(sofg_ctx* c, const sofg_forest* fo, const float* rows, uint64_t n_rows,
                  uint64_t d, int32_t* labels, double* votes) {

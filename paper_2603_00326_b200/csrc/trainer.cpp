@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "host_rng.hpp"
 #include "kernels.hpp"
@@ -83,6 +84,40 @@ std::vector<size_t> ThreadPool::chunks(size_t n, size_t grain,
   for (size_t i = 0; i <= c; ++i) b[i] = n * i / c;
   parallel_for(c, [&](size_t i) { f(i, b[i], b[i + 1]); });
   return b;
+}
+
+namespace {
+std::mutex g_recycle_mu;
+std::vector<FlatForest> g_recycled;
+}  // namespace
+
+void recycle_forest(FlatForest&& f) {
+  std::lock_guard<std::mutex> g(g_recycle_mu);
+  if (g_recycled.size() < 2) g_recycled.push_back(std::move(f));
+}
+
+void adopt_recycled(FlatForest& out) {
+  if (!out.left.empty()) return;  // appending to a non-empty forest: keep its arrays
+  std::lock_guard<std::mutex> g(g_recycle_mu);
+  if (g_recycled.empty()) return;
+  FlatForest& r = g_recycled.back();
+  auto take = [](auto& dst, auto& src) {
+    src.clear();
+    dst.swap(src);
+  };
+  take(out.left, r.left);
+  take(out.right, r.right);
+  take(out.pred, r.pred);
+  take(out.thr, r.thr);
+  take(out.feat, r.feat);
+  take(out.weight, r.weight);
+  r.tree_off.resize(out.tree_off.size());
+  std::copy(out.tree_off.begin(), out.tree_off.end(), r.tree_off.begin());
+  out.tree_off.swap(r.tree_off);
+  r.term_off.resize(out.term_off.size());
+  std::copy(out.term_off.begin(), out.term_off.end(), r.term_off.begin());
+  out.term_off.swap(r.term_off);
+  g_recycled.pop_back();
 }
 
 // ------------------------------------------------------------------------------ scheduler
@@ -537,6 +572,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     node_base[b + 1] = node_base[b] + trees[b].size();
     term_base[b + 1] = term_base[b] + pools[b].size();
   }
+  adopt_recycled(out);
   const size_t N0 = out.left.size(), Q0 = out.feat.size(), T0 = out.tree_off.size();
   out.left.resize(N0 + node_base[B]);
   out.right.resize(N0 + node_base[B]);

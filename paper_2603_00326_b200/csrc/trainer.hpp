@@ -54,6 +54,11 @@ struct FlatForest {
   uint64_t n_trees() const { return tree_off.size() - 1; }
 };
 
+// Freed forests' arrays are kept (up to two) and handed to the next training's output, so a
+// step does not fault in hundreds of MB of fresh pages for its forest.
+void recycle_forest(FlatForest&& f);
+void adopt_recycled(FlatForest& out);
+
 struct TrainParams {
   int mode = 2;  // 0 exact-only, 1 histogram-only, 2 dynamic
   uint64_t bins = 256;
