@@ -187,6 +187,9 @@ __global__ void __launch_bounds__(256) k_hist_count(
       const uint32_t rg = wk.row0 + uint32_t(g);
       if (rg < R && nb_g[size_t(h) * R + rg] > 0) live |= 1u << g;
     }
+    float root[8];  // each row's tree root (the median boundary): level 0 without a load
+#pragma unroll
+    for (int g = 0; g < 8; ++g) root[g] = bnd_s[g * bpad + 1];
     for (uint32_t j = uint32_t(threadIdx.x); j < wk.len; j += blockDim.x) {
       const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(wk.start + j) * Rp);
       const float4 a = __ldg(src), b = __ldg(src + 1);
@@ -197,9 +200,9 @@ __global__ void __launch_bounds__(256) k_hist_count(
         constexpr int BP = 1 << LT;
         int t[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) t[g] = 1;
+        for (int g = 0; g < 8; ++g) t[g] = 2 + (root[g] <= v[g] ? 1 : 0);  // level 0 from registers
 #pragma unroll
-        for (int l = 0; l < LT; ++l) {
+        for (int l = 1; l < LT; ++l) {
 #pragma unroll
           for (int g = 0; g < 8; ++g) t[g] = 2 * t[g] + (bnd_s[g * BP + t[g]] <= v[g] ? 1 : 0);
         }
