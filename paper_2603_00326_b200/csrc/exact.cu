@@ -317,6 +317,9 @@ __global__ void __launch_bounds__(128) k_exact_prune(
     }
   }
   __syncwarp();
+  uint32_t mid[GR];  // each row's middle pivot: the search's first step without a load
+#pragma unroll
+  for (int g = 0; g < GR; ++g) mid[g] = s_piv[w][g][pslot(kPB / 2 - 1)];
   for (uint32_t j = uint32_t(lane); j < n; j += 32) {
     const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(j) * Rp);
     const float4 a = __ldg(src), b = __ldg(src + 1);
@@ -324,9 +327,9 @@ __global__ void __launch_bounds__(128) k_exact_prune(
     const uint32_t y = uint32_t(__ldg(lab + nd.begin + j)) & 1u;
     uint32_t lo[GR];
 #pragma unroll
-    for (int g = 0; g < GR; ++g) lo[g] = 0;
+    for (int g = 0; g < GR; ++g) lo[g] = mid[g] <= order_key(v[g]) ? uint32_t(kPB / 2) : 0u;
 #pragma unroll
-    for (uint32_t step = kPB / 2; step > 0; step >>= 1) {
+    for (uint32_t step = kPB / 4; step > 0; step >>= 1) {
 #pragma unroll
       for (int g = 0; g < GR; ++g)
         if (s_piv[w][g][pslot(lo[g] + step - 1)] <= order_key(v[g])) lo[g] += step;
