@@ -334,3 +334,25 @@ def test_reupload_same_shape_alternating(gpu_ctx, oracle):
             gpu_ctx.upload(data, y, 2)
             gc, oc = _cfg(n_trees=3, mode="dynamic", breakeven=400, seed=5 + rep)
             assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(data, y, 2, oc)) == []
+
+
+def test_pinned_upload_in_flight(gpu_ctx, oracle):
+    """Uploads from page-locked memory (sofg_host_alloc) stay in flight on the engine stream while
+    training starts on the host; rewriting the same page-locked buffer between steps must still
+    give each step's own trees."""
+    import ctypes as C
+
+    X, y = oracle.generate_trunk(8000, 32, 13)
+    d, n = X.shape
+    L = gpu_ctx.L
+    ptr = L.sofg_host_alloc(n * d * 4)
+    assert ptr
+    try:
+        H = np.ctypeslib.as_array((C.c_float * (n * d)).from_address(ptr)).reshape(d, n)
+        for rep, data in enumerate((X, -X, np.round(X * 2) / 2)):
+            H[...] = data
+            gpu_ctx.upload_ptr(ptr, y, n, d, 2)
+            gc, oc = _cfg(n_trees=3, mode="dynamic", breakeven=400, seed=31 + rep)
+            assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(H.copy(), y, 2, oc)) == []
+    finally:
+        L.sofg_host_free(ptr)
