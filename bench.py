@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-trees", type=int, default=0, help="CPU baseline sample (0 = one per core)")
     p.add_argument("--holdout", type=int, default=20000, help="hold-out rows for the accuracy check")
+    p.add_argument("--classes", type=int, default=2, help="trunk-model classes (BASELINE config 5: 4)")
+    p.add_argument("--density", type=float, default=0.0,
+                   help="projection cell density (0 = the reference default; config 5 'dense' > 0)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="skip the untimed per-kernel profile step")
@@ -180,15 +183,16 @@ def cpu_reference_sample(X, y, n_trees, args, threads, predict_rows=None):
     import oracle_lib
 
     orc = oracle_lib.get("reference") if oracle_lib.have_reference() else oracle_lib.get("port")
-    ds = orc.dataset(X, y, 2)
+    k = int(getattr(args, "classes", 2))
+    ds = orc.dataset(X, y, k)
     cfg = oracle_lib.make_config(n_trees=n_trees, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
-                                 n_workers=threads)
+                                 n_workers=threads, cell_density=float(getattr(args, "density", 0.0)))
     timing = {}
     pred = None
     if predict_rows is None:
         forest = orc.train_forest_ds(ds, cfg, timing=timing)
     else:  # the reference's predict on the trained handle, outside the timed call
-        forest, (pred, _) = orc.train_forest_ds(ds, cfg, predict_rows=predict_rows, d=X.shape[0], k=2,
+        forest, (pred, _) = orc.train_forest_ds(ds, cfg, predict_rows=predict_rows, d=X.shape[0], k=k,
                                                 timing=timing)
     orc.dataset_free(ds)
     return forest, timing["train_s"], orc.kind, pred
@@ -228,7 +232,7 @@ def run_reference(args, rank, world):
             "steps_requested": args.steps, "warmup": 0, "ms_per_step": 1000 * statistics.median(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
             "data": "synthetic trunk model (numpy, host)", "impl": "reference",
-            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, trees to purity"
+            "config": {"workload": f"synthetic {args.n}x{args.d} {args.classes}-class, trees to purity"
                                    + (" (BASELINE config 3)" if (args.n, args.d) == (1_000_000, 4096) else ""),
                        "n_samples": args.n, "n_features": args.d, "trees_per_step": n_trees,
                        "breakeven": args.breakeven, "mode": args.mode, "seed": args.seed},
@@ -265,7 +269,7 @@ def main():
     torch.cuda.set_device(local)
     ctx = sofg.Context(local)
     t0 = time.perf_counter()
-    ctx.generate_trunk(args.n, args.d, 2, seed=1)
+    ctx.generate_trunk(args.n, args.d, args.classes, seed=1)
     gen_s = time.perf_counter() - t0
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     T = args.trees
@@ -277,7 +281,7 @@ def main():
         # host threads split between the ranks sharing this host (one rank per GPU)
         workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
         return sofg.TrainConfig(n_trees=total_trees, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
-                                n_workers=workers, tree_begin=b, tree_end=b + T)
+                                n_workers=workers, tree_begin=b, tree_end=b + T, cell_density=args.density)
 
     def barrier():
         if dist:
@@ -348,7 +352,7 @@ def main():
         for s in range(args.warmup + args.steps, args.warmup + args.steps + args.e2e_steps):
             torch.cuda.synchronize()
             ts = time.perf_counter()
-            ctx.upload_ptr(hptr, yh, args.n, args.d, 2)
+            ctx.upload_ptr(hptr, yh, args.n, args.d, args.classes)
             f = ctx.train_forest(cfg_for(s))
             torch.cuda.synchronize()
             t_e.append(time.perf_counter() - ts)
@@ -368,8 +372,13 @@ def main():
             Xh = np.zeros((args.d, args.n), np.float32)
             yh = np.zeros(args.n, np.int32)
             ctx.download(Xh, yh)
-        # hold-out rows: a second trunk draw, row-major
-        Xt, yt = host_trunk(args.holdout, args.d, seed=2)
+        # hold-out rows: a second draw of the same trunk model (device generator, seed 2)
+        hctx = sofg.Context(0)
+        Xt = np.zeros((args.d, args.holdout), np.float32)
+        yt = np.zeros(args.holdout, np.int32)
+        hctx.generate_trunk(args.holdout, args.d, args.classes, seed=2)
+        hctx.download(Xt, yt)
+        hctx.close()
         rows = np.ascontiguousarray(Xt.T)
         forest, dt, kind, cpu_lab = cpu_reference_sample(Xh, yh, n_cpu, args, threads, predict_rows=rows)
         import oracle_lib
@@ -387,7 +396,7 @@ def main():
         cpu = {"value": n_cpu / dt, "unit": "trees/s", "cores": threads, "kind": kind,
                "sample": f"trees 0..{n_cpu - 1} of the bench forest (full {args.n} x {args.d} trees, "
                          f"{threads} threads), {dt:.1f} s", "bitexact_trees": f"{same}/{n_cpu}",
-               "holdout": {"rows": int(args.holdout), "data": "trunk model, seed 2",
+               "holdout": {"rows": int(args.holdout), "data": "trunk model (device generator), seed 2",
                            f"cpu_accuracy_{n_cpu}_trees": round(float((cpu_lab == yt).mean()), 5),
                            f"gpu_accuracy_{n_cpu}_trees": round(float((gpu_lab_head == yt).mean()), 5),
                            "identical_labels": bool(np.array_equal(cpu_lab, gpu_lab_head)),
@@ -397,10 +406,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 values / f64 accumulate+gain",
             "data": "synthetic trunk model generated in HBM (counter-based RNG), inputs > L2",
-            "config": {"workload": f"synthetic {args.n}x{args.d} 2-class, {T} trees per GPU to purity"
+            "config": {"workload": f"synthetic {args.n}x{args.d} {args.classes}-class, {T} trees per GPU to purity"
                                    + (" (BASELINE config 3)" if (args.n, args.d) == (1_000_000, 4096) else ""),
                        "n_samples": args.n, "n_features": args.d, "trees_per_gpu_per_step": T,
                        "mode": args.mode, "breakeven": args.breakeven, "bin_count": 256, "seed": args.seed,
+                       "classes": args.classes, "cell_density": args.density or "reference default",
                        "parallelism": f"tree-sharded x{world}",
                        "l2": f"inputs {args.n * args.d * 4 / 1e9:.2f} GB table (+ row-major copy) vs 126 MB L2",
                        "nodes_per_step": nodes / args.steps, "datagen_s": round(gen_s, 2)},
