@@ -363,7 +363,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       if (b < kPruneFrom) prune_off += exact_b_count[size_t(b)];
       else prune_n += exact_b_count[size_t(b)];
     }
-    const bool prune = k == 2 && prune_n > 0 && !(std::getenv("SOFG_PRUNE") && std::atoi(std::getenv("SOFG_PRUNE")) == 0);
+    const bool prune = k <= 4 && prune_n > 0 && !(std::getenv("SOFG_PRUNE") && std::atoi(std::getenv("SOFG_PRUNE")) == 0);
     float* d_rowlb = nullptr;
     unsigned long long* d_xstar = nullptr;
     if (prune) {
@@ -373,11 +373,11 @@ void WaveRunner::submit(const WaveSpec& w) {
       size_t n_small = 0;
       for (int b = kPruneFrom; b <= 4; ++b) n_small += exact_b_count[size_t(b)];
       cuda_check(launch_exact_prune(d_nodes, d_exact + prune_off, int(n_small), R, d_rp, w.lab_in,
-                                    d_gbase, d_G, D.xl.p, d_rowlb, d_xstar, 32, st_),
+                                    d_gbase, d_G, D.xl.p, d_rowlb, d_xstar, 32, k, st_),
                  "exact_prune");
       cuda_check(launch_exact_prune(d_nodes, d_exact + prune_off + n_small, int(prune_n - n_small), R,
                                     d_rp, w.lab_in, d_gbase, d_G, D.xl.p, d_rowlb + n_small * R,
-                                    d_xstar + n_small, 64, st_),
+                                    d_xstar + n_small, 64, k, st_),
                  "exact_prune");
       ++launches;
       mark("exact_prune");

@@ -263,15 +263,16 @@ __device__ __forceinline__ double x_at(const double* __restrict__ xl, uint32_t l
 // 4 warps per CTA; per warp the sorted pivots and the bucket class counts of its 8 rows live in
 // shared memory.
 // kPB value buckets per row (32 or 64), kPBE per lane.
-template <int kPB>
+template <int kPB, int KC>
 __global__ void __launch_bounds__(128) k_exact_prune(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     const uint32_t* __restrict__ row_ptr, const uint8_t* __restrict__ lab,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
-    const double* __restrict__ xl, float* __restrict__ rowlb, unsigned long long* __restrict__ xstar) {
+    const double* __restrict__ xl, float* __restrict__ rowlb, unsigned long long* __restrict__ xstar,
+    int k) {
   constexpr int GR = 8;
   constexpr int kPBE = kPB / 32;
-  __shared__ uint32_t s_cnt[4][GR][kPB][2];
+  __shared__ uint32_t s_cnt[4][GR][kPB][KC];
   // pivot i at word i + i/32: positions i and i+32 fall in different banks (a search step's probes
   // are spread over both halves)
   constexpr int kPP = kPB + kPB / 32;
@@ -311,8 +312,8 @@ __global__ void __launch_bounds__(128) k_exact_prune(
 #pragma unroll
       for (int e = 0; e < kPBE; ++e) {
         s_piv[w][g][pslot(lane * kPBE + e)] = k[e];
-        s_cnt[w][g][lane * kPBE + e][0] = 0;
-        s_cnt[w][g][lane * kPBE + e][1] = 0;
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc) s_cnt[w][g][lane * kPBE + e][cc] = 0;
       }
     }
   }
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(128) k_exact_prune(
     const float4* src = reinterpret_cast<const float4*>(Vn + uint64_t(j) * Rp);
     const float4 a = __ldg(src), b = __ldg(src + 1);
     const float v[GR] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    const uint32_t y = uint32_t(__ldg(lab + nd.begin + j)) & 1u;
+    const uint32_t y = min(uint32_t(__ldg(lab + nd.begin + j)), uint32_t(KC - 1));
     uint32_t lo[GR];
 #pragma unroll
     for (int g = 0; g < GR; ++g) lo[g] = mid[g] <= order_key(v[g]) ? uint32_t(kPB / 2) : 0u;
@@ -349,42 +350,67 @@ __global__ void __launch_bounds__(128) k_exact_prune(
       if (lane == 0) *out = __int_as_float(0x7f800000);
       continue;
     }
-    uint32_t c0[kPBE], c1[kPBE], s0 = 0, s1 = 0;
+    uint32_t cnt[kPBE][KC], sum[KC];
 #pragma unroll
-    for (int e = 0; e < kPBE; ++e) {
-      c0[e] = s_cnt[w][g][lane * kPBE + e][0];
-      c1[e] = s_cnt[w][g][lane * kPBE + e][1];
-      s0 += c0[e];
-      s1 += c1[e];
-    }
-    uint32_t t0, t1;
-    uint32_t a0 = warp_excl_scan_u32(s0, lane, &t0);
-    uint32_t a1 = warp_excl_scan_u32(s1, lane, &t1);
-    const uint32_t tot[2] = {t0, t1};
+    for (int cc = 0; cc < KC; ++cc) sum[cc] = 0;
+#pragma unroll
+    for (int e = 0; e < kPBE; ++e)
+#pragma unroll
+      for (int cc = 0; cc < KC; ++cc) {
+        cnt[e][cc] = s_cnt[w][g][lane * kPBE + e][cc];
+        sum[cc] += cnt[e][cc];
+      }
+    uint32_t a[KC], tot[KC];
+#pragma unroll
+    for (int cc = 0; cc < KC; ++cc) a[cc] = warp_excl_scan_u32(sum[cc], lane, &tot[cc]);
+    auto xat = [&](const uint32_t (&left)[KC]) {
+      uint32_t nl = 0;
+#pragma unroll
+      for (int cc = 0; cc < KC; ++cc) nl += left[cc];
+      return impurity_sum<KC>(xl, left, tot, k, nl, n - nl);
+    };
     // X at every bucket's end point (its left counts after the bucket); the pivot candidates are
-    // the valid ones among them, and a bucket's box has corners start, end, (a0, L1), (L0, a1)
+    // the valid ones among them. A bucket's candidates lie in the box [a, L] of left counts; X is
+    // concave there, so its minimum is at a vertex (start and end are the shared end points; the
+    // other vertices only matter when at least two classes are present in the bucket).
     double xe[kPBE];
     double xp = inf, lb = inf;
 #pragma unroll
     for (int e = 0; e < kPBE; ++e) {
       const uint32_t bk = uint32_t(lane * kPBE + e);
-      const uint32_t L0 = a0 + c0[e], L1 = a1 + c1[e];
-      xe[e] = x_at<2>(xl, L0, L1, tot, 2, n);
+      uint32_t L[KC], nl = 0, classes = 0;
+#pragma unroll
+      for (int cc = 0; cc < KC; ++cc) {
+        L[cc] = a[cc] + cnt[e][cc];
+        nl += L[cc];
+        classes += cnt[e][cc] > 0 ? 1u : 0u;
+      }
+      xe[e] = xat(L);
       // pivot candidate: split after bucket bk ("v < pivot_bk"), a real gap when 0 < nl < n —
       // except at a +0 pivot, where -0 values (a smaller key, the same float) sit on the left
-      if (bk < uint32_t(kPB - 1) && L0 + L1 > 0 && L0 + L1 < n && s_piv[w][g][pslot(bk)] != 0x80000000u)
+      if (bk < uint32_t(kPB - 1) && nl > 0 && nl < n && s_piv[w][g][pslot(bk)] != 0x80000000u)
         xp = fmin(xp, xe[e]);
-      // gaps inside the bucket: the box [a0, L0] x [a1, L1]; X is concave, so its minimum is at a
-      // corner (one-class buckets: a segment, minimum at its ends)
-      if (c0[e] > 0 && c1[e] > 0)
-        lb = fmin(lb, fmin(x_at<2>(xl, a0, L1, tot, 2, n), x_at<2>(xl, L0, a1, tot, 2, n)));
+      if (classes >= 2) {
+#pragma unroll 1
+        for (uint32_t m = 1; m + 1 < (1u << KC); ++m) {
+          uint32_t v[KC];
+#pragma unroll
+          for (int cc = 0; cc < KC; ++cc) v[cc] = (m >> cc) & 1u ? L[cc] : a[cc];
+          lb = fmin(lb, xat(v));
+        }
+      }
       lb = fmin(lb, xe[e]);
-      a0 = L0;
-      a1 = L1;
+#pragma unroll
+      for (int cc = 0; cc < KC; ++cc) a[cc] = L[cc];
     }
     // start point of this lane's first bucket = end point of the previous lane's last one
     double xs0 = __shfl_up_sync(0xffffffffu, xe[kPBE - 1], 1);
-    if (lane == 0) xs0 = x_at<2>(xl, 0u, 0u, tot, 2, n);
+    if (lane == 0) {
+      uint32_t z[KC];
+#pragma unroll
+      for (int cc = 0; cc < KC; ++cc) z[cc] = 0;
+      xs0 = xat(z);
+    }
     lb = fmin(lb, xs0);
     lb = warp_min_f64(fmin(lb, xp));
     xbest = fmin(xbest, xp);
@@ -1054,17 +1080,24 @@ cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* li
 cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_list, uint32_t R,
                                const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
                                const float* G, const double* xl, float* rowlb,
-                               unsigned long long* xstar, int buckets, cudaStream_t st) {
+                               unsigned long long* xstar, int buckets, int k, cudaStream_t st) {
   if (n_list == 0) return cudaSuccess;
+  if (k < 2 || k > 4) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(xstar, 0x7f, sizeof(unsigned long long) * n_list, st);  // ~ +huge
   if (e != cudaSuccess) return e;
   const uint64_t warps = uint64_t(n_list) * ((R + 7) / 8);
-  if (buckets == 32)
-    dev::k_exact_prune<32><<<unsigned((warps + 3) / 4), 128, 0, st>>>(nodes, list, n_list, R, row_ptr,
-                                                                      lab, gbase, G, xl, rowlb, xstar);
-  else
-    dev::k_exact_prune<64><<<unsigned((warps + 3) / 4), 128, 0, st>>>(nodes, list, n_list, R, row_ptr,
-                                                                      lab, gbase, G, xl, rowlb, xstar);
+  const unsigned grid = unsigned((warps + 3) / 4);
+  if (k == 2) {
+    if (buckets == 32)
+      dev::k_exact_prune<32, 2><<<grid, 128, 0, st>>>(nodes, list, n_list, R, row_ptr, lab, gbase, G, xl, rowlb, xstar, k);
+    else
+      dev::k_exact_prune<64, 2><<<grid, 128, 0, st>>>(nodes, list, n_list, R, row_ptr, lab, gbase, G, xl, rowlb, xstar, k);
+  } else {  // 3 or 4 classes
+    if (buckets == 32)
+      dev::k_exact_prune<32, 4><<<grid, 128, 0, st>>>(nodes, list, n_list, R, row_ptr, lab, gbase, G, xl, rowlb, xstar, k);
+    else
+      dev::k_exact_prune<64, 4><<<grid, 128, 0, st>>>(nodes, list, n_list, R, row_ptr, lab, gbase, G, xl, rowlb, xstar, k);
+  }
   return cudaGetLastError();
 }
 

@@ -73,7 +73,7 @@ cudaError_t launch_exact_bucket(int bucket, const NodeIn* nodes, const uint32_t*
 cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_list, uint32_t R,
                                const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
                                const float* G, const double* xl, float* rowlb,
-                               unsigned long long* xstar, int buckets, cudaStream_t st);
+                               unsigned long long* xstar, int buckets, int k, cudaStream_t st);
 
 // exact_big.cu — exact splits of nodes above kExactSmemMax (device-wide segmented sort)
 cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const uint32_t* h_list,
