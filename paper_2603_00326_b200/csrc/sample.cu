@@ -26,7 +26,7 @@ namespace dev {
 __global__ void __launch_bounds__(128) k_sample_projection(
     const NodeIn* __restrict__ nodes, int n_nodes, uint32_t d, uint32_t R, int zpad,
     uint32_t* __restrict__ terms, uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ pos_after,
-    uint32_t* __restrict__ gkeys) {
+    uint32_t* __restrict__ gkeys, uint32_t* __restrict__ gaux) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -78,7 +78,46 @@ __global__ void __launch_bounds__(128) k_sample_projection(
   if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
   bool dup = false;
   for (int i = lane + 1; i < int(z); i += 32) dup |= keys[i] == keys[i - 1];
-  if (__any_sync(0xffffffffu, dup)) {
+  if (__any_sync(0xffffffffu, dup) && gaux) {
+    // Exact Floyd resolution (random.hpp:36-44) without the serial scan: draw i collides when its
+    // value appeared at an earlier index (C1, from the smallest index per sorted value), or when
+    // it equals J0 + j for an earlier colliding draw j (Floyd inserts J0 + j instead); the flags
+    // are a monotone fixpoint. The set is then {t_i : no collision} u {J0 + i : collision}.
+    const uint32_t J0 = uint32_t(cells - z);
+    uint32_t* minidx = gaux + size_t(node) * 2 * zpad;
+    uint32_t* flag = minidx + zpad;
+    auto lower = [&](uint32_t t) {
+      uint32_t lo = 0, hi = z;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (keys[mid] < t) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    for (uint32_t i = lane; i < z; i += 32) minidx[i] = 0xffffffffu;
+    __syncwarp();
+    for (uint32_t i = lane; i < z; i += 32) atomicMin(minidx + lower(draws[i]), i);
+    __syncwarp();
+    for (uint32_t i = lane; i < z; i += 32) flag[i] = minidx[lower(draws[i])] != i ? 1u : 0u;
+    __syncwarp();
+    for (;;) {
+      bool ch = false;
+      for (uint32_t i = lane; i < z; i += 32) {
+        if (flag[i]) continue;
+        const uint32_t t = draws[i];
+        if (t >= J0 && t - J0 < i && flag[t - J0]) {
+          flag[i] = 1u;
+          ch = true;
+        }
+      }
+      __syncwarp();
+      if (!__any_sync(0xffffffffu, ch)) break;
+    }
+    for (int i = lane; i < zpad; i += 32)
+      keys[i] = i < int(z) ? (flag[i] ? J0 + uint32_t(i) : draws[i]) : 0xffffffffu;
+    __syncwarp();
+    if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
+  } else if (__any_sync(0xffffffffu, dup)) {
     // Exact Floyd resolution in draw order (random.hpp:36-44): a collision inserts j instead.
     for (uint32_t i = 0; i < z; ++i) {
       const uint32_t t = draws[i];
@@ -384,9 +423,28 @@ cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t 
     }
     gkeys = static_cast<uint32_t*>(g_scratch);
   }
+  // collision resolution scratch for large matrices (the serial draw-order scan is O(z^2))
+  static thread_local void* g_aux = nullptr;
+  static thread_local size_t g_aux_cap = 0;
+  uint32_t* gaux = nullptr;
+  if (zpad >= 1024) {
+    const size_t bytes = size_t(n_nodes) * 2 * size_t(zpad) * 4;
+    if (bytes > g_aux_cap) {
+      if (g_aux) {
+        cudaDeviceSynchronize();
+        cudaFree(g_aux);
+      }
+      g_aux = nullptr;
+      g_aux_cap = 0;
+      cudaError_t e = cudaMalloc(&g_aux, bytes + bytes / 4);
+      if (e != cudaSuccess) return e;
+      g_aux_cap = bytes + bytes / 4;
+    }
+    gaux = static_cast<uint32_t*>(g_aux);
+  }
   const int grid = (n_nodes + warps - 1) / warps;
   dev::k_sample_projection<<<grid, warps * 32, smem, st>>>(nodes, n_nodes, d, R, zpad, terms,
-                                                           row_ptr, pos_after, gkeys);
+                                                           row_ptr, pos_after, gkeys, gaux);
   return cudaGetLastError();
 }
 

@@ -356,3 +356,12 @@ def test_pinned_upload_in_flight(gpu_ctx, oracle):
             assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(H.copy(), y, 2, oc)) == []
     finally:
         L.sofg_host_free(ptr)
+
+
+def test_dense_projection_collision_resolution(gpu_ctx, oracle):
+    """Matrices with thousands of cells (z ~ 10K of 49K cells): Floyd collisions are the rule, and
+    are resolved by the parallel fixpoint (smallest index per sorted value, then the J0 + j chain)."""
+    X, y = oracle.generate_trunk(2500, 1024, 17)
+    gpu_ctx.upload(X, y, 2)
+    gc, oc = _cfg(n_trees=2, mode="dynamic", breakeven=300, seed=9, cell_density=0.2)
+    assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, 2, oc)) == []
