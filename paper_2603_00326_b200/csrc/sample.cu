@@ -113,10 +113,56 @@ __global__ void __launch_bounds__(128) k_sample_projection(
       __syncwarp();
       if (!__any_sync(0xffffffffu, ch)) break;
     }
-    for (int i = lane; i < zpad; i += 32)
-      keys[i] = i < int(z) ? (flag[i] ? J0 + uint32_t(i) : draws[i]) : 0xffffffffu;
+    // The set is distinct(all t) u {J0 + i : collision} (every drawn value ends up in the set),
+    // both sides already sorted: merge them instead of sorting again.
+    uint32_t* uq = minidx;  // distinct sorted draw values (minidx is no longer needed)
+    uint32_t u = 0;
+    for (uint32_t b = 0; b < z; b += 32) {
+      const uint32_t p = b + uint32_t(lane);
+      const bool keep = p < z && (p == 0 || keys[p] != keys[p - 1]);
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) uq[u + __popc(m & ((1u << lane) - 1u))] = keys[p];
+      u += __popc(m);
+    }
     __syncwarp();
-    if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
+    auto in_uq = [&](uint32_t v) {  // binary search in uq[0..u)
+      uint32_t lo = 0, hi = u;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (uq[mid] < v) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    // replacement values J0 + i (increasing in i) not already drawn, compacted in place into
+    // draws[] (entries are only read at indices >= the write index)
+    uint32_t c = 0;
+    for (uint32_t b = 0; b < z; b += 32) {
+      const uint32_t i = b + uint32_t(lane);
+      bool add = false;
+      uint32_t v = 0;
+      if (i < z && flag[i]) {
+        v = J0 + i;
+        const uint32_t at = in_uq(v);
+        add = !(at < u && uq[at] == v);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, add);
+      __syncwarp();
+      if (add) draws[c + __popc(m & ((1u << lane) - 1u))] = v;
+      c += __popc(m);
+      __syncwarp();
+    }
+    // merge: final rank = own index + number of smaller elements of the other list
+    for (uint32_t p = lane; p < u; p += 32) {
+      const uint32_t v = uq[p];
+      uint32_t lo = 0, hi = c;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (draws[mid] < v) lo = mid + 1; else hi = mid;
+      }
+      keys[p + lo] = v;
+    }
+    for (uint32_t q = lane; q < c; q += 32) keys[q + in_uq(draws[q])] = draws[q];
+    __syncwarp();
   } else if (__any_sync(0xffffffffu, dup)) {
     // Exact Floyd resolution in draw order (random.hpp:36-44): a collision inserts j instead.
     for (uint32_t i = 0; i < z; ++i) {
