@@ -73,9 +73,62 @@ __global__ void __launch_bounds__(128) k_sample_projection(
   __syncwarp();
 
   // Set = {t_q} unless some t collides (prob ~ z^2 / 2 cells); sort and test neighbours.
-  for (int i = lane; i < zpad; i += 32) keys[i] = i < int(z) ? draws[i] : 0xffffffffu;
-  __syncwarp();
-  if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
+  if (gaux) {
+    // large matrices: warp LSD radix sort (8-bit digits over the bits of cells - 1), stable
+    // scatter by in-order 32-key chunks; ping-pong through the node's scratch
+    uint32_t* tmp = gaux + size_t(node) * 2 * zpad;  // [zpad]
+    uint32_t* cnt = tmp + zpad;                       // [256] digit offsets
+    int bits = 0;
+    while (bits < 32 && ((cells - 1) >> bits) != 0) bits += 8;
+    const uint32_t* src = draws;
+    uint32_t* dst = (bits / 8) % 2 ? keys : tmp;  // the last pass lands in keys
+    if (bits == 0) dst = keys;
+    for (int sh = 0; sh < bits; sh += 8) {
+      for (int b = lane; b < 256; b += 32) cnt[b] = 0;
+      __syncwarp();
+      for (uint32_t i = lane; i < z; i += 32) atomicAdd(cnt + ((src[i] >> sh) & 255u), 1u);
+      __syncwarp();
+      {  // exclusive scan of the 256 counts (8 per lane)
+        uint32_t c8[8], loc = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          c8[e] = cnt[lane * 8 + e];
+          loc += c8[e];
+        }
+        uint32_t tot;
+        uint32_t run = warp_excl_scan_u32(loc, lane, &tot);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          cnt[lane * 8 + e] = run;
+          run += c8[e];
+        }
+      }
+      __syncwarp();
+      for (uint32_t b = 0; b < z; b += 32) {
+        const uint32_t i = b + uint32_t(lane);
+        const uint32_t key = i < z ? src[i] : 0u;
+        const uint32_t dg = i < z ? ((key >> sh) & 255u) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        const uint32_t base = dg < 256u ? cnt[dg] : 0u;
+        if (i < z) dst[base + rank] = key;
+        __syncwarp();
+        if (dg < 256u && rank == 0) cnt[dg] = base + __popc(peers);
+        __syncwarp();
+      }
+      src = dst;
+      dst = dst == keys ? tmp : keys;
+    }
+    if (bits == 0)
+      for (uint32_t i = lane; i < z; i += 32) keys[i] = draws[i];
+    for (int i = int(z) + lane; i < zpad; i += 32) keys[i] = 0xffffffffu;
+    __syncwarp();
+  } else {
+    for (int i = lane; i < zpad; i += 32) keys[i] = i < int(z) ? draws[i] : 0xffffffffu;
+    __syncwarp();
+    if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
+  }
   bool dup = false;
   for (int i = lane + 1; i < int(z); i += 32) dup |= keys[i] == keys[i - 1];
   if (__any_sync(0xffffffffu, dup) && gaux) {
