@@ -128,7 +128,7 @@ def measured_peak():
 
 def committed_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the committed ncu launch list of this bench command
-    (profiles/r*_launches_bench_summary.json, written by scratch/launch_summary.py)."""
+    (profiles/r*_launches_bench_summary.json, written by tools/launch_summary.py)."""
     import glob
 
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_launches_bench_summary.json")))
