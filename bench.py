@@ -198,6 +198,48 @@ def cpu_reference_sample(X, y, n_trees, args, threads, predict_rows=None):
     return forest, timing["train_s"], orc.kind, pred
 
 
+def cpu_reference_trees(X, y, ids, n_trees_cfg, args, threads):
+    """Reference learner (oracle/_ref) on this host: trees `ids` of the bench forest, each through
+    the reference's train_tree on its derived stream (tree t: derive_seed(seed, t + 1); bootstrap
+    derive_seed(ts, 0), root derive_seed(ts, 1), forest.hpp:153-154,305 — exactly the per-tree work
+    train_forest's workers do, forest.hpp:302-306), on `threads` concurrent host threads. Timed:
+    the trees only (the dataset conversion is outside)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib
+
+    orc = oracle_lib.get("reference") if oracle_lib.have_reference() else oracle_lib.get("port")
+    k = int(getattr(args, "classes", 2))
+    n = X.shape[1]
+    ds = orc.dataset(X, y, k)
+    cfg = oracle_lib.make_config(n_trees=n_trees_cfg, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
+                                 n_workers=1, cell_density=float(getattr(args, "density", 0.0)))
+
+    def one(t):
+        ts = orc.derive_seed(args.seed, t + 1)
+        boot = orc.bootstrap(n, 0.632, orc.derive_seed(ts, 0))
+        return orc.train_tree_ds(ds, boot, cfg, orc.derive_seed(ts, 1))
+
+    try:
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max(1, min(threads, len(ids)))) as ex:
+            trees = list(ex.map(one, ids))
+        dt = time.perf_counter() - t0
+    finally:
+        orc.dataset_free(ds)
+    return trees, dt, orc.kind
+
+
+def physical_cores():
+    try:
+        import psutil
+
+        return psutil.cpu_count(logical=False)
+    except Exception:
+        return None
+
+
 def host_trunk(n, d, seed=1):
     """Trunk-model table on the host for the reference arm (multi-threaded numpy)."""
     from concurrent.futures import ThreadPoolExecutor
@@ -236,7 +278,7 @@ def run_reference(args, rank, world):
                                    + (" (BASELINE config 3)" if (args.n, args.d) == (1_000_000, 4096) else ""),
                        "n_samples": args.n, "n_features": args.d, "trees_per_step": n_trees,
                        "breakeven": args.breakeven, "mode": args.mode, "seed": args.seed},
-            "cpu_baseline": {"value": v, "unit": "trees/s", "cores": threads, "kind": kind,
+            "cpu_baseline": {"value": v, "unit": "trees/s", "cores": threads, "physical_cores": physical_cores(), "kind": kind,
                              "sample": f"{n_trees} full trees of the {args.n} x {args.d} forest on {threads} threads "
                                        f"per step; {steps} step(s), no warm-up (each step ~{times[0]:.0f} s)"},
             "e2e": {"value": v, "unit": "trees/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -296,11 +338,8 @@ def main():
         return float(t.item())
 
     # ---- warm-up ---------------------------------------------------------------------------------
-    first = None
     for s in range(args.warmup):
-        f = ctx.train_forest(cfg_for(s))
-        if s == 0:
-            first = f
+        ctx.train_forest(cfg_for(s))
     # ---- timed region (no per-kernel events, no accounting kernels) ---------------------------
     ctx.set_stats(0)
     ctx.reset_stats()
@@ -316,6 +355,8 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
+    last = f  # the last timed step's forest: trees last_begin .. last_begin + T - 1
+    last_begin = (args.warmup + args.steps - 1) * per_step + rank * T
     ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms)
     gpu_launches = int(ctx.stats()["kernel_launches"])
@@ -325,13 +366,11 @@ def main():
     #      on one stream (so a kernel's event time is its own), and sector accounting ---------------
     roofline = None
     if not args.no_profile:
-        os.environ["SOFG_GROUPS"] = "1"
         ctx.set_stats(2)
         ctx.reset_stats()
         ctx.train_forest(cfg_for(args.warmup + args.steps + args.e2e_steps))
         st = ctx.stats()
         ctx.set_stats(0)
-        os.environ.pop("SOFG_GROUPS", None)
         roofline = roofline_block(st, args)
 
     # ---- end to end through the C ABI with host buffers ---------------------------------------
@@ -380,22 +419,27 @@ def main():
         hctx.download(Xt, yt)
         hctx.close()
         rows = np.ascontiguousarray(Xt.T)
-        forest, dt, kind, cpu_lab = cpu_reference_sample(Xh, yh, n_cpu, args, threads, predict_rows=rows)
+        ids = list(range(last_begin, last_begin + n_cpu))
+        trees, dt, kind = cpu_reference_trees(Xh, yh, ids, total_trees, args, threads)
         import oracle_lib
 
-        ff = oracle_lib.FlatForest(first.tree_off, first.left, first.right, first.pred, first.thr, first.term_off,
-                                   first.feat, first.weight)
-        same = sum(ff.tree_equal(forest, t) for t in range(n_cpu))
-        e = int(first.tree_off[n_cpu])
-        q = int(first.term_off[e])
-        head = type(first)(first.tree_off[:n_cpu + 1].copy(), first.left[:e], first.right[:e], first.pred[:e],
-                           first.thr[:e], first.term_off[:e + 1].copy(), first.feat[:q], first.weight[:q],
-                           first.breakeven, first.class_count, first.n_features)
+        ff = oracle_lib.FlatForest(last.tree_off, last.left, last.right, last.pred, last.thr, last.term_off,
+                                   last.feat, last.weight)
+        same = sum(ff.tree_equal(tr, t, 0) for t, tr in enumerate(trees))
+        cpu_forest = oracle_lib.FlatForest.concat(trees)
+        orc = oracle_lib.get("reference") if oracle_lib.have_reference() else oracle_lib.get("port")
+        cpu_lab, _ = orc.predict_flat(cpu_forest, rows, args.d, args.classes)
+        hf = ff.head(n_cpu)
+        head = type(last)(hf.tree_off, hf.left, hf.right, hf.pred, hf.thr, hf.term_off, hf.feat, hf.weight,
+                          last.breakeven, last.class_count, last.n_features)
         gpu_lab_head, _ = ctx.predict(head, rows)
-        gpu_lab_all, _ = ctx.predict(first, rows)
-        cpu = {"value": n_cpu / dt, "unit": "trees/s", "cores": threads, "kind": kind,
-               "sample": f"trees 0..{n_cpu - 1} of the bench forest (full {args.n} x {args.d} trees, "
-                         f"{threads} threads), {dt:.1f} s", "bitexact_trees": f"{same}/{n_cpu}",
+        gpu_lab_all, _ = ctx.predict(last, rows)
+        cpu = {"value": n_cpu / dt, "unit": "trees/s", "cores": threads, "physical_cores": physical_cores(),
+               "kind": kind,
+               "sample": f"trees {ids[0]}..{ids[-1]} of the forest (the first {n_cpu} trees of the LAST TIMED step; "
+                         f"full {args.n} x {args.d} trees, each the reference's train_tree on its derived stream = "
+                         f"train_forest's per-tree work, forest.hpp:302-306), {n_cpu} concurrent threads, {dt:.1f} s",
+               "bitexact_trees": f"{same}/{n_cpu}",
                "holdout": {"rows": int(args.holdout), "data": "trunk model (device generator), seed 2",
                            f"cpu_accuracy_{n_cpu}_trees": round(float((cpu_lab == yt).mean()), 5),
                            f"gpu_accuracy_{n_cpu}_trees": round(float((gpu_lab_head == yt).mean()), 5),

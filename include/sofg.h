@@ -162,6 +162,8 @@ typedef struct sofg_stats {
      algorithmic bytes (table rows streamed + projected rows written + term lists read) */
   uint64_t sweep_waves, gather_waves;
   double sweep_alg_bytes;
+  /* sweep kernel variant of the widest sweep wave: CTA threads and term-entry bytes (2 or 4) */
+  uint32_t sweep_cta_threads, sweep_entry_bytes;
 } sofg_stats;
 /* enable: 1 = CUDA-event timing per phase (+ sector accounting when 2); 0 = off */
 int sofg_set_stats(sofg_ctx* ctx, int enable);

@@ -103,12 +103,24 @@ int orc_guard(F&& f) {
     std::memcpy(weight, f->weight.data(), f->weight.size() * 4);                               \
   }                                                                                            \
   extern "C" void orc_forest_free(orc_forest* f) { delete f; }                                 \
-  extern "C" int orc_predict(const orc_forest* f, const float* rows, uint64_t n_rows,          \
-                             uint64_t n_features, int32_t* out_label, double* out_votes) {     \
+  extern "C" int orc_forest_import(uint64_t n_trees, uint64_t n_features, int32_t k,            \
+                                   const int64_t* tree_off, const int32_t* left,               \
+                                   const int32_t* right, const int32_t* pred, const float* thr, \
+                                   const int64_t* term_off, const uint32_t* feat,              \
+                                   const float* weight, orc_forest** out) {                    \
     return orc_guard([&] {                                                                     \
-      if (n_features != f->n_features) throw std::invalid_argument("feature count mismatch");  \
-      for (uint64_t i = 0; i < n_rows; ++i)                                                    \
-        out_label[i] = f->predict_row(rows + i * n_features,                                   \
-                                      out_votes ? out_votes + i * f->class_count : nullptr);   \
+      auto* f = new orc_forest;                                                                \
+      const uint64_t N = uint64_t(tree_off[n_trees]), Q = uint64_t(term_off[N]);               \
+      f->tree_off.assign(tree_off, tree_off + n_trees + 1);                                    \
+      f->left.assign(left, left + N);                                                          \
+      f->right.assign(right, right + N);                                                       \
+      f->pred.assign(pred, pred + N);                                                          \
+      f->thr.assign(thr, thr + N);                                                             \
+      f->term_off.assign(term_off, term_off + N + 1);                                          \
+      f->feat.assign(feat, feat + Q);                                                          \
+      f->weight.assign(weight, weight + Q);                                                    \
+      f->class_count = k;                                                                      \
+      f->n_features = n_features;                                                              \
+      *out = f;                                                                                \
     });                                                                                        \
   }

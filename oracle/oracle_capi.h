@@ -63,6 +63,9 @@ int orc_train_forest_ds(const orc_dataset* ds, const orc_config* cfg, orc_forest
 int orc_train_tree(const float* X, const int32_t* labels, uint64_t n_samples, uint64_t n_features,
                    int32_t class_count, const uint32_t* active, uint64_t n_active,
                    const orc_config* cfg, uint64_t seed, uint64_t depth, orc_forest** out);
+/* Same on a dataset handle (no per-call copy of the table). */
+int orc_train_tree_ds(const orc_dataset* ds, const uint32_t* active, uint64_t n_active,
+                      const orc_config* cfg, uint64_t seed, uint64_t depth, orc_forest** out);
 
 uint64_t orc_forest_num_trees(const orc_forest* f);
 uint64_t orc_forest_num_nodes(const orc_forest* f);
@@ -73,6 +76,12 @@ void orc_forest_export(const orc_forest* f, int64_t* tree_off, int32_t* left, in
                        int32_t* pred, float* thr, int64_t* term_off, uint32_t* feat, float* weight);
 void orc_forest_free(orc_forest* f);
 
+/* Flat arrays (the layout orc_forest_export writes) -> forest handle, e.g. trees assembled from
+ * several orc_train_tree calls, for orc_predict. */
+int orc_forest_import(uint64_t n_trees, uint64_t n_features, int32_t class_count,
+                      const int64_t* tree_off, const int32_t* left, const int32_t* right,
+                      const int32_t* pred, const float* thr, const int64_t* term_off,
+                      const uint32_t* feat, const float* weight, orc_forest** out);
 /* predict (forest.hpp:110-121) for n_rows row-major samples; out_label[n_rows],
  * out_votes[n_rows*class_count] (may be NULL). */
 int orc_predict(const orc_forest* f, const float* rows, uint64_t n_rows, uint64_t n_features,

@@ -9,6 +9,15 @@ using namespace port;
 
 ORC_COMMON_EXPORTS
 
+extern "C" int orc_predict(const orc_forest* f, const float* rows, uint64_t n_rows, uint64_t n_features,
+                           int32_t* out_label, double* out_votes) {
+  return orc_guard([&] {
+    if (n_features != f->n_features) throw std::invalid_argument("feature count mismatch");
+    for (uint64_t i = 0; i < n_rows; ++i)
+      out_label[i] = f->predict_row(rows + i * n_features, out_votes ? out_votes + i * f->class_count : nullptr);
+  });
+}
+
 static Config to_cfg(const orc_config* c) {
   Config k;
   k.n_trees = c->n_trees;
@@ -88,6 +97,11 @@ extern "C" int orc_train_tree(const float* X, const int32_t* y, uint64_t n, uint
     f->add_tree(t);
     *out = f;
   });
+}
+
+extern "C" int orc_train_tree_ds(const orc_dataset* ds, const uint32_t* active, uint64_t n_active,
+                                 const orc_config* c, uint64_t seed, uint64_t depth, orc_forest** out) {
+  return orc_train_tree(ds->D.X, ds->D.y, ds->D.n, ds->D.d, ds->D.k, active, n_active, c, seed, depth, out);
 }
 
 extern "C" uint64_t orc_split_mix64(uint64_t x) { return split_mix64(x); }

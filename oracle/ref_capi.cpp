@@ -10,6 +10,7 @@
 #include <soforest/soforest.hpp>
 
 #include <cstring>
+#include <thread>
 #include <optional>
 
 #include "forest_flat.hpp"
@@ -17,6 +18,36 @@
 using namespace soforest;
 
 ORC_COMMON_EXPORTS
+
+// predict through the reference's own soforest::predict (forest.hpp:110-121) on a Forest rebuilt
+// from the flat arrays; rows in parallel.
+extern "C" int orc_predict(const orc_forest* f, const float* rows, uint64_t n_rows, uint64_t n_features,
+                           int32_t* out_label, double* out_votes) {
+  return orc_guard([&] {
+    Forest forest;
+    forest.n_features = std::uint32_t(f->n_features);
+    forest.class_count = f->class_count;
+    const uint64_t T = f->tree_off.size() - 1;
+    forest.trees.resize(T);
+    for (uint64_t t = 0; t < T; ++t)
+      for (int64_t q = f->tree_off[t]; q < f->tree_off[t + 1]; ++q) {
+        TreeNode<float> nd;
+        nd.left = f->left[q];
+        nd.right = f->right[q];
+        nd.predicted_class = f->pred[q];
+        nd.threshold = f->thr[q];
+        for (int64_t u = f->term_off[q]; u < f->term_off[q + 1]; ++u)
+          nd.projection.push_back({f->feat[u], f->weight[u]});
+        forest.trees[t].nodes.push_back(std::move(nd));
+      }
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    parallel_for(n_rows, hw, [&](std::size_t i, std::size_t) {
+      const Prediction p = soforest::predict(forest, std::span<const float>(rows + i * n_features, n_features));
+      out_label[i] = p.label;
+      if (out_votes) std::memcpy(out_votes + i * f->class_count, p.votes.data(), 8 * f->class_count);
+    });
+  });
+}
 
 namespace {
 
@@ -210,26 +241,33 @@ static void train_forest_impl(const ColumnarDataset& data, const orc_config* c, 
   }
 }
 
+static void train_tree_impl(const ColumnarDataset& data, const uint32_t* active, uint64_t n_active,
+                            const orc_config* c, uint64_t seed, uint64_t depth, orc_forest** out) {
+  SampleIndexSet s;
+  s.indices.assign(active, active + n_active);
+  auto* f = new orc_forest;
+  f->class_count = data.class_count();
+  f->n_features = data.n_features();
+  if (!custom_projection(c)) {
+    f->add_tree(train_tree(data, s, to_cfg(c), seed, depth));  // forest.hpp:250
+  } else {
+    const TrainConfig cfg = to_cfg(c);
+    f->add_tree(grow_custom(data, cfg, projection_for(c, data.n_features()),
+                            cfg.breakeven ? *cfg.breakeven : kFallbackBreakeven,
+                            std::move(s.indices), seed, std::uint32_t(depth)));
+  }
+  *out = f;
+}
+
 extern "C" int orc_train_tree(const float* X, const int32_t* y, uint64_t n, uint64_t d, int32_t k,
                               const uint32_t* active, uint64_t n_active, const orc_config* c,
                               uint64_t seed, uint64_t depth, orc_forest** out) {
-  return orc_guard([&] {
-    const ColumnarDataset data = make_data(X, y, n, d, k);
-    SampleIndexSet s;
-    s.indices.assign(active, active + n_active);
-    auto* f = new orc_forest;
-    f->class_count = k;
-    f->n_features = d;
-    if (!custom_projection(c)) {
-      f->add_tree(train_tree(data, s, to_cfg(c), seed, depth));  // forest.hpp:250
-    } else {
-      const TrainConfig cfg = to_cfg(c);
-      f->add_tree(grow_custom(data, cfg, projection_for(c, d),
-                              cfg.breakeven ? *cfg.breakeven : kFallbackBreakeven,
-                              std::move(s.indices), seed, std::uint32_t(depth)));
-    }
-    *out = f;
-  });
+  return orc_guard([&] { train_tree_impl(make_data(X, y, n, d, k), active, n_active, c, seed, depth, out); });
+}
+
+extern "C" int orc_train_tree_ds(const orc_dataset* ds, const uint32_t* active, uint64_t n_active,
+                                 const orc_config* c, uint64_t seed, uint64_t depth, orc_forest** out) {
+  return orc_guard([&] { train_tree_impl(ds->data, active, n_active, c, seed, depth, out); });
 }
 
 extern "C" uint64_t orc_split_mix64(uint64_t x) { return split_mix64(x); }

@@ -55,7 +55,8 @@ class _Stats(C.Structure):
                [(n, C.c_double) for n in ("hist_strict_bytes", "exact_strict_bytes", "hist_sector_bytes",
                                           "exact_sector_bytes", "ms_host_roots", "ms_host_prep", "ms_host_submit",
                                           "ms_host_spec", "ms_host_wait", "ms_host_post", "ms_host_final")] + \
-               [(n, C.c_uint64) for n in ("sweep_waves", "gather_waves")] + [("sweep_alg_bytes", C.c_double)]
+               [(n, C.c_uint64) for n in ("sweep_waves", "gather_waves")] + [("sweep_alg_bytes", C.c_double)] + \
+               [("sweep_cta_threads", C.c_uint32), ("sweep_entry_bytes", C.c_uint32)]
 
 
 _MODES = {"exact": 0, "histogram": 1, "dynamic": 2}

@@ -21,10 +21,6 @@ struct sofg_ctx {
   int pool_threads = 0;
   sofg::HostTimes times;
   int stats_mode = 0;
-  // second tree group in flight on the same GPU (own stream and host thread, shared table and
-  // pool): while one group prepares a level on the host, the other group's kernels run.
-  std::unique_ptr<sofg::WaveRunner> eng2;
-  sofg::HostTimes times2;
 };
 
 struct sofg_forest {
@@ -81,27 +77,21 @@ sofg::ThreadPool& pool_for(sofg_ctx* c, uint64_t n_workers) {
   return *c->pool;
 }
 
-sofg::WaveRunner& runner2(sofg_ctx* c) {
-  if (!c->eng2) {
-    // same stream as the first group: the groups' waves alternate on the GPU (no concurrent
-    // kernels), while each group's host phase overlaps the other group's wave
-    c->eng2.reset(new sofg::WaveRunner(c->eng->device(), c->eng->shared_data(), c->eng->stream()));
-    c->eng2->collect_stats = c->eng->collect_stats;
-    c->eng2->sector_accounting = c->eng->sector_accounting;
-  }
-  return *c->eng2;
-}
-
-void append_forest(sofg::FlatForest& dst, const sofg::FlatForest& src) {
-  const int64_t nb = int64_t(dst.left.size()), qb = int64_t(dst.feat.size());
-  dst.left.insert(dst.left.end(), src.left.begin(), src.left.end());
-  dst.right.insert(dst.right.end(), src.right.begin(), src.right.end());
-  dst.pred.insert(dst.pred.end(), src.pred.begin(), src.pred.end());
-  dst.thr.insert(dst.thr.end(), src.thr.begin(), src.thr.end());
-  dst.feat.insert(dst.feat.end(), src.feat.begin(), src.feat.end());
-  dst.weight.insert(dst.weight.end(), src.weight.begin(), src.weight.end());
-  for (size_t i = 1; i < src.tree_off.size(); ++i) dst.tree_off.push_back(src.tree_off[i] + nb);
-  for (size_t i = 1; i < src.term_off.size(); ++i) dst.term_off.push_back(src.term_off[i] + qb);
+// xlogx tables (split.hpp:55-62) indexed by node size: entries 0..m. A node's size is at most its
+// active set's length, which may exceed n_samples when an explicit active set repeats indices
+// (train_tree / find_node_split), so the tables grow to the largest set seen.
+void ensure_xlogx(sofg::DeviceData& D, uint64_t m, cudaStream_t st) {
+  if (D.xl_n >= m && D.xl.p) return;
+  const std::vector<double> xl = sofg::host::xlogx_table(m);
+  std::vector<float> xlf(xl.begin(), xl.end());
+  cuda_check(cudaStreamSynchronize(st), "sync tables");  // queued waves may read the old tables
+  D.xl.exact(m + 1);
+  D.xlf.exact(m + 1);
+  cuda_check(cudaMemcpyAsync(D.xl.p, xl.data(), 8 * (m + 1), cudaMemcpyHostToDevice, st), "H2D xlogx");
+  cuda_check(cudaMemcpyAsync(D.xlf.p, xlf.data(), 4 * (m + 1), cudaMemcpyHostToDevice, st),
+             "H2D xlogx f32");
+  cuda_check(cudaStreamSynchronize(st), "sync tables");  // the host vectors die here
+  D.xl_n = m;
 }
 
 // Dataset staging into HBM: ld = n rounded up to 32 samples (128 B column alignment).
@@ -148,17 +138,7 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   D.lab.exact(n);
   cuda_check(cudaMemcpyAsync(D.lab.p, l8, n, cudaMemcpyHostToDevice, st), "H2D labels");
   cuda_check(cudaEventRecord(D.lab_ev, st), "event");
-  if (D.xl_n != n) {  // xlogx tables depend on n only: rebuilt when the sample count changes
-    const std::vector<double> xl = sofg::host::xlogx_table(n);
-    std::vector<float> xlf(xl.begin(), xl.end());
-    D.xl.exact(n + 1);
-    D.xlf.exact(n + 1);
-    cuda_check(cudaMemcpyAsync(D.xl.p, xl.data(), 8 * (n + 1), cudaMemcpyHostToDevice, st), "H2D xlogx");
-    cuda_check(cudaMemcpyAsync(D.xlf.p, xlf.data(), 4 * (n + 1), cudaMemcpyHostToDevice, st),
-               "H2D xlogx f32");
-    cuda_check(cudaStreamSynchronize(st), "sync tables");  // the host vectors die here
-    D.xl_n = n;
-  }
+  ensure_xlogx(D, n, st);
 }
 
 struct PCfg {
@@ -303,6 +283,7 @@ int sofg_generate_trunk(sofg_ctx* c, uint64_t n, uint64_t d, int32_t k, uint64_t
     require_ctx(c);
     if (n < 2) throw std::invalid_argument("n_samples must be at least 2");
     if (d == 0) throw std::invalid_argument("n_features must be positive");
+    if (k < 1 || k > sofg::kMaxClasses) throw std::invalid_argument("class_count out of range");
     std::vector<int32_t> y(n);
     for (uint64_t i = 0; i < n; ++i) y[i] = int32_t(i % uint64_t(k));
     upload(c, n, d, y.data(), k, [&](float* dev, uint64_t ld) {
@@ -360,42 +341,7 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
       });
       c->times.ms_bootstrap +=
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tbs).count();
-      // Two tree groups in flight (SOFG_GROUPS=1 disables): group 2 runs on its own stream and
-      // host threads so each group's host-side level work overlaps the other's kernels.
-      const char* ge = std::getenv("SOFG_GROUPS");
-      const int groups = ge ? std::max(1, std::atoi(ge)) : 1;  // 2 groups measured slower (half-size waves)
-      if (groups >= 2 && B >= 16) {
-        const size_t h = B / 2;
-        std::vector<std::vector<uint32_t>> r1(std::make_move_iterator(roots.begin()),
-                                              std::make_move_iterator(roots.begin() + long(h)));
-        std::vector<std::vector<uint32_t>> r2(std::make_move_iterator(roots.begin() + long(h)),
-                                              std::make_move_iterator(roots.end()));
-        std::vector<uint64_t> s1(seeds.begin(), seeds.begin() + long(h)), s2(seeds.begin() + long(h), seeds.end());
-        sofg::WaveRunner& e2 = runner2(c);
-        sofg::FlatForest f1, f2;
-        std::exception_ptr err2;
-        std::mutex turn;  // host phases alternate between the groups; both use the full pool
-        std::thread th([&] {
-          try {
-            sofg::grow_trees(e2, P, pool, r2, s2, 0, f2, c->times2, &turn);
-          } catch (...) {
-            err2 = std::current_exception();
-          }
-        });
-        try {
-          sofg::grow_trees(*c->eng, P, pool, r1, s1, 0, f1, c->times, &turn);
-        } catch (...) {
-          th.join();
-          throw;
-        }
-        th.join();
-        if (err2) std::rethrow_exception(err2);
-        append_forest(res->f, f1);
-        append_forest(res->f, f2);
-        c->eng->set_pool(&pool);
-      } else {
-        sofg::grow_trees(*c->eng, P, pool, roots, seeds, 0, res->f, c->times);
-      }
+      sofg::grow_trees(*c->eng, P, pool, roots, seeds, 0, res->f, c->times);
     }
     *out = guard_res.release();
   });
@@ -414,6 +360,7 @@ int sofg_train_tree(sofg_ctx* c, const uint32_t* active, uint64_t n_active,
     if (cfg->bin_count > uint64_t(sofg::kMaxBins))
       throw std::invalid_argument("bin_count exceeds the GPU histogram splitter");
     sofg::TrainParams P = params_for(cfg, D, false);
+    ensure_xlogx(c->eng->data(), n_active, c->eng->stream());
     sofg::ThreadPool& pool = pool_for(c, cfg->n_workers);
     auto* res = new sofg_forest;
     std::unique_ptr<sofg_forest> guard_res(res);
@@ -483,10 +430,34 @@ int sofg_forest_import(uint64_t n_trees, uint64_t n_features, int32_t k, const i
                        const float* thr, const int64_t* term_off, const uint32_t* feat,
                        const float* weight, sofg_forest** out) {
   return guard([&] {
+    // Structural checks of the reference loader (model_io.hpp:255-277), plus child ids above the
+    // parent's (every trained tree satisfies it: ids are assigned at split time, depth first), so
+    // a malformed forest cannot send sofg_predict's traversal out of bounds or into a cycle.
+    if (k < 1) throw std::invalid_argument("class_count must be positive");
+    if (!tree_off || tree_off[0] != 0) throw std::invalid_argument("tree_off[0] must be 0");
+    for (uint64_t t = 0; t < n_trees; ++t)
+      if (tree_off[t + 1] <= tree_off[t]) throw std::invalid_argument("empty tree");
+    const uint64_t N = uint64_t(tree_off[n_trees]);
+    if (term_off[0] != 0) throw std::invalid_argument("term_off[0] must be 0");
+    for (uint64_t q = 0; q < N; ++q)
+      if (term_off[q + 1] < term_off[q]) throw std::invalid_argument("term offsets not monotone");
+    const uint64_t Q = uint64_t(term_off[N]);
+    for (uint64_t u = 0; u < Q; ++u)
+      if (feat[u] >= n_features) throw std::invalid_argument("projection feature out of range");
+    for (uint64_t t = 0; t < n_trees; ++t) {
+      const int64_t size = tree_off[t + 1] - tree_off[t];
+      for (int64_t i = 0; i < size; ++i) {
+        const uint64_t q = uint64_t(tree_off[t] + i);
+        if (left[q] < 0) {
+          if (pred[q] < 0 || pred[q] >= k) throw std::invalid_argument("leaf class out of range");
+        } else if (left[q] <= i || right[q] <= i || left[q] >= size || right[q] >= size ||
+                   term_off[q + 1] == term_off[q]) {
+          throw std::invalid_argument("malformed internal node");
+        }
+      }
+    }
     auto* r = new sofg_forest;
     sofg::FlatForest& f = r->f;
-    const uint64_t N = uint64_t(tree_off[n_trees]);
-    const uint64_t Q = uint64_t(term_off[N]);
     f.tree_off.assign(tree_off, tree_off + n_trees + 1);
     f.left.assign(left, left + N);
     f.right.assign(right, right + N);
@@ -632,6 +603,7 @@ int sofg_sample_projection(sofg_ctx* c, uint64_t d, uint64_t R, double density,
       zmax = std::max(zmax, z);
     }
     cudaStream_t st = c->eng->stream();
+    sofg::Scratch scratch;  // freed after the stream synchronization below
     DevBuf<sofg::NodeIn> dn;
     DevBuf<uint32_t> dterms, drp, dpos;
     dn.exact(n_nodes);
@@ -642,7 +614,7 @@ int sofg_sample_projection(sofg_ctx* c, uint64_t d, uint64_t R, double density,
                                cudaMemcpyHostToDevice, st),
                "H2D nodes");
     cuda_check(sofg::launch_sample_projection(dn.p, int(n_nodes), uint32_t(d), uint32_t(R),
-                                              uint32_t(zmax), dterms.p, drp.p, dpos.p, st),
+                                              uint32_t(zmax), dterms.p, drp.p, dpos.p, scratch, st),
                "sample_projection");
     std::vector<uint32_t> ht(off + 1), hrp(n_nodes * (R + 1)), hpos(n_nodes);
     cuda_check(cudaMemcpyAsync(ht.data(), dterms.p, 4 * (off + 1), cudaMemcpyDeviceToHost, st), "D2H");
@@ -673,6 +645,7 @@ int sofg_find_node_split(sofg_ctx* c, const uint32_t* active, uint64_t n, const 
     if (bins > uint64_t(sofg::kMaxBins)) throw std::invalid_argument("bin_count too large");
     for (uint64_t i = 0; i < n; ++i)
       if (active[i] >= D.n) throw std::out_of_range("sample index out of range");
+    ensure_xlogx(c->eng->data(), n, c->eng->stream());
     const uint64_t nnz = row_ptr[R];
     sofg::WaveSpec w;
     w.R = uint32_t(R);
@@ -745,11 +718,8 @@ int sofg_set_stats(sofg_ctx* c, int enable) {
   return guard([&] {
     require_ctx(c);
     c->stats_mode = enable;
-    for (sofg::WaveRunner* e : {c->eng.get(), c->eng2.get()}) {
-      if (!e) continue;
-      e->collect_stats = enable != 0;
-      e->sector_accounting = enable >= 2;
-    }
+    c->eng->collect_stats = enable != 0;
+    c->eng->sector_accounting = enable >= 2;
   });
 }
 
@@ -757,8 +727,7 @@ int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
   return guard([&] {
     require_ctx(c);
     std::memset(o, 0, sizeof(*o));
-    sofg::WaveStats s = c->eng->stats;  // both tree groups (kernel times of concurrent streams add)
-    if (c->eng2) s.merge(c->eng2->stats);
+    const sofg::WaveStats& s = c->eng->stats;
     o->ms_sample = s.ms_sample;
     o->ms_hist_rng = s.ms_hist_rng;
     o->ms_hist_count = s.ms_hist_count;
@@ -790,16 +759,13 @@ int sofg_get_stats(sofg_ctx* c, sofg_stats* o) {
     o->sweep_waves = s.sweep_waves;
     o->gather_waves = s.gather_waves;
     o->sweep_alg_bytes = s.sweep_alg_bytes;
+    o->sweep_cta_threads = s.sweep_cta_threads;
+    o->sweep_entry_bytes = s.sweep_entry_bytes;
   });
 }
 
 namespace {
-thread_local sofg::WaveStats g_merged;
-const sofg::WaveStats& merged_stats(sofg_ctx* c) {
-  g_merged = c->eng->stats;
-  if (c->eng2) g_merged.merge(c->eng2->stats);
-  return g_merged;
-}
+const sofg::WaveStats& merged_stats(sofg_ctx* c) { return c->eng->stats; }
 }  // namespace
 
 int sofg_stats_kernels(sofg_ctx* c) { return c && c->eng ? int(merged_stats(c).per_kernel.size()) : 0; }
@@ -819,9 +785,7 @@ int sofg_reset_stats(sofg_ctx* c) {
   return guard([&] {
     require_ctx(c);
     c->eng->stats = sofg::WaveStats{};
-    if (c->eng2) c->eng2->stats = sofg::WaveStats{};
     c->times = sofg::HostTimes{};
-    c->times2 = sofg::HostTimes{};
   });
 }
 

@@ -50,6 +50,29 @@ WaveRunner::~WaveRunner() {
   if (st_ && own_stream_) cudaStreamDestroy(st_);
 }
 
+Scratch::~Scratch() {
+  for (void* p : p_)
+    if (p) cudaFree(p);
+}
+
+void* Scratch::get(int slot, size_t bytes, cudaStream_t st) {
+  if (bytes <= cap_[slot] && p_[slot]) return p_[slot];
+  if (p_[slot]) {
+    cudaStreamSynchronize(st);  // launches already queued may still read the old block
+    cudaFree(p_[slot]);
+  }
+  p_[slot] = nullptr;
+  cap_[slot] = 0;
+  const size_t want = bytes + bytes / 4 + 256;
+  if (cudaMalloc(&p_[slot], want) != cudaSuccess) {
+    cudaGetLastError();
+    p_[slot] = nullptr;
+    return nullptr;
+  }
+  cap_[slot] = want;
+  return p_[slot];
+}
+
 namespace {
 struct Packer {
   std::vector<size_t> off;
@@ -305,7 +328,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   n_marks_ = 0;
   int launches = 0;
   if (!w.given_csr) {
-    cuda_check(launch_sample_projection(d_nodes, N, w.d, R, zmax, d_terms, d_rp, d_pos_proj, st_),
+    cuda_check(launch_sample_projection(d_nodes, N, w.d, R, zmax, d_terms, d_rp, d_pos_proj, scratch_, st_),
                "sample_projection");
     ++launches;
     mark("sample_projection");
@@ -318,6 +341,10 @@ void WaveRunner::submit(const WaveSpec& w) {
     uint4* d_qoff = qoff_.ensure(size_t(N));
     cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, d_qoff, st_), "aug_build");
     mark("sweep_prep");
+    if (uint64_t(N) > stats.sweep_widest_nodes) {
+      stats.sweep_widest_nodes = uint64_t(N);
+      row_sweep_variant(w.B, w.d, &stats.sweep_cta_threads, &stats.sweep_entry_bytes);
+    }
     cuda_check(launch_row_sweep(D.XR.p, D.ldr, uint32_t(D.n), w.inv, w.B, d_pos_node, d_nodes,
                                 d_gbase, d_aug, d_qoff, R, w.d, d_G, n_sm_, st_),
                "row_sweep");
@@ -407,7 +434,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       if (!(w.nodes[size_t(i)].flags & kNodeHist) && w.nodes[size_t(i)].n > uint32_t(kExactSmemMax))
         big.push_back(uint32_t(i));
     cuda_check(launch_exact_big(d_nodes, w.nodes.data(), big.data(), int(big.size()), R, k, d_rp,
-                                w.lab_in, d_gbase, d_G, D.xl.p, d_res, st_),
+                                w.lab_in, d_gbase, d_G, D.xl.p, d_res, scratch_, st_),
                "exact_big");
     launches += 4;
     mark("exact_big");

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "kernels.hpp"
 
 namespace sofg {
 
@@ -138,6 +139,8 @@ struct WaveStats {
   uint64_t hist_count_launches = 0, exact_launches = 0;
   uint64_t sweep_waves = 0, gather_waves = 0;
   double sweep_alg_bytes = 0;  // table rows streamed + V written + term lists read (sweep waves)
+  uint32_t sweep_cta_threads = 0, sweep_entry_bytes = 0;  // variant of the widest sweep wave
+  uint64_t sweep_widest_nodes = 0;
   std::vector<KernelTime> per_kernel;  // CUDA-event time per launch site (stats mode)
   void merge(const WaveStats& o) {
     ms_sample += o.ms_sample; ms_hist_rng += o.ms_hist_rng; ms_hist_count += o.ms_hist_count;
@@ -148,6 +151,11 @@ struct WaveStats {
     exact_sector_bytes += o.exact_sector_bytes; hist_count_launches += o.hist_count_launches;
     exact_launches += o.exact_launches; sweep_waves += o.sweep_waves; gather_waves += o.gather_waves;
     sweep_alg_bytes += o.sweep_alg_bytes;
+    if (o.sweep_widest_nodes > sweep_widest_nodes) {
+      sweep_widest_nodes = o.sweep_widest_nodes;
+      sweep_cta_threads = o.sweep_cta_threads;
+      sweep_entry_bytes = o.sweep_entry_bytes;
+    }
     for (const auto& k : o.per_kernel) {
       bool found = false;
       for (auto& m : per_kernel)
@@ -254,6 +262,7 @@ class WaveRunner {
   DevBuf<uint32_t> pos_node_;  // level position -> wave node (sweep mode)
   DevBuf<unsigned char> aug_;  // augmented term lists (sweep mode)
   DevBuf<uint4> qoff_;         // per-node sub-list offsets (sweep mode)
+  Scratch scratch_;                    // launch-sized temporaries (dense projections, exact_big)
   DevBuf<float> rowlb_;                // exact branch-and-bound: per (node, row) lower bounds
   DevBuf<unsigned long long> xstar_;   // and per node the best pivot-candidate impurity
   int n_sm_ = 148;

@@ -195,7 +195,7 @@ __global__ void k_big_select(const BigSeg* __restrict__ segs, int n_nodes, uint3
 cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const uint32_t* h_list,
                              int n, uint32_t R, int k, const uint32_t* row_ptr, const uint8_t* lab,
                              const uint64_t* vbase, const float* V, const double* xl, NodeRes* res,
-                             cudaStream_t st) {
+                             Scratch& scratch, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const uint64_t kMaxKeys = 256ull << 20;  // 2 GB of keys (x2 for the sort's double buffer)
   int i0 = 0;
@@ -218,38 +218,21 @@ cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const u
         off += h_nodes[node].n;
       }
     }
-    // scratch kept across calls (grow-only, per calling thread)
-    struct Arena {
-      void* p[7] = {};
-      size_t cap[7] = {};
-      void* get(int i, size_t bytes) {
-        if (bytes > cap[i]) {
-          if (p[i]) {
-            cudaDeviceSynchronize();  // earlier chunks may still read it
-            cudaFree(p[i]);
-          }
-          p[i] = nullptr;
-          cap[i] = 0;
-          if (cudaMalloc(&p[i], bytes + bytes / 4) != cudaSuccess) return nullptr;
-          cap[i] = bytes + bytes / 4;
-        }
-        return p[i];
-      }
-    };
-    static thread_local Arena ar;
-    dev::BigSeg* d_segs = static_cast<dev::BigSeg*>(ar.get(0, sizeof(dev::BigSeg) * nseg));
-    uint64_t* d_k0 = static_cast<uint64_t*>(ar.get(1, 8 * keys));
-    uint64_t* d_k1 = static_cast<uint64_t*>(ar.get(2, 8 * keys));
-    uint64_t* d_b = static_cast<uint64_t*>(ar.get(3, 8 * size_t(nseg)));
-    uint64_t* d_e = static_cast<uint64_t*>(ar.get(4, 8 * size_t(nseg)));
-    RowRes* d_rr = static_cast<RowRes*>(ar.get(5, sizeof(RowRes) * nseg));
+    // scratch kept across calls (grow-only, owned by the caller's WaveRunner)
+    auto ar_get = [&](int i, size_t bytes) { return scratch.get(Scratch::kBigFirst + i, bytes, st); };
+    dev::BigSeg* d_segs = static_cast<dev::BigSeg*>(ar_get(0, sizeof(dev::BigSeg) * nseg));
+    uint64_t* d_k0 = static_cast<uint64_t*>(ar_get(1, 8 * keys));
+    uint64_t* d_k1 = static_cast<uint64_t*>(ar_get(2, 8 * keys));
+    uint64_t* d_b = static_cast<uint64_t*>(ar_get(3, 8 * size_t(nseg)));
+    uint64_t* d_e = static_cast<uint64_t*>(ar_get(4, 8 * size_t(nseg)));
+    RowRes* d_rr = static_cast<RowRes*>(ar_get(5, sizeof(RowRes) * nseg));
     if (!d_segs || !d_k0 || !d_k1 || !d_b || !d_e || !d_rr) return cudaErrorMemoryAllocation;
     cudaError_t e = cudaMemcpyAsync(d_segs, segs.data(), sizeof(dev::BigSeg) * nseg, cudaMemcpyHostToDevice, st);
     if (e) return e;
     dev::k_big_keys<<<nseg, 256, 0, st>>>(nodes, d_segs, R, lab, vbase, V, d_k0, d_b, d_e);
     size_t tb = 0;
     e = cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tb, d_k0, d_k1, int64_t(keys), nseg, d_b, d_e, 0, 64, st);
-    void* d_tmp = e ? nullptr : ar.get(6, tb ? tb : 1);
+    void* d_tmp = e ? nullptr : ar_get(6, tb ? tb : 1);
     if (!e && !d_tmp) e = cudaErrorMemoryAllocation;
     if (!e) e = cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tb, d_k0, d_k1, int64_t(keys), nseg, d_b, d_e, 0, 64, st);
     if (e) return e;

@@ -13,10 +13,28 @@ namespace sofg {
 // process-wide, so per-launch values would race between the host threads of concurrent tree groups.
 constexpr int kSmemOptin = 226 * 1024;  // 227 KB opt-in minus room for static __shared__
 
+// Grow-only device scratch owned by a WaveRunner (so by one device and one stream): launchers whose
+// temporaries are sized at launch time take numbered slots from it. Growing a slot waits for the
+// stream first (an earlier launch may still read the old block).
+class Scratch {
+ public:
+  static constexpr int kSlots = 10;
+  enum : int { kSampleKeys = 0, kSampleAux = 1, kBigFirst = 2 };  // exact_big uses 2..8
+  Scratch() = default;
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch();
+  void* get(int slot, size_t bytes, cudaStream_t st);  // nullptr on allocation failure
+
+ private:
+  void* p_[kSlots] = {};
+  size_t cap_[kSlots] = {};
+};
+
 // sample.cu
 cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t d, uint32_t R,
                                      uint32_t zmax, uint32_t* terms, uint32_t* row_ptr,
-                                     uint32_t* pos_after, cudaStream_t st);
+                                     uint32_t* pos_after, Scratch& scratch, cudaStream_t st);
 cudaError_t launch_hist_draws(const NodeIn* nodes, const uint32_t* hist_nodes, int n_hist,
                               uint32_t R, uint32_t bins, const uint32_t* pos_after_proj,
                               uint32_t* draws, uint32_t* pos_split, cudaStream_t st);
@@ -50,6 +68,7 @@ cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* t
                              const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
                              uint4* qoff, cudaStream_t st);
 size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R);
+void row_sweep_variant(uint32_t B, uint32_t d, uint32_t* cta_threads, uint32_t* entry_bytes);
 cudaError_t launch_row_sweep(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
                              uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
                              const uint64_t* vbase, const void* aug, const uint4* qoff,
@@ -79,7 +98,7 @@ cudaError_t launch_exact_prune(const NodeIn* nodes, const uint32_t* list, int n_
 cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const uint32_t* h_list,
                              int n, uint32_t R, int k, const uint32_t* row_ptr, const uint8_t* lab,
                              const uint64_t* vbase, const float* V, const double* xl, NodeRes* res,
-                             cudaStream_t st);
+                             Scratch& scratch, cudaStream_t st);
 
 // partition.cu
 cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles, int n_tiles,

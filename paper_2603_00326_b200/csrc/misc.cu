@@ -26,8 +26,8 @@ __device__ __forceinline__ double hashed_normal(uint64_t seed, uint64_t i, uint6
 // mu_f = 1/sqrt(f+1), class = i % k — from a counter-based generator so 16 GB fills in ms.
 // s_{c,f} = -1 iff bit (f mod ceil(log2 k)) of c is set; for k = 2 that is the trunk sign.
 __global__ void k_generate_trunk(float* __restrict__ X, uint64_t ld, uint8_t* __restrict__ lab,
-                                 uint64_t n, uint64_t d, int k, int kbits, uint64_t seed) {
-  const uint64_t f = blockIdx.y;
+                                 uint64_t n, uint64_t f0, int k, int kbits, uint64_t seed) {
+  const uint64_t f = f0 + blockIdx.y;
   const double mu = 1.0 / sqrt(double(f + 1));
   const int bit = kbits > 0 ? int(f % uint64_t(kbits)) : 0;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -122,13 +122,14 @@ cudaError_t launch_generate_trunk(float* X, uint64_t ld, uint8_t* labels, uint64
   int kbits = 0;
   while ((1 << kbits) < k) ++kbits;
   const unsigned gx = unsigned(std::min<uint64_t>((n + 255) / 256, 4096));
+  if (k < 1) return cudaErrorInvalidValue;
   for (uint64_t f0 = 0; f0 < d; f0 += 65535) {
     const unsigned gy = unsigned(std::min<uint64_t>(65535, d - f0));
-    dev::k_generate_trunk<<<dim3(gx, gy), 256, 0, st>>>(X + f0 * ld, ld, f0 == 0 ? labels : nullptr,
-                                                         n, gy, k, kbits, seed);
-    if (f0 != 0) return cudaErrorNotSupported;  // d > 65535 not needed
+    dev::k_generate_trunk<<<dim3(gx, gy), 256, 0, st>>>(X, ld, labels, n, f0, k, kbits, seed);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 cudaError_t launch_apply_projection(const float* X, uint64_t ld, const uint32_t* terms, int nt,

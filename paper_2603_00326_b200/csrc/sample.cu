@@ -491,7 +491,7 @@ static int next_pow2(int x) {
 
 cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t d, uint32_t R,
                                      uint32_t zmax, uint32_t* terms, uint32_t* row_ptr,
-                                     uint32_t* pos_after, cudaStream_t st) {
+                                     uint32_t* pos_after, Scratch& scratch, cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
   const int zpad = next_pow2(int(zmax));
   const bool global_sets = size_t(2 * dev::kMtN) * 8 + size_t(2 * zpad) * 4 > 96 * 1024;
@@ -502,44 +502,17 @@ cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t 
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(dev::k_sample_projection, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemOptin);
-  // global scratch for very dense matrices: grow-only, per calling thread (no stream-ordered
-  // pool allocations on the hot path)
-  static thread_local void* g_scratch = nullptr;
-  static thread_local size_t g_cap = 0;
+  // global scratch for very dense matrices (owned by the caller's WaveRunner)
   uint32_t* gkeys = nullptr;
   if (global_sets) {
-    const size_t bytes = size_t(n_nodes) * 2 * size_t(zpad) * 4;
-    if (bytes > g_cap) {
-      if (g_scratch) {
-        cudaDeviceSynchronize();
-        cudaFree(g_scratch);
-      }
-      g_scratch = nullptr;
-      g_cap = 0;
-      cudaError_t e = cudaMalloc(&g_scratch, bytes + bytes / 4);
-      if (e != cudaSuccess) return e;
-      g_cap = bytes + bytes / 4;
-    }
-    gkeys = static_cast<uint32_t*>(g_scratch);
+    gkeys = static_cast<uint32_t*>(scratch.get(Scratch::kSampleKeys, size_t(n_nodes) * 2 * size_t(zpad) * 4, st));
+    if (!gkeys) return cudaErrorMemoryAllocation;
   }
   // collision resolution scratch for large matrices (the serial draw-order scan is O(z^2))
-  static thread_local void* g_aux = nullptr;
-  static thread_local size_t g_aux_cap = 0;
   uint32_t* gaux = nullptr;
   if (zpad >= 1024) {
-    const size_t bytes = size_t(n_nodes) * 2 * size_t(zpad) * 4;
-    if (bytes > g_aux_cap) {
-      if (g_aux) {
-        cudaDeviceSynchronize();
-        cudaFree(g_aux);
-      }
-      g_aux = nullptr;
-      g_aux_cap = 0;
-      cudaError_t e = cudaMalloc(&g_aux, bytes + bytes / 4);
-      if (e != cudaSuccess) return e;
-      g_aux_cap = bytes + bytes / 4;
-    }
-    gaux = static_cast<uint32_t*>(g_aux);
+    gaux = static_cast<uint32_t*>(scratch.get(Scratch::kSampleAux, size_t(n_nodes) * 2 * size_t(zpad) * 4, st));
+    if (!gaux) return cudaErrorMemoryAllocation;
   }
   const int grid = (n_nodes + warps - 1) / warps;
   dev::k_sample_projection<<<grid, warps * 32, smem, st>>>(nodes, n_nodes, d, R, zpad, terms,

@@ -513,6 +513,11 @@ static uint32_t sweep_k(uint64_t ldr, uint32_t B, uint32_t R) {
   return K;
 }
 
+void row_sweep_variant(uint32_t B, uint32_t d, uint32_t* cta_threads, uint32_t* entry_bytes) {
+  *cta_threads = uint32_t(sweep_threads(B));
+  *entry_bytes = aug_narrow(d) ? 2u : 4u;
+}
+
 size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R) {
   return sweep_smem_k(ldr, B, R, sweep_k(ldr, B, R));
 }

@@ -168,9 +168,7 @@ int32_t argmax_first(const uint32_t* c, int k) {  // std::max_element: first max
 void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
                 const std::vector<std::vector<uint32_t>>& roots,
                 const std::vector<uint64_t>& root_seeds, uint32_t root_depth, FlatForest& out,
-                HostTimes& times, std::mutex* turn) {
-  std::unique_lock<std::mutex> host_turn;
-  if (turn) host_turn = std::unique_lock<std::mutex>(*turn);
+                HostTimes& times) {
   const auto t_start = Clock::now();
   cuda_check(cudaSetDevice(eng.device()), "cudaSetDevice");
   DeviceData& D = eng.data();
@@ -464,11 +462,6 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       const double lv_spec = ms_since(t0);
       times.ms_spec += lv_spec;
       t0 = Clock::now();
-      if (turn) {
-        host_turn.unlock();  // the other groups prepare their waves meanwhile
-        eng.wait_wave();
-        host_turn.lock();
-      }
       double lv_sync = 0.0;
       if (level_log) {
         eng.wait_wave();

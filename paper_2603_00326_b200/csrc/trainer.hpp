@@ -107,12 +107,9 @@ struct HostTimes {
 
 // Grows one tree per root (sorted active set + root seed) at depth offset root_depth and
 // appends them, renumbered in the reference's node order, to `out`.
-// `turn`, when given, is held during every host phase and released only while waiting for the
-// GPU: several tree groups (one thread each, own WaveRunner/stream, shared pool) then take turns on
-// the host, so one group's level preparation overlaps the other groups' kernels.
 void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
                 const std::vector<std::vector<uint32_t>>& roots,
                 const std::vector<uint64_t>& root_seeds, uint32_t root_depth, FlatForest& out,
-                HostTimes& times, std::mutex* turn = nullptr);
+                HostTimes& times);
 
 }  // namespace sofg

@@ -93,6 +93,26 @@ class FlatForest:
     def n_trees(self) -> int:
         return len(self.tree_off) - 1
 
+    def head(self, m: int) -> "FlatForest":
+        """The first m trees."""
+        e = int(self.tree_off[m])
+        q = int(self.term_off[e])
+        return FlatForest(self.tree_off[:m + 1].copy(), self.left[:e], self.right[:e], self.pred[:e], self.thr[:e],
+                          self.term_off[:e + 1].copy(), self.feat[:q], self.weight[:q], self.breakeven)
+
+    @staticmethod
+    def concat(parts: "list[FlatForest]") -> "FlatForest":
+        to, so = [np.zeros(1, np.int64)], [np.zeros(1, np.int64)]
+        nb = qb = 0
+        for p in parts:
+            to.append(p.tree_off[1:] + nb)
+            so.append(p.term_off[1:] + qb)
+            nb += len(p.left)
+            qb += len(p.feat)
+        cat = lambda name: np.concatenate([getattr(p, name) for p in parts])
+        return FlatForest(np.concatenate(to), cat("left"), cat("right"), cat("pred"), cat("thr"), np.concatenate(so),
+                          cat("feat"), cat("weight"), parts[0].breakeven if parts else 0)
+
     def tree(self, t: int) -> "FlatForest":
         a, b = int(self.tree_off[t]), int(self.tree_off[t + 1])
         ta, tb = int(self.term_off[a]), int(self.term_off[b])
@@ -134,6 +154,8 @@ class Oracle:
         L.orc_dataset_free.argtypes = [vp]
         L.orc_train_forest_ds.argtypes = [vp, p(OrcConfig), p(vp)]
         L.orc_train_tree.argtypes = [vp, vp, u64, u64, i32, vp, u64, p(OrcConfig), u64, u64, p(vp)]
+        L.orc_forest_import.argtypes = [u64, u64, i32] + [vp] * 9
+        L.orc_train_tree_ds.argtypes = [vp, vp, u64, p(OrcConfig), u64, u64, p(vp)]
         for fn in ("orc_forest_num_trees", "orc_forest_num_nodes", "orc_forest_num_terms", "orc_forest_breakeven"):
             getattr(L, fn).restype = u64
             getattr(L, fn).argtypes = [vp]
@@ -244,6 +266,29 @@ class Oracle:
                                           C.byref(cfg), seed, depth, C.byref(h)), "train_tree")
         try:
             return self._export(h)
+        finally:
+            self.lib.orc_forest_free(h)
+
+    def train_tree_ds(self, ds, active, cfg, seed, depth=0) -> FlatForest:
+        """train_tree on a dataset handle (dataset()); releases the GIL, so threads run in parallel."""
+        a = np.ascontiguousarray(active, np.uint32)
+        h = C.c_void_p()
+        self._err(self.lib.orc_train_tree_ds(ds, a.ctypes.data, len(a), C.byref(cfg), seed, depth, C.byref(h)),
+                  "train_tree")
+        try:
+            return self._export(h)
+        finally:
+            self.lib.orc_forest_free(h)
+
+    def predict_flat(self, f: FlatForest, rows, d, k):
+        """predict (forest.hpp:110-121) with this oracle on a flat forest (e.g. assembled trees)."""
+        h = C.c_void_p()
+        arrs = [np.ascontiguousarray(a) for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off, f.feat,
+                                                  f.weight)]
+        self._err(self.lib.orc_forest_import(f.n_trees, d, k, *(a.ctypes.data for a in arrs), C.byref(h)),
+                  "forest_import")
+        try:
+            return self._predict(h, rows, d, k)
         finally:
             self.lib.orc_forest_free(h)
 
