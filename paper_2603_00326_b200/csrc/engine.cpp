@@ -338,17 +338,35 @@ void WaveRunner::submit(const WaveSpec& w) {
     const size_t abytes = aug_bytes(total_terms, uint32_t(N), R, w.d);
     void* d_aug = aug_.ensure(abytes);
     pend_sweep_bytes_ = double(D.n) * double(D.ldr) * 4.0 + double(g_total) * 4.0 + double(abytes);
-    uint4* d_qoff = qoff_.ensure(size_t(N));
-    cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, d_qoff, st_), "aug_build");
+    cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, st_), "aug_build");
     mark("sweep_prep");
     if (uint64_t(N) > stats.sweep_widest_nodes) {
       stats.sweep_widest_nodes = uint64_t(N);
       row_sweep_variant(w.B, w.d, &stats.sweep_cta_threads, &stats.sweep_entry_bytes);
     }
-    cuda_check(launch_row_sweep(D.XR.p, D.ldr, uint32_t(D.n), w.inv, w.B, d_pos_node, d_nodes,
-                                d_gbase, d_aug, d_qoff, R, w.d, d_G, n_sm_, st_),
-               "row_sweep");
-    launches += 3;
+    // Pipelined sweep (sweep_pipe.cu) when samples carry enough pairs to fill a ticket stream;
+    // the chunked kernel below it for sparse waves.
+    static const double pipe_min = std::getenv("SOFG_SWEEP_PIPE_MIN") ? std::atof(std::getenv("SOFG_SWEEP_PIPE_MIN")) : 16.0;
+    const double pairs_per_sample = double(g_total / vpitch(R)) / double(D.n);
+    const bool pipe = pairs_per_sample >= pipe_min && row_sweep_pipe_fits(D.ldr, w.B, R);
+    if (pipe) {
+      const uint32_t PB = (w.B + 1u) & ~1u;
+      void* d_recs = recs_.ensure(size_t(D.n) * PB * pair_rec_bytes());
+      uint32_t* d_pcnt = pcnt_.ensure(size_t(D.n));
+      cuda_check(launch_pair_build(w.inv, w.B, uint32_t(D.n), d_pos_node, d_nodes, d_gbase, R, w.d, d_recs,
+                                   d_pcnt, n_sm_, st_),
+                 "pair_build");
+      mark("pair_build");
+      cuda_check(launch_row_sweep_pipe(D.XR.p, D.ldr, uint32_t(D.n), d_recs, d_pcnt, w.B, d_aug, R, w.d, d_G,
+                                       n_sm_, st_),
+                 "row_sweep_pipe");
+      launches += 4;
+    } else {
+      cuda_check(launch_row_sweep(D.XR.p, D.ldr, uint32_t(D.n), w.inv, w.B, d_pos_node, d_nodes,
+                                  d_gbase, d_aug, R, w.d, d_G, n_sm_, st_),
+                 "row_sweep");
+      launches += 3;
+    }
     mark("row_sweep");
   } else {
     cuda_check(launch_project_gather(d_nodes, d_tiles, int(n_tiles), d_gbase, d_terms, d_rp, R,

@@ -261,7 +261,8 @@ class WaveRunner {
   DevBuf<float> V_;          // projected rows of the wave (sweep.cu)
   DevBuf<uint32_t> pos_node_;  // level position -> wave node (sweep mode)
   DevBuf<unsigned char> aug_;  // augmented term lists (sweep mode)
-  DevBuf<uint4> qoff_;         // per-node sub-list offsets (sweep mode)
+  DevBuf<unsigned char> recs_;  // per-sample pair lists (pipelined sweep)
+  DevBuf<uint32_t> pcnt_;       // pairs per sample (pipelined sweep)
   Scratch scratch_;                    // launch-sized temporaries (dense projections, exact_big)
   DevBuf<float> rowlb_;                // exact branch-and-bound: per (node, row) lower bounds
   DevBuf<unsigned long long> xstar_;   // and per node the best pivot-candidate impurity

@@ -28,6 +28,7 @@
 #include "common.hpp"
 #include "dev_util.cuh"
 #include "kernels.hpp"
+#include "sweep_common.cuh"
 
 namespace sofg {
 namespace dev {
@@ -85,30 +86,11 @@ __device__ __forceinline__ float project_from(const float* xs, const uint32_t* t
   return __double2float_rn(acc);
 }
 
-// ------------------------------------------------------------------------------------------
-// Augmented term lists for the sweep. A node's R rows are split into kQ contiguous row ranges
-// ("quarters"); each range gets its own list: the CSR terms of its rows in order, each entry
-// feature << 2 | last << 1 | negative (so entry & ~3 is the feature's byte offset in a row of XR),
-// with one dummy entry (feature d: the zero pad column of XR) for every empty row, so walking a
-// list completes its rows in order. Each list starts 16-byte aligned and is followed by neutral
-// pad entries (zero column, no row end). Entries are u16 when d < 8192, else u32.
-// Node i's block starts at aug_off(i); sub-list offsets (entries, relative) are in qoff[i].
-// ------------------------------------------------------------------------------------------
-constexpr int kQ = 4;
-
-template <typename E>
-__device__ __forceinline__ uint64_t aug_off(uint32_t term_off, uint32_t i, uint32_t R) {
-  constexpr uint64_t A = 16 / sizeof(E);
-  return (uint64_t(term_off) + uint64_t(i) * (R + 3 * kQ * A) + A - 1) & ~(A - 1);
-}
-__host__ __device__ __forceinline__ uint32_t q_row(uint32_t R, uint32_t c) { return R * c / kQ; }
-
 template <typename E>
 __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ nodes, int n_nodes,
                                                    const uint32_t* __restrict__ terms,
                                                    const uint32_t* __restrict__ row_ptr, uint32_t R,
-                                                   uint32_t d, E* __restrict__ aug,
-                                                   uint4* __restrict__ qoff) {
+                                                   uint32_t d, E* __restrict__ aug) {
   constexpr uint32_t A = 16 / sizeof(E);
   extern __shared__ uint32_t s_empty_pre[];  // [4 warps][R + 1]: empty rows before row r
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -129,45 +111,27 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
   }
   if (lane == 0) epre[R] = carry;
   __syncwarp();
-  // sub-list offsets: aligned, each followed by A neutral pads
-  uint32_t off[kQ + 1];
-  off[0] = 0;
-#pragma unroll
-  for (int c = 0; c < kQ; ++c) {
-    const uint32_t ra = q_row(R, uint32_t(c)), rb = q_row(R, uint32_t(c + 1));
-    const uint32_t len = (__ldg(rp + rb) - __ldg(rp + ra)) + (epre[rb] - epre[ra]);
-    off[c + 1] = (off[c] + len + A + A - 1) & ~(A - 1);
-  }
-  if (lane == 0) qoff[node] = make_uint4(off[0], off[1], off[2], off[3]);
+  // element e of list c -> entry ((e / A) * kQ + c) * A + e % A of the node block
+  auto at = [&](uint32_t c, uint32_t e) { return ((e / A) * kQ + c) * A + (e % A); };
   for (uint32_t r = uint32_t(lane); r < R; r += 32) {
-    const uint32_t c = r * kQ / R;  // quarter of row r: largest c with R*c/kQ <= r
-    uint32_t cc = 0;
-#pragma unroll
-    for (int k = 1; k < kQ; ++k)
-      if (q_row(R, uint32_t(k)) <= r) cc = uint32_t(k);
-    (void)c;
-    const uint32_t ra = q_row(R, cc);
-    uint32_t base = 0;
-#pragma unroll
-    for (int k = 0; k < kQ; ++k)
-      if (uint32_t(k) == cc) base = off[k];
+    const uint32_t c = q_of(R, r), ra = q_row(R, c);
     const uint32_t q0 = __ldg(rp + r), q1 = __ldg(rp + r + 1);
-    const uint32_t pos = base + (q0 - __ldg(rp + ra)) + (epre[r] - epre[ra]);
+    const uint32_t e0 = (q0 - __ldg(rp + ra)) + (epre[r] - epre[ra]);
     if (q1 == q0) {
-      out[pos] = E((d << 2) | 2u);
+      out[at(c, e0)] = E((d << 2) | 2u);
     } else {
       for (uint32_t q = q0; q < q1; ++q) {
         const uint32_t t = __ldg(tm + q);
-        out[pos + (q - q0)] = E(((t >> 1) << 2) | (q + 1 == q1 ? 2u : 0u) | (t & 1u));
+        out[at(c, e0 + (q - q0))] = E(((t >> 1) << 2) | (q + 1 == q1 ? 2u : 0u) | (t & 1u));
       }
     }
   }
-  // neutral pads after each sub-list
+  // neutral entries up to the end of each list's last chunk
 #pragma unroll
   for (int c = 0; c < kQ; ++c) {
     const uint32_t ra = q_row(R, uint32_t(c)), rb = q_row(R, uint32_t(c + 1));
     const uint32_t len = (__ldg(rp + rb) - __ldg(rp + ra)) + (epre[rb] - epre[ra]);
-    for (uint32_t i = uint32_t(lane); i < A; i += 32) out[off[c] + len + i] = E(d << 2);
+    for (uint32_t e = len + uint32_t(lane); e < (len + A - 1) / A * A; e += 32) out[at(uint32_t(c), e)] = E(d << 2);
   }
 }
 
@@ -179,9 +143,6 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
 // independent shared-memory loads, one double accumulator per row — and park their rows in a
 // per-lane staging slot, written to V at the end with vector stores.
 // ------------------------------------------------------------------------------------------
-#ifndef SOFG_SWEEP_DIRECT
-#define SOFG_SWEEP_DIRECT 0  // 1: rows straight to V with 4-byte stores (measured 2x slower: partial-sector writes)
-#endif
 constexpr int kSweepThreadsMax = 256;  // CTA size: 256 for ~60+ trees per wave, 128 below
 
 struct Pair {
@@ -196,36 +157,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-template <typename E>
-__device__ __forceinline__ void unpack16(const uint4& v, uint32_t (&e)[16 / sizeof(E)]) {
-  if constexpr (sizeof(E) == 2) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      e[2 * i] = w[i] & 0xffffu;
-      e[2 * i + 1] = w[i] >> 16;
-    }
-  } else {
-    e[0] = v.x;
-    e[1] = v.y;
-    e[2] = v.z;
-    e[3] = v.w;
-  }
-}
-
-__host__ __device__ __forceinline__ uint32_t sweep_out_pitch(uint32_t R) {
-  return ((R + kQ - 1) / kQ + 3u) / 4u * 4u + 4u;  // floats per lane (16B multiple, bank shift)
-}
-
 // smem: xs[K][ldr] | pairs[K*B] | out[NT][pitch]
 template <typename E, int NT>
 __global__ void __launch_bounds__(NT) k_row_sweep(
     const float* __restrict__ XR, uint64_t ldr, uint32_t N, uint32_t K,
     const uint32_t* __restrict__ inv, uint32_t B, const uint32_t* __restrict__ pos_node,
     const NodeIn* __restrict__ nodes, const uint64_t* __restrict__ vbase,
-    const E* __restrict__ aug, const uint4* __restrict__ qoff, uint32_t R,
-    float* __restrict__ V) {
-  constexpr int EPV = 16 / sizeof(E);  // entries per 16-byte load
+    const E* __restrict__ aug, uint32_t R, float* __restrict__ V) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* xs = reinterpret_cast<float*>(smem_raw);
   Pair* pairs = reinterpret_cast<Pair*>(smem_raw + size_t(K) * ldr * 4);
@@ -275,89 +213,21 @@ __global__ void __launch_bounds__(NT) k_row_sweep(
       uint32_t r = rb;  // rows done (this lane's range [ra, rb))
       const uint4* a4 = reinterpret_cast<const uint4*>(aug);
       const char* xb = reinterpret_cast<const char*>(xs);
-      float* vout = V;
+      uint64_t vout = 0;
       if (pi < cnt) {
         const Pair pr = pairs[pi];
-        const uint4 qo = __ldg(qoff + pr.node);
-        const uint32_t so = c == 0 ? qo.x : c == 1 ? qo.y : c == 2 ? qo.z : qo.w;
-        a4 = reinterpret_cast<const uint4*>(aug + aug_off<E>(__ldg(&nodes[pr.node].term_off), pr.node, R) + so);
+        a4 = reinterpret_cast<const uint4*>(aug + aug_off<E>(__ldg(&nodes[pr.node].term_off), pr.node, R)) + c;
         xb = reinterpret_cast<const char*>(xs + size_t(pr.k) * ldr);
-        vout = V + __ldg(vbase + pr.node) + uint64_t(pr.j) * Rp;
+        vout = __ldg(vbase + pr.node) + uint64_t(pr.j) * Rp;
         r = ra;
       }
       const uint32_t out_base = uint32_t(__cvta_generic_to_shared(sout)) - ra * 4u;
-      double acc = 0.0;
-      bool first = true;
-      // Term entries in 16-byte vectors; two register sets of four vectors ping-pong so the next
-      // four loads are in flight while the current four are consumed (sub-lists are followed by
-      // >= 128 readable bytes). A vector is consumed only while the lane still has rows to close:
-      // entries past its sub-list are either neutral pads or another list's.
-      auto consume = [&](const uint4& q) {
-        if (r >= rb) return;
-        uint32_t e[EPV];
-        unpack16<E>(q, e);
-        uint32_t xv[EPV];
-#pragma unroll
-        for (int u = 0; u < EPV; ++u) xv[u] = *reinterpret_cast<const uint32_t*>(xb + (e[u] & ~3u));
-#pragma unroll
-        for (int u = 0; u < EPV; ++u) {
-          const double dx = double(__uint_as_float(xv[u] ^ (e[u] << 31)));
-          const double sum = __dadd_rn(acc, dx);
-          acc = first ? dx : sum;
-          first = (e[u] & 2u) != 0u;
-          if (first) {
-            const float v = __double2float_rn(acc);
-#if SOFG_SWEEP_DIRECT
-            vout[r] = v;
-#else
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(out_base + r * 4u), "f"(v) : "memory");
-#endif
-            ++r;
-          }
-        }
-      };
-      uint4 A0 = make_uint4(0, 0, 0, 0), A1 = A0, A2 = A0, A3 = A0, B0 = A0, B1 = A0, B2 = A0, B3 = A0;
-      if (r < rb) {
-        A0 = __ldg(a4);
-        A1 = __ldg(a4 + 1);
-        A2 = __ldg(a4 + 2);
-        A3 = __ldg(a4 + 3);
-      }
-      for (uint32_t it = 4;; it += 8) {
-        if (!__any_sync(0xffffffffu, r < rb)) break;
-        if (r < rb) {
-          B0 = __ldg(a4 + it);
-          B1 = __ldg(a4 + it + 1);
-          B2 = __ldg(a4 + it + 2);
-          B3 = __ldg(a4 + it + 3);
-        }
-        consume(A0);
-        consume(A1);
-        consume(A2);
-        consume(A3);
-        if (!__any_sync(0xffffffffu, r < rb)) break;
-        if (r < rb) {
-          A0 = __ldg(a4 + it + 4);
-          A1 = __ldg(a4 + it + 5);
-          A2 = __ldg(a4 + it + 6);
-          A3 = __ldg(a4 + it + 7);
-        }
-        consume(B0);
-        consume(B1);
-        consume(B2);
-        consume(B3);
-      }
+      walk_rows<E>(a4, xb, r, rb, out_base);
       __syncwarp();
-      if (!SOFG_SWEEP_DIRECT && pi < cnt) {  // rows [ra, rb) of the pair -> V
-        if (((ra | Rp) & 3u) == 0u) {
-          const uint32_t n4 = (rb - ra) / 4;
-          for (uint32_t i = 0; i < n4; ++i)
-            reinterpret_cast<float4*>(vout + ra)[i] = reinterpret_cast<const float4*>(sout)[i];
-          for (uint32_t rr = ra + 4 * n4; rr < rb; ++rr) vout[rr] = sout[rr - ra];
-        } else {
-          for (uint32_t rr = ra; rr < rb; ++rr) vout[rr] = sout[rr - ra];
-        }
-      }
+      const uint32_t p_warp = rd * kPairsPerRound + (threadIdx.x & ~31u) / kQ;  // the warp's first pair
+      const uint32_t np = cnt > p_warp ? min(32u / kQ, cnt - p_warp) : 0u;
+      write_pairs(sout - size_t(lane) * pitch, pitch, R, np, V, vout, lane);
+      __syncwarp();
     }
     __syncthreads();
   }
@@ -470,21 +340,23 @@ cudaError_t launch_pos_fill(const NodeIn* nodes, const Tile* tiles, int n_tiles,
 bool aug_narrow(uint32_t d) { return d < 8192; }
 
 size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d) {
-  const size_t es = aug_narrow(d) ? 2 : 4;
-  return (size_t(total_terms) + size_t(n_nodes) * (R + 3 * dev::kQ * (16 / es)) + 512) * es;
+  const size_t es = aug_narrow(d) ? 2 : 4, A = 16 / es;
+  // kQ interleaved lists per node (aug_off), plus one chunk row of alignment and the walk's
+  // prefetch window (8 chunk rows) past the last block
+  return (size_t(dev::kQ) * (size_t(total_terms) + size_t(n_nodes) * (R + 2 * A)) + 9 * dev::kQ * A) * es;
 }
 
 cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
                              const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
-                             uint4* qoff, cudaStream_t st) {
+                             cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
   const size_t smem = size_t(4) * (R + 1) * 4;
   if (aug_narrow(d))
     dev::k_aug_build<uint16_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
-        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint16_t*>(aug), qoff);
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint16_t*>(aug));
   else
     dev::k_aug_build<uint32_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
-        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint32_t*>(aug), qoff);
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint32_t*>(aug));
   return cudaGetLastError();
 }
 
@@ -496,7 +368,7 @@ static int sweep_threads(uint32_t B) {
 
 static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
   return size_t(K) * ldr * 4 + size_t(K) * B * sizeof(dev::Pair) +
-         (SOFG_SWEEP_DIRECT ? 0 : size_t(sweep_threads(B)) * dev::sweep_out_pitch(R) * 4);
+         size_t(sweep_threads(B)) * dev::sweep_out_pitch(R) * 4;
 }
 
 // Samples per CTA iteration: enough (node, sample) pairs to fill the CTA's lanes (a sample sits
@@ -525,7 +397,7 @@ size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R) {
 template <typename E, int NT>
 static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
                                   uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
-                                  const uint64_t* vbase, const void* aug, const uint4* qoff,
+                                  const uint64_t* vbase, const void* aug,
                                   uint32_t R, float* V, int n_sm, cudaStream_t st) {
   const uint32_t K = sweep_k(ldr, B, R);
   const size_t smem = sweep_smem_k(ldr, B, R, K);
@@ -538,20 +410,20 @@ static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, con
   const uint32_t groups = (N + K - 1) / K;
   const unsigned grid = unsigned(std::max(1, std::min<int>(int(groups), n_sm * std::max(per_sm, 1))));
   dev::k_row_sweep<E, NT><<<grid, NT, smem, st>>>(
-      XR, ldr, N, K, inv, B, pos_node, nodes, vbase, static_cast<const E*>(aug), qoff, R, V);
+      XR, ldr, N, K, inv, B, pos_node, nodes, vbase, static_cast<const E*>(aug), R, V);
   return cudaGetLastError();
 }
 
 cudaError_t launch_row_sweep(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
                              uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
-                             const uint64_t* vbase, const void* aug, const uint4* qoff, uint32_t R,
+                             const uint64_t* vbase, const void* aug, uint32_t R,
                              uint32_t d, float* V, int n_sm, cudaStream_t st) {
   const bool wide = sweep_threads(B) == 256;
   if (aug_narrow(d))
-    return wide ? launch_sweep_t<uint16_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st)
-                : launch_sweep_t<uint16_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st);
-  return wide ? launch_sweep_t<uint32_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st)
-              : launch_sweep_t<uint32_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qoff, R, V, n_sm, st);
+    return wide ? launch_sweep_t<uint16_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st)
+                : launch_sweep_t<uint16_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st);
+  return wide ? launch_sweep_t<uint32_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st)
+              : launch_sweep_t<uint32_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st);
 }
 
 cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_tiles,

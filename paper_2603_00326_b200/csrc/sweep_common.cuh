@@ -1,0 +1,158 @@
+// Shared pieces of the two projection-sweep kernels (sweep.cu: k_row_sweep, sweep_pipe.cu:
+// k_row_sweep_pipe): the augmented term-list layout and the per-lane term walk.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.hpp"
+
+namespace sofg {
+namespace dev {
+
+// ------------------------------------------------------------------------------------------
+// Augmented term lists for the sweep. A node's R rows are split into kQ contiguous row ranges
+// ("quarters", rows [q_row(R, c), q_row(R, c + 1))); each range gets its own list: the CSR terms
+// of its rows in order, each entry feature << 2 | last << 1 | negative (so entry & ~3 is the
+// feature's byte offset in a row of XR), with one dummy entry (feature d: the zero pad column of
+// XR) for every empty row, so walking a list completes its rows in order. Entries are u16 when
+// d < 8192, else u32. The kQ lists of a node are interleaved in 16-byte chunks — chunk i of list
+// c at chunk index i * kQ + c of the node's block — so the kQ lanes that walk one (node, sample)
+// pair read one contiguous 64-byte span per step. A list's last chunk is filled up with neutral
+// entries (zero column, no row end); chunks past a list's end are never consumed.
+// Node i's block starts at entry aug_off(term_off_i, i, R).
+// ------------------------------------------------------------------------------------------
+constexpr int kQ = 4;
+
+template <typename E>
+__host__ __device__ __forceinline__ uint64_t aug_off(uint32_t term_off, uint32_t i, uint32_t R) {
+  constexpr uint64_t A = 16 / sizeof(E), CH = kQ * A;
+  return (kQ * (uint64_t(term_off) + uint64_t(i) * (R + 2 * A)) + CH - 1) / CH * CH;
+}
+__host__ __device__ __forceinline__ uint32_t q_row(uint32_t R, uint32_t c) { return R * c / kQ; }
+// quarter holding row r: the largest c with q_row(R, c) <= r
+__host__ __device__ __forceinline__ uint32_t q_of(uint32_t R, uint32_t r) { return (kQ * (r + 1) - 1) / R; }
+
+template <typename E>
+__device__ __forceinline__ void unpack16(const uint4& v, uint32_t (&e)[16 / sizeof(E)]) {
+  if constexpr (sizeof(E) == 2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      e[2 * i] = w[i] & 0xffffu;
+      e[2 * i + 1] = w[i] >> 16;
+    }
+  } else {
+    e[0] = v.x;
+    e[1] = v.y;
+    e[2] = v.z;
+    e[3] = v.w;
+  }
+}
+
+// Per-lane staging of completed rows: an odd number of floats per lane, so lanes storing the same
+// row index hit distinct banks.
+__host__ __device__ __forceinline__ uint32_t sweep_out_pitch(uint32_t R) { return ((R + kQ - 1) / kQ) | 1u; }
+
+// Warp write-out of the warp's np = 32 / kQ (or fewer) pairs: lane l's staging slot (stage +
+// l * pitch) holds rows [q_row(R, l % kQ), q_row(R, l % kQ + 1)) of pair l / kQ, whose rows go to
+// V + vout (16-byte aligned; every lane passes its own pair's vout). float4 stores over each
+// pair's contiguous R floats, so a warp store instruction covers whole 128-byte lines.
+__device__ __forceinline__ void write_pairs(const float* stage, uint32_t pitch, uint32_t R, uint32_t np,
+                                            float* V, uint64_t vout, int lane) {
+  const uint32_t R4 = R / 4, tail = R - 4 * R4;
+  constexpr uint32_t P = 32u / kQ;
+  for (uint32_t f0 = 0; f0 < P * R4; f0 += 32) {  // uniform trip count (the shuffle needs all lanes)
+    const uint32_t f = f0 + uint32_t(lane);
+    const uint32_t p = f / R4, r0 = 4 * (f - p * R4);
+    const uint64_t vo = __shfl_sync(0xffffffffu, vout, int(p * kQ) & 31);
+    if (f >= P * R4 || p >= np) continue;
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t r = r0 + uint32_t(u), c = q_of(R, r);
+      v[u] = stage[(p * kQ + c) * pitch + (r - q_row(R, c))];
+    }
+    *reinterpret_cast<float4*>(V + vo + r0) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  for (uint32_t f0 = 0; f0 < P * tail; f0 += 32) {
+    const uint32_t f = f0 + uint32_t(lane);
+    const uint32_t p = f / tail, r = 4 * R4 + (f - p * tail);
+    const uint64_t vo = __shfl_sync(0xffffffffu, vout, int(p * kQ) & 31);
+    if (f >= P * tail || p >= np) continue;
+    const uint32_t c = q_of(R, r);
+    V[vo + r] = stage[(p * kQ + c) * pitch + (r - q_row(R, c))];
+  }
+}
+
+// One lane's term walk: rows [r, rb) of a (node, sample) pair whose table row sits in shared memory
+// at xb, entries read from `a4` (global; 16-byte vectors). Each completed row is rounded to float
+// and stored to shared memory at byte address out_base + 4 * row. Terms combine exactly as the
+// reference (projection.hpp:101-105): ascending feature order, the first term assigns, later
+// terms add, in double, one rounding to float; empty rows come through as one zero-column entry.
+// Warp-synchronous: all 32 lanes call it (a lane with nothing to do passes r == rb).
+// Two register sets of four vectors ping-pong so the next four loads are in flight while the
+// current four are consumed (sub-lists are followed by >= 128 readable bytes). A vector is
+// consumed only while the lane still has rows to close: entries past its sub-list are neutral
+// pads or another list's. `a4` points at the lane's first chunk; chunks of one list are kQ apart.
+template <typename E>
+__device__ __forceinline__ void walk_rows(const uint4* __restrict__ a4, const char* xb, uint32_t r,
+                                          uint32_t rb, uint32_t out_base) {
+  constexpr int EPV = 16 / sizeof(E);  // entries per 16-byte load
+  double acc = 0.0;
+  bool first = true;
+  auto consume = [&](const uint4& q) {
+    if (r >= rb) return;
+    uint32_t e[EPV];
+    unpack16<E>(q, e);
+    uint32_t xv[EPV];
+#pragma unroll
+    for (int u = 0; u < EPV; ++u) xv[u] = *reinterpret_cast<const uint32_t*>(xb + (e[u] & ~3u));
+#pragma unroll
+    for (int u = 0; u < EPV; ++u) {
+      const double dx = double(__uint_as_float(xv[u] ^ (e[u] << 31)));
+      const double sum = __dadd_rn(acc, dx);
+      acc = first ? dx : sum;
+      first = (e[u] & 2u) != 0u;
+      if (first) {
+        const float v = __double2float_rn(acc);
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(out_base + r * 4u), "f"(v) : "memory");
+        ++r;
+      }
+    }
+  };
+  uint4 A0 = make_uint4(0, 0, 0, 0), A1 = A0, A2 = A0, A3 = A0, B0 = A0, B1 = A0, B2 = A0, B3 = A0;
+  if (r < rb) {
+    A0 = __ldg(a4);
+    A1 = __ldg(a4 + kQ);
+    A2 = __ldg(a4 + 2 * kQ);
+    A3 = __ldg(a4 + 3 * kQ);
+  }
+  for (uint32_t it = 4 * kQ;; it += 8 * kQ) {
+    if (!__any_sync(0xffffffffu, r < rb)) break;
+    if (r < rb) {
+      B0 = __ldg(a4 + it);
+      B1 = __ldg(a4 + it + kQ);
+      B2 = __ldg(a4 + it + 2 * kQ);
+      B3 = __ldg(a4 + it + 3 * kQ);
+    }
+    consume(A0);
+    consume(A1);
+    consume(A2);
+    consume(A3);
+    if (!__any_sync(0xffffffffu, r < rb)) break;
+    if (r < rb) {
+      A0 = __ldg(a4 + it + 4 * kQ);
+      A1 = __ldg(a4 + it + 5 * kQ);
+      A2 = __ldg(a4 + it + 6 * kQ);
+      A3 = __ldg(a4 + it + 7 * kQ);
+    }
+    consume(B0);
+    consume(B1);
+    consume(B2);
+    consume(B3);
+  }
+}
+
+}  // namespace dev
+}  // namespace sofg
