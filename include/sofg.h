@@ -30,6 +30,40 @@ extern "C" {
 typedef struct sofg_ctx sofg_ctx;
 typedef struct sofg_forest sofg_forest;
 
+/* Mirrors soforest::CalibrationOptions (calibrate.hpp:22-32); same fields and defaults. */
+typedef struct sofg_calibration_options {
+  uint64_t n_min;              /* 64 */
+  uint64_t n_max;              /* 65536 */
+  double budget_seconds;       /* 0.1 (soft; hard stop at twice that) */
+  uint64_t bin_count;          /* 256 */
+  int32_t two_level;           /* 1 (accepted; binning is exact either way) */
+  int32_t _pad;
+  uint64_t repetitions;        /* 5: median of this many runs per probe */
+  uint64_t seed;               /* 0xca11b8a7e5eed */
+} sofg_calibration_options;
+
+/* Mirrors soforest::CrossoverSample / CrossoverCalibration (calibrate.hpp:16-41). */
+typedef struct sofg_crossover_sample {
+  uint64_t n;
+  double exact_seconds;        /* per-node split-search device time, exact method */
+  double histogram_seconds;    /* same, histogram method */
+} sofg_crossover_sample;
+
+#define SOFG_MAX_CAL_SAMPLES 64
+typedef struct sofg_calibration {
+  uint64_t breakeven;          /* largest n still split exactly */
+  double elapsed_seconds;
+  int32_t fallback;            /* budget exhausted before a usable measurement (breakeven 1024) */
+  int32_t _pad;
+  uint64_t n_samples;
+  sofg_crossover_sample samples[SOFG_MAX_CAL_SAMPLES];  /* sorted by n */
+} sofg_calibration;
+
+/* Mirrors soforest::SplitPhaseTimes (timing.hpp:23-28), seconds. */
+typedef struct sofg_phase_times {
+  double sample_projections, apply_projections, build_histograms, evaluate_splits;
+} sofg_phase_times;
+
 /* Mirrors soforest::TrainConfig (forest.hpp:38-53); same field meaning and defaults. */
 typedef struct sofg_train_config {
   uint64_t n_trees;            /* 100 */
@@ -38,7 +72,8 @@ typedef struct sofg_train_config {
   uint64_t bin_count;          /* 256, 2..1024 */
   int32_t has_breakeven;       /* Dynamic: histogram iff n > breakeven (split.hpp:46-48) */
   int32_t has_max_depth;
-  uint64_t breakeven;          /* absent -> 1024 (calibrate.hpp:43 fallback) */
+  uint64_t breakeven;          /* absent: train_forest calibrates on the GPU (forest.hpp:285-293);
+                                  train_tree uses 1024 (forest.hpp:258) */
   uint64_t max_depth;
   double bootstrap_fraction;   /* 0.632 */
   uint64_t min_samples_split;  /* 2 */
@@ -51,6 +86,10 @@ typedef struct sofg_train_config {
   uint64_t batch_trees;        /* trees grown together per level (0 = all / memory bound) */
   uint64_t tree_begin;         /* train trees [tree_begin, tree_end) of the forest (sharding) */
   uint64_t tree_end;           /* 0 = n_trees */
+  /* soforest::TrainConfig::calibration (forest.hpp:52): used when Dynamic has no breakeven */
+  sofg_calibration_options calibration;
+  int32_t instrument;          /* 1: record soforest::TrainInstrumentation in the forest */
+  int32_t _pad2;
 } sofg_train_config;
 
 void sofg_default_config(sofg_train_config* cfg);
@@ -81,6 +120,10 @@ int sofg_download_dataset(sofg_ctx* ctx, float* X, int32_t* labels);
 /* train_forest (forest.hpp:267-313): trees tree_begin..tree_end-1 of the forest defined by cfg
  * (tree t is a pure function of (data, cfg, t), forest.hpp:264-266, so shards concatenate). */
 int sofg_train_forest(sofg_ctx* ctx, const sofg_train_config* cfg, sofg_forest** out);
+/* calibrate_crossover (calibrate.hpp:51-196): the reference's breakeven search with GPU probes —
+ * each probe is one wave of nodes of n samples of the resident table split by one method, timed
+ * with CUDA events. Uses cfg->calibration and cfg's projection settings. */
+int sofg_calibrate(sofg_ctx* ctx, const sofg_train_config* cfg, sofg_calibration* out);
 /* train_tree (forest.hpp:250-262): one tree grown from an explicit sorted active set. */
 int sofg_train_tree(sofg_ctx* ctx, const uint32_t* active, uint64_t n_active,
                     const sofg_train_config* cfg, uint64_t seed, uint64_t depth,
@@ -91,6 +134,15 @@ uint64_t sofg_forest_num_trees(const sofg_forest* f);
 uint64_t sofg_forest_num_nodes(const sofg_forest* f);
 uint64_t sofg_forest_num_terms(const sofg_forest* f);
 uint64_t sofg_forest_breakeven(const sofg_forest* f);
+/* Forest::calibration (forest.hpp:81): 1 and *out filled when train_forest calibrated, else 0. */
+int sofg_forest_calibration(const sofg_forest* f, sofg_calibration* out);
+/* soforest::TrainInstrumentation (timing.hpp:39-79) of a run with cfg.instrument = 1: per depth
+ * (every node, internal or leaf, at its depth) seconds / nodes / samples, the four split phases
+ * per depth bucket (depth / 5, capped at 3), split_seconds and total_seconds. Returns the number
+ * of depths (0 when not instrumented); arrays with room for `cap` depths, any may be NULL. */
+uint64_t sofg_forest_instrumentation(const sofg_forest* f, double* seconds, uint64_t* nodes,
+                                     uint64_t* samples, uint64_t cap, sofg_phase_times* phases4,
+                                     double* split_seconds, double* total_seconds);
 void sofg_forest_export(const sofg_forest* f, int64_t* tree_off, int32_t* left, int32_t* right,
                         int32_t* pred, float* thr, int64_t* term_off, uint32_t* feat,
                         float* weight);

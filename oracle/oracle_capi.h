@@ -156,6 +156,11 @@ int orc_train_save_model(const float* X, const int32_t* labels, uint64_t n_sampl
                          const char* path);
 /* load_model(path) with the reference's validating loader; totals of the loaded forest. */
 int orc_load_model_summary(const char* path, uint64_t* n_trees, uint64_t* n_nodes);
+int orc_train_forest_depths(const float* X, const int32_t* labels, uint64_t n_samples, uint64_t n_features,
+                            int32_t class_count, const orc_config* cfg, uint64_t* nodes, uint64_t* samples,
+                            uint64_t cap, uint64_t* n_depths);
+int orc_load_model_calibration(const char* path, uint64_t* breakeven, int32_t* has_cal,
+                               uint64_t* cal_breakeven, uint64_t* n_samples, int32_t* fallback);
 
 #ifdef __cplusplus
 }

@@ -446,3 +446,32 @@ extern "C" int orc_load_model_summary(const char* path, uint64_t* n_trees, uint6
     *n_nodes = nodes;
   });
 }
+
+// Forest::breakeven and Forest::calibration as the reference loader reads them (model_io.hpp:252-253).
+extern "C" int orc_load_model_calibration(const char* path, uint64_t* breakeven, int32_t* has_cal,
+                                          uint64_t* cal_breakeven, uint64_t* n_samples, int32_t* fallback) {
+  return orc_guard([&] {
+    const Forest f = load_model<float>(path);
+    *breakeven = f.breakeven;
+    *has_cal = f.calibration.has_value();
+    *cal_breakeven = f.calibration ? f.calibration->breakeven : 0;
+    *n_samples = f.calibration ? f.calibration->samples.size() : 0;
+    *fallback = f.calibration ? f.calibration->fallback : 0;
+  });
+}
+
+// TrainInstrumentation::by_depth node and sample counts of a reference train_forest run
+// (forest.hpp:237, timing.hpp:58-63); returns the number of depths (<= cap written).
+extern "C" int orc_train_forest_depths(const float* X, const int32_t* y, uint64_t n, uint64_t d, int32_t k,
+                                       const orc_config* c, uint64_t* nodes, uint64_t* samples, uint64_t cap,
+                                       uint64_t* n_depths) {
+  return orc_guard([&] {
+    TrainInstrumentation instr;
+    (void)train_forest(make_data(X, y, n, d, k), to_cfg(c), &instr);
+    *n_depths = instr.by_depth.size();
+    for (uint64_t i = 0; i < std::min<uint64_t>(cap, instr.by_depth.size()); ++i) {
+      nodes[i] = instr.by_depth[i].nodes;
+      samples[i] = instr.by_depth[i].samples;
+    }
+  });
+}

@@ -28,6 +28,26 @@ class SofgError(RuntimeError):
     pass
 
 
+class _CalOpts(C.Structure):
+    _fields_ = [("n_min", C.c_uint64), ("n_max", C.c_uint64), ("budget_seconds", C.c_double),
+                ("bin_count", C.c_uint64), ("two_level", C.c_int32), ("_pad", C.c_int32),
+                ("repetitions", C.c_uint64), ("seed", C.c_uint64)]
+
+
+class _CalSample(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("exact_seconds", C.c_double), ("histogram_seconds", C.c_double)]
+
+
+class _Cal(C.Structure):
+    _fields_ = [("breakeven", C.c_uint64), ("elapsed_seconds", C.c_double), ("fallback", C.c_int32),
+                ("_pad", C.c_int32), ("n_samples", C.c_uint64), ("samples", _CalSample * 64)]
+
+
+class _Phases(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("sample_projections", "apply_projections", "build_histograms",
+                                          "evaluate_splits")]
+
+
 class _Cfg(C.Structure):
     _fields_ = [
         ("n_trees", C.c_uint64), ("mode", C.c_int32), ("two_level_binning", C.c_int32),
@@ -36,7 +56,7 @@ class _Cfg(C.Structure):
         ("min_samples_split", C.c_uint64), ("max_split_retries", C.c_uint64),
         ("n_workers", C.c_uint64), ("seed", C.c_uint64), ("num_projections", C.c_uint64),
         ("cell_density", C.c_double), ("batch_trees", C.c_uint64), ("tree_begin", C.c_uint64),
-        ("tree_end", C.c_uint64),
+        ("tree_end", C.c_uint64), ("calibration", _CalOpts), ("instrument", C.c_int32), ("_pad2", C.c_int32),
     ]
 
 
@@ -85,6 +105,10 @@ def load():
     L.sofg_download_dataset.argtypes = [vp, vp, vp]
     L.sofg_train_forest.argtypes = [vp, P(_Cfg), P(vp)]
     L.sofg_train_tree.argtypes = [vp, vp, u64, P(_Cfg), u64, u64, P(vp)]
+    L.sofg_calibrate.argtypes = [vp, P(_Cfg), P(_Cal)]
+    L.sofg_forest_calibration.argtypes = [vp, P(_Cal)]
+    L.sofg_forest_instrumentation.restype = u64
+    L.sofg_forest_instrumentation.argtypes = [vp, vp, vp, vp, u64, P(_Phases), P(f64), P(f64)]
     for fn in ("sofg_forest_num_trees", "sofg_forest_num_nodes", "sofg_forest_num_terms",
                "sofg_forest_breakeven"):
         getattr(L, fn).restype = u64
@@ -143,6 +167,8 @@ class TrainConfig:
     batch_trees: int = 0
     tree_begin: int = 0
     tree_end: int = 0
+    calibration: "CalibrationOptions | None" = None  # soforest::CalibrationOptions; None = defaults
+    instrument: bool = False  # record soforest::TrainInstrumentation (Forest.instrumentation)
 
     def to_c(self) -> _Cfg:
         c = _Cfg()
@@ -165,6 +191,13 @@ class TrainConfig:
         c.batch_trees = self.batch_trees
         c.tree_begin = self.tree_begin
         c.tree_end = self.tree_end
+        if self.calibration is not None:
+            co = self.calibration
+            c.calibration.n_min, c.calibration.n_max = co.n_min, co.n_max
+            c.calibration.budget_seconds, c.calibration.bin_count = co.budget_seconds, co.bin_count
+            c.calibration.two_level, c.calibration.repetitions = int(co.two_level), co.repetitions
+            c.calibration.seed = co.seed
+        c.instrument = int(self.instrument)
         return c
 
 
@@ -183,6 +216,8 @@ class Forest:
     breakeven: int = 0
     class_count: int = 0
     n_features: int = 0
+    calibration: "Calibration | None" = None          # Forest::calibration (forest.hpp:81)
+    instrumentation: "Instrumentation | None" = None  # TrainInstrumentation of the run
 
     @property
     def n_trees(self) -> int:
@@ -201,6 +236,47 @@ def _export(h) -> Forest:
                int(L.sofg_forest_breakeven(h)))
     L.sofg_forest_export(h, *(a.ctypes.data for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off,
                                                        f.feat, f.weight)))
+    return f
+
+
+@dataclass
+class Instrumentation:
+    """soforest::TrainInstrumentation (timing.hpp:39-79): per-depth device seconds, node and
+    sample counts; split phases per depth bucket ("0-4", "5-9", "10-14", "15+")."""
+
+    seconds: list
+    nodes: list
+    samples: list
+    phases: list  # 4 buckets x dict(sample_projections, apply_projections, build_histograms, evaluate_splits)
+    split_seconds: float
+    total_seconds: float
+
+
+def _cal_from_c(c: "_Cal"):
+    from .model_io import Calibration
+
+    return Calibration(breakeven=int(c.breakeven),
+                       samples=[(int(c.samples[i].n), float(c.samples[i].exact_seconds),
+                                 float(c.samples[i].histogram_seconds)) for i in range(int(c.n_samples))],
+                       elapsed_seconds=float(c.elapsed_seconds), fallback=bool(c.fallback))
+
+
+def _records(h, f: "Forest") -> "Forest":
+    """Attach the calibration record and instrumentation of library forest `h` to `f`."""
+    L = load()
+    cal = _Cal()
+    if L.sofg_forest_calibration(h, C.byref(cal)):
+        f.calibration = _cal_from_c(cal)
+    nd = L.sofg_forest_instrumentation(h, None, None, None, 0, None, None, None)
+    if nd:
+        sec, nodes, samp = np.zeros(nd), np.zeros(nd, np.uint64), np.zeros(nd, np.uint64)
+        ph = (_Phases * 4)()
+        split_s, total_s = C.c_double(), C.c_double()
+        L.sofg_forest_instrumentation(h, sec.ctypes.data, nodes.ctypes.data, samp.ctypes.data, nd, ph,
+                                      C.byref(split_s), C.byref(total_s))
+        f.instrumentation = Instrumentation(
+            sec.tolist(), [int(x) for x in nodes], [int(x) for x in samp],
+            [{n: getattr(ph[b], n) for n, _ in _Phases._fields_} for b in range(4)], split_s.value, total_s.value)
     return f
 
 
@@ -303,13 +379,21 @@ class Context:
         _check(self.L.sofg_train_forest(self.h, C.byref(c), C.byref(h)), "train_forest")
         if os.environ.get("SOFG_COPY_EXPORT"):
             try:
-                f = _export(h)
+                f = _records(h, _export(h))
             finally:
                 self.L.sofg_forest_free(h)
         else:
-            f = _adopt(h)  # zero-copy; the library forest is freed with the arrays
+            f = _records(h, _adopt(h))  # zero-copy; the library forest is freed with the arrays
         f.class_count, f.n_features = self.class_count, self.n_features
         return f
+
+    def calibrate(self, cfg: TrainConfig | None = None):
+        """soforest::calibrate_crossover (calibrate.hpp:51-196) with GPU probes on the resident table;
+        returns a model_io.Calibration record."""
+        c = (cfg or TrainConfig()).to_c()
+        out = _Cal()
+        _check(self.L.sofg_calibrate(self.h, C.byref(c), C.byref(out)), "calibrate")
+        return _cal_from_c(out)
 
     def train_tree(self, active, cfg: TrainConfig, seed: int, depth: int = 0) -> Forest:
         a = np.ascontiguousarray(active, np.uint32)
@@ -318,7 +402,7 @@ class Context:
         _check(self.L.sofg_train_tree(self.h, a.ctypes.data, len(a), C.byref(c), seed, depth, C.byref(h)),
                "train_tree")
         try:
-            f = _export(h)
+            f = _records(h, _export(h))
         finally:
             self.L.sofg_forest_free(h)
         f.class_count, f.n_features = self.class_count, self.n_features

@@ -1,4 +1,5 @@
 // C ABI (include/sofg.h) and C++ API (include/sofg/soforest_gpu.hpp) over the level-wise trainer.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -9,7 +10,7 @@
 #include <string>
 
 #include "../../include/sofg.h"
-#include "../../include/sofg/soforest_gpu.hpp"
+#include "calibrate.hpp"
 #include "engine.hpp"
 #include "host_rng.hpp"
 #include "kernels.hpp"
@@ -25,6 +26,11 @@ struct sofg_ctx {
 
 struct sofg_forest {
   sofg::FlatForest f;
+  bool has_cal = false;
+  sofg_calibration cal{};
+  bool has_prof = false;
+  sofg::DepthProfile prof;
+  double total_seconds = 0.0;
 };
 
 using sofg::cuda_check;
@@ -203,6 +209,34 @@ uint64_t auto_batch(uint64_t n_root, uint64_t n_trees, const sofg::TrainParams& 
   return std::min(n_trees, cap);
 }
 
+sofg::CalOptions cal_options(const sofg_calibration_options& o) {
+  sofg::CalOptions c;
+  c.n_min = o.n_min;
+  c.n_max = o.n_max;
+  c.budget_seconds = o.budget_seconds;
+  c.bin_count = o.bin_count;
+  c.two_level = o.two_level != 0;
+  c.repetitions = o.repetitions;
+  c.seed = o.seed;
+  return c;
+}
+
+void run_calibration(sofg_ctx* c, const sofg_train_config* cfg, const sofg::TrainParams& P,
+                     sofg_calibration* out) {
+  const sofg::CalOptions opt = cal_options(cfg->calibration);
+  if (opt.n_max >= (1ull << 31)) throw std::invalid_argument("calibration n_max too large");
+  ensure_xlogx(c->eng->data(), opt.n_max, c->eng->stream());
+  sofg::ThreadPool& pool = pool_for(c, cfg->n_workers);
+  const sofg::CalResult r = sofg::calibrate_crossover(*c->eng, pool, P, opt);
+  std::memset(out, 0, sizeof(*out));
+  out->breakeven = r.breakeven;
+  out->elapsed_seconds = r.elapsed_seconds;
+  out->fallback = r.fallback;
+  out->n_samples = std::min<uint64_t>(r.samples.size(), SOFG_MAX_CAL_SAMPLES);
+  for (uint64_t i = 0; i < out->n_samples; ++i)
+    out->samples[i] = {r.samples[i].n, r.samples[i].exact_seconds, r.samples[i].histogram_seconds};
+}
+
 }  // namespace
 
 // =============================================================================== C ABI
@@ -218,6 +252,13 @@ void sofg_default_config(sofg_train_config* c) {
   c->min_samples_split = 2;
   c->max_split_retries = 1;
   c->n_workers = 1;
+  c->calibration.n_min = 64;  // calibrate.hpp:22-32
+  c->calibration.n_max = 65536;
+  c->calibration.budget_seconds = 0.1;
+  c->calibration.bin_count = 256;
+  c->calibration.two_level = 1;
+  c->calibration.repetitions = 5;
+  c->calibration.seed = 0xca11b8a7e5eedull;
 }
 
 const char* sofg_last_error(void) { return g_err.c_str(); }
@@ -318,12 +359,29 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
     const uint64_t tb = cfg->tree_begin;
     const uint64_t te = cfg->tree_end ? std::min(cfg->tree_end, cfg->n_trees) : cfg->n_trees;
     if (tb > te) throw std::invalid_argument("tree_begin > tree_end");
-    sofg::ThreadPool& pool = pool_for(c, cfg->n_workers);
+    const auto t_start = std::chrono::steady_clock::now();
     auto* res = new sofg_forest;
     std::unique_ptr<sofg_forest> guard_res(res);
     res->f.class_count = D.k;
     res->f.n_features = D.d;
+    if (cfg->mode == 2 && !cfg->has_breakeven) {  // forest.hpp:285-293: calibrate when absent
+      run_calibration(c, cfg, P, &res->cal);
+      res->has_cal = true;
+      P.breakeven = res->cal.breakeven;
+    }
     res->f.breakeven = cfg->mode == 2 ? P.breakeven : 0;
+    sofg::ThreadPool& pool = pool_for(c, cfg->n_workers);
+    const bool had_stats = c->eng->collect_stats;
+    if (cfg->instrument) {  // TrainInstrumentation: per-wave CUDA-event timing for this call
+      res->has_prof = true;
+      P.profile = &res->prof;
+      c->eng->collect_stats = true;
+    }
+    struct StatsRestore {
+      sofg_ctx* c;
+      bool on;
+      ~StatsRestore() { c->eng->collect_stats = on; }
+    } stats_restore{c, had_stats};
     uint64_t k0 = uint64_t(std::llround(cfg->bootstrap_fraction * double(D.n)));
     k0 = std::clamp<uint64_t>(k0, 1, D.n);
     const uint64_t batch = P.batch_trees ? P.batch_trees : auto_batch(k0, te - tb, P, D.d);
@@ -343,7 +401,19 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tbs).count();
       sofg::grow_trees(*c->eng, P, pool, roots, seeds, 0, res->f, c->times);
     }
+    res->total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     *out = guard_res.release();
+  });
+}
+
+int sofg_calibrate(sofg_ctx* c, const sofg_train_config* cfg, sofg_calibration* out) {
+  return guard([&] {
+    require_data(c);
+    if (!out) throw std::invalid_argument("null output");
+    const sofg::DeviceData& D = c->eng->data();
+    validate_cfg(cfg, D);
+    const sofg::TrainParams P = params_for(cfg, D, true);
+    run_calibration(c, cfg, P, out);
   });
 }
 
@@ -366,9 +436,22 @@ int sofg_train_tree(sofg_ctx* c, const uint32_t* active, uint64_t n_active,
     std::unique_ptr<sofg_forest> guard_res(res);
     res->f.class_count = D.k;
     res->f.n_features = D.d;
+    const auto t_start = std::chrono::steady_clock::now();
+    const bool had_stats = c->eng->collect_stats;
+    if (cfg->instrument) {
+      res->has_prof = true;
+      P.profile = &res->prof;
+      c->eng->collect_stats = true;
+    }
+    struct StatsRestore {
+      sofg_ctx* c;
+      bool on;
+      ~StatsRestore() { c->eng->collect_stats = on; }
+    } stats_restore{c, had_stats};
     std::vector<std::vector<uint32_t>> roots{std::vector<uint32_t>(active, active + n_active)};
     std::vector<uint64_t> seeds{seed};
     sofg::grow_trees(*c->eng, P, pool, roots, seeds, uint32_t(depth), res->f, c->times);
+    res->total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     *out = guard_res.release();
   });
 }
@@ -377,6 +460,31 @@ uint64_t sofg_forest_num_trees(const sofg_forest* f) { return f->f.n_trees(); }
 uint64_t sofg_forest_num_nodes(const sofg_forest* f) { return f->f.left.size(); }
 uint64_t sofg_forest_num_terms(const sofg_forest* f) { return f->f.feat.size(); }
 uint64_t sofg_forest_breakeven(const sofg_forest* f) { return f->f.breakeven; }
+
+int sofg_forest_calibration(const sofg_forest* f, sofg_calibration* out) {
+  if (!f || !f->has_cal) return 0;
+  if (out) *out = f->cal;
+  return 1;
+}
+
+uint64_t sofg_forest_instrumentation(const sofg_forest* f, double* seconds, uint64_t* nodes,
+                                     uint64_t* samples, uint64_t cap, sofg_phase_times* phases,
+                                     double* split_seconds, double* total_seconds) {
+  if (!f || !f->has_prof) return 0;
+  const sofg::DepthProfile& p = f->prof;
+  const uint64_t nd = p.seconds.size();
+  for (uint64_t i = 0; i < std::min(nd, cap); ++i) {
+    if (seconds) seconds[i] = p.seconds[i];
+    if (nodes) nodes[i] = p.nodes[i];
+    if (samples) samples[i] = p.samples[i];
+  }
+  if (phases)
+    for (int b = 0; b < sofg::DepthProfile::kBuckets; ++b)
+      phases[b] = {p.phases[b][0], p.phases[b][1], p.phases[b][2], p.phases[b][3]};
+  if (split_seconds) *split_seconds = p.split_seconds;
+  if (total_seconds) *total_seconds = f->total_seconds;
+  return nd;
+}
 
 void sofg_forest_arrays(const sofg_forest* fo, const void** a) {
   const sofg::FlatForest& f = fo->f;
@@ -790,150 +898,3 @@ int sofg_reset_stats(sofg_ctx* c) {
 }
 
 }  // extern "C"
-
-// =============================================================================== C++ API
-namespace sofg {
-
-ColumnarDataset::ColumnarDataset(std::vector<std::vector<float>> columns,
-                                 std::vector<std::int32_t> labels,
-                                 std::vector<std::string> label_names)
-    : columns_(std::move(columns)), labels_(std::move(labels)), label_names_(std::move(label_names)) {
-  for (const auto& col : columns_)  // dataset.hpp:35-44
-    if (col.size() != labels_.size())
-      throw std::invalid_argument("column length does not match label count");
-  for (std::int32_t y : labels_)
-    if (y < 0 || static_cast<std::size_t>(y) >= label_names_.size())
-      throw std::invalid_argument("label id out of range");
-}
-
-namespace {
-
-sofg_train_config to_c(const TrainConfig& t) {
-  sofg_train_config c;
-  sofg_default_config(&c);
-  c.n_trees = t.n_trees;
-  c.mode = t.mode == SplitMode::kExactOnly ? 0 : t.mode == SplitMode::kHistogramOnly ? 1 : 2;
-  c.two_level_binning = t.two_level_binning;
-  c.bin_count = t.bin_count;
-  c.has_breakeven = t.breakeven.has_value();
-  c.breakeven = t.breakeven.value_or(0);
-  c.has_max_depth = t.max_depth.has_value();
-  c.max_depth = t.max_depth.value_or(0);
-  c.bootstrap_fraction = t.bootstrap_fraction;
-  c.min_samples_split = t.min_samples_split;
-  c.max_split_retries = t.max_split_retries;
-  c.n_workers = t.n_workers;
-  c.seed = t.seed;
-  c.num_projections = t.num_projections;
-  c.cell_density = t.cell_density;
-  c.batch_trees = t.batch_trees;
-  return c;
-}
-
-void throw_last(int rc) {
-  const std::string m = sofg_last_error();
-  if (rc == 1) throw std::invalid_argument(m);
-  if (rc == 2) throw std::out_of_range(m);
-  throw std::runtime_error(m);
-}
-
-struct CtxHolder {
-  sofg_ctx* c = nullptr;
-  explicit CtxHolder(int dev) {
-    const int rc = sofg_create(dev, &c);
-    if (rc) throw_last(rc);
-  }
-  ~CtxHolder() { sofg_destroy(c); }
-};
-
-void upload_dataset(sofg_ctx* c, const ColumnarDataset& data) {
-  std::vector<const float*> cols(data.n_features());
-  for (std::size_t f = 0; f < cols.size(); ++f) cols[f] = data.column(f).data();
-  const int rc = sofg_upload_columns(c, cols.data(), data.n_samples(), data.n_features(),
-                                     data.labels().data(), data.class_count());
-  if (rc) throw_last(rc);
-}
-
-std::vector<Tree> to_trees(const sofg_forest* f) {
-  const FlatForest& F = f->f;
-  std::vector<Tree> out(F.n_trees());
-  for (std::size_t t = 0; t < out.size(); ++t) {
-    for (int64_t q = F.tree_off[t]; q < F.tree_off[t + 1]; ++q) {
-      TreeNode nd;
-      nd.left = F.left[size_t(q)];
-      nd.right = F.right[size_t(q)];
-      nd.predicted_class = F.pred[size_t(q)];
-      nd.threshold = F.thr[size_t(q)];
-      for (int64_t u = F.term_off[size_t(q)]; u < F.term_off[size_t(q) + 1]; ++u)
-        nd.projection.push_back({F.feat[size_t(u)], F.weight[size_t(u)]});
-      out[t].nodes.push_back(std::move(nd));
-    }
-  }
-  return out;
-}
-
-}  // namespace
-
-Forest train_forest(const ColumnarDataset& data, const TrainConfig& cfg) {
-  CtxHolder h(cfg.device);
-  upload_dataset(h.c, data);
-  const sofg_train_config c = to_c(cfg);
-  sofg_forest* f = nullptr;
-  const int rc = sofg_train_forest(h.c, &c, &f);
-  if (rc) throw_last(rc);
-  Forest out;
-  out.n_features = std::uint32_t(data.n_features());
-  out.class_count = data.class_count();
-  out.label_names = data.label_names();
-  out.config = cfg;
-  out.breakeven = f->f.breakeven;
-  out.trees = to_trees(f);
-  sofg_forest_free(f);
-  return out;
-}
-
-Tree train_tree(const ColumnarDataset& data, const SampleIndexSet& active, const TrainConfig& cfg,
-                std::uint64_t seed, std::size_t depth) {
-  CtxHolder h(cfg.device);
-  upload_dataset(h.c, data);
-  const sofg_train_config c = to_c(cfg);
-  sofg_forest* f = nullptr;
-  const int rc = sofg_train_tree(h.c, active.indices.data(), active.indices.size(), &c, seed,
-                                 depth, &f);
-  if (rc) throw_last(rc);
-  Tree t = std::move(to_trees(f)[0]);
-  sofg_forest_free(f);
-  return t;
-}
-
-Prediction predict(const Forest& forest, std::span<const float> sample) {  // forest.hpp:110-121
-  if (sample.size() != forest.n_features)
-    throw std::invalid_argument("sample has " + std::to_string(sample.size()) +
-                                " features, model expects " + std::to_string(forest.n_features));
-  FlatForest F;
-  F.class_count = forest.class_count;
-  F.n_features = forest.n_features;
-  for (const Tree& t : forest.trees) {
-    for (const TreeNode& nd : t.nodes) {
-      F.left.push_back(nd.left);
-      F.right.push_back(nd.right);
-      F.pred.push_back(nd.predicted_class);
-      F.thr.push_back(nd.threshold);
-      for (const auto& term : nd.projection) {
-        F.feat.push_back(term.feature);
-        F.weight.push_back(term.weight);
-      }
-      F.term_off.push_back(int64_t(F.feat.size()));
-    }
-    F.tree_off.push_back(int64_t(F.left.size()));
-  }
-  sofg_forest holder{std::move(F)};
-  CtxHolder h(forest.config.device);
-  Prediction p;
-  p.votes.assign(std::size_t(forest.class_count), 0.0);
-  const int rc = sofg_predict(h.c, &holder, sample.data(), 1, sample.size(), &p.label, p.votes.data());
-  if (rc) throw_last(rc);
-  return p;
-}
-
-}  // namespace sofg

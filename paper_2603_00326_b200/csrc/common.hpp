@@ -21,6 +21,7 @@ constexpr int kExactSmemMax = 2048;  // largest node the shared-memory exact spl
 constexpr int kTileElems = 1024;     // partition tile
 constexpr int kWinTermsMax = 16;     // winning-row terms returned inline per node
 constexpr int kHistRowsPerCta = 8;   // rows (one per warp) per histogram CTA
+constexpr uint64_t kFallbackBreakeven = 1024;  // reference calibrate.hpp:43
 
 enum NodeFlags : uint32_t {
   kNodeHist = 1u,         // histogram method (else exact), split.hpp:46-48

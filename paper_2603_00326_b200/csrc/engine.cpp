@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <string>
 
 #include "kernels.hpp"
 #include "trainer.hpp"
@@ -85,6 +86,15 @@ struct Packer {
     return o;
   }
 };
+// Launch site -> reference split phase (timing.hpp:23-28); -1 = outside the split search.
+int phase_of(const char* site) {
+  const std::string s(site);
+  if (s == "sample_projection") return 0;
+  if (s == "sweep_prep" || s == "pair_build" || s == "row_sweep" || s == "project_gather") return 1;
+  if (s == "hist_draws" || s == "hist_boundaries" || s == "hist_count") return 2;
+  if (s == "partition") return -1;
+  return 3;  // hist_select, exact_prune, exact buckets, exact_big
+}
 int pow2_at_least(int x, int lo) {
   int p = lo;
   while (p < x) p <<= 1;
@@ -397,6 +407,7 @@ void WaveRunner::submit(const WaveSpec& w) {
     mark("hist_count");
     cuda_check(launch_hist_select(d_hist, int(nh), R, d_rowres, d_res, st_), "hist_select");
     launches += 2;
+    mark("hist_select");
   }
   if (timing) cudaEventRecord(ev_[3], st_);
   {
@@ -555,10 +566,13 @@ const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
     stats.ms_total += tt;
     last_wave_ms_ = tt;
     static const bool wave_log = std::getenv("SOFG_LEVEL_LOG") != nullptr;
+    for (float& p : last_phase_ms_) p = 0.f;
     for (int i = 0; i < n_marks_; ++i) {
       float dt;
       cudaEventElapsedTime(&dt, mk_[i], mk_[i + 1]);
       stats.add_kernel(mk_name_[i], dt);
+      const int ph = phase_of(mk_name_[i]);
+      if (ph >= 0) last_phase_ms_[ph] += dt;
       if (wave_log) std::fprintf(stderr, "%s%s %.2f", i ? ", " : "  [wave] ", mk_name_[i], double(dt));
     }
     if (wave_log && n_marks_) std::fprintf(stderr, "\n");

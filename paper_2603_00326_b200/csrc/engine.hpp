@@ -211,6 +211,11 @@ class WaveRunner {
   // take their host turn and call collect_view().
   bool last_was_sweep() const { return pend_sweep_; }
   float last_wave_ms() const { return last_wave_ms_; }  // device time of the last collected wave (stats on)
+  // Device time of the last collected wave (stats on) by the reference's split phases
+  // (timing.hpp:23-28): 0 sample_projections, 1 apply_projections, 2 build_histograms (boundary
+  // sampling + binning), 3 evaluate_splits (histogram scan / exact splitters); partition excluded.
+  const float* last_phase_ms() const { return last_phase_ms_; }
+  float last_split_ms() const { return last_phase_ms_[2] + last_phase_ms_[3]; }
   void wait_wave();
   // Page-locked staging reused across calls (root segments).
   PinnedBuf<unsigned char> staging;
@@ -278,6 +283,7 @@ class WaveRunner {
   NodeRes* pend_dres_ = nullptr;
   int pend_n_ = 0, pend_launches_ = 0;
   float last_wave_ms_ = 0.f;
+  float last_phase_ms_[4] = {};
   size_t pend_hist_ = 0, pend_exact_ = 0;
   bool pend_sweep_ = false;
   double pend_sweep_bytes_ = 0;

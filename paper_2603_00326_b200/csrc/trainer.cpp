@@ -274,6 +274,9 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
     }
   });
   times.ms_roots += ms_since(t0);
+  DepthProfile* prof = P.profile;
+  if (prof) prof->add(root_depth, 0.0, B, total);
+  std::vector<uint64_t> part_splits(prof ? NP : 0), part_split_n(prof ? NP : 0);
 
   int cur = 0;
   static const bool level_log = std::getenv("SOFG_LEVEL_LOG") != nullptr;
@@ -495,12 +498,29 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       }
       times.ms_wait += lv_wait;
 
+      if (prof) {
+        uint32_t depth = 0;
+        for (size_t p = 0; p < NP; ++p)
+          if (!sp[p].empty()) {
+            depth = sp[p][0].depth;
+            break;
+          }
+        const float* ph = eng.last_phase_ms();
+        const int bk = DepthProfile::bucket(depth);
+        prof->add(depth, 1e-3 * double(eng.last_wave_ms()), 0, 0);
+        for (int i = 0; i < 4; ++i) {
+          prof->phases[bk][i] += 1e-3 * double(ph[i]);
+          prof->split_seconds += 1e-3 * double(ph[i]);
+        }
+      }
+
       t0 = Clock::now();
       // Critical pass: the children (the next wave's input) and retries. The tree records of this
       // wave (thresholds, terms, links, leaf predictions) are filled by bookkeep() after the next
       // wave is submitted, overlapping its kernels.
       pool.parallel_for(NP, [&](size_t p) {
         rt[p].clear();
+        uint64_t n_splits = 0, n_split_samples = 0;
         for (size_t j = 0; j < sp[p].size(); ++j) {
           const size_t i = poff[p] + j;
           const Open& o = sp[p][j];
@@ -530,6 +550,8 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
             }
             if (can_split(l)) nx[p].push_back(l);
             if (can_split(rr)) nx[p].push_back(rr);
+            ++n_splits;
+            n_split_samples += o.n;
           } else if (o.attempt < P.max_split_retries) {  // forest.hpp:187,211: next attempt
             Open a = o;
             a.attempt++;
@@ -538,9 +560,27 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
             rt[p].push_back(a);
           }
         }
+        if (prof) {
+          part_splits[p] = n_splits;
+          part_split_n[p] = n_split_samples;
+        }
         dn[p].swap(sp[p]);
         sp[p].swap(rt[p]);
       });
+      if (prof) {  // children of this wave's splits: two nodes each at depth + 1
+        uint64_t ns = 0, nn = 0;
+        for (size_t p = 0; p < NP; ++p) {
+          ns += part_splits[p];
+          nn += part_split_n[p];
+        }
+        uint32_t depth = 0;
+        for (size_t p = 0; p < NP; ++p)
+          if (!dn[p].empty()) {
+            depth = dn[p][0].depth;
+            break;
+          }
+        if (ns) prof->add(size_t(depth) + 1, 0.0, 2 * ns, nn);
+      }
       dres = res;
       dpoff = poff;
       pending = true;

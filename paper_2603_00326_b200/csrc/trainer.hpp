@@ -5,6 +5,7 @@
 // (forest.hpp:183,226,228), so level order does not change any random stream, and node ids are
 // restored by replaying the reference's depth-first split order at the end.
 #pragma once
+#include <algorithm>
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
@@ -59,6 +60,30 @@ struct FlatForest {
 void recycle_forest(FlatForest&& f);
 void adopt_recycled(FlatForest& out);
 
+// Per-depth accounting of a training run, the GPU counterpart of soforest::TrainInstrumentation
+// (timing.hpp:39-79): every tree node (internal and leaf) is counted at its depth with its sample
+// count; seconds are the device time of the waves at that depth (CUDA events; a wave is every open
+// node of the depth across the tree batch), and the split phases are summed per depth bucket
+// (timing.hpp:50-56: depth / 5, capped at 3).
+struct DepthProfile {
+  static constexpr int kBuckets = 4;
+  std::vector<double> seconds;
+  std::vector<uint64_t> nodes, samples;
+  double phases[kBuckets][4] = {};  // sample_projections, apply_projections, build_histograms, evaluate_splits
+  double split_seconds = 0.0;
+  void add(size_t depth, double s, uint64_t n_nodes, uint64_t n_samples) {
+    if (seconds.size() <= depth) {
+      seconds.resize(depth + 1, 0.0);
+      nodes.resize(depth + 1, 0);
+      samples.resize(depth + 1, 0);
+    }
+    seconds[depth] += s;
+    nodes[depth] += n_nodes;
+    samples[depth] += n_samples;
+  }
+  static int bucket(size_t depth) { return int(std::min<size_t>(depth / 5, kBuckets - 1)); }
+};
+
 struct TrainParams {
   int mode = 2;  // 0 exact-only, 1 histogram-only, 2 dynamic
   uint64_t bins = 256;
@@ -70,6 +95,7 @@ struct TrainParams {
   double density = 0.0;    // cell density
   uint64_t batch_trees = 0;
   int host_threads = 0;
+  DepthProfile* profile = nullptr;  // filled when set (requires WaveRunner::collect_stats)
 };
 
 // Minimal fork-join pool for the per-node host work (binomial draws, bootstraps).

@@ -59,7 +59,9 @@ def model_bytes(forest, cfg, label_names=None, calibration_options: CalibrationO
     """The complete file contents save_model would write (model_io.hpp:124-184)."""
     k = int(forest.class_count)
     names = [str(c) for c in range(k)] if label_names is None else list(label_names)
-    co = calibration_options or CalibrationOptions()
+    co = calibration_options or getattr(cfg, "calibration", None) or CalibrationOptions()
+    if calibration is None:
+        calibration = getattr(forest, "calibration", None)  # Forest::calibration of a calibrated run
     out = bytearray()
     out += struct.pack("<BIi", 4, int(forest.n_features), k)
     out += struct.pack("<I", len(names))
@@ -185,13 +187,14 @@ def load_model(path: str):
     if mode > 2:
         raise RuntimeError(f"{path}: invalid split mode")
     has_md, md, mss, retries, workers, seed = r.take("<BQQQQQ")
-    r.take("<QQdQBQQ")  # calibration options
+    co = CalibrationOptions(*r.take("<QQdQBQQ"))
+    co.two_level = bool(co.two_level)
     breakeven = r.take("<Q")
+    calibration = None
     if r.take("<B"):
-        r.take("<QdB")
-        for _ in range(r.take("<Q")):
-            r.take("<Qdd")
-    cfg = TrainConfig(n_trees=n_trees, mode=_MODE_NAMES[mode], bin_count=bins, two_level_binning=bool(two_level),
+        cb, ce, cf = r.take("<QdB")
+        calibration = Calibration(cb, ce, bool(cf), [r.take("<Qdd") for _ in range(r.take("<Q"))])
+    cfg = TrainConfig(calibration=co, n_trees=n_trees, mode=_MODE_NAMES[mode], bin_count=bins, two_level_binning=bool(two_level),
                       breakeven=be if has_be else None, bootstrap_fraction=frac,
                       max_depth=md if has_md else None, min_samples_split=mss, max_split_retries=retries,
                       n_workers=workers, seed=seed)
@@ -225,5 +228,5 @@ def load_model(path: str):
         raise RuntimeError(f"{path}: trailing bytes after model payload")
     f = Forest(np.array(tree_off, np.int64), np.array(left, np.int32), np.array(right, np.int32),
                np.array(pred, np.int32), np.array(thr, np.float32), np.array(term_off, np.int64),
-               np.array(feat, np.uint32), np.array(weight, np.float32), breakeven, k, n_features)
+               np.array(feat, np.uint32), np.array(weight, np.float32), breakeven, k, n_features, calibration)
     return f, cfg, names

@@ -188,6 +188,8 @@ class Oracle:
         if kind == "reference":
             L.orc_train_save_model.argtypes = [vp, vp, u64, u64, i32, p(OrcConfig), C.c_char_p]
             L.orc_load_model_summary.argtypes = [C.c_char_p, p(u64), p(u64)]
+            L.orc_train_forest_depths.argtypes = [vp, vp, u64, u64, i32, p(OrcConfig), vp, vp, u64, p(u64)]
+            L.orc_load_model_calibration.argtypes = [C.c_char_p, p(u64), p(i32), p(u64), p(u64), p(i32)]
         L.orc_find_node_split.restype = OrcSplit
         L.orc_find_node_split.argtypes = [vp, vp, u64, i32, vp, u64, vp, u64, vp, vp, i32, u64, u64, u64,
                                           p(u64), vp]
@@ -312,6 +314,26 @@ class Oracle:
         t, nn = C.c_uint64(), C.c_uint64()
         self._err(self.lib.orc_load_model_summary(path.encode(), C.byref(t), C.byref(nn)), "load_model")
         return t.value, nn.value
+
+    def train_forest_depths(self, X: np.ndarray, y: np.ndarray, k: int, cfg: OrcConfig):
+        """TrainInstrumentation::by_depth (nodes, samples) of the reference's train_forest."""
+        X = np.ascontiguousarray(X, np.float32)
+        y = np.ascontiguousarray(y, np.int32)
+        d, n = X.shape
+        cap = 4096
+        nodes, samples, nd = np.zeros(cap, np.uint64), np.zeros(cap, np.uint64), C.c_uint64()
+        self._err(self.lib.orc_train_forest_depths(X.ctypes.data, y.ctypes.data, n, d, k, C.byref(cfg),
+                                                   nodes.ctypes.data, samples.ctypes.data, cap, C.byref(nd)),
+                  "train_forest_depths")
+        return [int(v) for v in nodes[:nd.value]], [int(v) for v in samples[:nd.value]]
+
+    def load_model_calibration(self, path: str):
+        """(forest.breakeven, has_calibration, calibration.breakeven, n_samples, fallback) as the
+        reference's load_model reads them."""
+        be, hc, cb, ns, fb = C.c_uint64(), C.c_int32(), C.c_uint64(), C.c_uint64(), C.c_int32()
+        self._err(self.lib.orc_load_model_calibration(path.encode(), C.byref(be), C.byref(hc), C.byref(cb),
+                                                      C.byref(ns), C.byref(fb)), "load_model")
+        return be.value, bool(hc.value), cb.value, ns.value, bool(fb.value)
 
     # -- primitives --------------------------------------------------------------------------
     def split_mix64(self, x):

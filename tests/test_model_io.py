@@ -57,3 +57,23 @@ def test_load_model_round_trip_and_validation(tmp_path):
         model_io.load_model(bad)
     with pytest.raises(RuntimeError):
         ref.load_model_summary(bad)
+
+
+def test_calibration_record_read_by_reference_loader(tmp_path):
+    """A calibrated GPU forest stores Forest::calibration (model_io.hpp:155-157); the reference's
+    validating loader reads the record back (here a synthetic record on an oracle forest)."""
+    ref = oracle_lib.get("reference")
+    X, y = ref.generate_trunk(1200, 8, 2)
+    kw = dict(n_trees=2, mode="dynamic", breakeven=700, seed=4, n_workers=1)
+    flat = oracle_lib.get("port").train_forest(X, y, 2, oracle_lib.make_config(**kw))
+    f = _forest(flat, 2, 8)
+    f.calibration = model_io.Calibration(breakeven=700, elapsed_seconds=0.0123, fallback=False,
+                                         samples=[(64, 1e-6, 3e-6), (700, 5e-6, 6e-6), (65536, 9e-4, 2e-4)])
+    cfg = sofg.TrainConfig(n_trees=2, mode="dynamic", seed=4, n_workers=1)  # breakeven absent: calibrated
+    path = str(tmp_path / "cal.model")
+    model_io.save_model(f, cfg, path)
+    assert ref.load_model_calibration(path) == (700, True, 700, 3, False)
+    f2, cfg2, _ = model_io.load_model(path)
+    assert f2.calibration.samples == [(64, 1e-6, 3e-6), (700, 5e-6, 6e-6), (65536, 9e-4, 2e-4)]
+    assert cfg2.breakeven is None and cfg2.calibration.n_max == 65536
+    assert model_io.model_bytes(f2, cfg2) == open(path, "rb").read()
