@@ -159,6 +159,7 @@ int orc_load_model_summary(const char* path, uint64_t* n_trees, uint64_t* n_node
 int orc_train_forest_depths(const float* X, const int32_t* labels, uint64_t n_samples, uint64_t n_features,
                             int32_t class_count, const orc_config* cfg, uint64_t* nodes, uint64_t* samples,
                             uint64_t cap, uint64_t* n_depths);
+uint64_t orc_csv_number(double v, char* out, uint64_t cap);
 int orc_load_model_calibration(const char* path, uint64_t* breakeven, int32_t* has_cal,
                                uint64_t* cal_breakeven, uint64_t* n_samples, int32_t* fallback);
 

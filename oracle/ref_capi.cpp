@@ -7,6 +7,8 @@
 // ProjectionConfig::for_features at forest.hpp:257,295), which drives the reference's own
 // sample_projection_matrix / find_node_split / bootstrap_sample through a depth-first loop that
 // mirrors TreeGrower::grow_from (forest.hpp:157-240).
+#include <sstream>
+#include <soforest/bench.hpp>
 #include <soforest/soforest.hpp>
 
 #include <cstring>
@@ -474,4 +476,15 @@ extern "C" int orc_train_forest_depths(const float* X, const int32_t* y, uint64_
       samples[i] = instr.by_depth[i].samples;
     }
   });
+}
+
+// bench.hpp:36-40 number formatting (std::to_chars), for the CSV schema tests.
+extern "C" uint64_t orc_csv_number(double v, char* out, uint64_t cap) {
+  std::ostringstream os;
+  soforest::detail::csv_number(os, v);
+  const std::string s = os.str();
+  const uint64_t n = std::min<uint64_t>(s.size(), cap ? cap - 1 : 0);
+  std::memcpy(out, s.data(), n);
+  if (cap) out[n] = 0;
+  return s.size();
 }

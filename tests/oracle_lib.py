@@ -188,6 +188,8 @@ class Oracle:
         if kind == "reference":
             L.orc_train_save_model.argtypes = [vp, vp, u64, u64, i32, p(OrcConfig), C.c_char_p]
             L.orc_load_model_summary.argtypes = [C.c_char_p, p(u64), p(u64)]
+            L.orc_csv_number.restype = u64
+            L.orc_csv_number.argtypes = [C.c_double, C.c_char_p, u64]
             L.orc_train_forest_depths.argtypes = [vp, vp, u64, u64, i32, p(OrcConfig), vp, vp, u64, p(u64)]
             L.orc_load_model_calibration.argtypes = [C.c_char_p, p(u64), p(i32), p(u64), p(u64), p(i32)]
         L.orc_find_node_split.restype = OrcSplit
@@ -314,6 +316,11 @@ class Oracle:
         t, nn = C.c_uint64(), C.c_uint64()
         self._err(self.lib.orc_load_model_summary(path.encode(), C.byref(t), C.byref(nn)), "load_model")
         return t.value, nn.value
+
+    def csv_number(self, v: float) -> str:
+        buf = C.create_string_buffer(64)
+        self.lib.orc_csv_number(float(v), buf, 64)
+        return buf.value.decode()
 
     def train_forest_depths(self, X: np.ndarray, y: np.ndarray, k: int, cfg: OrcConfig):
         """TrainInstrumentation::by_depth (nodes, samples) of the reference's train_forest."""

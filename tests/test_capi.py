@@ -64,6 +64,11 @@ def test_default_config_mirrors_reference_train_config(lib):
     # forest.hpp:38-53 defaults
     assert (c.n_trees, c.mode, c.bin_count, c.min_samples_split, c.max_split_retries, c.seed) == (100, 2, 256, 2, 1, 0)
     assert abs(c.bootstrap_fraction - 0.632) < 1e-15 and c.has_breakeven == 0 and c.has_max_depth == 0
+    # calibrate.hpp:22-32 CalibrationOptions defaults
+    k = c.calibration
+    assert (k.n_min, k.n_max, k.bin_count, k.two_level, k.repetitions, k.seed) == (64, 65536, 256, 1, 5,
+                                                                                  0xCA11B8A7E5EED)
+    assert k.budget_seconds == 0.1 and c.instrument == 0
 
 
 def test_no_gpu_fails_loudly(lib):
