@@ -348,7 +348,8 @@ void WaveRunner::submit(const WaveSpec& w) {
     const size_t abytes = aug_bytes(total_terms, uint32_t(N), R, w.d);
     void* d_aug = aug_.ensure(abytes);
     pend_sweep_bytes_ = double(D.n) * double(D.ldr) * 4.0 + double(g_total) * 4.0 + double(abytes);
-    cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, st_), "aug_build");
+    uint16_t* d_qs = qsplit_.ensure(size_t(N) * 4);
+    cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, d_qs, st_), "aug_build");
     mark("sweep_prep");
     if (uint64_t(N) > stats.sweep_widest_nodes) {
       stats.sweep_widest_nodes = uint64_t(N);
@@ -358,12 +359,14 @@ void WaveRunner::submit(const WaveSpec& w) {
     // the chunked kernel below it for sparse waves.
     static const double pipe_min = std::getenv("SOFG_SWEEP_PIPE_MIN") ? std::atof(std::getenv("SOFG_SWEEP_PIPE_MIN")) : 16.0;
     const double pairs_per_sample = double(g_total / vpitch(R)) / double(D.n);
-    const bool pipe = pairs_per_sample >= pipe_min && row_sweep_pipe_fits(D.ldr, w.B, R);
+    // (pair records hold 32-bit V block (/ 8) and term-list offsets)
+    const bool pipe = pairs_per_sample >= pipe_min && row_sweep_pipe_fits(D.ldr, w.B, R) &&
+                      g_total / 8 < (uint64_t(1) << 32) && abytes / (aug_narrow(w.d) ? 2 : 4) < (uint64_t(1) << 32);
     if (pipe) {
       const uint32_t PB = (w.B + 1u) & ~1u;
       void* d_recs = recs_.ensure(size_t(D.n) * PB * pair_rec_bytes());
       uint32_t* d_pcnt = pcnt_.ensure(size_t(D.n));
-      cuda_check(launch_pair_build(w.inv, w.B, uint32_t(D.n), d_pos_node, d_nodes, d_gbase, R, w.d, d_recs,
+      cuda_check(launch_pair_build(w.inv, w.B, uint32_t(D.n), d_pos_node, d_nodes, d_gbase, d_qs, R, w.d, d_recs,
                                    d_pcnt, n_sm_, st_),
                  "pair_build");
       mark("pair_build");
@@ -373,7 +376,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       launches += 4;
     } else {
       cuda_check(launch_row_sweep(D.XR.p, D.ldr, uint32_t(D.n), w.inv, w.B, d_pos_node, d_nodes,
-                                  d_gbase, d_aug, R, w.d, d_G, n_sm_, st_),
+                                  d_gbase, d_aug, d_qs, R, w.d, d_G, n_sm_, st_),
                  "row_sweep");
       launches += 3;
     }

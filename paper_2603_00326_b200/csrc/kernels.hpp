@@ -66,7 +66,7 @@ cudaError_t launch_pos_fill(const NodeIn* nodes, const Tile* tiles, int n_tiles,
 size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d);
 cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
                              const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
-                             cudaStream_t st);
+                             uint16_t* qsplit, cudaStream_t st);
 size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R);
 void row_sweep_variant(uint32_t B, uint32_t d, uint32_t* cta_threads, uint32_t* entry_bytes);
 bool aug_narrow(uint32_t d);  // 16-bit term entries (d < 8192)
@@ -74,16 +74,16 @@ bool aug_narrow(uint32_t d);  // 16-bit term entries (d < 8192)
 bool row_sweep_pipe_fits(uint64_t ldr, uint32_t B, uint32_t R);
 size_t pair_rec_bytes();
 cudaError_t launch_pair_build(const uint32_t* inv, uint32_t B, uint32_t N, const uint32_t* pos_node,
-                              const NodeIn* nodes, const uint64_t* vbase, uint32_t R,
-                              uint32_t d, void* recs, uint32_t* pcnt, int n_sm,
+                              const NodeIn* nodes, const uint64_t* vbase, const uint16_t* qsplit,
+                              uint32_t R, uint32_t d, void* recs, uint32_t* pcnt, int n_sm,
                               cudaStream_t st);
 cudaError_t launch_row_sweep_pipe(const float* XR, uint64_t ldr, uint32_t N, const void* recs,
                                   const uint32_t* pcnt, uint32_t B, const void* aug, uint32_t R,
                                   uint32_t d, float* V, int n_sm, cudaStream_t st);
 cudaError_t launch_row_sweep(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
                              uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
-                             const uint64_t* vbase, const void* aug, uint32_t R, uint32_t d,
-                             float* V, int n_sm, cudaStream_t st);
+                             const uint64_t* vbase, const void* aug, const uint16_t* qsplit, uint32_t R,
+                             uint32_t d, float* V, int n_sm, cudaStream_t st);
 cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_tiles,
                                   const uint64_t* vbase, const uint32_t* terms,
                                   const uint32_t* row_ptr, uint32_t R, uint32_t zmax,

@@ -90,7 +90,8 @@ template <typename E>
 __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ nodes, int n_nodes,
                                                    const uint32_t* __restrict__ terms,
                                                    const uint32_t* __restrict__ row_ptr, uint32_t R,
-                                                   uint32_t d, E* __restrict__ aug) {
+                                                   uint32_t d, E* __restrict__ aug,
+                                                   uint16_t* __restrict__ qsplit) {
   constexpr uint32_t A = 16 / sizeof(E);
   extern __shared__ uint32_t s_empty_pre[];  // [4 warps][R + 1]: empty rows before row r
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -111,10 +112,33 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
   }
   if (lane == 0) epre[R] = carry;
   __syncwarp();
+  // Quarter boundaries balanced by entry count: entries before row r are
+  // E(r) = (rp[r] - rp[0]) + epre[r] (strictly increasing: every row has >= 1 entry); quarter c
+  // starts at the first row with E(r) >= c * T / kQ.
+  const uint32_t rp0 = __ldg(rp);
+  const uint32_t T = (__ldg(rp + R) - rp0) + carry;
+  uint32_t qs[kQ + 1];
+  qs[0] = 0;
+  qs[kQ] = R;
+#pragma unroll
+  for (int c = 1; c < kQ; ++c) {
+    const uint32_t target = (uint32_t(c) * T + kQ / 2) / kQ;
+    uint32_t below = 0;
+    for (uint32_t r0 = 0; r0 <= R; r0 += 32) {
+      const uint32_t r = r0 + uint32_t(lane);
+      const bool lt = r <= R && (__ldg(rp + r) - rp0) + epre[r] < target;
+      below += __popc(__ballot_sync(0xffffffffu, lt));
+    }
+    qs[c] = min(below, R);
+  }
+  if (lane < kQ) qsplit[size_t(node) * kQ + lane] = uint16_t(lane + 1 < kQ ? qs[lane + 1] : R);
   // element e of list c -> entry ((e / A) * kQ + c) * A + e % A of the node block
   auto at = [&](uint32_t c, uint32_t e) { return ((e / A) * kQ + c) * A + (e % A); };
   for (uint32_t r = uint32_t(lane); r < R; r += 32) {
-    const uint32_t c = q_of(R, r), ra = q_row(R, c);
+    uint32_t c = 0;
+#pragma unroll
+    for (int cc = 1; cc < kQ; ++cc) c += r >= qs[cc] ? 1u : 0u;
+    const uint32_t ra = qs[c];
     const uint32_t q0 = __ldg(rp + r), q1 = __ldg(rp + r + 1);
     const uint32_t e0 = (q0 - __ldg(rp + ra)) + (epre[r] - epre[ra]);
     if (q1 == q0) {
@@ -129,7 +153,7 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
   // neutral entries up to the end of each list's last chunk
 #pragma unroll
   for (int c = 0; c < kQ; ++c) {
-    const uint32_t ra = q_row(R, uint32_t(c)), rb = q_row(R, uint32_t(c + 1));
+    const uint32_t ra = qs[c], rb = qs[c + 1];
     const uint32_t len = (__ldg(rp + rb) - __ldg(rp + ra)) + (epre[rb] - epre[ra]);
     for (uint32_t e = len + uint32_t(lane); e < (len + A - 1) / A * A; e += 32) out[at(uint32_t(c), e)] = E(d << 2);
   }
@@ -163,20 +187,22 @@ __global__ void __launch_bounds__(NT) k_row_sweep(
     const float* __restrict__ XR, uint64_t ldr, uint32_t N, uint32_t K,
     const uint32_t* __restrict__ inv, uint32_t B, const uint32_t* __restrict__ pos_node,
     const NodeIn* __restrict__ nodes, const uint64_t* __restrict__ vbase,
-    const E* __restrict__ aug, uint32_t R, float* __restrict__ V) {
+    const E* __restrict__ aug, const uint16_t* __restrict__ qsplit, uint32_t R, float* __restrict__ V) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* xs = reinterpret_cast<float*>(smem_raw);
   Pair* pairs = reinterpret_cast<Pair*>(smem_raw + size_t(K) * ldr * 4);
-  const uint32_t pitch = sweep_out_pitch(R);
-  float* sout = reinterpret_cast<float*>(pairs + size_t(K) * B) + size_t(threadIdx.x) * pitch;
-  __shared__ uint32_t s_cnt;
+  const uint32_t pitch = stage_pitch(R);
+  constexpr uint32_t P = 32u / kQ;
   const int lane = threadIdx.x & 31;
+  float* wstage = reinterpret_cast<float*>(pairs + size_t(K) * B) + size_t(threadIdx.x >> 5) * P * pitch;
+  __shared__ uint32_t s_cnt;
   const uint32_t Rp = vpitch(R);
   const uint32_t nvec = uint32_t(ldr / 4);
   const uint32_t KB = K * B;
   const uint32_t c = threadIdx.x % kQ;  // my sub-list
-  const uint32_t ra = q_row(R, c), rb = q_row(R, c + 1);
   constexpr uint32_t kPairsPerRound = NT / kQ;
+  for (uint32_t i = uint32_t(lane); i < P * (Rp - R); i += 32)  // pad rows of the staging stay zero
+    wstage[(i / (Rp - R)) * pitch + R + i % (Rp - R)] = 0.f;
 
   for (uint32_t s0 = blockIdx.x * K; s0 < N; s0 += gridDim.x * K) {
     if (threadIdx.x == 0) s_cnt = 0;
@@ -210,7 +236,7 @@ __global__ void __launch_bounds__(NT) k_row_sweep(
     const uint32_t rounds = (cnt + kPairsPerRound - 1) / kPairsPerRound;  // uniform
     for (uint32_t rd = 0; rd < rounds; ++rd) {
       const uint32_t pi = rd * kPairsPerRound + threadIdx.x / kQ;
-      uint32_t r = rb;  // rows done (this lane's range [ra, rb))
+      uint32_t ra = 0, rb = 0;  // this lane's rows (none when the slot is empty)
       const uint4* a4 = reinterpret_cast<const uint4*>(aug);
       const char* xb = reinterpret_cast<const char*>(xs);
       uint64_t vout = 0;
@@ -219,14 +245,14 @@ __global__ void __launch_bounds__(NT) k_row_sweep(
         a4 = reinterpret_cast<const uint4*>(aug + aug_off<E>(__ldg(&nodes[pr.node].term_off), pr.node, R)) + c;
         xb = reinterpret_cast<const char*>(xs + size_t(pr.k) * ldr);
         vout = __ldg(vbase + pr.node) + uint64_t(pr.j) * Rp;
-        r = ra;
+        quarter_rows(qsplit + size_t(pr.node) * kQ, c, R, ra, rb);
       }
-      const uint32_t out_base = uint32_t(__cvta_generic_to_shared(sout)) - ra * 4u;
-      walk_rows<E>(a4, xb, r, rb, out_base);
+      const uint32_t out_base = uint32_t(__cvta_generic_to_shared(wstage + (uint32_t(lane) / kQ) * pitch));
+      walk_rows<E>(a4, xb, ra, rb, out_base);
       __syncwarp();
       const uint32_t p_warp = rd * kPairsPerRound + (threadIdx.x & ~31u) / kQ;  // the warp's first pair
-      const uint32_t np = cnt > p_warp ? min(32u / kQ, cnt - p_warp) : 0u;
-      write_pairs(sout - size_t(lane) * pitch, pitch, R, np, V, vout, lane);
+      const uint32_t np = cnt > p_warp ? min(P, cnt - p_warp) : 0u;
+      write_pairs(wstage, pitch, Rp, np, V, vout, lane);
       __syncwarp();
     }
     __syncthreads();
@@ -348,15 +374,16 @@ size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d)
 
 cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
                              const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
-                             cudaStream_t st) {
+                             uint16_t* qsplit, cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
+  if (R > 65535) return cudaErrorInvalidValue;
   const size_t smem = size_t(4) * (R + 1) * 4;
   if (aug_narrow(d))
     dev::k_aug_build<uint16_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
-        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint16_t*>(aug));
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint16_t*>(aug), qsplit);
   else
     dev::k_aug_build<uint32_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
-        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint32_t*>(aug));
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint32_t*>(aug), qsplit);
   return cudaGetLastError();
 }
 
@@ -368,7 +395,7 @@ static int sweep_threads(uint32_t B) {
 
 static size_t sweep_smem_k(uint64_t ldr, uint32_t B, uint32_t R, uint32_t K) {
   return size_t(K) * ldr * 4 + size_t(K) * B * sizeof(dev::Pair) +
-         size_t(sweep_threads(B)) * dev::sweep_out_pitch(R) * 4;
+         size_t(sweep_threads(B) / 32) * (32 / dev::kQ) * dev::stage_pitch(R) * 4;
 }
 
 // Samples per CTA iteration: enough (node, sample) pairs to fill the CTA's lanes (a sample sits
@@ -397,7 +424,7 @@ size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R) {
 template <typename E, int NT>
 static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
                                   uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
-                                  const uint64_t* vbase, const void* aug,
+                                  const uint64_t* vbase, const void* aug, const uint16_t* qsplit,
                                   uint32_t R, float* V, int n_sm, cudaStream_t st) {
   const uint32_t K = sweep_k(ldr, B, R);
   const size_t smem = sweep_smem_k(ldr, B, R, K);
@@ -410,20 +437,20 @@ static cudaError_t launch_sweep_t(const float* XR, uint64_t ldr, uint32_t N, con
   const uint32_t groups = (N + K - 1) / K;
   const unsigned grid = unsigned(std::max(1, std::min<int>(int(groups), n_sm * std::max(per_sm, 1))));
   dev::k_row_sweep<E, NT><<<grid, NT, smem, st>>>(
-      XR, ldr, N, K, inv, B, pos_node, nodes, vbase, static_cast<const E*>(aug), R, V);
+      XR, ldr, N, K, inv, B, pos_node, nodes, vbase, static_cast<const E*>(aug), qsplit, R, V);
   return cudaGetLastError();
 }
 
 cudaError_t launch_row_sweep(const float* XR, uint64_t ldr, uint32_t N, const uint32_t* inv,
                              uint32_t B, const uint32_t* pos_node, const NodeIn* nodes,
-                             const uint64_t* vbase, const void* aug, uint32_t R,
+                             const uint64_t* vbase, const void* aug, const uint16_t* qsplit, uint32_t R,
                              uint32_t d, float* V, int n_sm, cudaStream_t st) {
   const bool wide = sweep_threads(B) == 256;
   if (aug_narrow(d))
-    return wide ? launch_sweep_t<uint16_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st)
-                : launch_sweep_t<uint16_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st);
-  return wide ? launch_sweep_t<uint32_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st)
-              : launch_sweep_t<uint32_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, R, V, n_sm, st);
+    return wide ? launch_sweep_t<uint16_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qsplit, R, V, n_sm, st)
+                : launch_sweep_t<uint16_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qsplit, R, V, n_sm, st);
+  return wide ? launch_sweep_t<uint32_t, 256>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qsplit, R, V, n_sm, st)
+              : launch_sweep_t<uint32_t, 128>(XR, ldr, N, inv, B, pos_node, nodes, vbase, aug, qsplit, R, V, n_sm, st);
 }
 
 cudaError_t launch_project_gather(const NodeIn* nodes, const Tile* tiles, int n_tiles,

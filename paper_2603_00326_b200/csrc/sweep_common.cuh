@@ -12,15 +12,18 @@ namespace dev {
 
 // ------------------------------------------------------------------------------------------
 // Augmented term lists for the sweep. A node's R rows are split into kQ contiguous row ranges
-// ("quarters", rows [q_row(R, c), q_row(R, c + 1))); each range gets its own list: the CSR terms
-// of its rows in order, each entry feature << 2 | last << 1 | negative (so entry & ~3 is the
-// feature's byte offset in a row of XR), with one dummy entry (feature d: the zero pad column of
-// XR) for every empty row, so walking a list completes its rows in order. Entries are u16 when
+// ("quarters"; quarter c = rows [qs_c, qs_{c+1}) with qs_0 = 0, qs_kQ = R), each with its own list:
+// the CSR terms of its rows in order, each entry feature << 2 | last << 1 | negative (so entry & ~3
+// is the feature's byte offset in a row of XR), with one dummy entry (feature d: the zero pad
+// column of XR) for every empty row, so walking a list completes its rows in order. The quarter
+// boundaries are chosen per node (k_aug_build) so the kQ lists hold about the same number of
+// entries — the kQ lanes of a (node, sample) pair then finish together. Entries are u16 when
 // d < 8192, else u32. The kQ lists of a node are interleaved in 16-byte chunks — chunk i of list
 // c at chunk index i * kQ + c of the node's block — so the kQ lanes that walk one (node, sample)
 // pair read one contiguous 64-byte span per step. A list's last chunk is filled up with neutral
 // entries (zero column, no row end); chunks past a list's end are never consumed.
-// Node i's block starts at entry aug_off(term_off_i, i, R).
+// Node i's block starts at entry aug_off(term_off_i, i, R); its boundaries qs_1..qs_{kQ-1} are
+// qsplit[i * kQ + 0 .. kQ - 2] (u16; qsplit[i * kQ + kQ - 1] = R).
 // ------------------------------------------------------------------------------------------
 constexpr int kQ = 4;
 
@@ -29,9 +32,12 @@ __host__ __device__ __forceinline__ uint64_t aug_off(uint32_t term_off, uint32_t
   constexpr uint64_t A = 16 / sizeof(E), CH = kQ * A;
   return (kQ * (uint64_t(term_off) + uint64_t(i) * (R + 2 * A)) + CH - 1) / CH * CH;
 }
-__host__ __device__ __forceinline__ uint32_t q_row(uint32_t R, uint32_t c) { return R * c / kQ; }
-// quarter holding row r: the largest c with q_row(R, c) <= r
-__host__ __device__ __forceinline__ uint32_t q_of(uint32_t R, uint32_t r) { return (kQ * (r + 1) - 1) / R; }
+// rows [ra, rb) of quarter c from the node's boundaries (qsplit layout above)
+__device__ __forceinline__ void quarter_rows(const uint16_t* q, uint32_t c, uint32_t R, uint32_t& ra,
+                                             uint32_t& rb) {
+  ra = c == 0 ? 0u : uint32_t(q[c - 1]);
+  rb = c + 1 == kQ ? R : uint32_t(q[c]);
+}
 
 template <typename E>
 __device__ __forceinline__ void unpack16(const uint4& v, uint32_t (&e)[16 / sizeof(E)]) {
@@ -50,38 +56,27 @@ __device__ __forceinline__ void unpack16(const uint4& v, uint32_t (&e)[16 / size
   }
 }
 
-// Per-lane staging of completed rows: an odd number of floats per lane, so lanes storing the same
-// row index hit distinct banks.
-__host__ __device__ __forceinline__ uint32_t sweep_out_pitch(uint32_t R) { return ((R + kQ - 1) / kQ) | 1u; }
+// Staging of completed rows, per (node, sample) pair: pair p of a warp at stage + p * pitch
+// floats, row r at + r; rows [R, vpitch(R)) stay zero. pitch = 4 (mod 32) words spreads the 8 pairs
+// of a warp over the banks.
+__host__ __device__ __forceinline__ uint32_t stage_pitch(uint32_t R) { return (vpitch(R) + 31u) / 32u * 32u + 4u; }
 
-// Warp write-out of the warp's np = 32 / kQ (or fewer) pairs: lane l's staging slot (stage +
-// l * pitch) holds rows [q_row(R, l % kQ), q_row(R, l % kQ + 1)) of pair l / kQ, whose rows go to
-// V + vout (16-byte aligned; every lane passes its own pair's vout). float4 stores over each
-// pair's contiguous R floats, so a warp store instruction covers whole 128-byte lines.
-__device__ __forceinline__ void write_pairs(const float* stage, uint32_t pitch, uint32_t R, uint32_t np,
+// Warp write-out of the warp's np = 32 / kQ (or fewer) staged pairs to V: pair p's vpitch(R)
+// floats go to V + vout_p (vout_p = the vout of lane p * kQ; 32-byte aligned) as float4 copies, so
+// a warp store instruction covers whole 128-byte lines. The pair index of a float4 comes from a
+// multiply-high by the reciprocal (exact for the f < 2^32 / R4 used here), not a division.
+__device__ __forceinline__ void write_pairs(const float* stage, uint32_t pitch, uint32_t Rp, uint32_t np,
                                             float* V, uint64_t vout, int lane) {
-  const uint32_t R4 = R / 4, tail = R - 4 * R4;
+  const uint32_t R4 = Rp / 4;
+  const uint32_t magic = 0xffffffffu / R4 + 1u;
   constexpr uint32_t P = 32u / kQ;
   for (uint32_t f0 = 0; f0 < P * R4; f0 += 32) {  // uniform trip count (the shuffle needs all lanes)
     const uint32_t f = f0 + uint32_t(lane);
-    const uint32_t p = f / R4, r0 = 4 * (f - p * R4);
+    const uint32_t p = __umulhi(f, magic);
     const uint64_t vo = __shfl_sync(0xffffffffu, vout, int(p * kQ) & 31);
     if (f >= P * R4 || p >= np) continue;
-    float v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t r = r0 + uint32_t(u), c = q_of(R, r);
-      v[u] = stage[(p * kQ + c) * pitch + (r - q_row(R, c))];
-    }
-    *reinterpret_cast<float4*>(V + vo + r0) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-  for (uint32_t f0 = 0; f0 < P * tail; f0 += 32) {
-    const uint32_t f = f0 + uint32_t(lane);
-    const uint32_t p = f / tail, r = 4 * R4 + (f - p * tail);
-    const uint64_t vo = __shfl_sync(0xffffffffu, vout, int(p * kQ) & 31);
-    if (f >= P * tail || p >= np) continue;
-    const uint32_t c = q_of(R, r);
-    V[vo + r] = stage[(p * kQ + c) * pitch + (r - q_row(R, c))];
+    const uint32_t r0 = 4 * (f - p * R4);
+    *reinterpret_cast<float4*>(V + vo + r0) = *reinterpret_cast<const float4*>(stage + p * pitch + r0);
   }
 }
 
@@ -101,8 +96,10 @@ __device__ __forceinline__ void walk_rows(const uint4* __restrict__ a4, const ch
   constexpr int EPV = 16 / sizeof(E);  // entries per 16-byte load
   double acc = 0.0;
   bool first = true;
+  uint32_t oa = out_base + 4u * r;  // shared address of the next row to close
+  const uint32_t oe = out_base + 4u * rb;
   auto consume = [&](const uint4& q) {
-    if (r >= rb) return;
+    if (oa >= oe) return;
     uint32_t e[EPV];
     unpack16<E>(q, e);
     uint32_t xv[EPV];
@@ -116,21 +113,21 @@ __device__ __forceinline__ void walk_rows(const uint4* __restrict__ a4, const ch
       first = (e[u] & 2u) != 0u;
       if (first) {
         const float v = __double2float_rn(acc);
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(out_base + r * 4u), "f"(v) : "memory");
-        ++r;
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(oa), "f"(v) : "memory");
+        oa += 4u;
       }
     }
   };
   uint4 A0 = make_uint4(0, 0, 0, 0), A1 = A0, A2 = A0, A3 = A0, B0 = A0, B1 = A0, B2 = A0, B3 = A0;
-  if (r < rb) {
+  if (oa < oe) {
     A0 = __ldg(a4);
     A1 = __ldg(a4 + kQ);
     A2 = __ldg(a4 + 2 * kQ);
     A3 = __ldg(a4 + 3 * kQ);
   }
   for (uint32_t it = 4 * kQ;; it += 8 * kQ) {
-    if (!__any_sync(0xffffffffu, r < rb)) break;
-    if (r < rb) {
+    if (!__any_sync(0xffffffffu, oa < oe)) break;
+    if (oa < oe) {
       B0 = __ldg(a4 + it);
       B1 = __ldg(a4 + it + kQ);
       B2 = __ldg(a4 + it + 2 * kQ);
@@ -140,8 +137,8 @@ __device__ __forceinline__ void walk_rows(const uint4* __restrict__ a4, const ch
     consume(A1);
     consume(A2);
     consume(A3);
-    if (!__any_sync(0xffffffffu, r < rb)) break;
-    if (r < rb) {
+    if (!__any_sync(0xffffffffu, oa < oe)) break;
+    if (oa < oe) {
       A0 = __ldg(a4 + it + 4 * kQ);
       A1 = __ldg(a4 + it + 5 * kQ);
       A2 = __ldg(a4 + it + 6 * kQ);

@@ -32,8 +32,9 @@ namespace sofg {
 namespace dev {
 
 struct PairRec {
-  uint64_t vout;  // float index of the pair's row block in V
-  uint64_t aug;   // entry index of the node's block of interleaved term lists
+  uint32_t vout8;         // float index of the pair's row block in V, / 8 (blocks are 32-byte aligned)
+  uint32_t aug;           // entry index of the node's block of interleaved term lists
+  uint16_t q[kQ];         // the node's quarter boundaries (qsplit, sweep_common.cuh)
 };
 static_assert(sizeof(PairRec) == 16, "PairRec layout");
 
@@ -81,7 +82,8 @@ template <typename E>
 __global__ void __launch_bounds__(256) k_pair_build(const uint32_t* __restrict__ inv, uint32_t B,
                                                     uint32_t N, const uint32_t* __restrict__ pos_node,
                                                     const NodeIn* __restrict__ nodes,
-                                                    const uint64_t* __restrict__ vbase, uint32_t R,
+                                                    const uint64_t* __restrict__ vbase,
+                                                    const uint16_t* __restrict__ qsplit, uint32_t R,
                                                     uint32_t PB, PairRec* __restrict__ recs,
                                                     uint32_t* __restrict__ pcnt) {
   const int lane = threadIdx.x & 31;
@@ -100,11 +102,14 @@ __global__ void __launch_bounds__(256) k_pair_build(const uint32_t* __restrict__
       const unsigned m = __ballot_sync(0xffffffffu, act);
       if (act) {
         const uint32_t j = p - __ldg(&nodes[node].begin);
-        PairRec rec;
-        rec.vout = __ldg(vbase + node) + uint64_t(j) * Rp;
-        rec.aug = aug_off<E>(__ldg(&nodes[node].term_off), node, R);
+        const uint2 qv = __ldg(reinterpret_cast<const uint2*>(qsplit) + node);
+        uint4 rec;
+        rec.x = uint32_t((__ldg(vbase + node) + uint64_t(j) * Rp) >> 3);
+        rec.y = uint32_t(aug_off<E>(__ldg(&nodes[node].term_off), node, R));
+        rec.z = qv.x;
+        rec.w = qv.y;
         const uint32_t idx = cnt + __popc(m & ((1u << lane) - 1u));
-        *reinterpret_cast<uint4*>(recs + uint64_t(s) * PB + idx) = *reinterpret_cast<const uint4*>(&rec);
+        *reinterpret_cast<uint4*>(recs + uint64_t(s) * PB + idx) = rec;
       }
       cnt += __popc(m);
     }
@@ -128,10 +133,12 @@ __global__ void __launch_bounds__((kPipeConsumers + 1) * 32, 1) k_row_sweep_pipe
   uint4* queue = reinterpret_cast<uint4*>(empty + S);
   uint32_t* done = reinterpret_cast<uint32_t*>(queue + QN);
   uint32_t* ticket = done + S;
-  const uint32_t pitch = sweep_out_pitch(R);
+  const uint32_t pitch = stage_pitch(R);
+  constexpr uint32_t P = 32u / kQ;
   float* stage_out = reinterpret_cast<float*>(smem_raw) +
                      ((reinterpret_cast<unsigned char*>(ticket + 1) - smem_raw + 15) / 16) * 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t Rp = vpitch(R);
 
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < S; ++i) {
@@ -164,9 +171,10 @@ __global__ void __launch_bounds__((kPipeConsumers + 1) * 32, 1) k_row_sweep_pipe
       bulk_g2s(rows + size_t(slot) * ldr, XR + uint64_t(s) * ldr, row_bytes, full + slot);
       bulk_g2s(recs + size_t(slot) * PB, recs_g + uint64_t(s) * PB, cnt * uint32_t(sizeof(PairRec)),
                full + slot);
+      const uint32_t ticket_stage = slot | ((k & 1u) << 16);  // slot and full-barrier parity
       for (uint32_t p0 = 0; p0 < cnt; p0 += kChunkPairs, ++t) {
         volatile uint32_t* q = vq + 4 * (t % QN);
-        q[1] = stage;
+        q[1] = ticket_stage;
         q[2] = p0 | (min(kChunkPairs, cnt - p0) << 16);
         q[3] = cnt;
         __threadfence_block();
@@ -185,9 +193,10 @@ __global__ void __launch_bounds__((kPipeConsumers + 1) * 32, 1) k_row_sweep_pipe
 
   // ------------------------------------------------------------------------------ consumers
   const uint32_t c = uint32_t(lane) % kQ;  // my sub-list
-  const uint32_t ra = q_row(R, c), rb = q_row(R, c + 1);
-  float* sout = stage_out + size_t(threadIdx.x) * pitch;
-  const uint32_t out_base = smem_u32(sout) - ra * 4u;
+  float* wstage = stage_out + size_t(warp) * P * pitch;
+  for (uint32_t i = uint32_t(lane); i < P * (Rp - R); i += 32)  // pad rows of the staging stay zero
+    wstage[(i / (Rp - R)) * pitch + R + i % (Rp - R)] = 0.f;
+  const uint32_t out_base = smem_u32(wstage + (uint32_t(lane) / kQ) * pitch);
   for (;;) {
     uint32_t T = 0;
     if (lane == 0) T = atomicAdd(ticket, 1u);
@@ -205,23 +214,25 @@ __global__ void __launch_bounds__((kPipeConsumers + 1) * 32, 1) k_row_sweep_pipe
     if (stg == kEndStage) break;
     pn = __shfl_sync(0xffffffffu, pn, 0);
     cnt = __shfl_sync(0xffffffffu, cnt, 0);
-    const uint32_t slot = stg % S;
-    mbar_wait(full + slot, (stg / S) & 1u);
+    const uint32_t slot = stg & 0xffffu;
+    mbar_wait(full + slot, stg >> 16);
     const uint32_t p0 = pn & 0xffffu, np = pn >> 16;
     const uint32_t pl = uint32_t(lane) / kQ;
     const bool act = pl < np;
-    uint32_t r = rb;
+    uint32_t ra = 0, rb = 0;
     const uint4* a4 = reinterpret_cast<const uint4*>(aug);
     uint64_t vout = 0;
     if (act) {
-      const PairRec& pr = recs[size_t(slot) * PB + p0 + pl];
-      a4 = reinterpret_cast<const uint4*>(aug + pr.aug) + c;
-      vout = pr.vout;
-      r = ra;
+      const uint4 pr = *reinterpret_cast<const uint4*>(recs + size_t(slot) * PB + p0 + pl);
+      a4 = reinterpret_cast<const uint4*>(aug + pr.y) + c;
+      vout = uint64_t(pr.x) << 3;
+      const uint64_t qv = uint64_t(pr.z) | (uint64_t(pr.w) << 32);  // qsplit: starts of quarters 1..3, R
+      ra = c ? uint32_t(qv >> (16 * (c - 1))) & 0xffffu : 0u;
+      rb = uint32_t(qv >> (16 * c)) & 0xffffu;
     }
-    walk_rows<E>(a4, reinterpret_cast<const char*>(rows + size_t(slot) * ldr), r, rb, out_base);
+    walk_rows<E>(a4, reinterpret_cast<const char*>(rows + size_t(slot) * ldr), ra, rb, out_base);
     __syncwarp();
-    write_pairs(sout - size_t(lane) * pitch, pitch, R, np, V, vout, lane);
+    write_pairs(wstage, pitch, Rp, np, V, vout, lane);
     __syncwarp();
     if (lane == 0) {
       const uint32_t before = atomicAdd(done + slot, np);
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__((kPipeConsumers + 1) * 32, 1) k_row_sweep_pipe
 
 namespace {
 size_t pipe_fixed_smem(uint32_t R, uint32_t QN) {
-  return size_t(QN) * 16 + 256 + size_t(dev::kPipeConsumers) * 32 * dev::sweep_out_pitch(R) * 4;
+  return size_t(QN) * 16 + 256 + size_t(dev::kPipeConsumers) * (32 / dev::kQ) * dev::stage_pitch(R) * 4;
 }
 size_t pipe_stage_bytes(uint64_t ldr, uint32_t PB) { return size_t(ldr) * 4 + size_t(PB) * sizeof(dev::PairRec) + 16 + 4; }
 uint32_t pipe_pb(uint32_t B) { return (B + 1u) & ~1u; }
@@ -259,15 +270,15 @@ bool row_sweep_pipe_fits(uint64_t ldr, uint32_t B, uint32_t R) { return pipe_sta
 size_t pair_rec_bytes() { return sizeof(dev::PairRec); }
 
 cudaError_t launch_pair_build(const uint32_t* inv, uint32_t B, uint32_t N, const uint32_t* pos_node,
-                              const NodeIn* nodes, const uint64_t* vbase, uint32_t R, uint32_t d,
-                              void* recs, uint32_t* pcnt, int n_sm, cudaStream_t st) {
+                              const NodeIn* nodes, const uint64_t* vbase, const uint16_t* qsplit, uint32_t R,
+                              uint32_t d, void* recs, uint32_t* pcnt, int n_sm, cudaStream_t st) {
   const uint32_t PB = pipe_pb(B);
   const unsigned grid = unsigned(std::min<uint64_t>((uint64_t(N) + 7) / 8, uint64_t(n_sm) * 16));
   if (aug_narrow(d))
-    dev::k_pair_build<uint16_t><<<grid, 256, 0, st>>>(inv, B, N, pos_node, nodes, vbase, R, PB,
+    dev::k_pair_build<uint16_t><<<grid, 256, 0, st>>>(inv, B, N, pos_node, nodes, vbase, qsplit, R, PB,
                                                       static_cast<dev::PairRec*>(recs), pcnt);
   else
-    dev::k_pair_build<uint32_t><<<grid, 256, 0, st>>>(inv, B, N, pos_node, nodes, vbase, R, PB,
+    dev::k_pair_build<uint32_t><<<grid, 256, 0, st>>>(inv, B, N, pos_node, nodes, vbase, qsplit, R, PB,
                                                       static_cast<dev::PairRec*>(recs), pcnt);
   return cudaGetLastError();
 }
