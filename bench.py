@@ -126,28 +126,35 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def committed_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu launch list of this bench command
-    (profiles/r*_launches_bench_summary.json, written by tools/launch_summary.py)."""
+def step_profile_key(args):
+    return {"n": args.n, "d": args.d, "trees": args.trees, "mode": args.mode, "breakeven": args.breakeven,
+            "classes": args.classes, "density": args.density}
+
+
+def committed_step_profile(args):
+    """ncu launch list of ONE training step of exactly this workload (tools/step_profile.py under
+    ncu, summarised by tools/launch_summary.py into profiles/r*_step_dram*.json). None when no
+    committed profile matches the configuration."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_launches_bench_summary.json")))
-    if not files:
-        return None, None
-    try:
-        with open(files[-1]) as fh:
-            d = json.load(fh)
-        for k, v in d.items():
-            if k.startswith(kernel):
-                return v["dram_bytes_per_launch"], os.path.basename(files[-1])
-    except Exception:
-        pass
+    key = step_profile_key(args)
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_step_dram*.json")), reverse=True):
+        try:
+            with open(path) as fh:
+                d = json.load(fh)
+        except Exception:
+            continue
+        if d.get("config") == key:
+            return d, os.path.basename(path)
     return None, None
 
 
 def roofline_block(st, args):
-    """Dominant kernel k_row_sweep: algorithmic bytes (table rows streamed + projected rows written +
-    term lists read, engine accounting) per launch over its CUDA-event time per launch."""
+    """Dominant kernel, the projection sweep (k_row_sweep / k_row_sweep_pipe): algorithmic bytes
+    (table rows streamed + projected rows written + term lists read, engine accounting) per launch
+    over its CUDA-event time per launch. `traffic` = ncu DRAM bytes per sweep launch of the same
+    workload (committed step profile), null when none matches. The split finder's fraction is DRAM
+    bytes actually moved by all wave kernels of a step (same profile) over their CUDA-event time."""
     peak, peak_kind = measured_peak()
     kern = st.get("kernels", {})
     rs = kern.get("row_sweep", {"ms": 0.0, "launches": 0})
@@ -155,22 +162,38 @@ def roofline_block(st, args):
     avg_ms = rs["ms"] / launches if rs["launches"] else 0.0
     alg = st["sweep_alg_bytes"] / launches
     achieved = alg / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
-    traffic, src = committed_traffic("k_row_sweep")
-    split_ms = st["ms_waves_total"]
+    prof, src = committed_step_profile(args)
+    traffic = None
+    split = {"ms_per_step": round(st["ms_waves_total"], 2)}
+    if prof:
+        ks = prof["kernels"]
+        sw = [v for k, v in ks.items() if k.startswith("k_row_sweep")]
+        if sw:
+            traffic = sum(v["dram_bytes"] for v in sw) / sum(v["launches"] for v in sw)
+        dram = prof["total_dram_bytes"]
+        split.update({"dram_bytes_per_step": dram,
+                      "dram_GBps": round(dram / (st["ms_waves_total"] / 1e3) / 1e9, 1),
+                      "dram_frac": round(dram / (st["ms_waves_total"] / 1e3) / 1e9 / peak, 4),
+                      "dram_source": src,
+                      "note": "DRAM bytes actually moved by every wave kernel of one step (ncu, same workload) "
+                              "over the waves' CUDA-event time this run"})
     sector = st["hist_sector_bytes"] + st["exact_sector_bytes"]
     strict = st["hist_strict_bytes"] + st["exact_strict_bytes"]
-    return {"bound": "hbm", "kernel": "k_row_sweep (projection: sample-major sweep of the row-major table)",
+    split_ms = st["ms_waves_total"]
+    if split_ms:
+        split["secondary_sector_model"] = {
+            "GBps": round(sector / (split_ms / 1e3) / 1e9, 1),
+            "frac": round(sector / (split_ms / 1e3) / 1e9 / peak, 4),
+            "strict_GBps": round(strict / (split_ms / 1e3) / 1e9, 1),
+            "note": "SURVEY 8(d) sector model: bytes a per-node GATHER implementation would move (32 B per "
+                    "gathered value), not bytes this implementation moves"}
+    return {"bound": "hbm", "kernel": "projection sweep (k_row_sweep_pipe / k_row_sweep): sample-major sweep of the row-major table",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "peak_kind": peak_kind, "traffic": traffic, "traffic_source": src,
             "algorithmic_bytes_per_launch": alg, "avg_launch_ms": round(avg_ms, 3), "launches": launches,
             "algorithmic_bytes_definition": "XR rows streamed (n*ldr*4) + V written (sum n_i*Rp*4) + "
                                             "augmented term lists read, per sweep launch",
-            "split_finder": {"ms_per_step": round(split_ms, 2),
-                             "sector_model_GBps": round(sector / (split_ms / 1e3) / 1e9, 1) if split_ms else 0.0,
-                             "sector_model_frac": round(sector / (split_ms / 1e3) / 1e9 / peak, 4) if split_ms else 0.0,
-                             "strict_GBps": round(strict / (split_ms / 1e3) / 1e9, 1) if split_ms else 0.0,
-                             "note": "SURVEY 8(d) sector model: 32 B per gathered value of a per-node gather "
-                                     "implementation, over the whole split finder's device time"},
+            "split_finder": split,
             "phase_ms": {k: round(st[k], 2) for k in ("ms_sample", "ms_hist_rng", "ms_hist_count", "ms_exact",
                                                       "ms_partition", "ms_waves_total", "ms_train_total")},
             "kernel_ms": kern, "profile_step": "one extra untimed step, one tree group, CUDA events per launch site"}

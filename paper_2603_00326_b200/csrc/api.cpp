@@ -128,11 +128,29 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   // previous allocation is reused when it is large enough (a 16 GB free + malloc per upload costs
   // hundreds of ms).
   D.ldr = (d + 1 + 31) / 32 * 32;  // >= one zero pad column (the sweep's empty-row term)
-  if (std::getenv("SOFG_NO_ROW_TABLE")) {
-    D.XR.release();
-  } else {
-    D.XR.exact(n * D.ldr);
+  // The copy is an accelerator, not a requirement: when it would not leave room for the wave
+  // buffers (projected rows, level buffers: ~16 GB kept free) or its allocation fails, the table
+  // stays column-major only and every wave uses the gather producer (same results).
+  bool row_table = std::getenv("SOFG_NO_ROW_TABLE") == nullptr;
+  if (row_table && !(D.XR.p && D.XR.cap >= n * D.ldr)) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t need = n * D.ldr * 4, reserve = size_t(16) << 30;
+    const size_t avail = free_b + (D.XR.p ? D.XR.cap * 4 : 0);
+    if (avail < need + reserve) row_table = false;
+  }
+  if (row_table) {
+    try {
+      D.XR.exact(n * D.ldr);
+    } catch (const sofg::CudaError&) {
+      cudaGetLastError();
+      row_table = false;
+    }
+  }
+  if (row_table) {
     cuda_check(sofg::launch_transpose_rows(D.X.p, D.ld, n, d, D.XR.p, D.ldr, st), "transpose_rows");
+  } else {
+    D.XR.release();
   }
   D.labels_host.assign(labels, labels + n);
   // labels through page-locked staging, on the engine stream (the staging is rewritten only
@@ -183,6 +201,7 @@ sofg::TrainParams params_for(const sofg_train_config* cfg, const sofg::DeviceDat
   sofg::TrainParams P;
   P.mode = cfg->mode;
   P.bins = cfg->bin_count;
+  P.two_level = cfg->two_level_binning != 0;
   // train_forest stores the resolved breakeven only for Dynamic (forest.hpp:285-293);
   // train_tree uses cfg.breakeven or the fallback regardless of mode (forest.hpp:258).
   P.breakeven = cfg->has_breakeven ? cfg->breakeven : sofg::kFallbackBreakeven;

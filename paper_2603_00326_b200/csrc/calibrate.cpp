@@ -48,6 +48,7 @@ class WaveProbe {
     w_.R = P_.R;
     w_.d = uint32_t(D.d);
     w_.bins = uint32_t(opt_.bin_count);
+    w_.two_level = opt_.two_level;
     w_.k = D.k;
     w_.force_mode = 0;  // no inverse map: the gather projection producer
     w_.nodes.resize(M);

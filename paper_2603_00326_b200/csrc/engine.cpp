@@ -404,7 +404,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   if (timing) cudaEventRecord(ev_[2], st_);
   if (nh) {
     cuda_check(launch_hist_count(d_nodes, d_hslot, d_work, int(n_work), d_mslot, R, bins, k,
-                                 w.chunk_cap, d_terms, d_rp, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
+                                 w.chunk_cap, w.two_level ? 1 : 0, d_terms, d_rp, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
                                  D.xl.p, d_gcnt, d_done, d_rowres, st_),
                "hist_count");
     mark("hist_count");

@@ -40,16 +40,26 @@ struct DevBuf {
     if (n <= cap && p) return p;
     release();
     size_t want = n < 64 ? 64 : n + n / 4;
-    cuda_check(cudaMalloc(&p, want * sizeof(T)), "cudaMalloc");
-    cap = want;
+    alloc(want);
     return p;
   }
   T* exact(size_t n) {  // no slack (large one-off buffers)
     if (n <= cap && p) return p;
     release();
-    cuda_check(cudaMalloc(&p, (n ? n : 1) * sizeof(T)), "cudaMalloc");
-    cap = n ? n : 1;
+    alloc(n ? n : 1);
     return p;
+  }
+
+ private:
+  void alloc(size_t n) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+    if (e != cudaSuccess) {
+      cudaGetLastError();  // clear the sticky-free allocation error
+      cuda_check(e, "cudaMalloc");
+    }
+    p = static_cast<T*>(q);
+    cap = n;
   }
 };
 
@@ -103,6 +113,7 @@ struct WaveSpec {
   uint32_t R = 0, d = 0, bins = 256;
   int k = 2;
   int chunk_cap = 8192;
+  bool two_level = true;  // TrainConfig::two_level_binning (decides the NaN bin, split.hpp:281-283)
   std::vector<NodeIn> nodes;
   // optional host-supplied projection matrices (kNodeGivenCsr on every node)
   bool given_csr = false;

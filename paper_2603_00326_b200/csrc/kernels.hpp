@@ -48,7 +48,7 @@ cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nod
 size_t hist_count_smem(uint32_t bins, int k, int chunk_cap);
 cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slot,
                               const HistWork* work, int n_work, const uint32_t* multi_slot,
-                              uint32_t R, uint32_t bins, int k, int chunk_cap,
+                              uint32_t R, uint32_t bins, int k, int chunk_cap, int two_level,
                               const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
                               const uint64_t* gbase, const float* G, const float* bnd,
                               const uint32_t* nb, const double* xl, uint32_t* gcnt,

@@ -127,7 +127,7 @@ template <int KC, int LT>
 __global__ void __launch_bounds__(256) k_hist_count(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ node_hist_slot,
     const HistWork* __restrict__ work, const uint32_t* __restrict__ multi_slot,
-    uint32_t R, uint32_t bins, int bpad, int k, int chunk_cap,
+    uint32_t R, uint32_t bins, int bpad, int k, int chunk_cap, int two_level,
     const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
     const float* __restrict__ G, const float* __restrict__ bnd_g,
@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
   float* bnd_s = reinterpret_cast<float*>(cnt_s + size_t(8) * bpad * k);      // [8][bpad]
   uint8_t* lab_s = reinterpret_cast<uint8_t*>(bnd_s + size_t(8) * bpad);     // [chunk_cap]
   __shared__ int s_last;
+  __shared__ int s_nan_leaf[8];  // search-tree leaf of NaN values per row (see below)
 
   const uint32_t r = wk.row0 + uint32_t(w);  // the row this warp scans at the end
   const bool row_ok = r < R;
@@ -172,6 +173,15 @@ __global__ void __launch_bounds__(256) k_hist_count(
     bnd_s[i] = v;
   }
   for (int i = threadIdx.x; i < 8 * bpad * k; i += blockDim.x) cnt_s[i] = 0;
+  // NaN values: bin 0 under the reference's two-level table (used for 63 or 255 boundaries when
+  // two_level_binning is set: every `boundary <= NaN` is false), bin nb under its scalar
+  // std::upper_bound lookup (histogram.hpp:72-75,118-131; split.hpp:281-283).
+  if (threadIdx.x < 8) {
+    const uint32_t rg = wk.row0 + threadIdx.x;
+    const uint32_t nbr = rg < R ? nb_g[size_t(h) * R + rg] : 0u;
+    const bool scalar = !(two_level && (nbr == 63 || nbr == 255));
+    s_nan_leaf[threadIdx.x] = bpad + (scalar ? int(nbr) : 0);
+  }
   // stage the chunk's labels
   const uint8_t* lseg = lab + nd.begin + wk.start;
   for (uint32_t j = threadIdx.x; j < wk.len; j += blockDim.x) lab_s[j] = lseg[j];
@@ -206,6 +216,14 @@ __global__ void __launch_bounds__(256) k_hist_count(
 #pragma unroll
           for (int g = 0; g < 8; ++g) t[g] = 2 * t[g] + (bnd_s[g * BP + t[g]] <= v[g] ? 1 : 0);
         }
+        bool nan = false;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) nan |= v[g] != v[g];
+        if (nan) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (v[g] != v[g]) t[g] = s_nan_leaf[g];
+        }
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           if (live & (1u << g))  // uniform
@@ -217,6 +235,7 @@ __global__ void __launch_bounds__(256) k_hist_count(
           const float* tr = bnd_s + g * bpad;
           int t = 1;
           for (int l = 0; l < L; ++l) t = 2 * t + (tr[t] <= v[g] ? 1 : 0);
+          if (v[g] != v[g]) t = s_nan_leaf[g];
           atomicAdd(&cnt_s[(size_t(g) * bpad + size_t(t - bpad)) * k + y], 1u);
         }
       }
@@ -305,7 +324,7 @@ size_t hist_count_smem(uint32_t bins, int k, int chunk_cap) {
 
 cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slot,
                               const HistWork* work, int n_work, const uint32_t* multi_slot,
-                              uint32_t R, uint32_t bins, int k, int chunk_cap,
+                              uint32_t R, uint32_t bins, int k, int chunk_cap, int two_level,
                               const uint32_t* terms, const uint32_t* row_ptr, const uint8_t* lab,
                               const uint64_t* gbase, const float* G, const float* bnd,
                               const uint32_t* nb, const double* xl, uint32_t* gcnt,
@@ -322,7 +341,7 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
                      : (bpad == 256 ? dev::k_hist_count<kMaxClasses, 8> : dev::k_hist_count<kMaxClasses, 0>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   kern<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins, bpad, k,
-                                  chunk_cap, terms, row_ptr, lab, gbase, G, bnd, nb, xl, gcnt,
+                                  chunk_cap, two_level, terms, row_ptr, lab, gbase, G, bnd, nb, xl, gcnt,
                                   done, rowres);
   return cudaGetLastError();
 }

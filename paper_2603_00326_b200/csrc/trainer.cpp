@@ -287,6 +287,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   w.R = P.R;
   w.d = uint32_t(D.d);
   w.bins = uint32_t(P.bins);
+  w.two_level = P.two_level;
   w.k = k;
   w.inv = use_inv ? inv.p : nullptr;
   w.B = uint32_t(B);

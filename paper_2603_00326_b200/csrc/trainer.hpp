@@ -87,6 +87,7 @@ struct DepthProfile {
 struct TrainParams {
   int mode = 2;  // 0 exact-only, 1 histogram-only, 2 dynamic
   uint64_t bins = 256;
+  bool two_level = true;   // two_level_binning
   uint64_t breakeven = 1024;
   std::optional<uint64_t> max_depth;
   uint64_t min_samples_split = 2;

@@ -303,9 +303,9 @@ def test_exact_large_nodes_segmented_sort(gpu_ctx, oracle, mode, breakeven):
 @pytest.mark.parametrize("with_inf,mode,breakeven", [(False, "dynamic", 300), (True, "dynamic", 300),
                                                      (False, "exact", None), (True, "histogram", None)])
 def test_sweep_special_values(gpu_ctx, oracle, with_inf, mode, breakeven):
-    """Signed zeros and subnormals through the sweep's exact float -> double widening (integer
-    construction + exact scaling); an infinite table value switches the sweep to the conversion
-    unit (upload flags the table as non-finite)."""
+    """Signed zeros, subnormals and infinities through both projection producers (sweep and
+    gather: float -> double widening, FP64 accumulation, one rounding) and both splitters; one
+    infinite feature makes projections +-inf (never NaN: a row holds a feature at most once)."""
     X, y = oracle.generate_trunk(3000, 24, 8)
     X = X.copy()
     rng = np.random.default_rng(8)
