@@ -53,6 +53,14 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
                               const uint64_t* gbase, const float* G, const float* bnd,
                               const uint32_t* nb, const double* xl, uint32_t* gcnt,
                               uint32_t* done, RowRes* rowres, cudaStream_t st);
+// lane = row counting (two classes, <= 256 bins), CTA = 32 rows x chunk (HistWork.row0 % 32 == 0)
+bool hist_count_lane_rows(uint32_t R, uint32_t bins, int k);
+size_t hist_count_lr_smem(uint32_t bins, int chunk_cap);
+cudaError_t launch_hist_count_lr(const NodeIn* nodes, const uint32_t* node_hist_slot, const HistWork* work,
+                                 int n_work, const uint32_t* multi_slot, uint32_t R, uint32_t bins, int chunk_cap,
+                                 int two_level, const uint8_t* lab, const uint64_t* gbase, const float* G,
+                                 const float* bnd, const uint32_t* nb, const double* xl, uint32_t* gcnt,
+                                 uint32_t* done, RowRes* rowres, cudaStream_t st);
 cudaError_t launch_hist_select(const uint32_t* hist_nodes, int n_hist, uint32_t R,
                                const RowRes* rowres, NodeRes* res, cudaStream_t st);
 // sweep.cu — projection stage: node rows into V (per node n x Rp floats, sample-major)

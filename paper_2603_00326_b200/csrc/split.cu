@@ -21,10 +21,10 @@ namespace dev {
 
 // Count-vector scan of one histogram row, warp-cooperative. cnt is bin-major [nbins][k] in
 // shared memory, nb boundaries in bnd. Returns the reference's best candidate for this row.
-template <int KC>
-__device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t nb, int k,
-                                int bpad, double parent, const double* __restrict__ xl,
-                                int lane) {
+template <int KC, class Get>
+__device__ RowRes hist_row_scan_g(const Get& cnt_at, const float* bnd, uint32_t nb, int k,
+                                  int bpad, double parent, const double* __restrict__ xl,
+                                  int lane) {
   RowRes res;
   res.valid = 0;
   res.gain = 0.0;
@@ -41,7 +41,7 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
     if (b <= int(nb)) {
 #pragma unroll
       for (int c = 0; c < KC; ++c)
-        if (c < k) loc[c] += cnt[b * k + c];
+        if (c < k) loc[c] += cnt_at(b, c);
     }
   }
   uint32_t n = 0;
@@ -71,7 +71,7 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
 #pragma unroll
       for (int c = 0; c < KC; ++c)
         if (c < k) {
-          left[c] += cnt[b * k + c];
+          left[c] += cnt_at(b, c);
           nl += left[c];
         }
       const uint32_t nr = n - nl;
@@ -98,7 +98,7 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
 #pragma unroll
       for (int c = 0; c < KC; ++c)
         if (c < k) {
-          left[c] += cnt[b * k + c];
+          left[c] += cnt_at(b, c);
           nl += left[c];
         }
       const uint32_t nr = n - nl;
@@ -119,6 +119,14 @@ __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t 
   res.threshold = __ldg(bnd + fb);  // sorted boundaries (global)
   res.n_left = nl;
   return res;
+}
+
+// Bin-major counts [nbins][k] of one row in shared memory.
+template <int KC>
+__device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t nb, int k,
+                                int bpad, double parent, const double* __restrict__ xl,
+                                int lane) {
+  return hist_row_scan_g<KC>([&](int b, int c) { return cnt[b * k + c]; }, bnd, nb, k, bpad, parent, xl, lane);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -284,6 +292,232 @@ __global__ void __launch_bounds__(256) k_hist_count(
 }
 
 // ------------------------------------------------------------------------------------------
+// Histogram counting, lane = row (two classes, <= 256 bins). One CTA = 32 consecutive rows
+// (row0 = 32 g) x one chunk of a node's samples; lane s of every warp owns row row0 + s. Each row's
+// search tree lives in shared memory transposed — word t of row s at [t * 32 + s] — and so do its
+// counters (u16 class 0 | u16 class 1 per bin; chunk <= 65535), so lane s only ever touches bank
+// s: the search and the count atomics have no bank conflicts and no same-address collisions (the
+// lane = sample layout of k_hist_count spends 57 % of its shared wavefronts on conflict replays:
+// profiles/r01_ncu_hist_count.txt). Warp w takes samples w U + 8 U i with U = 8 searches in flight
+// per lane; a warp's V load of one sample is 32 consecutive rows. The counters are then transposed
+// 32 x 32 tile by tile (conflict-free both ways) into skewed row-major rows and each warp scans 4
+// rows; multi-chunk nodes merge into the global counters first and the chunk that completes a
+// (node, row group) scans.
+constexpr int kLrU = 8;
+template <int LT>
+struct LrLayout {
+  static constexpr int BP = 1 << LT;
+  static constexpr int E = BP / 32;            // bins per lane in hist_row_scan_g
+  static constexpr int PITCH = BP + 32 + 1;    // skewed row: bin b at b + b / E (lane-contiguous bins hit distinct banks)
+  static constexpr int AREA = BP * 32 > 32 * PITCH ? BP * 32 : 32 * PITCH;  // words: trees, then rows
+  __device__ static int at(int s, int b) { return s * PITCH + b + b / E; }
+};
+
+template <int LT>
+__global__ void __launch_bounds__(256) k_hist_count_lr(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ node_hist_slot,
+    const HistWork* __restrict__ work, const uint32_t* __restrict__ multi_slot, uint32_t R, uint32_t bins,
+    int two_level, const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
+    const float* __restrict__ G, const float* __restrict__ bnd_g, const uint32_t* __restrict__ nb_g,
+    const double* __restrict__ xl, uint32_t* __restrict__ gcnt, uint32_t* __restrict__ done,
+    RowRes* __restrict__ rowres) {
+  using Lay = LrLayout<LT>;
+  constexpr int BP = Lay::BP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tree = reinterpret_cast<float*>(smem_raw);                       // [BP][32], then rows
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw) + Lay::AREA;       // [BP][32] packed
+  uint32_t* lbits = cnt + BP * 32;                                         // [chunk / 32] label bits
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const HistWork wk = work[blockIdx.x];
+  const NodeIn nd = nodes[wk.node];
+  const uint32_t h = node_hist_slot[wk.node];
+  const uint32_t r = wk.row0 + uint32_t(lane);  // this lane's row
+  const uint32_t nb = r < R ? nb_g[size_t(h) * R + r] : 0u;
+  // Eytzinger trees of the 32 rows (as k_hist_count), NaN pads: pad <= v is false for every v.
+  // Warp w moves sorted boundaries [32 w, 32 w + 32) of all 32 rows: coalesced row reads, a
+  // 32 x 32 transpose through XOR-swizzled staging (conflict-free), then lane l writes row l's
+  // words (bank l). Sorted index q sits at Eytzinger node t: i = q + 1, z = ctz(i),
+  // t = 2^(LT-1-z) + (i >> (z + 1)).
+  const float pad = __int_as_float(0x7fc00000);
+  {
+    uint32_t* stage = cnt + w * 1024;  // the counters are zeroed afterwards
+    for (int m = w; m < BP / 32; m += 8) {
+      for (int i = 0; i < 32; ++i) {  // row i of the group, boundaries 32 m + lane
+        const uint32_t rg = wk.row0 + uint32_t(i);
+        const uint32_t q = uint32_t(32 * m + lane);
+        float v = pad;
+        if (rg < R && q < __ldg(nb_g + size_t(h) * R + rg)) v = __ldg(bnd_g + (size_t(h) * R + rg) * (bins - 1) + q);
+        stage[i * 32 + (lane ^ i)] = __float_as_uint(v);
+      }
+      __syncwarp();
+      for (int i = 0; i < 32; ++i) {  // boundary 32 m + i of row `lane`
+        const uint32_t q1 = uint32_t(32 * m + i + 1);
+        if (q1 < uint32_t(BP)) {
+          const int z = __ffs(int(q1)) - 1;
+          const int t = (1 << (LT - 1 - z)) + int(q1 >> (z + 1));
+          tree[t * 32 + lane] = __uint_as_float(stage[lane * 32 + (i ^ lane)]);
+        }
+      }
+      __syncwarp();
+    }
+    tree[lane] = pad;  // node 0 (unused)
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < BP * 32; i += blockDim.x) cnt[i] = 0;
+  const uint8_t* lseg = lab + nd.begin + wk.start;
+  for (uint32_t j0 = uint32_t(threadIdx.x) & ~31u; j0 < wk.len; j0 += blockDim.x) {
+    const uint32_t j = j0 + uint32_t(lane);
+    const unsigned b = __ballot_sync(0xffffffffu, j < wk.len && lseg[j] != 0);
+    if (lane == 0) lbits[j0 >> 5] = b;
+  }
+  // NaN: bin 0 under the two-level table (63 / 255 boundaries with two_level_binning), bin nb
+  // under the scalar upper_bound lookup (histogram.hpp:72-75,118-131; split.hpp:281-283)
+  const int nan_leaf = BP + ((two_level && (nb == 63 || nb == 255)) ? 0 : int(nb));
+  __syncthreads();
+
+  {
+    const uint32_t Rp = vpitch(R);
+    const float root = tree[32 + lane];
+    const float* Vl = G + gbase[wk.node] + uint64_t(wk.start) * Rp + min(r, Rp - 1);
+    const uint32_t len = wk.len;
+    // The search walks shared byte addresses A(t) = tree + 128 t + 4 lane: A(2t + p) =
+    // 2 A(t) + (p ? 128 : 0) - (tree + 4 lane), one select and one shift-add per level.
+    const uint32_t lane_base = uint32_t(__cvta_generic_to_shared(tree)) + 4u * uint32_t(lane);
+    const uint32_t k0 = 0u - lane_base, k1 = 128u - lane_base;
+    auto step = [&](const float (&v)[kLrU], const uint32_t (&inc)[kLrU], bool nan_fix) {
+      uint32_t a[kLrU];
+#pragma unroll
+      for (int u = 0; u < kLrU; ++u) a[u] = lane_base + (root <= v[u] ? 3u * 128u : 2u * 128u);
+#pragma unroll
+      for (int l = 1; l < LT; ++l) {
+#pragma unroll
+        for (int u = 0; u < kLrU; ++u) {
+          float b;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(b) : "r"(a[u]));
+          a[u] = 2u * a[u] + (b <= v[u] ? k1 : k0);
+        }
+      }
+      int t[kLrU];
+#pragma unroll
+      for (int u = 0; u < kLrU; ++u) t[u] = int((a[u] - lane_base) >> 7);
+      if (nan_fix) {  // warp-uniform: NaN falls to leaf BP (bin 0) by itself; scalar rows move it
+#pragma unroll
+        for (int u = 0; u < kLrU; ++u)
+          if (v[u] != v[u]) t[u] = nan_leaf;
+      }
+#pragma unroll
+      for (int u = 0; u < kLrU; ++u) atomicAdd(&cnt[(t[u] - BP) * 32 + lane], inc[u]);
+    };
+    const bool nan_fix = __any_sync(0xffffffffu, nan_leaf != BP);
+    // full steps: U consecutive samples per warp, the next step's values loaded while this one
+    // searches (software pipeline); j0 is a multiple of U, so a step's labels sit in one word
+    uint32_t j0 = uint32_t(w) * kLrU;
+    float vn[kLrU];
+    if (j0 + kLrU <= len) {
+#pragma unroll
+      for (int u = 0; u < kLrU; ++u) vn[u] = __ldg(Vl + uint64_t(j0 + u) * Rp);
+    }
+    for (; j0 + kLrU <= len; j0 += 8 * kLrU) {
+      float v[kLrU];
+      uint32_t inc[kLrU];
+      const uint32_t bits = lbits[j0 >> 5] >> (j0 & 31);
+#pragma unroll
+      for (int u = 0; u < kLrU; ++u) {
+        v[u] = vn[u];
+        inc[u] = ((bits >> u) & 1u) ? 0x10000u : 1u;
+      }
+      const uint32_t jn = j0 + 8 * kLrU;
+      if (jn + kLrU <= len) {
+#pragma unroll
+        for (int u = 0; u < kLrU; ++u) vn[u] = __ldg(Vl + uint64_t(jn + u) * Rp);
+      }
+      step(v, inc, nan_fix);
+    }
+    if (j0 < len) {  // this warp's last, partial step
+      float v[kLrU];
+      uint32_t inc[kLrU];
+#pragma unroll
+      for (int u = 0; u < kLrU; ++u) {
+        const uint32_t j = j0 + uint32_t(u);
+        const bool ok = j < len;
+        v[u] = ok ? __ldg(Vl + uint64_t(j) * Rp) : 0.f;
+        inc[u] = ok ? (((lbits[j >> 5] >> (j & 31)) & 1u) ? 0x10000u : 1u) : 0u;
+      }
+      step(v, inc, nan_fix);
+    }
+  }
+  __syncthreads();
+  // transpose the packed counters into skewed row-major rows (32 x 32 tiles through registers)
+  uint32_t* rows = reinterpret_cast<uint32_t*>(smem_raw);
+  for (int T = w; T < BP / 32; T += 8) {
+    uint32_t x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = cnt[(T * 32 + i) * 32 + lane];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) rows[Lay::at(lane, T * 32 + i)] = x[i];
+  }
+  __syncthreads();
+
+  if (wk.n_chunks == 1) {
+    for (int sl = w; sl < 32; sl += 8) {
+      const uint32_t rg = wk.row0 + uint32_t(sl);
+      if (rg >= R) break;
+      const uint32_t nbr = nb_g[size_t(h) * R + rg];
+      RowRes rr{};
+      if (nbr > 0) {
+        const uint32_t* row = rows;
+        rr = hist_row_scan_g<2>(
+            [&](int b, int c) {
+              const uint32_t x = row[Lay::at(sl, b)];
+              return c ? x >> 16 : x & 0xffffu;
+            },
+            bnd_g + (size_t(h) * R + rg) * (bins - 1), nbr, 2, BP, nd.parent, xl, lane);
+      }
+      if (lane == 0) rowres[size_t(h) * R + rg] = rr;
+    }
+    return;
+  }
+  // multi-chunk: merge into the global counters [ms][R][BP][2]; the last chunk of this
+  // (node, row group) scans the totals
+  const uint32_t ms = multi_slot[wk.node];
+  for (int sl = w; sl < 32; sl += 8) {
+    const uint32_t rg = wk.row0 + uint32_t(sl);
+    if (rg >= R) break;
+    uint32_t* g = gcnt + (size_t(ms) * R + rg) * size_t(BP) * 2;
+    for (int b = lane; b < BP; b += 32) {
+      const uint32_t x = rows[Lay::at(sl, b)];
+      if (x & 0xffffu) atomicAdd(g + 2 * b, x & 0xffffu);
+      if (x >> 16) atomicAdd(g + 2 * b + 1, x >> 16);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(&done[size_t(ms) * ((R + 31) / 32) + wk.row0 / 32], 1u);
+    s_last = prev == wk.n_chunks - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  uint32_t* mine = reinterpret_cast<uint32_t*>(smem_raw) + size_t(w) * BP * 2;  // [BP][2] per warp
+  for (int sl = w; sl < 32; sl += 8) {
+    const uint32_t rg = wk.row0 + uint32_t(sl);
+    if (rg >= R) break;
+    const uint32_t nbr = nb_g[size_t(h) * R + rg];
+    RowRes rr{};
+    if (nbr > 0) {
+      const uint32_t* g = gcnt + (size_t(ms) * R + rg) * size_t(BP) * 2;
+      for (int i = lane; i < int(nbr + 1) * 2; i += 32) mine[i] = __ldcg(g + i);
+      __syncwarp();
+      rr = hist_row_scan<2>(mine, bnd_g + (size_t(h) * R + rg) * (bins - 1), nbr, 2, BP, nd.parent, xl, lane);
+      __syncwarp();
+    }
+    if (lane == 0) rowres[size_t(h) * R + rg] = rr;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 __global__ void k_hist_select(const uint32_t* __restrict__ hist_nodes, int n_hist, uint32_t R,
                               const RowRes* __restrict__ rowres, NodeRes* __restrict__ res) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
@@ -343,6 +577,38 @@ cudaError_t launch_hist_count(const NodeIn* nodes, const uint32_t* node_hist_slo
   kern<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins, bpad, k,
                                   chunk_cap, two_level, terms, row_ptr, lab, gbase, G, bnd, nb, xl, gcnt,
                                   done, rowres);
+  return cudaGetLastError();
+}
+
+bool hist_count_lane_rows(uint32_t R, uint32_t bins, int k) {
+  // lane = row needs two classes and <= 256 bins; a row group of 32 is worth it when it is
+  // mostly full (measured ~2.2x the lane = sample kernel's throughput per value)
+  return k == 2 && bins <= 256 && (R + 31) / 32 * 32 < 2 * R;
+}
+
+size_t hist_count_lr_smem(uint32_t bins, int chunk_cap) {
+  const int bpad = pow2_at_least(int(bins), 32);
+  const int pitch = bpad + 33;
+  const int area = bpad * 32 > 32 * pitch ? bpad * 32 : 32 * pitch;
+  return size_t(area) * 4 + size_t(bpad) * 32 * 4 + size_t((chunk_cap + 31) / 32) * 4 + 16;
+}
+
+cudaError_t launch_hist_count_lr(const NodeIn* nodes, const uint32_t* node_hist_slot, const HistWork* work,
+                                 int n_work, const uint32_t* multi_slot, uint32_t R, uint32_t bins, int chunk_cap,
+                                 int two_level, const uint8_t* lab, const uint64_t* gbase, const float* G,
+                                 const float* bnd, const uint32_t* nb, const double* xl, uint32_t* gcnt,
+                                 uint32_t* done, RowRes* rowres, cudaStream_t st) {
+  if (n_work == 0) return cudaSuccess;
+  const int bpad = pow2_at_least(int(bins), 32);
+  const size_t smem = hist_count_lr_smem(bins, chunk_cap);
+  auto kern = bpad == 256 ? dev::k_hist_count_lr<8>
+              : bpad == 128 ? dev::k_hist_count_lr<7>
+              : bpad == 64  ? dev::k_hist_count_lr<6>
+                            : dev::k_hist_count_lr<5>;
+  if (bpad > 256) return cudaErrorInvalidValue;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
+  kern<<<n_work, 256, smem, st>>>(nodes, node_hist_slot, work, multi_slot, R, bins, two_level, lab, gbase, G, bnd,
+                                  nb, xl, gcnt, done, rowres);
   return cudaGetLastError();
 }
 

@@ -35,7 +35,9 @@ def test_train_forest_calibrates_when_breakeven_absent(gpu_ctx, oracle, tmp_path
     assert g.breakeven == cal.breakeven
     assert 64 <= cal.breakeven <= 65537
     ns = [s[0] for s in cal.samples]
-    assert ns == sorted(ns) and len(ns) >= 2 and ns[0] == 64
+    assert ns == sorted(ns) and ns[0] == 64
+    if len(ns) == 1:  # the histogram probe already won at n_min (calibrate.hpp:84)
+        assert cal.breakeven == 64
     assert all(e > 0 and h > 0 for _, e, h in cal.samples)
     assert cal.elapsed_seconds > 0
     # the trees are the reference's at the calibrated breakeven

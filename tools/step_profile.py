@@ -18,9 +18,21 @@ p.add_argument("--mode", default="dynamic")
 p.add_argument("--classes", type=int, default=2)
 p.add_argument("--density", type=float, default=0.0)
 p.add_argument("--seed", type=int, default=7)
+p.add_argument("--stats", action="store_true", help="print CUDA-event time per launch site (3 steps)")
 a = p.parse_args()
 with sofg.Context(0) as ctx:
     ctx.generate_trunk(a.n, a.d, a.classes, seed=1)
-    f = ctx.train_forest(sofg.TrainConfig(n_trees=a.trees, mode=a.mode, breakeven=a.breakeven, seed=a.seed,
-                                          cell_density=a.density, n_workers=0))
+    cfg = sofg.TrainConfig(n_trees=a.trees, mode=a.mode, breakeven=a.breakeven, seed=a.seed,
+                           cell_density=a.density, n_workers=0)
+    f = ctx.train_forest(cfg)
     print("trees", f.n_trees, "nodes", len(f.left))
+    if a.stats:
+        import time
+        ctx.set_stats(1)
+        ctx.reset_stats()
+        t = time.perf_counter()
+        for _ in range(2):
+            ctx.train_forest(cfg)
+        t = (time.perf_counter() - t) / 2
+        st = ctx.stats()
+        print(f"step {t * 1e3:.1f} ms (stats on)", {k: round(v["ms"] / 2, 1) for k, v in st["kernels"].items()})
