@@ -16,7 +16,35 @@
 #include "kernels.hpp"
 #include "trainer.hpp"
 
+// Bootstrap samples computed ahead in the host's idle time during training (the waits for long
+// waves): the next batch of the same call, or the tree range a following call with the same
+// seed would train next. Tree t's sample is a pure function of (n, fraction, seed, t)
+// (forest.hpp:153,305), so a prefetched sample is the one the call would compute.
+struct BootAhead {
+  uint64_t n = 0, seed = 0, t0 = 0, t1 = 0, next = 0;
+  double frac = 0.0;
+  std::vector<std::vector<uint32_t>> roots;  // trees [t0, t1); filled for [t0, next)
+  void plan(uint64_t n_, double f, uint64_t s, uint64_t a, uint64_t b) {
+    if (n == n_ && frac == f && seed == s && t0 == a && t1 == b) return;  // keep what is done
+    n = n_;
+    frac = f;
+    seed = s;
+    t0 = a;
+    t1 = b;
+    next = a;
+    roots.assign(size_t(b - a), {});
+  }
+  bool take(uint64_t n_, double f, uint64_t s, uint64_t t, std::vector<uint32_t>& out) {
+    if (n != n_ || frac != f || seed != s || t < t0 || t >= next) return false;
+    std::vector<uint32_t>& r = roots[size_t(t - t0)];
+    if (r.empty()) return false;
+    out.swap(r);
+    return true;
+  }
+};
+
 struct sofg_ctx {
+  BootAhead ahead;
   std::unique_ptr<sofg::WaveRunner> eng;
   std::unique_ptr<sofg::ThreadPool> pool;
   int pool_threads = 0;
@@ -410,15 +438,32 @@ int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** o
       std::vector<std::vector<uint32_t>> roots(B);
       std::vector<uint64_t> seeds(B);
       const auto tbs = std::chrono::steady_clock::now();
+      BootAhead& ah = c->ahead;
       pool.parallel_for(B, [&](size_t b) {
         const uint64_t ts = sofg::host::derive_seed(cfg->seed, t0 + b + 1);  // forest.hpp:305
-        roots[b] = sofg::host::bootstrap_indices(D.n, cfg->bootstrap_fraction,
-                                                 sofg::host::derive_seed(ts, 0));
+        if (!ah.take(D.n, cfg->bootstrap_fraction, cfg->seed, t0 + b, roots[b]))
+          roots[b] = sofg::host::bootstrap_indices(D.n, cfg->bootstrap_fraction,
+                                                   sofg::host::derive_seed(ts, 0));
         seeds[b] = sofg::host::derive_seed(ts, 1);
       });
       c->times.ms_bootstrap +=
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tbs).count();
-      sofg::grow_trees(*c->eng, P, pool, roots, seeds, 0, res->f, c->times);
+      // the next batch's samples (this call's, else the range a next call would train)
+      const uint64_t n0 = t1 < te ? t1 : te, n1 = t1 < te ? std::min(te, t1 + batch) : te + (t1 - t0);
+      ah.plan(D.n, cfg->bootstrap_fraction, cfg->seed, n0, n1);
+      sofg::TrainParams Pb = P;
+      if (!std::getenv("SOFG_NO_BOOT_AHEAD"))
+        Pb.idle_work = [&ah, &pool]() {
+          if (ah.next >= ah.t1) return false;
+          const uint64_t a = ah.next, b = std::min(ah.t1, a + uint64_t(pool.size()));
+          pool.parallel_for(size_t(b - a), [&](size_t i) {
+            const uint64_t ts = sofg::host::derive_seed(ah.seed, a + i + 1);
+            ah.roots[size_t(a + i - ah.t0)] = sofg::host::bootstrap_indices(ah.n, ah.frac, sofg::host::derive_seed(ts, 0));
+          });
+          ah.next = b;
+          return ah.next < ah.t1;
+        };
+      sofg::grow_trees(*c->eng, Pb, pool, roots, seeds, 0, res->f, c->times);
     }
     res->total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     *out = guard_res.release();

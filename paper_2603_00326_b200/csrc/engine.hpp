@@ -228,6 +228,7 @@ class WaveRunner {
   const float* last_phase_ms() const { return last_phase_ms_; }
   float last_split_ms() const { return last_phase_ms_[2] + last_phase_ms_[3]; }
   void wait_wave();
+  bool wave_done() const { return pend_n_ == 0 || cudaEventQuery(done_ev_) == cudaSuccess; }
   // Page-locked staging reused across calls (root segments).
   PinnedBuf<unsigned char> staging;
   // Terms of node `node`'s winning row in the last collected wave, for rows longer than the

@@ -165,11 +165,12 @@ int32_t argmax_first(const uint32_t* c, int k) {  // std::max_element: first max
 
 }  // namespace
 
-void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
+void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
                 const std::vector<std::vector<uint32_t>>& roots,
                 const std::vector<uint64_t>& root_seeds, uint32_t root_depth, FlatForest& out,
                 HostTimes& times) {
   const auto t_start = Clock::now();
+  TrainParams P = P0;  // local copy: idle_work is dropped once it reports no more work
   cuda_check(cudaSetDevice(eng.device()), "cudaSetDevice");
   DeviceData& D = eng.data();
   const int k = D.k;
@@ -279,6 +280,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
   std::vector<uint64_t> part_splits(prof ? NP : 0), part_split_n(prof ? NP : 0);
 
   int cur = 0;
+  double prev_wave_ms = 0.0, idle_chunk_ms = 1.0;
   static const bool level_log = std::getenv("SOFG_LEVEL_LOG") != nullptr;
   std::vector<uint32_t>&spec_z = S.spec_z, &spec_pos = S.spec_pos;
   std::vector<size_t> poff(NP + 1);
@@ -441,6 +443,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
       const double lv_prep = ms_since(t0);
       times.ms_prep += lv_prep;
       t0 = Clock::now();
+      const auto t_submit = t0;
       eng.submit(w);
       const double lv_submit = ms_since(t0);
       times.ms_submit += lv_submit;
@@ -471,7 +474,19 @@ void grow_trees(WaveRunner& eng, const TrainParams& P, ThreadPool& pool,
         eng.wait_wave();
         lv_sync = ms_since(t0);
       }
+      if (P.idle_work && prev_wave_ms > 0.0) {
+        // only chunks expected to end before the wave does (this level's wave is at least as
+        // long as the last one while the frontier grows; later levels stop the work)
+        bool more = true;
+        while (more && !eng.wave_done() && ms_since(t_submit) + idle_chunk_ms < prev_wave_ms) {
+          const auto tc = Clock::now();
+          more = P.idle_work();
+          idle_chunk_ms = std::max(idle_chunk_ms, ms_since(tc));
+        }
+        if (!more) P.idle_work = nullptr;
+      }
       const NodeRes* res = eng.collect_view(w);
+      prev_wave_ms = ms_since(t_submit);
       const double lv_wait = ms_since(t0);
       if (std::getenv("SOFG_WAVE_HASH")) {  // debugging aid: per-wave result digest
         uint64_t hsh = 1469598103934665603ull;

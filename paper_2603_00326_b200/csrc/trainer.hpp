@@ -97,6 +97,10 @@ struct TrainParams {
   uint64_t batch_trees = 0;
   int host_threads = 0;
   DepthProfile* profile = nullptr;  // filled when set (requires WaveRunner::collect_stats)
+  // Background host work run in the waits for a wave (levels whose kernels outlast the host's
+  // work): called repeatedly while the wave is in flight, each call one bounded chunk; returns
+  // false when nothing is left.
+  std::function<bool()> idle_work;
 };
 
 // Minimal fork-join pool for the per-node host work (binomial draws, bootstraps).
