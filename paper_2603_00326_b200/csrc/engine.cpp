@@ -123,14 +123,20 @@ void WaveRunner::submit(const WaveSpec& w) {
   // value), lane = row below (no setup-dominated small CTAs with bank-conflicting searches).
   static const int lr_env = std::getenv("SOFG_HIST_LR") ? std::atoi(std::getenv("SOFG_HIST_LR")) : -1;
   static const uint32_t lr_max_env =
-      std::getenv("SOFG_HIST_LR_MAXN") ? uint32_t(std::atoi(std::getenv("SOFG_HIST_LR_MAXN"))) : 65504u;
+      std::getenv("SOFG_HIST_LR_MAXN") ? uint32_t(std::atoi(std::getenv("SOFG_HIST_LR_MAXN"))) : 0xffffffffu;
+  // Nodes above lr_chunk samples are counted in chunks of lr_chunk (u16 packed counters per CTA),
+  // merged in the global counters like the lane = sample kernel's multi-chunk nodes.
+  static const uint32_t lr_chunk_env =
+      std::getenv("SOFG_HIST_LR_CHUNK") ? uint32_t(std::atoi(std::getenv("SOFG_HIST_LR_CHUNK"))) : 32768u;
   const bool lr_ok = k == 2 && bins <= 256 && (lr_env >= 0 ? lr_env != 0 : hist_count_lane_rows(R, bins, k));
-  const uint32_t lr_max = lr_ok ? (lr_env == 1 ? 65504u : std::min(lr_max_env, 65504u)) : 0u;
+  const uint32_t lr_max = lr_ok ? (lr_env == 1 ? 0xffffffffu : lr_max_env) : 0u;
+  const uint32_t lr_chunk = std::max(1024u, std::min(lr_chunk_env, 65504u));
   const uint32_t groups = (R + kHistRowsPerCta - 1) / kHistRowsPerCta;
   const uint32_t groups_lr = (R + 31) / 32;
   const uint32_t cap = uint32_t(w.chunk_cap);
   struct Cnt {
     uint64_t hist = 0, multi = 0, work = 0, work_lr = 0, tiles = 0, g = 0, items = 0;
+    uint32_t lr_len = 0;  // longest lane = row chunk
     uint64_t exact[kExactBuckets] = {};
     uint32_t zmax = 32;
     uint64_t terms_end = 0;
@@ -159,7 +165,10 @@ void WaveRunner::submit(const WaveSpec& w) {
         if (nd.flags & kNodeHist) {
           t.hist++;
           if (nd.n <= lr_max) {
-            t.work_lr += groups_lr;
+            const uint32_t chunks = (nd.n + lr_chunk - 1) / lr_chunk;
+            if (chunks > 1) t.multi++;
+            t.work_lr += uint64_t(groups_lr) * chunks;
+            t.lr_len = std::max(t.lr_len, std::min(nd.n, lr_chunk));
           } else {
             const uint32_t chunks = (nd.n + cap - 1) / cap;
             if (chunks > 1) t.multi++;
@@ -197,6 +206,7 @@ void WaveRunner::submit(const WaveSpec& w) {
     tot.items += cc[c].items;
     tot.big += cc[c].big;
     tot.zmax = std::max(tot.zmax, cc[c].zmax);
+    tot.lr_len = std::max(tot.lr_len, cc[c].lr_len);
     tot.terms_end = std::max(tot.terms_end, cc[c].terms_end);
   }
   uint64_t bucket_base[kExactBuckets + 1] = {0};
@@ -263,8 +273,14 @@ void WaveRunner::submit(const WaveSpec& w) {
         p_hslot[i] = uint32_t(o.hist);
         p_hist[o.hist++] = uint32_t(i);
         if (nd.n <= lr_max) {  // lane = row items after the lane = sample ones
+          const uint32_t chunks = (nd.n + lr_chunk - 1) / lr_chunk;
+          if (chunks > 1) p_mslot[i] = uint32_t(o.multi++);
           for (uint32_t g = 0; g < groups_lr; ++g)
-            p_work[n_work_old + o.work_lr++] = {uint32_t(i), g * 32u, 0u, nd.n, 0u, 1u};
+            for (uint32_t ch = 0; ch < chunks; ++ch) {
+              const uint32_t s0 = ch * lr_chunk;
+              p_work[n_work_old + o.work_lr++] = {uint32_t(i), g * 32u, s0, std::min(nd.n - s0, lr_chunk), ch,
+                                                  chunks};
+            }
         } else {
           const uint32_t chunks = (nd.n + cap - 1) / cap;
           if (chunks > 1) p_mslot[i] = uint32_t(o.multi++);
@@ -427,7 +443,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   if (nh) {
     if (n_work > n_work_old)
       cuda_check(launch_hist_count_lr(d_nodes, d_hslot, d_work + n_work_old, int(n_work - n_work_old), d_mslot, R,
-                                      bins, int(lr_max), w.two_level ? 1 : 0, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
+                                      bins, int(std::max(tot.lr_len, 32u)), w.two_level ? 1 : 0, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
                                       D.xl.p, d_gcnt, d_done, d_rowres, st_),
                  "hist_count_lr");
     if (n_work_old)

@@ -121,6 +121,93 @@ __device__ RowRes hist_row_scan_g(const Get& cnt_at, const float* bnd, uint32_t 
   return res;
 }
 
+// Two-class form of hist_row_scan_g for E = bpad / 32 candidates per lane (compile time): every
+// candidate's six table values are loaded before any is used (no data-dependent exits in the load
+// phase) and the impurity sums stay in registers for the first-maximum pass. Same operations in
+// the same order as impurity_sum<2> / gain_from_x, so the result is identical.
+template <int E, class Get>
+__device__ RowRes hist_row_scan2(const Get& cnt_at, const float* bnd, uint32_t nb, double parent,
+                                 const double* __restrict__ xl, int lane) {
+  RowRes res;
+  res.valid = 0;
+  res.gain = 0.0;
+  res.threshold = 0.f;
+  res.n_left = 0;
+  res._pad = 0;
+  const int b0 = lane * E;
+  uint32_t c0[E], c1[E], s0 = 0, s1 = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const bool in = b0 + e <= int(nb);
+    c0[e] = in ? cnt_at(b0 + e, 0) : 0u;
+    c1[e] = in ? cnt_at(b0 + e, 1) : 0u;
+    s0 += c0[e];
+    s1 += c1[e];
+  }
+  uint32_t t0, t1;
+  const uint32_t p0 = warp_excl_scan_u32(s0, lane, &t0), p1 = warp_excl_scan_u32(s1, lane, &t1);
+  const uint32_t n = t0 + t1;
+  if (n < 2) return res;  // split.hpp:101
+  const double dn = double(n);
+  double X[E];
+  bool ok[E];
+  uint32_t nlv[E];
+  {
+    uint32_t l0 = p0, l1 = p1;
+    uint32_t i0[E], i1[E], inl[E], inr[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      l0 += c0[e];
+      l1 += c1[e];
+      const uint32_t nl = l0 + l1, nr = n - nl;
+      ok[e] = b0 + e < int(nb) && nl != 0 && nr != 0;
+      nlv[e] = nl;
+      i0[e] = ok[e] ? l0 : 0u;
+      i1[e] = ok[e] ? l1 : 0u;
+      inl[e] = ok[e] ? nl : 0u;
+      inr[e] = ok[e] ? nr : 0u;
+    }
+    double a0[E], a1[E], r0[E], r1[E], fl[E], fr[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      a0[e] = __ldg(xl + i0[e]);
+      a1[e] = __ldg(xl + i1[e]);
+      r0[e] = __ldg(xl + (ok[e] ? t0 - i0[e] : 0u));
+      r1[e] = __ldg(xl + (ok[e] ? t1 - i1[e] : 0u));
+      fl[e] = __ldg(xl + inl[e]);
+      fr[e] = __ldg(xl + inr[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double sl = __dadd_rn(a0[e], a1[e]), sr = __dadd_rn(r0[e], r1[e]);
+      X[e] = __dsub_rn(__dadd_rn(__dsub_rn(fl[e], sl), fr[e]), sr);
+    }
+  }
+  double xmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (ok[e]) xmin = fmin(xmin, X[e]);
+  xmin = warp_min_f64(xmin);
+  if (!(xmin < __longlong_as_double(0x7ff0000000000000ll))) return res;
+  const double gbest = gain_from_x(parent, xmin, dn);
+  if (!(gbest > 0.0)) return res;
+  const double win = x_window(parent, xmin, dn);
+  uint32_t first = 0xffffffffu, first_nl = 0;
+#pragma unroll
+  for (int e = E - 1; e >= 0; --e)  // the lowest qualifying candidate of this lane wins
+    if (ok[e] && X[e] <= win && gain_from_x(parent, X[e], dn) == gbest) {
+      first = uint32_t(b0 + e);
+      first_nl = nlv[e];
+    }
+  const uint32_t fb = warp_min_u32(first);
+  const uint32_t src = __ffs(__ballot_sync(0xffffffffu, first == fb)) - 1;
+  res.valid = 1;
+  res.gain = gbest;
+  res.threshold = __ldg(bnd + fb);  // sorted boundaries (global)
+  res.n_left = __shfl_sync(0xffffffffu, first_nl, src);
+  return res;
+}
+
 // Bin-major counts [nbins][k] of one row in shared memory.
 template <int KC>
 __device__ RowRes hist_row_scan(const uint32_t* cnt, const float* bnd, uint32_t nb, int k,
@@ -342,14 +429,17 @@ __global__ void __launch_bounds__(256) k_hist_count_lr(
   const float pad = __int_as_float(0x7fc00000);
   {
     uint32_t* stage = cnt + w * 1024;  // the counters are zeroed afterwards
+    const float* brow = bnd_g + size_t(h) * R * (bins - 1);
     for (int m = w; m < BP / 32; m += 8) {
-      for (int i = 0; i < 32; ++i) {  // row i of the group, boundaries 32 m + lane
-        const uint32_t rg = wk.row0 + uint32_t(i);
-        const uint32_t q = uint32_t(32 * m + lane);
-        float v = pad;
-        if (rg < R && q < __ldg(nb_g + size_t(h) * R + rg)) v = __ldg(bnd_g + (size_t(h) * R + rg) * (bins - 1) + q);
-        stage[i * 32 + (lane ^ i)] = __float_as_uint(v);
+      float v[32];  // all 32 rows' loads in flight before the first store
+      const uint32_t q = uint32_t(32 * m + lane);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {  // row i of the group, boundaries 32 m + lane (nb 0 past R)
+        const uint32_t nbi = __shfl_sync(0xffffffffu, nb, i);
+        v[i] = q < nbi ? __ldg(brow + (wk.row0 + uint32_t(i)) * (bins - 1) + q) : pad;
       }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) stage[i * 32 + (lane ^ i)] = __float_as_uint(v[i]);
       __syncwarp();
       for (int i = 0; i < 32; ++i) {  // boundary 32 m + i of row `lane`
         const uint32_t q1 = uint32_t(32 * m + i + 1);
@@ -467,12 +557,12 @@ __global__ void __launch_bounds__(256) k_hist_count_lr(
       RowRes rr{};
       if (nbr > 0) {
         const uint32_t* row = rows;
-        rr = hist_row_scan_g<2>(
+        rr = hist_row_scan2<Lay::E>(
             [&](int b, int c) {
               const uint32_t x = row[Lay::at(sl, b)];
               return c ? x >> 16 : x & 0xffffu;
             },
-            bnd_g + (size_t(h) * R + rg) * (bins - 1), nbr, 2, BP, nd.parent, xl, lane);
+            bnd_g + (size_t(h) * R + rg) * (bins - 1), nbr, nd.parent, xl, lane);
       }
       if (lane == 0) rowres[size_t(h) * R + rg] = rr;
     }
@@ -510,7 +600,8 @@ __global__ void __launch_bounds__(256) k_hist_count_lr(
       const uint32_t* g = gcnt + (size_t(ms) * R + rg) * size_t(BP) * 2;
       for (int i = lane; i < int(nbr + 1) * 2; i += 32) mine[i] = __ldcg(g + i);
       __syncwarp();
-      rr = hist_row_scan<2>(mine, bnd_g + (size_t(h) * R + rg) * (bins - 1), nbr, 2, BP, nd.parent, xl, lane);
+      rr = hist_row_scan2<Lay::E>([&](int b, int c) { return mine[2 * b + c]; },
+                                  bnd_g + (size_t(h) * R + rg) * (bins - 1), nbr, nd.parent, xl, lane);
       __syncwarp();
     }
     if (lane == 0) rowres[size_t(h) * R + rg] = rr;
