@@ -9,6 +9,8 @@
 //                  labels into the next level's buffers.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.hpp"
 #include "dev_util.cuh"
 #include "kernels.hpp"
@@ -153,6 +155,97 @@ __global__ void __launch_bounds__(256) k_part_scatter(
   }
 }
 
+// Warp-per-tile forms of k_part_flags / k_part_scatter (same flag-word layout: word l / 32 of the
+// tile's 32 words covers elements [32 word, 32 word + 32)). A CTA takes 8 tiles, so the many
+// small nodes of deep levels do not each occupy a 256-thread CTA for a few dozen elements.
+__global__ void __launch_bounds__(256) k_part_flags_w(
+    const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, int n_tiles, uint32_t R, int k,
+    const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase, const float* __restrict__ G,
+    NodeRes* __restrict__ res, uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_left) {
+  const int lane = threadIdx.x & 31;
+  const int ti = int(blockIdx.x) * 8 + int(threadIdx.x >> 5);
+  if (ti >= n_tiles) return;
+  const Tile tl = tiles[ti];
+  const int row = res[tl.node].row;
+  if (row < 0) return;
+  const NodeIn nd = nodes[tl.node];
+  const float thr = res[tl.node].threshold;
+  const uint32_t Rp = vpitch(R);
+  const float* Vn = G + gbase[tl.node] + row + uint64_t(tl.start) * Rp;
+  const uint8_t* ln = lab + nd.begin + tl.start;
+  uint32_t my_left = 0;
+  uint32_t cls[kMaxClasses];
+#pragma unroll
+  for (int c = 0; c < kMaxClasses; ++c) cls[c] = 0;
+  const int words = int((tl.len + 31) / 32);
+#pragma unroll 4
+  for (int wd = 0; wd < words; ++wd) {
+    const uint32_t l = uint32_t(wd * 32 + lane);
+    bool f = false;
+    uint32_t y = 0;
+    if (l < tl.len) {
+      f = __ldg(Vn + uint64_t(l) * Rp) <= thr;
+      y = ln[l];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) flags[size_t(ti) * 32 + wd] = m;
+    if (f) {
+      ++my_left;
+#pragma unroll
+      for (int c = 0; c < kMaxClasses; ++c) cls[c] += (c == int(y));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) my_left += __shfl_xor_sync(0xffffffffu, my_left, o);
+  if (lane == 0) tile_left[ti] = my_left;
+#pragma unroll
+  for (int c = 0; c < kMaxClasses; ++c) {
+    if (c >= k) break;
+    uint32_t x = cls[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicAdd(&res[tl.node].left_counts[c], x);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_part_scatter_w(
+    const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, int n_tiles,
+    const NodeRes* __restrict__ res, const uint32_t* __restrict__ flags,
+    const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ idx_in,
+    const uint8_t* __restrict__ lab_in, uint32_t* __restrict__ idx_out,
+    uint8_t* __restrict__ lab_out, uint32_t* __restrict__ inv, uint32_t B) {
+  const int lane = threadIdx.x & 31;
+  const int ti = int(blockIdx.x) * 8 + int(threadIdx.x >> 5);
+  if (ti >= n_tiles) return;
+  const Tile tl = tiles[ti];
+  if (res[tl.node].row < 0) return;
+  const NodeIn nd = nodes[tl.node];
+  const uint32_t n_left = res[tl.node].n_left;
+  const uint32_t* fw = flags + size_t(ti) * 32;
+  const int words = int((tl.len + 31) / 32);
+  const uint32_t mw = lane < words ? fw[lane] : 0u;
+  uint32_t tot;
+  const uint32_t wpre = warp_excl_scan_u32(__popc(mw), lane, &tot);
+  const uint32_t off = tile_off[ti];
+#pragma unroll 4
+  for (int wd = 0; wd < words; ++wd) {
+    const uint32_t l = uint32_t(wd * 32 + lane);
+    const uint32_t m = __shfl_sync(0xffffffffu, mw, wd);
+    const uint32_t pre = __shfl_sync(0xffffffffu, wpre, wd);
+    if (l >= tl.len) continue;
+    const uint32_t lrank = pre + __popc(m & ((1u << lane) - 1u));
+    const uint32_t p = tl.start + l;             // position inside the node
+    const uint32_t L = off + lrank;              // left elements before p
+    const bool left = (m >> lane) & 1u;
+    const uint32_t dst = left ? L : n_left + (p - L);
+    const uint32_t src = nd.begin + p;
+    const uint32_t smp = idx_in[src];
+    idx_out[nd.begin + dst] = smp;
+    lab_out[nd.begin + dst] = lab_in[src];
+    if (inv) inv[uint64_t(smp) * B + nd.tree] = nd.begin + dst;  // sweep.cu inverse map
+  }
+}
+
 // Roofline accounting: number of distinct 32-byte sectors {idx >> 3} in each node's (sorted)
 // sample-id set. Every projection term gathers one column over that set, so the node's gather
 // traffic in the sector model is 32 * sectors * z.
@@ -216,14 +309,21 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
                              uint32_t* tile_left, uint32_t* inv, uint32_t B, cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
-  if (n_tiles > 0)
+  static const bool cta_tiles = std::getenv("SOFG_PART_CTA") != nullptr;  // CTA-per-tile forms
+  if (n_tiles > 0 && cta_tiles)
     dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, lab_in, gbase,
                                                G, res, flags, tile_left);
+  else if (n_tiles > 0)
+    dev::k_part_flags_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, R, k, lab_in, gbase, G, res,
+                                                           flags, tile_left);
   dev::k_part_scan<<<(n_nodes + 3) / 4, 128, 0, st>>>(nodes, n_nodes, R, tile_first, terms,
                                                       row_ptr, pos_proj, pos_split, tile_left, res);
-  if (n_tiles > 0)
+  if (n_tiles > 0 && cta_tiles)
     dev::k_part_scatter<<<n_tiles, 256, 0, st>>>(nodes, tiles, res, flags, tile_left, idx_in,
                                                  lab_in, idx_out, lab_out, inv, B);
+  else if (n_tiles > 0)
+    dev::k_part_scatter_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, res, flags, tile_left, idx_in,
+                                                             lab_in, idx_out, lab_out, inv, B);
   return cudaGetLastError();
 }
 
