@@ -12,7 +12,10 @@
 // recurrence steps instead of 312 + a full twist.
 #pragma once
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <cstring>
+#include <limits>
 #include <new>
 #include <random>
 #include <vector>
@@ -83,6 +86,8 @@ class LazyMt64 {
     for (int j = 0; j < M; ++j) g[j].seeded_ = upto + 1;
   }
 
+  static constexpr int kBatch = 8;  // engines primed together by BinomialDraw::batch
+
  private:
   static constexpr int kN = 312, kM = 156;
   static uint64_t mix(uint64_t cur, uint64_t nxt, uint64_t far) {
@@ -114,17 +119,156 @@ class LazyMt64 {
   uint64_t count_ = 0;
 };
 
-// Binomial nonzero count of one projection matrix: a fresh distribution per draw (the
-// reference constructs it inside sample_projection_matrix, so no normal variate is carried
-// over between nodes); the parameter block is precomputed once.
-struct BinomialDraw {
-  std::binomial_distribution<long long>::param_type param;
-  BinomialDraw(uint64_t cells, double density) : param((long long)cells, density) {}
+// Binomial nonzero count of one projection matrix: the reference constructs a fresh
+// std::binomial_distribution<long long>(cells, density) per matrix (projection.hpp:66-67), so no
+// normal variate carries over between nodes. FastBinomial restates that draw — libstdc++ 13
+// binomial_distribution::operator() (bits/random.tcc:1563-1680, Devroye's rejection method, and
+// _M_waiting :1532-1551) — for one fixed parameter:
+//  * the parameter block is the library's own (param_type::_M_initialize, read back from a
+//    genuine param_type object), not recomputed;
+//  * every uniform, normal, log and exponential is the same libstdc++/glibc call in the same
+//    order with the same expressions (so the compiler contracts them the same way);
+//  * the acceptance test's lgamma(np + x + 1) + lgamma(t - (np + x) + 1) depends only on the
+//    integer x: it is tabulated once per parameter (the same glibc lgamma values) for the x the
+//    sampler produces in practice, and computed inline outside that window. Besides the two calls
+//    per draw this removes glibc lgamma's store to the process-global `signgam`, which made
+//    concurrent draws contend for one cache line (16 host threads: 47 ns per draw with
+//    std::binomial_distribution vs 10 ns, tools/mb/binom_mb.cpp on the B200 host).
+// tests/cpp/binomial_test.cpp checks it against std::binomial_distribution draw for draw
+// (values and engine outputs consumed).
+class FastBinomial {
+ public:
+  FastBinomial(long long t, double p) {
+    const std::binomial_distribution<long long>::param_type prm(t, p);
+    static_assert(sizeof(Mirror) == sizeof(prm), "libstdc++ binomial param_type layout");
+    std::memcpy(&m_, &prm, sizeof(m_));
+    if (!m_.easy) {
+      const double p12 = m_.p <= 0.5 ? m_.p : 1.0 - m_.p;
+      np_ = std::floor(m_.t * p12);
+      lo_ = -std::min<long long>(kWin, (long long)np_);
+      const long long hi = std::min<long long>(kWin, m_.t - (long long)np_);
+      lfx_.resize(size_t(hi - lo_ + 1));
+      for (long long x = lo_; x <= hi; ++x) lfx_[size_t(x - lo_)] = lfx_direct(double(x));
+    }
+  }
 
-  // Draws for m fresh engines make_rng(seeds[i]) (no skipped outputs), eight at a time with
+  template <class G>
+  long long operator()(G& g) const {
+    long long ret;
+    const long long t = m_.t;
+    const double p = m_.p;
+    const double p12 = p <= 0.5 ? p : 1.0 - p;
+    if (!m_.easy) {
+      double x = 0.0;
+      const double naf = (1 - std::numeric_limits<double>::epsilon()) / 2;
+      const double thr = std::numeric_limits<long long>::max() + naf;
+      const double np = std::floor(t * p12);
+      const double spi_2 = 1.2533141373155002512078826424055226L;  // sqrt(pi / 2)
+      const double a1 = m_.a1;
+      const double a12 = a1 + m_.s2 * spi_2;
+      const double a123 = m_.a123;
+      const double s1s = m_.s1 * m_.s1;
+      const double s2s = m_.s2 * m_.s2;
+      std::normal_distribution<double> nd;  // binomial_distribution::_M_nd of a fresh object
+      bool reject;
+      do {
+        const double u = m_.s * canon(g);
+        double v = 0.0;
+        if (u <= a1) {
+          const double n = nd(g);
+          const double y = m_.s1 * std::abs(n);
+          reject = y >= m_.d1;
+          if (!reject) {
+            const double e = -std::log(1.0 - canon(g));
+            x = std::floor(y);
+            v = -e - n * n / 2 + m_.c;
+          }
+        } else if (u <= a12) {
+          const double n = nd(g);
+          const double y = m_.s2 * std::abs(n);
+          reject = y >= m_.d2;
+          if (!reject) {
+            const double e = -std::log(1.0 - canon(g));
+            x = std::floor(-y);
+            v = -e - n * n / 2;
+          }
+        } else if (u <= a123) {
+          const double e1 = -std::log(1.0 - canon(g));
+          const double e2 = -std::log(1.0 - canon(g));
+          const double y = m_.d1 + 2 * s1s * e1 / m_.d1;
+          x = std::floor(y);
+          v = (-e2 + m_.d1 * (1 / (t - np) - y / (2 * s1s)));
+          reject = false;
+        } else {
+          const double e1 = -std::log(1.0 - canon(g));
+          const double e2 = -std::log(1.0 - canon(g));
+          const double y = m_.d2 + 2 * s2s * e1 / m_.d2;
+          x = std::floor(-y);
+          v = -e2 - m_.d2 * y / (2 * s2s);
+          reject = false;
+        }
+        reject = reject || x < -np || x > t - np;
+        if (!reject) {
+          const double lfx = lfx_of(x);
+          reject = v > m_.lf - lfx + x * m_.lp1p;
+        }
+        reject |= x + np >= thr;
+      } while (reject);
+      x += np + naf;
+      const long long z = waiting(g, t - (long long)(x), m_.q);
+      ret = (long long)(x) + z;
+    } else {
+      ret = waiting(g, t, m_.q);
+    }
+    if (p12 != p) ret = t - ret;
+    return ret;
+  }
+
+ private:
+  struct Mirror {  // binomial_distribution<long long>::param_type (bits/random.h), in order
+    long long t;
+    double p, q, d1, d2, s1, s2, c, a1, a123, s, lf, lp1p;
+    bool easy;
+  };
+  static constexpr long long kWin = 4096;
+  template <class G>
+  static double canon(G& g) {  // __detail::_Adaptor<G, double>
+    return std::generate_canonical<double, std::numeric_limits<double>::digits>(g);
+  }
+  template <class G>
+  static long long waiting(G& g, long long t, double q) {
+    long long x = 0;
+    double sum = 0.0;
+    do {
+      if (t == x) return x;
+      const double e = -std::log(1.0 - canon(g));
+      sum += e / (t - x);
+      x += 1;
+    } while (sum <= q);
+    return x - 1;
+  }
+  double lfx_direct(double x) const { return std::lgamma(np_ + x + 1) + std::lgamma(m_.t - (np_ + x) + 1); }
+  double lfx_of(double x) const {
+    const long long xi = (long long)x;  // an integer (floor) inside [-np, t - np]
+    const long long i = xi - lo_;
+    if (i >= 0 && i < (long long)lfx_.size()) return lfx_[size_t(i)];
+    return lfx_direct(x);
+  }
+  Mirror m_;
+  double np_ = 0.0;
+  long long lo_ = 0;
+  std::vector<double> lfx_;
+};
+
+// Binomial draws of fresh engines make_rng(seed): the projection nonzero count of a matrix.
+struct BinomialDraw {
+  FastBinomial dist;
+  BinomialDraw(uint64_t cells, double density) : dist((long long)cells, density) {}
+
+  // Draws for m fresh engines make_rng(seeds[i]) (no skipped outputs), a batch at a time with
   // their seeding recurrences primed together (a draw typically reads outputs 0..6).
   void batch(const uint64_t* seeds, size_t m, uint32_t* z, uint32_t* used) const {
-    constexpr int M = 8;
+    constexpr int M = LazyMt64::kBatch;
     for (size_t i0 = 0; i0 < m; i0 += M) {
       const int c = int(std::min<size_t>(M, m - i0));
       alignas(64) unsigned char mem[M * sizeof(LazyMt64)];
@@ -132,7 +276,6 @@ struct BinomialDraw {
       for (int j = 0; j < M; ++j) new (g + j) LazyMt64(seeds[i0 + size_t(j < c ? j : 0)]);
       LazyMt64::prime<M>(g, 156 + 8);
       for (int j = 0; j < c; ++j) {
-        std::binomial_distribution<long long> dist(param);
         z[i0 + size_t(j)] = uint32_t(dist(g[j]));
         used[i0 + size_t(j)] = uint32_t(g[j].consumed());
       }
@@ -143,7 +286,6 @@ struct BinomialDraw {
   uint64_t operator()(uint64_t seed, uint64_t skip, uint64_t* used) const {
     LazyMt64 g(seed);
     for (uint64_t i = 0; i < skip; ++i) g();
-    std::binomial_distribution<long long> dist(param);
     const long long z = dist(g);
     *used = g.consumed();
     return uint64_t(z);
