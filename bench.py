@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--classes", type=int, default=2, help="trunk-model classes (BASELINE config 5: 4)")
     p.add_argument("--density", type=float, default=0.0,
                    help="projection cell density (0 = the reference default; config 5 'dense' > 0)")
+    p.add_argument("--workers", type=int, default=0,
+                   help="host threads of the trainer (0 = this rank's share of the host's cores)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="skip the untimed per-kernel profile step")
@@ -341,10 +343,11 @@ def main():
     per_step = T * world
     total_trees = (args.warmup + args.steps + args.e2e_steps + 1) * per_step
 
+    # host threads split between the ranks sharing this host (one rank per GPU)
+    workers = args.workers or max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+
     def cfg_for(step):
         b = step * per_step + rank * T
-        # host threads split between the ranks sharing this host (one rank per GPU)
-        workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
         return sofg.TrainConfig(n_trees=total_trees, mode=args.mode, breakeven=args.breakeven, seed=args.seed,
                                 n_workers=workers, tree_begin=b, tree_end=b + T, cell_density=args.density)
 
@@ -478,7 +481,7 @@ def main():
                        "n_samples": args.n, "n_features": args.d, "trees_per_gpu_per_step": T,
                        "mode": args.mode, "breakeven": args.breakeven, "bin_count": 256, "seed": args.seed,
                        "classes": args.classes, "cell_density": args.density or "reference default",
-                       "parallelism": f"tree-sharded x{world}",
+                       "parallelism": f"tree-sharded x{world}", "host_threads_per_rank": workers,
                        "l2": f"inputs {args.n * args.d * 4 / 1e9:.2f} GB table (+ row-major copy) vs 126 MB L2",
                        "nodes_per_step": nodes / args.steps, "datagen_s": round(gen_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
