@@ -100,7 +100,8 @@ const char* sofg_version(void);
 int sofg_create(int device, sofg_ctx** out);
 int sofg_destroy(sofg_ctx* ctx);
 /* Upload a dataset (replaces constructing BasicColumnarDataset<float>, dataset.hpp:28-45).
- * labels: int32 in [0, class_count). Validates like the reference constructor.
+ * labels: int32 in [0, class_count). Validates like the reference constructor; class_count <= 64
+ * (more than 8 classes run the wide-class splitters, wide.cu; the reference has no bound).
  * X page-locked (e.g. from sofg_host_alloc): the copy is left in flight and overlaps the next
  * call's host work; keep X unchanged until the next training / download call on this context
  * returns. Pageable X: the copy has landed when this returns. */

@@ -134,8 +134,8 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   if (n < 1 || d < 1) throw std::invalid_argument("empty dataset");
   if (n >= (1ull << 31)) throw std::invalid_argument("n_samples must be < 2^31");
   if (k < 1) throw std::invalid_argument("class_count must be positive");
-  if (k > sofg::kMaxClasses)
-    throw std::invalid_argument("class_count > " + std::to_string(sofg::kMaxClasses) +
+  if (k > sofg::kMaxClassesWide)
+    throw std::invalid_argument("class_count > " + std::to_string(sofg::kMaxClassesWide) +
                                 " is not supported by the GPU splitter");
   for (uint64_t i = 0; i < n; ++i)  // dataset.hpp:41-44
     if (labels[i] < 0 || labels[i] >= k) throw std::invalid_argument("label id out of range");
@@ -371,7 +371,7 @@ int sofg_generate_trunk(sofg_ctx* c, uint64_t n, uint64_t d, int32_t k, uint64_t
     require_ctx(c);
     if (n < 2) throw std::invalid_argument("n_samples must be at least 2");
     if (d == 0) throw std::invalid_argument("n_features must be positive");
-    if (k < 1 || k > sofg::kMaxClasses) throw std::invalid_argument("class_count out of range");
+    if (k < 1 || k > sofg::kMaxClassesWide) throw std::invalid_argument("class_count out of range");
     std::vector<int32_t> y(n);
     for (uint64_t i = 0; i < n; ++i) y[i] = int32_t(i % uint64_t(k));
     upload(c, n, d, y.data(), k, [&](float* dev, uint64_t ld) {
@@ -832,7 +832,7 @@ int sofg_find_node_split(sofg_ctx* c, const uint32_t* active, uint64_t n, const 
     }
     w.given_row_ptr.assign(row_ptr, row_ptr + R + 1);
     w.given_pos = {uint32_t(skip)};
-    uint32_t counts[sofg::kMaxClasses] = {0};
+    std::vector<uint32_t> counts(size_t(D.k), 0u);
     std::vector<uint8_t> l8(n);
     for (uint64_t i = 0; i < n; ++i) {
       l8[i] = uint8_t(D.labels_host[active[i]]);
@@ -845,7 +845,7 @@ int sofg_find_node_split(sofg_ctx* c, const uint32_t* active, uint64_t n, const 
     nd.z = uint32_t(nnz);
     nd.pos = uint32_t(skip);
     nd.flags = sofg::kNodeGivenCsr | (method == 1 ? sofg::kNodeHist : 0u);
-    nd.parent = sofg::host::entropy(counts, D.k);
+    nd.parent = sofg::host::entropy(counts.data(), D.k);
     w.nodes = {nd};
     cudaStream_t st = c->eng->stream();
     DevBuf<uint32_t> di, dio;

@@ -58,7 +58,7 @@ class WaveProbe {
     binom_.batch(seeds.data(), M, z.data(), used.data());
     uint64_t term_off = 0;
     for (uint64_t i = 0; i < M; ++i) {
-      uint32_t counts[kMaxClasses] = {};
+      std::vector<uint32_t> counts(size_t(D.k), 0u);
       for (uint64_t j = 0; j < n; ++j) {
         const uint64_t q = i * n + j;
         const uint32_t s = uint32_t((q * 0x9E3779B97F4A7C15ull >> 17) % D.n);
@@ -74,7 +74,7 @@ class WaveProbe {
       nd.z = z[i];
       nd.pos = used[i];
       nd.term_off = uint32_t(term_off);
-      nd.parent = host::entropy(counts, D.k);
+      nd.parent = host::entropy(counts.data(), D.k);
       term_off += z[i];
     }
     cudaStream_t st = eng_.stream();

@@ -15,7 +15,8 @@
 
 namespace sofg {
 
-constexpr int kMaxClasses = 8;       // class_count supported by the kernels
+constexpr int kMaxClasses = 8;       // class counts carried inline (NodeRes, host frontier, register kernels)
+constexpr int kMaxClassesWide = 64;  // class_count supported (above kMaxClasses: wide.cu, side arrays)
 constexpr int kMaxBins = 1024;       // bin_count supported by the histogram splitter
 constexpr int kExactSmemMax = 2048;  // largest node the shared-memory exact splitter sorts
 constexpr int kTileElems = 1024;     // partition tile

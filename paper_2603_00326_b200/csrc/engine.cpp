@@ -128,7 +128,9 @@ void WaveRunner::submit(const WaveSpec& w) {
   // merged in the global counters like the lane = sample kernel's multi-chunk nodes.
   static const uint32_t lr_chunk_env =
       std::getenv("SOFG_HIST_LR_CHUNK") ? uint32_t(std::atoi(std::getenv("SOFG_HIST_LR_CHUNK"))) : 32768u;
-  const bool lr_ok = k == 2 && bins <= 256 && (lr_env >= 0 ? lr_env != 0 : hist_count_lane_rows(R, bins, k));
+  const bool wide = k > kMaxClasses;  // wide.cu kernels, class counts in side arrays
+  constexpr uint32_t kWideChunk = 65535;  // u16 counters per CTA
+  const bool lr_ok = !wide && k == 2 && bins <= 256 && (lr_env >= 0 ? lr_env != 0 : hist_count_lane_rows(R, bins, k));
   const uint32_t lr_max = lr_ok ? (lr_env == 1 ? 0xffffffffu : lr_max_env) : 0u;
   const uint32_t lr_chunk = std::max(1024u, std::min(lr_chunk_env, 65504u));
   const uint32_t groups = (R + kHistRowsPerCta - 1) / kHistRowsPerCta;
@@ -137,6 +139,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   struct Cnt {
     uint64_t hist = 0, multi = 0, work = 0, work_lr = 0, tiles = 0, g = 0, items = 0;
     uint32_t lr_len = 0;  // longest lane = row chunk
+    uint32_t exact_nmax = 0;  // largest shared-memory exact node
     uint64_t exact[kExactBuckets] = {};
     uint32_t zmax = 32;
     uint64_t terms_end = 0;
@@ -164,7 +167,11 @@ void WaveRunner::submit(const WaveSpec& w) {
         t.terms_end = std::max<uint64_t>(t.terms_end, uint64_t(nd.term_off) + nd.z);
         if (nd.flags & kNodeHist) {
           t.hist++;
-          if (nd.n <= lr_max) {
+          if (wide) {  // one item per (row, chunk of <= 65535 samples): wide.cu
+            const uint32_t chunks = (nd.n + kWideChunk - 1) / kWideChunk;
+            if (chunks > 1) t.multi++;
+            t.work += uint64_t(R) * chunks;
+          } else if (nd.n <= lr_max) {
             const uint32_t chunks = (nd.n + lr_chunk - 1) / lr_chunk;
             if (chunks > 1) t.multi++;
             t.work_lr += uint64_t(groups_lr) * chunks;
@@ -178,6 +185,7 @@ void WaveRunner::submit(const WaveSpec& w) {
           t.big++;  // device-wide segmented sort path (exact_big.cu)
         } else {
           t.exact[exact_bucket(nd.n)]++;
+          t.exact_nmax = std::max(t.exact_nmax, nd.n);
         }
         t.tiles += (nd.n + kTileElems - 1) / kTileElems;
         t.g += uint64_t(vpitch(R)) * nd.n;
@@ -207,6 +215,7 @@ void WaveRunner::submit(const WaveSpec& w) {
     tot.big += cc[c].big;
     tot.zmax = std::max(tot.zmax, cc[c].zmax);
     tot.lr_len = std::max(tot.lr_len, cc[c].lr_len);
+    tot.exact_nmax = std::max(tot.exact_nmax, cc[c].exact_nmax);
     tot.terms_end = std::max(tot.terms_end, cc[c].terms_end);
   }
   uint64_t bucket_base[kExactBuckets + 1] = {0};
@@ -272,7 +281,15 @@ void WaveRunner::submit(const WaveSpec& w) {
       if (nd.flags & kNodeHist) {
         p_hslot[i] = uint32_t(o.hist);
         p_hist[o.hist++] = uint32_t(i);
-        if (nd.n <= lr_max) {  // lane = row items after the lane = sample ones
+        if (wide) {
+          const uint32_t chunks = (nd.n + kWideChunk - 1) / kWideChunk;
+          if (chunks > 1) p_mslot[i] = uint32_t(o.multi++);
+          for (uint32_t r = 0; r < R; ++r)
+            for (uint32_t ch = 0; ch < chunks; ++ch) {
+              const uint32_t s0 = ch * kWideChunk;
+              p_work[o.work++] = {uint32_t(i), r, s0, std::min(nd.n - s0, kWideChunk), ch, chunks};
+            }
+        } else if (nd.n <= lr_max) {  // lane = row items after the lane = sample ones
           const uint32_t chunks = (nd.n + lr_chunk - 1) / lr_chunk;
           if (chunks > 1) p_mslot[i] = uint32_t(o.multi++);
           for (uint32_t g = 0; g < groups_lr; ++g)
@@ -343,8 +360,14 @@ void WaveRunner::submit(const WaveSpec& w) {
   float* d_bnd = bnd_.ensure(std::max<size_t>(1, nh * R * (bins - 1)));
   uint32_t* d_nb = nb_.ensure(std::max<size_t>(1, nh * R));
   RowRes* d_rowres = rowres_.ensure(std::max<size_t>(1, nh * R));
-  uint32_t* d_gcnt = gcnt_.ensure(std::max<size_t>(1, size_t(n_multi) * R * bpad * k));
-  uint32_t* d_done = done_.ensure(std::max<size_t>(1, size_t(n_multi) * groups));
+  // multi-chunk counters: [slot][R][bpad][2] (lane = row), [slot][R][bins][k] (wide), [slot][R][bpad][k]
+  const size_t gcnt_n = size_t(n_multi) * R * std::max<size_t>(bpad, bins) * size_t(k);
+  const size_t done_n = size_t(n_multi) * std::max<size_t>(groups, R);
+  uint32_t* d_gcnt = gcnt_.ensure(std::max<size_t>(1, gcnt_n));
+  uint32_t* d_done = done_.ensure(std::max<size_t>(1, done_n));
+  // wide: the partition's left class counts [N][k] (NodeRes carries kMaxClasses), exact row results
+  uint32_t* d_cl = wide ? cl_.ensure(size_t(N) * size_t(k)) : nullptr;
+  RowRes* d_rowres_ex = wide ? rowres_ex_.ensure(std::max<size_t>(1, size_t(exact_total) * R)) : nullptr;
   NodeRes* d_res = res_.ensure(size_t(N));
   float* d_G = V_.ensure(std::max<uint64_t>(1, g_total));
   // Projection stage: sweep the row-major table when the wave's gathers would touch a sizeable
@@ -361,9 +384,10 @@ void WaveRunner::submit(const WaveSpec& w) {
 
   cuda_check(cudaMemsetAsync(d_res, 0, sizeof(NodeRes) * N, st_), "memset res");
   if (n_multi) {
-    cuda_check(cudaMemsetAsync(d_gcnt, 0, 4 * size_t(n_multi) * R * bpad * k, st_), "memset gcnt");
-    cuda_check(cudaMemsetAsync(d_done, 0, 4 * size_t(n_multi) * groups, st_), "memset done");
+    cuda_check(cudaMemsetAsync(d_gcnt, 0, 4 * gcnt_n, st_), "memset gcnt");
+    cuda_check(cudaMemsetAsync(d_done, 0, 4 * done_n, st_), "memset done");
   }
+  if (wide) cuda_check(cudaMemsetAsync(d_cl, 0, 4 * size_t(N) * size_t(k), st_), "memset class counts");
 
   const bool timing = collect_stats;
   if (sector_accounting)
@@ -446,7 +470,11 @@ void WaveRunner::submit(const WaveSpec& w) {
                                       bins, int(std::max(tot.lr_len, 32u)), w.two_level ? 1 : 0, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
                                       D.xl.p, d_gcnt, d_done, d_rowres, st_),
                  "hist_count_lr");
-    if (n_work_old)
+    if (n_work_old && wide)
+      cuda_check(launch_hist_wide(d_nodes, d_hslot, d_work, int(n_work_old), d_mslot, R, bins, k, w.two_level ? 1 : 0,
+                                  w.lab_in, d_gbase, d_G, d_bnd, d_nb, D.xl.p, d_gcnt, d_done, d_rowres, st_),
+                 "hist_wide");
+    else if (n_work_old)
       cuda_check(launch_hist_count(d_nodes, d_hslot, d_work, int(n_work_old), d_mslot, R, bins, k,
                                    w.chunk_cap, w.two_level ? 1 : 0, d_terms, d_rp, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
                                    D.xl.p, d_gcnt, d_done, d_rowres, st_),
@@ -485,8 +513,16 @@ void WaveRunner::submit(const WaveSpec& w) {
       ++launches;
       mark("exact_prune");
     }
+    if (wide && exact_total) {  // every shared-memory exact node at once, then its best row
+      cuda_check(launch_exact_wide(d_nodes, d_exact, int(exact_total), tot.exact_nmax, R, k, d_rp, w.lab_in, d_gbase,
+                                   d_G, D.xl.p, d_rowres_ex, st_),
+                 "exact_wide");
+      cuda_check(launch_hist_select(d_exact, int(exact_total), R, d_rowres_ex, d_res, st_), "exact_wide_select");
+      launches += 2;
+      mark("exact_wide");
+    }
     size_t off = 0;
-    for (int b = 0; b < kExactBuckets; ++b) {
+    for (int b = 0; b < kExactBuckets && !wide; ++b) {
       const size_t m = exact_b_count[size_t(b)];
       if (!m) continue;
       const bool pb = prune && b >= kPruneFrom;
@@ -518,7 +554,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   if (timing) cudaEventRecord(ev_[4], st_);
   cuda_check(launch_partition(d_nodes, N, d_tiles, int(n_tiles), d_tfirst, R, k, d_terms,
                               d_rp, d_pos_proj, d_pos_split, w.idx_in, w.lab_in, w.idx_out,
-                              w.lab_out, d_gbase, d_G, d_res, d_flags, d_tleft, w.inv, w.B, st_),
+                              w.lab_out, d_gbase, d_G, d_res, d_flags, d_tleft, w.inv, w.B, d_cl, st_),
              "partition");
   launches += 3;
   mark("partition");
@@ -529,6 +565,12 @@ void WaveRunner::submit(const WaveSpec& w) {
   h_res_p_ = hr;
   cuda_check(cudaMemcpyAsync(hr, d_res, sizeof(NodeRes) * N, cudaMemcpyDeviceToHost, st_),
              "D2H res");
+  h_cl_p_ = nullptr;
+  if (wide) {
+    uint32_t* hc = h_cl_buf_[h_res_cur_].ensure(size_t(N) * size_t(k));
+    h_cl_p_ = hc;
+    cuda_check(cudaMemcpyAsync(hc, d_cl, 4 * size_t(N) * size_t(k), cudaMemcpyDeviceToHost, st_), "D2H class counts");
+  }
   cuda_check(cudaEventRecord(done_ev_, st_), "record wave end");
   pend_dres_ = d_res;
   pend_launches_ = launches;

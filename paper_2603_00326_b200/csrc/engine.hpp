@@ -218,6 +218,9 @@ class WaveRunner {
   void collect(const WaveSpec& w, std::vector<NodeRes>& res);
   // Same wait, no copy: the node results in page-locked memory, valid until the next submit().
   const NodeRes* collect_view(const WaveSpec& w);
+  // More than kMaxClasses classes: the partition's left class counts of the collected wave,
+  // [node][k] (NodeRes::left_counts is not filled); nullptr otherwise.
+  const uint32_t* class_counts_view() const { return h_cl_p_; }
   // Only the wait for the wave (no host pool use): callers sharing a pool wait first, then
   // take their host turn and call collect_view().
   bool last_was_sweep() const { return pend_sweep_; }
@@ -269,6 +272,10 @@ class WaveRunner {
   PinnedBuf<NodeRes> h_res_buf_[2];  // alternate per wave: a wave's results stay readable while
   int h_res_cur_ = 0;                 // the next wave's are copied back
   NodeRes* h_res_p_ = nullptr;
+  PinnedBuf<uint32_t> h_cl_buf_[2];   // wide classes: left class counts [N][k], same alternation
+  uint32_t* h_cl_p_ = nullptr;
+  DevBuf<uint32_t> cl_;
+  DevBuf<RowRes> rowres_ex_;          // wide classes: exact results per (node, row)
   // device scratch
   DevBuf<uint32_t> terms_, row_ptr_, pos_proj_, pos_split_, draws_, nb_, flags_, tile_left_,
       gcnt_, done_, sectors_;

@@ -20,6 +20,7 @@
 #include "common.hpp"
 #include "dev_util.cuh"
 #include "kernels.hpp"
+#include "wide.cuh"
 
 namespace sofg {
 namespace dev {
@@ -163,6 +164,28 @@ __global__ void __launch_bounds__(kBigThreads) k_big_scan(const NodeIn* __restri
   }
 }
 
+// More than kMaxClasses classes: one CTA per segment, class counts in shared memory (wide.cuh).
+__global__ void __launch_bounds__(kWideThreads) k_big_scan_wide(const NodeIn* __restrict__ nodes,
+                                                                const BigSeg* __restrict__ segs, uint32_t R, int k,
+                                                                const uint32_t* __restrict__ row_ptr,
+                                                                const uint64_t* __restrict__ keys,
+                                                                const double* __restrict__ xl,
+                                                                RowRes* __restrict__ rowres) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const BigSeg sg = segs[blockIdx.x];
+  const NodeIn nd = nodes[sg.node];
+  const uint32_t* rp = row_ptr + size_t(sg.node) * (R + 1);
+  if (rp[sg.row + 1] == rp[sg.row]) {  // empty rows are skipped in exact mode (split.hpp:308)
+    if (threadIdx.x == 0) rowres[blockIdx.x] = RowRes{};
+    return;
+  }
+  const WideShared s = wide_carve(smem_raw, k);
+  const uint64_t* kk = keys + sg.off;
+  const RowRes rr = wide_exact_scan([&](uint32_t p) { return __ldg(kk + p); }, nd.n, k, nd.parent, xl, s.base,
+                                    s.run, s.tot, nullptr, s.red, s.ured);
+  if (threadIdx.x == 0) rowres[blockIdx.x] = rr;
+}
+
 // Best row of each big node: rows arrive in increasing order per node (segments are node-major).
 __global__ void k_big_select(const BigSeg* __restrict__ segs, int n_nodes, uint32_t R,
                              const RowRes* __restrict__ rowres, NodeRes* __restrict__ res) {
@@ -238,8 +261,11 @@ cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const u
     if (e) return e;
     if (k == 2)
       dev::k_big_scan<2><<<nseg, dev::kBigThreads, 0, st>>>(nodes, d_segs, R, k, row_ptr, d_k1, xl, d_rr);
-    else
+    else if (k <= kMaxClasses)
       dev::k_big_scan<kMaxClasses><<<nseg, dev::kBigThreads, 0, st>>>(nodes, d_segs, R, k, row_ptr, d_k1, xl, d_rr);
+    else
+      dev::k_big_scan_wide<<<nseg, dev::kWideThreads, dev::wide_carve_bytes(k), st>>>(nodes, d_segs, R, k, row_ptr,
+                                                                                     d_k1, xl, d_rr);
     dev::k_big_select<<<(nn + 127) / 128, 128, 0, st>>>(d_segs, nn, R, d_rr, res);
     e = cudaGetLastError();
     if (e) return e;

@@ -126,7 +126,8 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint32_t* pos_split, const uint32_t* idx_in,
                              const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
                              const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
-                             uint32_t* tile_left, uint32_t* inv, uint32_t B, cudaStream_t st);
+                             uint32_t* tile_left, uint32_t* inv, uint32_t B, uint32_t* class_left,
+                             cudaStream_t st);  // class_left: [node][k] when k > kMaxClasses, else nullptr
 
 cudaError_t launch_win_terms(const NodeIn* nodes, const NodeRes* res, const uint32_t* row_ptr,
                              const uint32_t* terms, uint32_t R, const uint32_t* list, int n_list,
@@ -135,9 +136,10 @@ cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_ti
                                 const uint32_t* idx, NodeRes* res, cudaStream_t st);
 
 // misc.cu
+// lab_out[p] = labels[idx[p]]; counts[b * k + c] = class-c count of tree b's root segment
 cudaError_t launch_root_labels(const uint32_t* idx, const uint64_t* off, uint32_t B,
                                uint64_t max_per_tree, const uint8_t* labels, uint8_t* lab_out,
-                               uint32_t* counts, cudaStream_t st);
+                               int k, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_generate_trunk(float* X, uint64_t ld, uint8_t* labels, uint64_t n, uint64_t d,
                                   int k, uint64_t seed, cudaStream_t st);
 cudaError_t launch_apply_projection(const float* X, uint64_t ld, const uint32_t* terms, int nt,
@@ -147,5 +149,18 @@ cudaError_t launch_predict(const float* rows, uint64_t n_rows, uint64_t d, const
                            int n_trees, const int32_t* left, const int32_t* right,
                            const int32_t* pred, const float* thr, const int64_t* term_off,
                            const uint32_t* terms, int k, uint32_t* votes, cudaStream_t st);
+
+// wide.cu: more than kMaxClasses classes (RowRes per (node, row); k_hist_select picks the row)
+size_t exact_wide_smem(uint32_t nmax, int k);
+cudaError_t launch_exact_wide(const NodeIn* nodes, const uint32_t* list, int n_list, uint32_t nmax, uint32_t R,
+                              int k, const uint32_t* row_ptr, const uint8_t* lab, const uint64_t* gbase,
+                              const float* G, const double* xl, RowRes* rowres, cudaStream_t st);
+size_t hist_wide_smem(uint32_t bins, int k);
+// work items: one per (node, row = row0, chunk of <= 65535 samples)
+cudaError_t launch_hist_wide(const NodeIn* nodes, const uint32_t* node_hist_slot, const HistWork* work, int n_work,
+                             const uint32_t* multi_slot, uint32_t R, uint32_t bins, int k, int two_level,
+                             const uint8_t* lab, const uint64_t* gbase, const float* G, const float* bnd,
+                             const uint32_t* nb, const double* xl, uint32_t* gcnt, uint32_t* done, RowRes* rowres,
+                             cudaStream_t st);
 
 }  // namespace sofg

@@ -79,41 +79,38 @@ __global__ void k_predict(const float* __restrict__ rows, uint64_t n_rows, uint6
 __global__ void __launch_bounds__(256) k_root_labels(const uint32_t* __restrict__ idx,
                                                      const uint64_t* __restrict__ off,
                                                      const uint8_t* __restrict__ labels,
-                                                     uint8_t* __restrict__ lab_out,
+                                                     uint8_t* __restrict__ lab_out, int k,
                                                      uint32_t* __restrict__ counts) {
-  __shared__ uint32_t s_cnt[kMaxClasses];
+  __shared__ uint32_t s_cnt[kMaxClassesWide];
   const uint32_t b = blockIdx.y;
-  if (threadIdx.x < kMaxClasses) s_cnt[threadIdx.x] = 0;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) s_cnt[c] = 0;
   __syncthreads();
-  uint32_t c[kMaxClasses] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (uint64_t p = off[b] + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < off[b + 1];
-       p += uint64_t(gridDim.x) * blockDim.x) {
-    const uint8_t y = labels[idx[p]];
-    lab_out[p] = y;
-#pragma unroll
-    for (int k = 0; k < kMaxClasses; ++k) c[k] += (k == int(y));
-  }
-#pragma unroll
-  for (int k = 0; k < kMaxClasses; ++k) {
-    uint32_t x = c[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_cnt[k], x);
+  const int lane = threadIdx.x & 31;
+  const uint64_t p1 = off[b + 1];
+  for (uint64_t p0 = off[b] + uint64_t(blockIdx.x) * blockDim.x; p0 < p1; p0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = p0 + threadIdx.x;
+    int y = -1;
+    if (p < p1) {
+      y = labels[idx[p]];
+      lab_out[p] = uint8_t(y);
+    }
+    const unsigned same = __match_any_sync(0xffffffffu, y);  // one shared atomic per distinct label
+    if (y >= 0 && (__ffs(same) - 1) == lane) atomicAdd(&s_cnt[y], uint32_t(__popc(same)));
   }
   __syncthreads();
-  if (threadIdx.x < kMaxClasses && s_cnt[threadIdx.x])
-    atomicAdd(&counts[size_t(b) * kMaxClasses + threadIdx.x], s_cnt[threadIdx.x]);
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    if (s_cnt[c]) atomicAdd(&counts[size_t(b) * k + c], s_cnt[c]);
 }
 
 }  // namespace dev
 
 cudaError_t launch_root_labels(const uint32_t* idx, const uint64_t* off, uint32_t B,
                                uint64_t max_per_tree, const uint8_t* labels, uint8_t* lab_out,
-                               uint32_t* counts, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(uint32_t) * kMaxClasses * B, st);
+                               int k, uint32_t* counts, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(uint32_t) * size_t(k) * B, st);
   if (e != cudaSuccess || B == 0) return e;
   const unsigned gx = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((max_per_tree + 255) / 256, 256)));
-  dev::k_root_labels<<<dim3(gx, B), 256, 0, st>>>(idx, off, labels, lab_out, counts);
+  dev::k_root_labels<<<dim3(gx, B), 256, 0, st>>>(idx, off, labels, lab_out, k, counts);
   return cudaGetLastError();
 }
 

@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(256) k_part_scatter(
 __global__ void __launch_bounds__(256) k_part_flags_w(
     const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, int n_tiles, uint32_t R, int k,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase, const float* __restrict__ G,
-    NodeRes* __restrict__ res, uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_left) {
+    NodeRes* __restrict__ res, uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_left,
+    uint32_t* __restrict__ class_left) {
   const int lane = threadIdx.x & 31;
   const int ti = int(blockIdx.x) * 8 + int(threadIdx.x >> 5);
   if (ti >= n_tiles) return;
@@ -189,7 +190,11 @@ __global__ void __launch_bounds__(256) k_part_flags_w(
     }
     const unsigned m = __ballot_sync(0xffffffffu, f);
     if (lane == 0) flags[size_t(ti) * 32 + wd] = m;
-    if (f) {
+    if (class_left) {  // more than kMaxClasses classes: one atomic per distinct label of the step
+      const unsigned same = __match_any_sync(0xffffffffu, f ? int(y) : -1);
+      if (f && (__ffs(same) - 1) == lane) atomicAdd(&class_left[size_t(tl.node) * k + y], uint32_t(__popc(same)));
+      my_left += f ? 1u : 0u;
+    } else if (f) {
       ++my_left;
 #pragma unroll
       for (int c = 0; c < kMaxClasses; ++c) cls[c] += (c == int(y));
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(256) k_part_flags_w(
   if (lane == 0) tile_left[ti] = my_left;
 #pragma unroll
   for (int c = 0; c < kMaxClasses; ++c) {
-    if (c >= k) break;
+    if (c >= k || class_left) break;
     uint32_t x = cls[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -307,15 +312,16 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint32_t* pos_split, const uint32_t* idx_in,
                              const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
                              const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
-                             uint32_t* tile_left, uint32_t* inv, uint32_t B, cudaStream_t st) {
+                             uint32_t* tile_left, uint32_t* inv, uint32_t B, uint32_t* class_left,
+                             cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
-  static const bool cta_tiles = std::getenv("SOFG_PART_CTA") != nullptr;  // CTA-per-tile forms
+  const bool cta_tiles = std::getenv("SOFG_PART_CTA") != nullptr && !class_left;  // CTA-per-tile forms
   if (n_tiles > 0 && cta_tiles)
     dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, lab_in, gbase,
                                                G, res, flags, tile_left);
   else if (n_tiles > 0)
     dev::k_part_flags_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, R, k, lab_in, gbase, G, res,
-                                                           flags, tile_left);
+                                                           flags, tile_left, class_left);
   dev::k_part_scan<<<(n_nodes + 3) / 4, 128, 0, st>>>(nodes, n_nodes, R, tile_first, terms,
                                                       row_ptr, pos_proj, pos_split, tile_left, res);
   if (n_tiles > 0 && cta_tiles)

@@ -152,6 +152,7 @@ struct GrowScratch {
   std::vector<std::vector<BNode>> trees;
   std::vector<std::vector<uint32_t>> pools;
   std::vector<std::vector<Open>> fr, sp, nx, rt, dn;
+  std::vector<std::vector<uint32_t>> wide;  // class counts per tree node (k > kMaxClasses)
   std::vector<uint32_t> spec_z, spec_pos;
   std::vector<NodeIn> nodes;
 };
@@ -197,25 +198,25 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
   for (size_t b = 0; b < B; ++b) maxn = std::max<uint64_t>(maxn, roots[b].size());
   DevBuf<uint64_t>& d_off = eng.tree_off;
   d_off.ensure(B + 1);
-  std::vector<uint32_t> root_counts(B * kMaxClasses);
+  std::vector<uint32_t> root_counts(B * size_t(k));
   {
-    unsigned char* stg = eng.staging.ensure(4 * total + 8 * (B + 1) + 4 * kMaxClasses * B);
+    unsigned char* stg = eng.staging.ensure(4 * total + 8 * (B + 1) + 4 * size_t(k) * B);
     uint32_t* hi = reinterpret_cast<uint32_t*>(stg);
     uint64_t* ho = reinterpret_cast<uint64_t*>(stg + 4 * total);
     uint32_t* hc = reinterpret_cast<uint32_t*>(stg + 4 * total + 8 * (B + 1));
     pool.parallel_for(B, [&](size_t b) { std::memcpy(hi + off[b], roots[b].data(), 4 * roots[b].size()); });
     std::memcpy(ho, off.data(), 8 * (B + 1));
     DevBuf<uint32_t>& d_cnt = eng.root_counts;
-    d_cnt.ensure(kMaxClasses * B);
+    d_cnt.ensure(size_t(k) * B);
     cuda_check(cudaMemcpyAsync(idx[0].p, hi, 4 * total, cudaMemcpyHostToDevice, eng.stream()), "H2D idx");
     cuda_check(cudaMemcpyAsync(d_off.p, ho, 8 * (B + 1), cudaMemcpyHostToDevice, eng.stream()), "H2D off");
-    cuda_check(launch_root_labels(idx[0].p, d_off.p, uint32_t(B), maxn, D.lab.p, lab[0].p, d_cnt.p,
+    cuda_check(launch_root_labels(idx[0].p, d_off.p, uint32_t(B), maxn, D.lab.p, lab[0].p, k, d_cnt.p,
                                   eng.stream()),
                "root_labels");
-    cuda_check(cudaMemcpyAsync(hc, d_cnt.p, 4 * kMaxClasses * B, cudaMemcpyDeviceToHost, eng.stream()),
+    cuda_check(cudaMemcpyAsync(hc, d_cnt.p, 4 * size_t(k) * B, cudaMemcpyDeviceToHost, eng.stream()),
                "D2H root counts");
     cuda_check(cudaStreamSynchronize(eng.stream()), "root sync");
-    std::memcpy(root_counts.data(), hc, 4 * kMaxClasses * B);
+    std::memcpy(root_counts.data(), hc, 4 * size_t(k) * B);
   }
   // Inverse map for the projection sweep (sweep.cu): needs each tree's samples to be distinct
   // (bootstrap_sample returns a sorted set; explicit active sets are checked).
@@ -244,10 +245,18 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
   static thread_local GrowScratch S;
   std::vector<std::vector<BNode>>& trees = S.trees;
   std::vector<std::vector<uint32_t>>& pools = S.pools;
+  // More than kMaxClasses classes: class counts live in per-tree side arrays (node v of tree b at
+  // wc[b][v * k, v * k + k)) instead of Open::counts; the wave returns left counts the same way.
+  const bool wide = k > kMaxClasses;
+  std::vector<std::vector<uint32_t>>& wc = S.wide;
   if (trees.size() < B) {
     trees.resize(B);
     pools.resize(B);
   }
+  if (wide && wc.size() < B) wc.resize(B);
+  auto counts_of = [&](const Open& o) -> const uint32_t* {
+    return wide ? wc[o.tree].data() + size_t(o.bnode) * size_t(k) : o.counts;
+  };
   // The frontier is kept in P parts; part p owns trees [B*p/P, B*(p+1)/P), so parts are processed
   // in parallel without sharing a tree and never need to be concatenated.
   const size_t NP = std::max<size_t>(1, std::min<size_t>(B, size_t(pool.size()) * 4));
@@ -270,7 +279,10 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
       o.n = uint32_t(roots[b].size());
       o.depth = root_depth;
       o.seed = root_seeds[b];
-      for (int c = 0; c < k; ++c) o.counts[c] = root_counts[b * kMaxClasses + size_t(c)];
+      if (wide)
+        wc[b].assign(root_counts.begin() + ptrdiff_t(b * size_t(k)), root_counts.begin() + ptrdiff_t((b + 1) * size_t(k)));
+      else
+        for (int c = 0; c < k; ++c) o.counts[c] = root_counts[b * size_t(k) + size_t(c)];
       fr[p].push_back(o);
     }
   });
@@ -305,12 +317,12 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
   };
 
   // forest.hpp:178-179: a node is split iff it is impure, large enough and above max_depth
-  auto can_split = [&](const Open& o) {
+  auto can_split_c = [&](const uint32_t* counts, uint32_t n, uint32_t depth) {
     uint32_t top = 0;
-    for (int cc = 0; cc < k; ++cc) top = std::max(top, o.counts[cc]);
-    return top < o.n && o.n >= P.min_samples_split && o.n >= 2 &&
-           (!P.max_depth || o.depth < *P.max_depth);
+    for (int cc = 0; cc < k; ++cc) top = std::max(top, counts[cc]);
+    return top < n && n >= P.min_samples_split && n >= 2 && (!P.max_depth || depth < *P.max_depth);
   };
+  auto can_split = [&](const Open& o) { return can_split_c(counts_of(o), o.n, o.depth); };
   // The roots are filtered here; children are filtered when they are created (post below), so
   // every later level's frontier is already the list of nodes to split.
   pool.parallel_for(NP, [&](size_t p) {
@@ -319,7 +331,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
       if (can_split(o))
         keep.push_back(o);
       else
-        trees[o.tree][size_t(o.bnode)].pred = argmax_first(o.counts, k);  // forest.hpp:233-236
+        trees[o.tree][size_t(o.bnode)].pred = argmax_first(counts_of(o), k);  // forest.hpp:233-236
     }
     fr[p].swap(keep);
   });
@@ -359,21 +371,22 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
           }
           tr.emplace_back();
           tr.emplace_back();
-          uint32_t lc[kMaxClasses] = {}, rc[kMaxClasses] = {};
-          for (int c = 0; c < k; ++c) {
-            lc[c] = r.left_counts[c];
-            rc[c] = o.counts[c] - r.left_counts[c];
+          uint32_t lcb[kMaxClasses] = {}, rcb[kMaxClasses] = {};
+          const uint32_t* lc = lcb;
+          const uint32_t* rc = rcb;
+          if (wide) {  // written by the critical pass (post) at the children's node ids
+            lc = wc[o.tree].data() + size_t(L) * size_t(k);
+            rc = lc + k;
+          } else {
+            for (int c = 0; c < k; ++c) {
+              lcb[c] = r.left_counts[c];
+              rcb[c] = o.counts[c] - r.left_counts[c];
+            }
           }
-          Open l{}, rr{};
-          l.n = r.n_left;
-          rr.n = o.n - r.n_left;
-          l.depth = rr.depth = o.depth + 1;
-          std::memcpy(l.counts, lc, sizeof(lc));
-          std::memcpy(rr.counts, rc, sizeof(rc));
-          if (!can_split(l)) tr[size_t(L)].pred = argmax_first(lc, k);
-          if (!can_split(rr)) tr[size_t(L) + 1].pred = argmax_first(rc, k);
+          if (!can_split_c(lc, r.n_left, o.depth + 1)) tr[size_t(L)].pred = argmax_first(lc, k);
+          if (!can_split_c(rc, o.n - r.n_left, o.depth + 1)) tr[size_t(L) + 1].pred = argmax_first(rc, k);
         } else if (o.attempt >= P.max_split_retries) {
-          tr[size_t(o.bnode)].pred = argmax_first(o.counts, k);
+          tr[size_t(o.bnode)].pred = argmax_first(counts_of(o), k);
         }
       }
     });
@@ -407,7 +420,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
             o.has_z = 1;
           }
           NodeIn& nd = w.nodes[poff[p] + j];
-          nd.parent = host::entropy(o.counts, k);
+          nd.parent = host::entropy(counts_of(o), k);
           nd.seed = o.seed;
           nd.begin = o.begin;
           nd.n = o.n;
@@ -486,6 +499,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
         if (!more) P.idle_work = nullptr;
       }
       const NodeRes* res = eng.collect_view(w);
+      const uint32_t* wcl = eng.class_counts_view();  // wide classes: left counts [node][k]
       prev_wave_ms = ms_since(t_submit);
       const double lv_wait = ms_since(t0);
       if (std::getenv("SOFG_WAVE_HASH")) {  // debugging aid: per-wave result digest
@@ -560,9 +574,21 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
             rr.z = spec_z[2 * i + 1];
             rr.zpos = spec_pos[2 * i + 1];
             l.has_z = rr.has_z = 1;
-            for (int c = 0; c < k; ++c) {
-              l.counts[c] = r.left_counts[c];
-              rr.counts[c] = o.counts[c] - r.left_counts[c];
+            if (wide) {  // children's counts at node ids L, L + 1 of the tree's side array
+              std::vector<uint32_t>& v = wc[o.tree];
+              if (v.size() < size_t(L + 2) * size_t(k)) v.resize(std::max(v.size() * 2, size_t(L + 2) * size_t(k)));
+              const uint32_t* pc = v.data() + size_t(o.bnode) * size_t(k);
+              const uint32_t* cl = wcl + i * size_t(k);
+              uint32_t* lc = v.data() + size_t(L) * size_t(k);
+              for (int c = 0; c < k; ++c) {
+                lc[c] = cl[c];
+                lc[k + c] = pc[c] - cl[c];
+              }
+            } else {
+              for (int c = 0; c < k; ++c) {
+                l.counts[c] = r.left_counts[c];
+                rr.counts[c] = o.counts[c] - r.left_counts[c];
+              }
             }
             if (can_split(l)) nx[p].push_back(l);
             if (can_split(rr)) nx[p].push_back(rr);
