@@ -2,20 +2,20 @@
 // shared-memory splitter's range (reference best_split_exact, split.hpp:142-194, for every
 // non-empty row, split.hpp:306-312).
 //
-//  1. k_big_keys    per (node, row) segment: the reference's packed sort key
-//                   order_key(v) << 32 | label for every sample, from the wave's V block;
-//  2. cub::DeviceSegmentedRadixSort sorts every segment (device-wide, all segments at once);
-//  3. k_big_scan    one CTA per segment: block scans of the class counts over the sorted keys,
-//                   impurity at every gap between distinct values in the reference's FP64 order,
-//                   minimum X, then the first position whose gain equals the best (first maximum);
-//  4. k_big_select  best row per node (strict '>', lowest row wins, split.hpp:259-263).
+//  1. k_big_keys      per (node, row) segment: the reference's packed sort key
+//                     order_key(v) << 32 | label for every sample, from the wave's V block;
+//  2. k_seg_radix     one CTA per segment, least-significant-digit radix sort in global memory:
+//                     four stable passes (the label byte, then the 32-bit value key in 11 + 11 +
+//                     10 bits); each pass counts its digits, then scatters the segment tile by
+//                     tile, ranking keys of equal digit in input order (warp match + per-warp
+//                     digit offsets in shared memory);
+//  3. k_big_scan_wide one CTA per segment (wide.cuh): class counts at every gap between distinct
+//                     values, impurity in the reference's FP64 order, minimum X, then the first
+//                     position whose gain equals the best (first maximum);
+//  4. k_big_select    best row per node (strict '>', lowest row wins, split.hpp:259-263).
 #include <cuda_runtime.h>
 
 #include <vector>
-
-#include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
-#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "common.hpp"
 #include "dev_util.cuh"
@@ -52,119 +52,84 @@ __global__ void __launch_bounds__(256) k_big_keys(const NodeIn* __restrict__ nod
                        uint64_t(lab[nd.begin + j]);
 }
 
-constexpr int kBigThreads = 256;
+// ------------------------------------------------------------------------------------------
+// Segmented LSD radix sort, one CTA per segment: keys [beg, end) of `src` sorted into `dst`
+// (ascending 64-bit keys; only bits 0-7 (label) and 32-63 (value key) can be non-zero).
+constexpr int kRadixThreads = 256;
+constexpr int kRadixMaxDigit = 2048;  // 11-bit digits
 
-// One CTA per segment; the segment's sorted keys are walked in tiles of kBigThreads.
-template <int KC>
-__global__ void __launch_bounds__(kBigThreads) k_big_scan(const NodeIn* __restrict__ nodes,
-                                                          const BigSeg* __restrict__ segs,
-                                                          uint32_t R, int k,
-                                                          const uint32_t* __restrict__ row_ptr,
-                                                          const uint64_t* __restrict__ keys,
-                                                          const double* __restrict__ xl,
-                                                          RowRes* __restrict__ rowres) {
-  using Scan = cub::BlockScan<uint32_t, kBigThreads>;
-  using RedD = cub::BlockReduce<double, kBigThreads>;
-  using RedU = cub::BlockReduce<uint32_t, kBigThreads>;
-  __shared__ union {
-    typename Scan::TempStorage scan;
-    typename RedD::TempStorage redd;
-    typename RedU::TempStorage redu;
-  } tmp;
-  __shared__ uint32_t s_carry[KC];
-  __shared__ double s_xmin;
-  __shared__ uint32_t s_first;
-  const BigSeg sg = segs[blockIdx.x];
-  const NodeIn nd = nodes[sg.node];
-  const uint32_t n = nd.n;
-  const uint64_t* K = keys + sg.off;
-  RowRes out{};
-  const uint32_t* rp = row_ptr + size_t(sg.node) * (R + 1);
-  if (rp[sg.row + 1] == rp[sg.row]) {  // empty rows are skipped in exact mode (split.hpp:308)
-    if (threadIdx.x == 0) rowres[blockIdx.x] = out;
-    return;
-  }
-  // class totals
-  uint32_t tot[KC];
-  {
-    uint32_t c[KC];
-#pragma unroll
-    for (int cc = 0; cc < KC; ++cc) c[cc] = 0;
-    for (uint32_t j = threadIdx.x; j < n; j += kBigThreads) {
-      const int y = int(K[j] & 0xffu);
-#pragma unroll
-      for (int cc = 0; cc < KC; ++cc) c[cc] += (cc == y);
-    }
-#pragma unroll
-    for (int cc = 0; cc < KC; ++cc) {
-      const uint32_t t = RedU(tmp.redu).Sum(c[cc]);
-      if (threadIdx.x == 0) s_carry[cc] = t;
-      __syncthreads();
-      tot[cc] = s_carry[cc];
-      __syncthreads();
-    }
-  }
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  const double dn = double(n);
-  // Walk the sorted keys; visit(p, X, a, b) for every candidate gap after position p.
-  auto walk = [&](auto&& visit) {
-    if (threadIdx.x < KC) s_carry[threadIdx.x] = 0;
-    __syncthreads();
-    for (uint32_t base = 0; base < n; base += kBigThreads) {
-      const uint32_t p = base + threadIdx.x;
-      const uint64_t key = p < n ? K[p] : ~0ull;
-      const int y = int(key & 0xffu);
-      uint32_t left[KC];
-#pragma unroll
-      for (int cc = 0; cc < KC; ++cc) {
-        uint32_t agg;
-        Scan(tmp.scan).InclusiveSum(p < n && cc == y ? 1u : 0u, left[cc], agg);
-        __syncthreads();
-        left[cc] += s_carry[cc];
-        __syncthreads();
-        if (threadIdx.x == kBigThreads - 1) s_carry[cc] = left[cc];
-      }
-      __syncthreads();
-      if (p + 1 < n) {
-        const float a = order_key_inv(uint32_t(key >> 32));
-        const float b = order_key_inv(uint32_t(K[p + 1] >> 32));
-        if (a < b) {
-          const uint32_t nl = p + 1;
-          const double X = impurity_sum<KC>(xl, left, tot, k, nl, n - nl);
-          visit(p, X, a, b);
-        }
-      }
-    }
-  };
-  double xmin = inf;
-  walk([&](uint32_t, double X, float, float) { xmin = fmin(xmin, X); });
-  const double bx = RedD(tmp.redd).Reduce(xmin, [](double x, double y) { return fmin(x, y); });
-  if (threadIdx.x == 0) s_xmin = bx;
-  __syncthreads();
-  xmin = s_xmin;
-  const double g = gain_from_x(nd.parent, xmin, dn);
-  if (!(xmin < inf) || !(g > 0.0)) {
-    if (threadIdx.x == 0) rowres[blockIdx.x] = out;
-    return;
-  }
-  const double win = x_window(nd.parent, xmin, dn);
-  uint32_t first = 0xffffffffu;
-  walk([&](uint32_t p, double X, float, float) {
-    if (first == 0xffffffffu && X <= win && (X == xmin || gain_from_x(nd.parent, X, dn) == g)) first = p;
-  });
-  const uint32_t bf = RedU(tmp.redu).Reduce(first, [](uint32_t x, uint32_t y) { return min(x, y); });
-  if (threadIdx.x == 0) {
-    const float a = order_key_inv(uint32_t(K[bf] >> 32));
-    const float b = order_key_inv(uint32_t(K[bf + 1] >> 32));
-    out.valid = 1;
-    out.gain = g;
-    out.threshold = midpoint_down(a, b);
-    out.n_left = bf + 1;
-    rowres[blockIdx.x] = out;
+__device__ __forceinline__ uint32_t radix_digit(uint64_t key, int pass) {
+  switch (pass) {
+    case 0: return uint32_t(key) & 0xffu;                     // label
+    case 1: return uint32_t(key >> 32) & 0x7ffu;              // value key bits 0-10
+    case 2: return uint32_t(key >> 43) & 0x7ffu;              // bits 11-21
+    default: return uint32_t(key >> 54) & 0x3ffu;             // bits 22-31
   }
 }
 
-// More than kMaxClasses classes: one CTA per segment, class counts in shared memory (wide.cuh).
+__global__ void __launch_bounds__(kRadixThreads) k_seg_radix(const uint64_t* __restrict__ seg_begin,
+                                                             const uint64_t* __restrict__ seg_end,
+                                                             uint64_t* __restrict__ a, uint64_t* __restrict__ b) {
+  __shared__ uint32_t s_base[kRadixMaxDigit];  // next output position of each digit
+  extern __shared__ uint32_t s_wc[];           // [8 warps][D]: the current tile's digit counts per warp
+  const uint64_t beg = seg_begin[blockIdx.x];
+  const uint32_t n = uint32_t(seg_end[blockIdx.x] - beg);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = kRadixThreads / 32;
+  for (int i = threadIdx.x; i < NW * kRadixMaxDigit; i += kRadixThreads) s_wc[i] = 0;
+  for (int pass = 0; pass < 4; ++pass) {  // a -> b -> a -> b -> a
+    const uint32_t D = pass == 0 ? 256u : pass == 3 ? 1024u : 2048u;
+    const uint64_t* src = (pass & 1) ? b : a;
+    uint64_t* dst = (pass & 1) ? a : b;
+    // 1. digit counts, then their exclusive prefix (warp 0)
+    for (uint32_t d = threadIdx.x; d < D; d += kRadixThreads) s_base[d] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += kRadixThreads) {
+      const uint32_t d = radix_digit(src[beg + i], pass);
+      const unsigned peers = __match_any_sync(__activemask(), d);
+      if ((__ffs(peers) - 1) == lane) atomicAdd(&s_base[d], uint32_t(__popc(peers)));
+    }
+    __syncthreads();
+    if (w == 0) {
+      uint32_t carry = 0;
+      for (uint32_t c0 = 0; c0 < D; c0 += 32) {
+        const uint32_t x = s_base[c0 + lane];
+        uint32_t tot;
+        const uint32_t ex = warp_excl_scan_u32(x, lane, &tot);
+        s_base[c0 + lane] = carry + ex;
+        carry += tot;
+      }
+    }
+    __syncthreads();
+    // 2. stable scatter: tiles of 256 keys, thread t holding key t of the tile; a key's place among
+    //    the tile's keys of its digit = (keys of that digit in earlier warps) + (earlier lanes)
+    for (uint32_t t0 = 0; t0 < n; t0 += kRadixThreads) {
+      const uint32_t i = t0 + threadIdx.x;
+      const bool in = i < n;
+      const uint64_t key = in ? src[beg + i] : 0ull;
+      const uint32_t d = in ? radix_digit(key, pass) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t cnt = uint32_t(__popc(peers));
+      const bool leader = in && (__ffs(peers) - 1) == lane;
+      if (leader) s_wc[w * D + d] = cnt;
+      __syncthreads();
+      uint32_t before = 0, after = 0;
+      if (in) {
+        for (int ww = 0; ww < w; ++ww) before += s_wc[ww * D + d];
+        for (int ww = w + 1; ww < NW; ++ww) after += s_wc[ww * D + d];
+        dst[beg + s_base[d] + before + uint32_t(__popc(peers & ((1u << lane) - 1u)))] = key;
+      }
+      __syncthreads();
+      if (leader) {
+        if (after == 0) s_base[d] += before + cnt;  // the tile's last warp of digit d advances it
+        s_wc[w * D + d] = 0;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// The scan: one CTA per segment, class counts in shared memory (wide.cuh), any class count.
 __global__ void __launch_bounds__(kWideThreads) k_big_scan_wide(const NodeIn* __restrict__ nodes,
                                                                 const BigSeg* __restrict__ segs, uint32_t R, int k,
                                                                 const uint32_t* __restrict__ row_ptr,
@@ -253,19 +218,13 @@ cudaError_t launch_exact_big(const NodeIn* nodes, const NodeIn* h_nodes, const u
     cudaError_t e = cudaMemcpyAsync(d_segs, segs.data(), sizeof(dev::BigSeg) * nseg, cudaMemcpyHostToDevice, st);
     if (e) return e;
     dev::k_big_keys<<<nseg, 256, 0, st>>>(nodes, d_segs, R, lab, vbase, V, d_k0, d_b, d_e);
-    size_t tb = 0;
-    e = cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tb, d_k0, d_k1, int64_t(keys), nseg, d_b, d_e, 0, 64, st);
-    void* d_tmp = e ? nullptr : ar_get(6, tb ? tb : 1);
-    if (!e && !d_tmp) e = cudaErrorMemoryAllocation;
-    if (!e) e = cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tb, d_k0, d_k1, int64_t(keys), nseg, d_b, d_e, 0, 64, st);
+    constexpr size_t kRadixSmem = sizeof(uint32_t) * 8 * dev::kRadixMaxDigit;  // 64 KB per-warp digit counts
+    e = cudaFuncSetAttribute(dev::k_seg_radix, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRadixSmem));
     if (e) return e;
-    if (k == 2)
-      dev::k_big_scan<2><<<nseg, dev::kBigThreads, 0, st>>>(nodes, d_segs, R, k, row_ptr, d_k1, xl, d_rr);
-    else if (k <= kMaxClasses)
-      dev::k_big_scan<kMaxClasses><<<nseg, dev::kBigThreads, 0, st>>>(nodes, d_segs, R, k, row_ptr, d_k1, xl, d_rr);
-    else
-      dev::k_big_scan_wide<<<nseg, dev::kWideThreads, dev::wide_carve_bytes(k), st>>>(nodes, d_segs, R, k, row_ptr,
-                                                                                     d_k1, xl, d_rr);
+    dev::k_seg_radix<<<nseg, dev::kRadixThreads, kRadixSmem, st>>>(d_b, d_e, d_k0, d_k1);
+    // sorted keys are back in d_k0 (four passes)
+    dev::k_big_scan_wide<<<nseg, dev::kWideThreads, dev::wide_carve_bytes(k), st>>>(nodes, d_segs, R, k, row_ptr, d_k0,
+                                                                                   xl, d_rr);
     dev::k_big_select<<<(nn + 127) / 128, 128, 0, st>>>(d_segs, nn, R, d_rr, res);
     e = cudaGetLastError();
     if (e) return e;
