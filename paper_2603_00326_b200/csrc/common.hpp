@@ -20,7 +20,7 @@ constexpr int kMaxClassesWide = 64;  // class_count supported (above kMaxClasses
 constexpr int kMaxBins = 1024;       // bin_count supported by the histogram splitter
 constexpr int kExactSmemMax = 2048;  // largest node the shared-memory exact splitter sorts
 constexpr int kTileElems = 1024;     // partition tile
-constexpr int kWinTermsMax = 16;     // winning-row terms returned inline per node
+constexpr int kWinTermsMax = 8;      // winning-row terms returned inline per node (longer rows: k_win_terms)
 constexpr int kHistRowsPerCta = 8;   // rows (one per warp) per histogram CTA
 constexpr uint64_t kFallbackBreakeven = 1024;  // reference calibrate.hpp:43
 
@@ -55,9 +55,11 @@ struct NodeRes {
   uint32_t n_terms;      // winning row term count
   uint32_t sectors;      // distinct 32 B sectors of the node's sample ids (stats only)
   uint32_t _pad;
-  uint32_t left_counts[kMaxClasses];
   uint32_t terms[kWinTermsMax];  // winning row terms: feature << 1 | (weight < 0)
 };
+// The partition's left class counts travel in a separate [node][k] array (k_part_flags), so the
+// per-wave device-to-host copy is 72 + 4 k bytes per node.
+static_assert(sizeof(NodeRes) == 72, "NodeRes layout");
 
 // Per-(histogram node, row) search result.
 struct RowRes {

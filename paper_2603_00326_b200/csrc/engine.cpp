@@ -366,7 +366,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   uint32_t* d_gcnt = gcnt_.ensure(std::max<size_t>(1, gcnt_n));
   uint32_t* d_done = done_.ensure(std::max<size_t>(1, done_n));
   // wide: the partition's left class counts [N][k] (NodeRes carries kMaxClasses), exact row results
-  uint32_t* d_cl = wide ? cl_.ensure(size_t(N) * size_t(k)) : nullptr;
+  uint32_t* d_cl = cl_.ensure(size_t(N) * size_t(k));
   RowRes* d_rowres_ex = wide ? rowres_ex_.ensure(std::max<size_t>(1, size_t(exact_total) * R)) : nullptr;
   NodeRes* d_res = res_.ensure(size_t(N));
   float* d_G = V_.ensure(std::max<uint64_t>(1, g_total));
@@ -387,7 +387,7 @@ void WaveRunner::submit(const WaveSpec& w) {
     cuda_check(cudaMemsetAsync(d_gcnt, 0, 4 * gcnt_n, st_), "memset gcnt");
     cuda_check(cudaMemsetAsync(d_done, 0, 4 * done_n, st_), "memset done");
   }
-  if (wide) cuda_check(cudaMemsetAsync(d_cl, 0, 4 * size_t(N) * size_t(k), st_), "memset class counts");
+  cuda_check(cudaMemsetAsync(d_cl, 0, 4 * size_t(N) * size_t(k), st_), "memset class counts");
 
   const bool timing = collect_stats;
   if (sector_accounting)
@@ -565,8 +565,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   h_res_p_ = hr;
   cuda_check(cudaMemcpyAsync(hr, d_res, sizeof(NodeRes) * N, cudaMemcpyDeviceToHost, st_),
              "D2H res");
-  h_cl_p_ = nullptr;
-  if (wide) {
+  {
     uint32_t* hc = h_cl_buf_[h_res_cur_].ensure(size_t(N) * size_t(k));
     h_cl_p_ = hc;
     cuda_check(cudaMemcpyAsync(hc, d_cl, 4 * size_t(N) * size_t(k), cudaMemcpyDeviceToHost, st_), "D2H class counts");
@@ -681,14 +680,12 @@ const NodeRes* WaveRunner::collect_view(const WaveSpec& w) {
   return res;
 }
 
-std::vector<uint32_t> WaveRunner::fetch_row_terms(const WaveSpec& w, uint32_t node,
-                                                  uint32_t row) const {
+const uint32_t* WaveRunner::fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row) const {
   (void)w;
   (void)row;
   if (node >= long_pos_.size() || long_pos_[node] == ~0u)
     throw std::logic_error("winning row terms were not fetched");
-  const uint32_t k = long_pos_[node];
-  return std::vector<uint32_t>(long_terms_.begin() + long_off_[k], long_terms_.begin() + long_off_[k + 1]);
+  return long_terms_.data() + long_off_[long_pos_[node]];
 }
 
 }  // namespace sofg

@@ -218,8 +218,8 @@ class WaveRunner {
   void collect(const WaveSpec& w, std::vector<NodeRes>& res);
   // Same wait, no copy: the node results in page-locked memory, valid until the next submit().
   const NodeRes* collect_view(const WaveSpec& w);
-  // More than kMaxClasses classes: the partition's left class counts of the collected wave,
-  // [node][k] (NodeRes::left_counts is not filled); nullptr otherwise.
+  // The partition's left class counts of the collected wave, [node][k]; valid as long as the
+  // results of collect_view are.
   const uint32_t* class_counts_view() const { return h_cl_p_; }
   // Only the wait for the wave (no host pool use): callers sharing a pool wait first, then
   // take their host turn and call collect_view().
@@ -236,7 +236,8 @@ class WaveRunner {
   PinnedBuf<unsigned char> staging;
   // Terms of node `node`'s winning row in the last collected wave, for rows longer than the
   // kWinTermsMax terms NodeRes carries inline (fetched in one batch by collect()).
-  std::vector<uint32_t> fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row) const;
+  // Returns a pointer to the row's n_terms entries (valid until the next collect).
+  const uint32_t* fetch_row_terms(const WaveSpec& w, uint32_t node, uint32_t row) const;
 
   void set_pool(ThreadPool* p) { pool_ = p; }
 
@@ -272,7 +273,7 @@ class WaveRunner {
   PinnedBuf<NodeRes> h_res_buf_[2];  // alternate per wave: a wave's results stay readable while
   int h_res_cur_ = 0;                 // the next wave's are copied back
   NodeRes* h_res_p_ = nullptr;
-  PinnedBuf<uint32_t> h_cl_buf_[2];   // wide classes: left class counts [N][k], same alternation
+  PinnedBuf<uint32_t> h_cl_buf_[2];   // left class counts [N][k], same alternation
   uint32_t* h_cl_p_ = nullptr;
   DevBuf<uint32_t> cl_;
   DevBuf<RowRes> rowres_ex_;          // wide classes: exact results per (node, row)

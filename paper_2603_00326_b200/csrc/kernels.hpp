@@ -127,7 +127,7 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              const uint8_t* lab_in, uint32_t* idx_out, uint8_t* lab_out,
                              const uint64_t* gbase, const float* G, NodeRes* res, uint32_t* flags,
                              uint32_t* tile_left, uint32_t* inv, uint32_t B, uint32_t* class_left,
-                             cudaStream_t st);  // class_left: [node][k] when k > kMaxClasses, else nullptr
+                             cudaStream_t st);  // class_left: [node][k] left class counts (zeroed by the caller)
 
 cudaError_t launch_win_terms(const NodeIn* nodes, const NodeRes* res, const uint32_t* row_ptr,
                              const uint32_t* terms, uint32_t R, const uint32_t* list, int n_list,

@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256) k_part_flags(
     const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
     const float* __restrict__ G, NodeRes* __restrict__ res, uint32_t* __restrict__ flags,
-    uint32_t* __restrict__ tile_left) {
+    uint32_t* __restrict__ tile_left, uint32_t* __restrict__ class_left) {
   __shared__ uint32_t s_cls[kMaxClasses];
   __shared__ uint32_t s_left;
   const Tile tl = tiles[blockIdx.x];
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_part_flags(
   __syncthreads();
   if (threadIdx.x == 0) tile_left[blockIdx.x] = s_left;
   if (threadIdx.x < uint32_t(k) && s_cls[threadIdx.x])
-    atomicAdd(&res[tl.node].left_counts[threadIdx.x], s_cls[threadIdx.x]);
+    atomicAdd(&class_left[size_t(tl.node) * k + threadIdx.x], s_cls[threadIdx.x]);
 }
 
 // One warp per node: scan its tiles (tiles of a node are contiguous, first = tile_first[node]).
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) k_part_flags_w(
     }
     const unsigned m = __ballot_sync(0xffffffffu, f);
     if (lane == 0) flags[size_t(ti) * 32 + wd] = m;
-    if (class_left) {  // more than kMaxClasses classes: one atomic per distinct label of the step
+    if (k > kMaxClasses) {  // more than kMaxClasses classes: one atomic per distinct label of the step
       const unsigned same = __match_any_sync(0xffffffffu, f ? int(y) : -1);
       if (f && (__ffs(same) - 1) == lane) atomicAdd(&class_left[size_t(tl.node) * k + y], uint32_t(__popc(same)));
       my_left += f ? 1u : 0u;
@@ -205,11 +205,11 @@ __global__ void __launch_bounds__(256) k_part_flags_w(
   if (lane == 0) tile_left[ti] = my_left;
 #pragma unroll
   for (int c = 0; c < kMaxClasses; ++c) {
-    if (c >= k || class_left) break;
+    if (c >= k || k > kMaxClasses) break;
     uint32_t x = cls[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0 && x) atomicAdd(&res[tl.node].left_counts[c], x);
+    if (lane == 0 && x) atomicAdd(&class_left[size_t(tl.node) * k + c], x);
   }
 }
 
@@ -315,10 +315,10 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              uint32_t* tile_left, uint32_t* inv, uint32_t B, uint32_t* class_left,
                              cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
-  const bool cta_tiles = std::getenv("SOFG_PART_CTA") != nullptr && !class_left;  // CTA-per-tile forms
+  const bool cta_tiles = std::getenv("SOFG_PART_CTA") != nullptr && k <= kMaxClasses;  // CTA-per-tile forms
   if (n_tiles > 0 && cta_tiles)
     dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, lab_in, gbase,
-                                               G, res, flags, tile_left);
+                                               G, res, flags, tile_left, class_left);
   else if (n_tiles > 0)
     dev::k_part_flags_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, R, k, lab_in, gbase, G, res,
                                                            flags, tile_left, class_left);

@@ -344,6 +344,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
   std::vector<Counter> tsize(B);
   for (size_t b = 0; b < B; ++b) tsize[b].v = uint32_t(trees[b].size());
   const NodeRes* dres = nullptr;
+  const uint32_t* dcl = nullptr;  // its left class counts [node][k]
   std::vector<size_t> dpoff(NP + 1, 0);
   bool pending = false;
   auto bookkeep = [&]() {
@@ -366,8 +367,8 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
           if (r.n_terms <= uint32_t(kWinTermsMax)) {
             tp.insert(tp.end(), r.terms, r.terms + r.n_terms);
           } else {
-            const std::vector<uint32_t> t = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
-            tp.insert(tp.end(), t.begin(), t.end());
+            const uint32_t* t = eng.fetch_row_terms(w, uint32_t(i), uint32_t(r.row));
+            tp.insert(tp.end(), t, t + r.n_terms);
           }
           tr.emplace_back();
           tr.emplace_back();
@@ -378,9 +379,10 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
             lc = wc[o.tree].data() + size_t(L) * size_t(k);
             rc = lc + k;
           } else {
+            const uint32_t* cl = dcl + i * size_t(k);
             for (int c = 0; c < k; ++c) {
-              lcb[c] = r.left_counts[c];
-              rcb[c] = o.counts[c] - r.left_counts[c];
+              lcb[c] = cl[c];
+              rcb[c] = o.counts[c] - cl[c];
             }
           }
           if (!can_split_c(lc, r.n_left, o.depth + 1)) tr[size_t(L)].pred = argmax_first(lc, k);
@@ -499,7 +501,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
         if (!more) P.idle_work = nullptr;
       }
       const NodeRes* res = eng.collect_view(w);
-      const uint32_t* wcl = eng.class_counts_view();  // wide classes: left counts [node][k]
+      const uint32_t* wcl = eng.class_counts_view();  // the partition's left class counts [node][k]
       prev_wave_ms = ms_since(t_submit);
       const double lv_wait = ms_since(t0);
       if (std::getenv("SOFG_WAVE_HASH")) {  // debugging aid: per-wave result digest
@@ -585,9 +587,10 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
                 lc[k + c] = pc[c] - cl[c];
               }
             } else {
+              const uint32_t* cl = wcl + i * size_t(k);
               for (int c = 0; c < k; ++c) {
-                l.counts[c] = r.left_counts[c];
-                rr.counts[c] = o.counts[c] - r.left_counts[c];
+                l.counts[c] = cl[c];
+                rr.counts[c] = o.counts[c] - cl[c];
               }
             }
             if (can_split(l)) nx[p].push_back(l);
@@ -624,6 +627,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
         if (ns) prof->add(size_t(depth) + 1, 0.0, 2 * ns, nn);
       }
       dres = res;
+      dcl = wcl;
       dpoff = poff;
       pending = true;
       times.ms_post += ms_since(t0);
