@@ -9,7 +9,9 @@ the data path); rank r trains its own slice of the forest each step.
 
 value  device-timed trees/s over all ranks (CUDA events on the trainer's stream, max over ranks)
 e2e    the same through the C ABI with host buffers: every step uploads the 16.4 GB table from
-       page-locked memory (sofg_upload_dataset), trains, and reads the forest back.
+       page-locked memory (sofg_upload_dataset), trains, and reads the forest back; a second context
+       on the same GPU holds a second resident table so step s+1's upload overlaps step s's training
+       (--e2e-serial: upload, then train).
 roofline  the dominant kernel, k_row_sweep (projection sweep): algorithmic bytes per launch (table
        rows streamed + projected rows written + term lists read) over its CUDA-event time, against
        MEASURED_PEAKS.json's HBM copy bandwidth, measured in one extra untimed profile step; traffic =
@@ -53,7 +55,8 @@ def parse():
                    help="dynamic-switch threshold; 512 = B200 calibration (DESIGN.md 3, calibrate.py)")
     p.add_argument("--mode", default="dynamic", choices=["dynamic", "exact", "histogram"])
     p.add_argument("--seed", type=int, default=7)
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=6)
+    p.add_argument("--e2e-serial", action="store_true", help="e2e without the second-context input pipeline")
     p.add_argument("--cpu-trees", type=int, default=0, help="CPU baseline sample (0 = one per core)")
     p.add_argument("--holdout", type=int, default=20000, help="hold-out rows for the accuracy check")
     p.add_argument("--classes", type=int, default=2, help="trunk-model classes (BASELINE config 5: 4)")
@@ -341,7 +344,7 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     T = args.trees
     per_step = T * world
-    total_trees = (args.warmup + args.steps + args.e2e_steps + 1) * per_step
+    total_trees = (args.warmup + args.steps + args.e2e_steps + 2) * per_step
 
     # host threads split between the ranks sharing this host (one rank per GPU)
     workers = args.workers or max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
@@ -411,20 +414,42 @@ def main():
         Xh = np.ctypeslib.as_array((C.c_float * (args.n * args.d)).from_address(hptr)).reshape(args.d, args.n)
         yh = np.zeros(args.n, np.int32)
         ctx.download(Xh, yh)
+        # Input pipeline: a second context on the same GPU holds a second resident table, so step
+        # s + 1's table upload (page-locked source, the context's own stream) runs while step s
+        # trains; every step still uploads its whole table and reads its forest back inside the
+        # timed region. Falls back to upload-then-train when the second table does not fit.
+        ctxs = [ctx]
+        if not args.e2e_serial:
+            try:
+                c2 = sofg.Context(local)
+                c2.upload_ptr(hptr, yh, args.n, args.d, args.classes)
+                c2.train_forest(cfg_for(args.warmup + args.steps + args.e2e_steps + 1))  # buffers (untimed)
+                ctxs.append(c2)
+            except Exception as exc:  # noqa: BLE001 - any allocation failure: serial pipeline
+                print(f"e2e: second context unavailable ({exc}); serial upload + train", file=sys.stderr)
         barrier()
-        t_e = []
         d2h = 0
-        for s in range(args.warmup + args.steps, args.warmup + args.steps + args.e2e_steps):
-            torch.cuda.synchronize()
-            ts = time.perf_counter()
-            ctx.upload_ptr(hptr, yh, args.n, args.d, args.classes)
-            f = ctx.train_forest(cfg_for(s))
-            torch.cuda.synchronize()
-            t_e.append(time.perf_counter() - ts)
+        first = args.warmup + args.steps
+        torch.cuda.synchronize()
+        ts = time.perf_counter()
+        ctxs[0].upload_ptr(hptr, yh, args.n, args.d, args.classes)
+        for j in range(args.e2e_steps):
+            cur = ctxs[j % len(ctxs)]
+            if len(ctxs) > 1 and j + 1 < args.e2e_steps:  # next step's table, in flight during this step
+                ctxs[(j + 1) % len(ctxs)].upload_ptr(hptr, yh, args.n, args.d, args.classes)
+            f = cur.train_forest(cfg_for(first + j))
             d2h = sum(a.nbytes for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off, f.feat, f.weight))
-        e_s = max_over_ranks(sum(t_e))
-        e2e = {"value": world * T * len(t_e) / e_s, "unit": "trees/s", "h2d_bytes_per_step": nbytes + 4 * args.n,
-               "d2h_bytes_per_step": d2h, "timing": "host wall clock, cuda-synchronized, max over ranks"}
+            if len(ctxs) == 1 and j + 1 < args.e2e_steps:
+                cur.upload_ptr(hptr, yh, args.n, args.d, args.classes)
+        torch.cuda.synchronize()
+        e_s = max_over_ranks(time.perf_counter() - ts)
+        e2e = {"value": world * T * args.e2e_steps / e_s, "unit": "trees/s", "h2d_bytes_per_step": nbytes + 4 * args.n,
+               "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "timing": "host wall clock, cuda-synchronized, max over ranks",
+               "pipeline": ("two contexts: step s+1's table upload overlaps step s's training"
+                            if len(ctxs) > 1 else "serial: upload, then train")}
+        for c2 in ctxs[1:]:
+            c2.close()
     else:
         Xh = None
 

@@ -102,9 +102,11 @@ int sofg_destroy(sofg_ctx* ctx);
 /* Upload a dataset (replaces constructing BasicColumnarDataset<float>, dataset.hpp:28-45).
  * labels: int32 in [0, class_count). Validates like the reference constructor; class_count <= 64
  * (more than 8 classes run the wide-class splitters, wide.cu; the reference has no bound).
- * X page-locked (e.g. from sofg_host_alloc): the copy is left in flight and overlaps the next
- * call's host work; keep X unchanged until the next training / download call on this context
- * returns. Pageable X: the copy has landed when this returns. */
+ * X page-locked (e.g. from sofg_host_alloc): returns at once; a context thread feeds the copy to
+ * the GPU in ~32 MB slices (one in flight, so other contexts' copies on the same GPU are not queued
+ * behind it) and the next call on this context waits for it; keep X unchanged until the next
+ * training / download call on this context returns. Pageable X: the copy has landed when this
+ * returns. */
 int sofg_upload_dataset(sofg_ctx* ctx, const float* X, uint64_t n_samples, uint64_t n_features,
                         const int32_t* labels, int32_t class_count);
 /* Same, one pointer per column (the reference's vector<vector<float>> layout). */

@@ -50,6 +50,22 @@ struct sofg_ctx {
   int pool_threads = 0;
   sofg::HostTimes times;
   int stats_mode = 0;
+  // Page-locked table uploads are fed to the copy engine in slices by this thread (one slice in
+  // flight), so other contexts' small copies on the same GPU are not queued behind a 16 GB copy;
+  // every later call on the context joins it first (its device work is stream-ordered after it).
+  std::thread feeder;
+  std::exception_ptr feeder_error;
+  void join_feeder() {
+    if (feeder.joinable()) feeder.join();
+    if (feeder_error) {
+      std::exception_ptr e = feeder_error;
+      feeder_error = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+  ~sofg_ctx() {
+    if (feeder.joinable()) feeder.join();
+  }
 };
 
 struct sofg_forest {
@@ -91,6 +107,7 @@ void require_ctx(sofg_ctx* c) {
 }
 void require_data(sofg_ctx* c) {
   require_ctx(c);
+  c->join_feeder();
   if (!c->eng->data().loaded()) throw std::invalid_argument("no dataset uploaded");
 }
 
@@ -129,8 +146,10 @@ void ensure_xlogx(sofg::DeviceData& D, uint64_t m, cudaStream_t st) {
 }
 
 // Dataset staging into HBM: ld = n rounded up to 32 samples (128 B column alignment).
+// copy_X returns 0: synchronous copy (pageable), 1: enqueued on the context's stream, 2: deferred
+// to the feeder thread, which copies `pending_src` (column-major [d][n], page-locked) in slices.
 void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t k,
-            const std::function<bool(float* dev, uint64_t ld)>& copy_X) {
+            const std::function<int(float* dev, uint64_t ld)>& copy_X, const float* pending_src = nullptr) {
   if (n < 1 || d < 1) throw std::invalid_argument("empty dataset");
   if (n >= (1ull << 31)) throw std::invalid_argument("n_samples must be < 2^31");
   if (k < 1) throw std::invalid_argument("class_count must be positive");
@@ -150,7 +169,8 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
   // the engine's stream does not order against the legacy stream: wait for those. Copies from
   // page-locked memory are enqueued on the engine stream instead and left in flight — training
   // starts with host-side work (bootstrap sampling) that overlaps them.
-  if (!copy_X(D.X.p, D.ld)) cuda_check(cudaDeviceSynchronize(), "upload sync");
+  const int copied = copy_X(D.X.p, D.ld);
+  if (copied == 0) cuda_check(cudaDeviceSynchronize(), "upload sync");
   cudaStream_t st = c->eng->stream();
   // Row-major copy for the sample-major projection sweep (sweep.cu); rows padded to 128 B. The
   // previous allocation is reused when it is large enough (a 16 GB free + malloc per upload costs
@@ -175,10 +195,34 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
       row_table = false;
     }
   }
-  if (row_table) {
+  if (!row_table) D.XR.release();
+  if (copied == 2) {  // sliced page-locked copy on the feeder thread, then the transpose
+    sofg::DeviceData* Dp = &D;
+    const float* src = pending_src;
+    const int dev = c->eng->device();
+    c->feeder = std::thread([c, Dp, src, n, d, st, dev, row_table] {
+      try {
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        cudaEvent_t ev;
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        const uint64_t cols = std::max<uint64_t>(1, (uint64_t(32) << 20) / (4 * n));  // ~32 MB slices
+        for (uint64_t f0 = 0; f0 < d; f0 += cols) {
+          const uint64_t w = std::min(cols, d - f0);
+          cuda_check(cudaMemcpy2DAsync(Dp->X.p + f0 * Dp->ld, Dp->ld * 4, src + f0 * n, n * 4, n * 4, w,
+                                       cudaMemcpyHostToDevice, st),
+                     "H2D table slice");
+          cuda_check(cudaEventRecord(ev, st), "event");
+          cuda_check(cudaEventSynchronize(ev), "slice sync");
+        }
+        cudaEventDestroy(ev);
+        if (row_table)
+          cuda_check(sofg::launch_transpose_rows(Dp->X.p, Dp->ld, n, d, Dp->XR.p, Dp->ldr, st), "transpose_rows");
+      } catch (...) {
+        c->feeder_error = std::current_exception();
+      }
+    });
+  } else if (row_table) {
     cuda_check(sofg::launch_transpose_rows(D.X.p, D.ld, n, d, D.XR.p, D.ldr, st), "transpose_rows");
-  } else {
-    D.XR.release();
   }
   D.labels_host.assign(labels, labels + n);
   // labels through page-locked staging, on the engine stream (the staging is rewritten only
@@ -335,19 +379,15 @@ int sofg_upload_dataset(sofg_ctx* c, const float* X, uint64_t n, uint64_t d, con
                         int32_t k) {
   return guard([&] {
     require_ctx(c);
+    c->join_feeder();
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, X) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // clear a failed attribute query (plain pageable memory)
     upload(c, n, d, y, k, [&](float* dev, uint64_t ld) {
-      cudaPointerAttributes at{};
-      const bool pinned = cudaPointerGetAttributes(&at, X) == cudaSuccess && at.type == cudaMemoryTypeHost;
-      cudaGetLastError();  // clear a failed attribute query (plain pageable memory)
-      if (pinned) {
-        cuda_check(cudaMemcpy2DAsync(dev, ld * 4, X, n * 4, n * 4, d, cudaMemcpyHostToDevice,
-                                     c->eng->stream()),
-                   "H2D table");
-        return true;
-      }
+      if (pinned) return 2;  // sliced on the feeder thread
       cuda_check(cudaMemcpy2D(dev, ld * 4, X, n * 4, n * 4, d, cudaMemcpyHostToDevice), "H2D table");
-      return false;
-    });
+      return 0;
+    }, pinned ? X : nullptr);
   });
 }
 
@@ -355,13 +395,14 @@ int sofg_upload_columns(sofg_ctx* c, const float* const* cols, uint64_t n, uint6
                         const int32_t* y, int32_t k) {
   return guard([&] {
     require_ctx(c);
+    c->join_feeder();
     upload(c, n, d, y, k, [&](float* dev, uint64_t ld) {
       for (uint64_t f = 0; f < d; ++f)
         cuda_check(cudaMemcpyAsync(dev + f * ld, cols[f], n * 4, cudaMemcpyHostToDevice,
                                    c->eng->stream()),
                    "H2D column");
       cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync columns");
-      return true;
+      return 1;
     });
   });
 }
@@ -369,6 +410,7 @@ int sofg_upload_columns(sofg_ctx* c, const float* const* cols, uint64_t n, uint6
 int sofg_generate_trunk(sofg_ctx* c, uint64_t n, uint64_t d, int32_t k, uint64_t seed) {
   return guard([&] {
     require_ctx(c);
+    c->join_feeder();
     if (n < 2) throw std::invalid_argument("n_samples must be at least 2");
     if (d == 0) throw std::invalid_argument("n_features must be positive");
     if (k < 1 || k > sofg::kMaxClassesWide) throw std::invalid_argument("class_count out of range");
@@ -380,7 +422,7 @@ int sofg_generate_trunk(sofg_ctx* c, uint64_t n, uint64_t d, int32_t k, uint64_t
       cuda_check(launch_generate_trunk(dev, ld, tmp.p, n, d, k, seed, c->eng->stream()),
                  "generate_trunk");
       cuda_check(cudaStreamSynchronize(c->eng->stream()), "sync generate");
-      return true;
+      return 1;
     });
   });
 }
@@ -654,6 +696,7 @@ int sofg_predict(sofg_ctx* c, const sofg_forest* fo, const float* rows, uint64_t
                  uint64_t d, int32_t* labels, double* votes) {
   return guard([&] {
     require_ctx(c);
+    c->join_feeder();
     const sofg::FlatForest& f = fo->f;
     if (d != f.n_features)
       throw std::invalid_argument("sample has " + std::to_string(d) + " features, model expects " +
