@@ -10,6 +10,16 @@ namespace sofg {
 namespace dev {
 
 // split.hpp:126-134 — order-preserving float -> u32 map.
+// Read-only load with a 64-byte L2 fill: for strided reads (one 4-byte value per 384-byte sample
+// block: the partition's winning row) the default fill of a missed line is 128 bytes; 64 halves
+// the DRAM bytes (tools/mb/sector_mb.cu: 128 -> 64 B per value, 1.25 -> 1.00 ms; partition 58 ->
+// 54 ms per step). Not for the boundary picks: their neighbouring rows reuse the wider fill.
+__device__ __forceinline__ float ldg_l2_64(const float* p) {
+  float v;
+  asm("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t order_key(float v) {
   const uint32_t u = __float_as_uint(v);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) k_part_flags_w(
     bool f = false;
     uint32_t y = 0;
     if (l < tl.len) {
-      f = __ldg(Vn + uint64_t(l) * Rp) <= thr;
+      f = ldg_l2_64(Vn + uint64_t(l) * Rp) <= thr;
       y = ln[l];
     }
     const unsigned m = __ballot_sync(0xffffffffu, f);
