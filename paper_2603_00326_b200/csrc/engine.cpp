@@ -116,14 +116,11 @@ void WaveRunner::submit(const WaveSpec& w) {
   // ---- derived work lists (built straight into the page-locked staging buffer) ------------
   // Per node: histogram work items (row groups x chunks), partition tiles, exact bucket, G block
   // offset and gather-item count. Two parallel passes over node chunks: counts, then fills.
-  // Histogram counting: nodes up to lr_max samples go to the lane = row kernel (32 rows per CTA,
-  // one chunk), larger nodes to the lane = sample kernel (8 rows per CTA, chunks of chunk_cap,
-  // merged in global counters). Measured per level at 1M x 4096: lane = sample is faster while
-  // nodes hold more than ~4K samples (shared-memory bound either way, fewer instructions per
-  // value), lane = row below (no setup-dominated small CTAs with bank-conflicting searches).
+  // Histogram counting: two classes and <= 256 bins go to the lane = row kernel for every node
+  // size (32 rows per CTA, chunks of lr_chunk samples merged in global counters: 241 -> 177 ms per
+  // 1M x 4096 step against the lane = sample kernel above 64K samples); other class / bin counts to
+  // the lane = sample kernel (8 rows per CTA, chunks of chunk_cap), more than 8 classes to wide.cu.
   static const int lr_env = std::getenv("SOFG_HIST_LR") ? std::atoi(std::getenv("SOFG_HIST_LR")) : -1;
-  static const uint32_t lr_max_env =
-      std::getenv("SOFG_HIST_LR_MAXN") ? uint32_t(std::atoi(std::getenv("SOFG_HIST_LR_MAXN"))) : 0xffffffffu;
   // Nodes above lr_chunk samples are counted in chunks of lr_chunk (u16 packed counters per CTA),
   // merged in the global counters like the lane = sample kernel's multi-chunk nodes.
   static const uint32_t lr_chunk_env =
@@ -131,7 +128,7 @@ void WaveRunner::submit(const WaveSpec& w) {
   const bool wide = k > kMaxClasses;  // wide.cu kernels, class counts in side arrays
   constexpr uint32_t kWideChunk = 65535;  // u16 counters per CTA
   const bool lr_ok = !wide && k == 2 && bins <= 256 && (lr_env >= 0 ? lr_env != 0 : hist_count_lane_rows(R, bins, k));
-  const uint32_t lr_max = lr_ok ? (lr_env == 1 ? 0xffffffffu : lr_max_env) : 0u;
+  const uint32_t lr_max = lr_ok ? 0xffffffffu : 0u;
   const uint32_t lr_chunk = std::max(1024u, std::min(lr_chunk_env, 65504u));
   const uint32_t groups = (R + kHistRowsPerCta - 1) / kHistRowsPerCta;
   const uint32_t groups_lr = (R + 31) / 32;

@@ -1067,8 +1067,8 @@ cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* li
     case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
-    case 3: return std::getenv("SOFG_TEAM256") ? launch_team<1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st) : launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
-    case 4: return std::getenv("SOFG_REG512") ? launch_bucket<16, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st) : launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);  // register E=16 measured slower
+    case 3: return launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);  // (a register E = 16 sort measured slower)
     case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     default: return cudaErrorInvalidValue;

@@ -1,15 +1,13 @@
 // Stable two-way partition of every split node's segment (reference forest.hpp:197-212:
 // values <= threshold stay left in order, the rest follow in order).
 //
-//  k_part_flags    per 1024-element tile: recompute the winning row's projected value, flag
-//                  v <= thr, store the flag bits, count lefts per tile and per class.
-//  k_part_scan     per node: exclusive scan of tile left-counts; fills n_left, the stream
-//                  position after the attempt and the winning row's terms in NodeRes.
-//  k_part_scatter  per tile: rank inside the tile from the flag bits, scatter sample ids and
-//                  labels into the next level's buffers.
+//  k_part_flags_w    per 1024-element tile (one warp): read the winning row's projected value,
+//                    flag v <= thr, store the flag bits, count lefts per tile and per class.
+//  k_part_scan       per node: exclusive scan of tile left-counts; fills n_left, the stream
+//                    position after the attempt and the winning row's terms in NodeRes.
+//  k_part_scatter_w  per tile (one warp): rank inside the tile from the flag bits, scatter sample
+//                    ids and labels into the next level's buffers.
 #include <cuda_runtime.h>
-
-#include <cstdlib>
 
 #include "common.hpp"
 #include "dev_util.cuh"
@@ -17,69 +15,6 @@
 
 namespace sofg {
 namespace dev {
-
-__global__ void __launch_bounds__(256) k_part_flags(
-    const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, uint32_t R, int k,
-    const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
-    const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
-    const float* __restrict__ G, NodeRes* __restrict__ res, uint32_t* __restrict__ flags,
-    uint32_t* __restrict__ tile_left, uint32_t* __restrict__ class_left) {
-  __shared__ uint32_t s_cls[kMaxClasses];
-  __shared__ uint32_t s_left;
-  const Tile tl = tiles[blockIdx.x];
-  const NodeIn nd = nodes[tl.node];
-  const int row = res[tl.node].row;
-  if (row < 0) return;
-  const float thr = res[tl.node].threshold;
-  if (threadIdx.x < kMaxClasses) s_cls[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_left = 0;
-  __syncthreads();
-  const uint32_t Rp = vpitch(R);
-  const float* Vn = G + gbase[tl.node] + row;  // winning row of the node's V block (sweep.cu)
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  uint32_t my_left = 0;
-  uint32_t cls[kMaxClasses];
-#pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c) cls[c] = 0;
-  float v[4];
-  uint8_t y[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const uint32_t l = uint32_t(e * 256 + threadIdx.x);
-    if (l < tl.len) {
-      v[e] = __ldg(Vn + uint64_t(tl.start + l) * Rp);
-      y[e] = lab[nd.begin + tl.start + l];
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const uint32_t l = uint32_t(e * 256 + threadIdx.x);
-    const bool f = l < tl.len && v[e] <= thr;
-    const unsigned m = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) flags[size_t(blockIdx.x) * 32 + e * 8 + w] = m;
-    if (f) {
-      ++my_left;
-#pragma unroll
-      for (int c = 0; c < kMaxClasses; ++c) cls[c] += (c == int(y[e]));
-    }
-  }
-  // reduce
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) my_left += __shfl_xor_sync(0xffffffffu, my_left, o);
-  if (lane == 0) atomicAdd(&s_left, my_left);
-#pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c) {
-    uint32_t x = cls[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0 && c < k && x) atomicAdd(&s_cls[c], x);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) tile_left[blockIdx.x] = s_left;
-  if (threadIdx.x < uint32_t(k) && s_cls[threadIdx.x])
-    atomicAdd(&class_left[size_t(tl.node) * k + threadIdx.x], s_cls[threadIdx.x]);
-}
 
 // One warp per node: scan its tiles (tiles of a node are contiguous, first = tile_first[node]).
 __global__ void k_part_scan(const NodeIn* __restrict__ nodes, int n_nodes, uint32_t R,
@@ -116,48 +51,9 @@ __global__ void k_part_scan(const NodeIn* __restrict__ nodes, int n_nodes, uint3
   for (uint32_t q = lane; q < nt && q < uint32_t(kWinTermsMax); q += 32) o.terms[q] = rt[q];
 }
 
-__global__ void __launch_bounds__(256) k_part_scatter(
-    const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles,
-    const NodeRes* __restrict__ res, const uint32_t* __restrict__ flags,
-    const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ idx_in,
-    const uint8_t* __restrict__ lab_in, uint32_t* __restrict__ idx_out,
-    uint8_t* __restrict__ lab_out, uint32_t* __restrict__ inv, uint32_t B) {
-  __shared__ uint32_t s_wpre[32];
-  const Tile tl = tiles[blockIdx.x];
-  if (res[tl.node].row < 0) return;
-  const NodeIn nd = nodes[tl.node];
-  const uint32_t n_left = res[tl.node].n_left;
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const uint32_t* fw = flags + size_t(blockIdx.x) * 32;
-  if (w == 0) {
-    uint32_t tot;
-    s_wpre[lane] = warp_excl_scan_u32(__popc(fw[lane]), lane, &tot);
-  }
-  __syncthreads();
-  const uint32_t off = tile_off[blockIdx.x];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const uint32_t l = uint32_t(e * 256 + threadIdx.x);
-    if (l >= tl.len) continue;
-    const int word = e * 8 + w;
-    const uint32_t m = fw[word];
-    const uint32_t lrank = s_wpre[word] + __popc(m & ((1u << lane) - 1u));
-    const uint32_t p = tl.start + l;             // position inside the node
-    const uint32_t L = off + lrank;              // left elements before p
-    const bool left = (m >> lane) & 1u;
-    const uint32_t dst = left ? L : n_left + (p - L);
-    const uint32_t src = nd.begin + p;
-    const uint32_t smp = idx_in[src];
-    idx_out[nd.begin + dst] = smp;
-    lab_out[nd.begin + dst] = lab_in[src];
-    if (inv) inv[uint64_t(smp) * B + nd.tree] = nd.begin + dst;  // sweep.cu inverse map
-  }
-}
-
-// Warp-per-tile forms of k_part_flags / k_part_scatter (same flag-word layout: word l / 32 of the
-// tile's 32 words covers elements [32 word, 32 word + 32)). A CTA takes 8 tiles, so the many
-// small nodes of deep levels do not each occupy a 256-thread CTA for a few dozen elements.
+// Flags and scatter, one warp per partition tile (flag word l / 32 of the tile's 32 words covers
+// elements [32 word, 32 word + 32)). A CTA takes 8 tiles, so the many small nodes of deep levels
+// do not each occupy a 256-thread CTA for a few dozen elements.
 __global__ void __launch_bounds__(256) k_part_flags_w(
     const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, int n_tiles, uint32_t R, int k,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase, const float* __restrict__ G,
@@ -315,19 +211,12 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              uint32_t* tile_left, uint32_t* inv, uint32_t B, uint32_t* class_left,
                              cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
-  const bool cta_tiles = std::getenv("SOFG_PART_CTA") != nullptr && k <= kMaxClasses;  // CTA-per-tile forms
-  if (n_tiles > 0 && cta_tiles)
-    dev::k_part_flags<<<n_tiles, 256, 0, st>>>(nodes, tiles, R, k, terms, row_ptr, lab_in, gbase,
-                                               G, res, flags, tile_left, class_left);
-  else if (n_tiles > 0)
+  if (n_tiles > 0)
     dev::k_part_flags_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, R, k, lab_in, gbase, G, res,
                                                            flags, tile_left, class_left);
   dev::k_part_scan<<<(n_nodes + 3) / 4, 128, 0, st>>>(nodes, n_nodes, R, tile_first, terms,
                                                       row_ptr, pos_proj, pos_split, tile_left, res);
-  if (n_tiles > 0 && cta_tiles)
-    dev::k_part_scatter<<<n_tiles, 256, 0, st>>>(nodes, tiles, res, flags, tile_left, idx_in,
-                                                 lab_in, idx_out, lab_out, inv, B);
-  else if (n_tiles > 0)
+  if (n_tiles > 0)
     dev::k_part_scatter_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, res, flags, tile_left, idx_in,
                                                              lab_in, idx_out, lab_out, inv, B);
   return cudaGetLastError();
