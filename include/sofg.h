@@ -69,7 +69,7 @@ typedef struct sofg_train_config {
   uint64_t n_trees;            /* 100 */
   int32_t mode;                /* 0 exact-only, 1 histogram-only, 2 dynamic (forest.hpp:20) */
   int32_t two_level_binning;   /* accepted, results identical either way (histogram.hpp:118) */
-  uint64_t bin_count;          /* 256, 2..1024 */
+  uint64_t bin_count;          /* 256, 2..8192 (bins x classes bounded) */
   int32_t has_breakeven;       /* Dynamic: histogram iff n > breakeven (split.hpp:46-48) */
   int32_t has_max_depth;
   uint64_t breakeven;          /* absent: train_forest calibrates on the GPU (forest.hpp:285-293);

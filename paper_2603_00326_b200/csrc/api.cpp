@@ -253,6 +253,17 @@ PCfg projection_config(uint64_t d, uint64_t num_projections, double cell_density
   return p;
 }
 
+// Histogram bin counts the GPU splitter takes: up to kMaxBins; the shared-memory counters of the
+// wide-class / large-bin counting kernel (wide.cu) bound bins x classes there.
+void check_bins(uint64_t bins, int k) {
+  if (bins < 2) throw std::invalid_argument("bin_count must be at least 2");
+  if (bins > uint64_t(sofg::kMaxBins))
+    throw std::invalid_argument("bin_count > " + std::to_string(sofg::kMaxBins) +
+                                " is not supported by the GPU histogram splitter");
+  if ((k > sofg::kMaxClasses || bins > 1024) && sofg::hist_wide_smem(uint32_t(bins), k) > size_t(sofg::kSmemOptin))
+    throw std::invalid_argument("bin_count x class_count too large for the GPU histogram splitter");
+}
+
 void validate_cfg(const sofg_train_config* cfg, const sofg::DeviceData& D) {  // forest.hpp:270-276
   if (cfg->n_trees < 1) throw std::invalid_argument("n_trees must be positive");
   if (cfg->bin_count < 2) throw std::invalid_argument("bin_count must be at least 2");
@@ -262,9 +273,7 @@ void validate_cfg(const sofg_train_config* cfg, const sofg::DeviceData& D) {  //
     throw std::invalid_argument("bootstrap fraction must be in (0, 1]");
   if (D.n < 2) throw std::invalid_argument("need at least 2 samples");
   if (D.k < 2) throw std::invalid_argument("need at least 2 classes");
-  if (cfg->bin_count > uint64_t(sofg::kMaxBins))
-    throw std::invalid_argument("bin_count > " + std::to_string(sofg::kMaxBins) +
-                                " is not supported by the GPU histogram splitter");
+  check_bins(cfg->bin_count, D.k);
   if (cfg->mode < 0 || cfg->mode > 2) throw std::invalid_argument("unknown split mode");
 }
 
@@ -532,9 +541,7 @@ int sofg_train_tree(sofg_ctx* c, const uint32_t* active, uint64_t n_active,
     if (n_active == 0) throw std::invalid_argument("active sample set is empty");  // forest.hpp:254
     for (uint64_t i = 0; i < n_active; ++i)
       if (active[i] >= D.n) throw std::out_of_range("sample index out of range");  // :256
-    if (cfg->bin_count < 2) throw std::invalid_argument("bin_count must be at least 2");
-    if (cfg->bin_count > uint64_t(sofg::kMaxBins))
-      throw std::invalid_argument("bin_count exceeds the GPU histogram splitter");
+    check_bins(cfg->bin_count, D.k);
     sofg::TrainParams P = params_for(cfg, D, false);
     ensure_xlogx(c->eng->data(), n_active, c->eng->stream());
     sofg::ThreadPool& pool = pool_for(c, cfg->n_workers);
@@ -856,8 +863,7 @@ int sofg_find_node_split(sofg_ctx* c, const uint32_t* active, uint64_t n, const 
     const sofg::DeviceData& D = c->eng->data();
     std::memset(out, 0, sizeof(*out));
     if (n < 2) return;  // split.hpp:238
-    if (bins < 2) throw std::invalid_argument("bin_count must be at least 2");
-    if (bins > uint64_t(sofg::kMaxBins)) throw std::invalid_argument("bin_count too large");
+    check_bins(bins, D.k);
     for (uint64_t i = 0; i < n; ++i)
       if (active[i] >= D.n) throw std::out_of_range("sample index out of range");
     ensure_xlogx(c->eng->data(), n, c->eng->stream());

@@ -17,7 +17,7 @@ namespace sofg {
 
 constexpr int kMaxClasses = 8;       // class counts carried inline (NodeRes, host frontier, register kernels)
 constexpr int kMaxClassesWide = 64;  // class_count supported (above kMaxClasses: wide.cu, side arrays)
-constexpr int kMaxBins = 1024;       // bin_count supported by the histogram splitter
+constexpr int kMaxBins = 8192;       // bin_count supported by the histogram splitter (> 1024: CTA boundaries, wide.cu counts)
 constexpr int kExactSmemMax = 2048;  // largest node the shared-memory exact splitter sorts
 constexpr int kTileElems = 1024;     // partition tile
 constexpr int kWinTermsMax = 8;      // winning-row terms returned inline per node (longer rows: k_win_terms)

@@ -126,8 +126,10 @@ void WaveRunner::submit(const WaveSpec& w) {
   static const uint32_t lr_chunk_env =
       std::getenv("SOFG_HIST_LR_CHUNK") ? uint32_t(std::atoi(std::getenv("SOFG_HIST_LR_CHUNK"))) : 32768u;
   const bool wide = k > kMaxClasses;  // wide.cu kernels, class counts in side arrays
+  // histogram counting by wide.cu also above 1024 bins (the register / lane = row kernels' limit)
+  const bool wide_hist = wide || bins > 1024;
   constexpr uint32_t kWideChunk = 65535;  // u16 counters per CTA
-  const bool lr_ok = !wide && k == 2 && bins <= 256 && (lr_env >= 0 ? lr_env != 0 : hist_count_lane_rows(R, bins, k));
+  const bool lr_ok = !wide_hist && k == 2 && bins <= 256 && (lr_env >= 0 ? lr_env != 0 : hist_count_lane_rows(R, bins, k));
   const uint32_t lr_max = lr_ok ? 0xffffffffu : 0u;
   const uint32_t lr_chunk = std::max(1024u, std::min(lr_chunk_env, 65504u));
   const uint32_t groups = (R + kHistRowsPerCta - 1) / kHistRowsPerCta;
@@ -164,7 +166,7 @@ void WaveRunner::submit(const WaveSpec& w) {
         t.terms_end = std::max<uint64_t>(t.terms_end, uint64_t(nd.term_off) + nd.z);
         if (nd.flags & kNodeHist) {
           t.hist++;
-          if (wide) {  // one item per (row, chunk of <= 65535 samples): wide.cu
+          if (wide_hist) {  // one item per (row, chunk of <= 65535 samples): wide.cu
             const uint32_t chunks = (nd.n + kWideChunk - 1) / kWideChunk;
             if (chunks > 1) t.multi++;
             t.work += uint64_t(R) * chunks;
@@ -278,7 +280,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       if (nd.flags & kNodeHist) {
         p_hslot[i] = uint32_t(o.hist);
         p_hist[o.hist++] = uint32_t(i);
-        if (wide) {
+        if (wide_hist) {
           const uint32_t chunks = (nd.n + kWideChunk - 1) / kWideChunk;
           if (chunks > 1) p_mslot[i] = uint32_t(o.multi++);
           for (uint32_t r = 0; r < R; ++r)
@@ -467,7 +469,7 @@ void WaveRunner::submit(const WaveSpec& w) {
                                       bins, int(std::max(tot.lr_len, 32u)), w.two_level ? 1 : 0, w.lab_in, d_gbase, d_G, d_bnd, d_nb,
                                       D.xl.p, d_gcnt, d_done, d_rowres, st_),
                  "hist_count_lr");
-    if (n_work_old && wide)
+    if (n_work_old && wide_hist)
       cuda_check(launch_hist_wide(d_nodes, d_hslot, d_work, int(n_work_old), d_mslot, R, bins, k, w.two_level ? 1 : 0,
                                   w.lab_in, d_gbase, d_G, d_bnd, d_nb, D.xl.p, d_gcnt, d_done, d_rowres, st_),
                  "hist_wide");

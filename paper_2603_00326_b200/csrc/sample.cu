@@ -480,6 +480,141 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
   if (lane == 0) nb_out[size_t(h) * R + r] = total;
 }
 
+// Boundaries for more than 1024 bins (sample_boundaries with m = min(bins, n) up to kMaxBins picks,
+// histogram.hpp:42-61): one CTA of 256 threads per (node, row), thread t owning draws
+// [t EPT, (t + 1) EPT); the same three steps as k_hist_boundaries (hash of first indices, the
+// D-fixpoint, gather) with the picked keys bitonic-sorted in shared memory and the midpoints
+// compacted by a block scan. Shared memory: 2 * MP hash slots (value, index) + MP keys + MP flags.
+constexpr int kBndCtaThreads = 256;
+template <int MP>
+__global__ void __launch_bounds__(kBndCtaThreads) k_hist_boundaries_cta(
+    const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist, uint32_t R,
+    uint32_t bins, const uint32_t* __restrict__ draws, const uint64_t* __restrict__ gbase,
+    const float* __restrict__ G, float* __restrict__ bnd, uint32_t* __restrict__ nb_out) {
+  constexpr int EPT = MP / kBndCtaThreads;
+  constexpr uint32_t TS = 2u * MP;
+  constexpr int TB = 31 - __builtin_clz(TS);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* hk = reinterpret_cast<uint32_t*>(smem_raw);  // [TS] draw values (~0 = empty)
+  uint32_t* hi = hk + TS;                                // [TS] smallest index holding the value
+  uint32_t* keys = hi + TS;                              // [MP]
+  uint8_t* col = reinterpret_cast<uint8_t*>(keys + MP);  // [MP]
+  __shared__ uint32_t s_warp[kBndCtaThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t h = uint32_t(blockIdx.x / R), r = uint32_t(blockIdx.x % R);
+  if (h >= uint32_t(n_hist)) return;
+  const uint32_t node = hist_nodes[h];
+  const uint32_t n = nodes[node].n;
+  float* out = bnd + (size_t(h) * R + r) * (bins - 1);
+  if (n < 2 || bins < 2) {
+    if (tid == 0) nb_out[size_t(h) * R + r] = 0;
+    return;
+  }
+  const uint32_t m = min(bins, n), J0 = n - m, Rp = vpitch(R);
+  const float* Vn = G + gbase[node] + r;
+  const uint32_t i0 = uint32_t(tid * EPT);
+  if (m < n) {
+    const uint32_t* t = draws + size_t(h) * R * bins + size_t(r) * m;
+    uint32_t tv[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) tv[e] = i0 + e < m ? __ldg(t + i0 + e) : 0u;
+    for (uint32_t i = tid; i < TS; i += kBndCtaThreads) {
+      hk[i] = ~0u;
+      hi[i] = ~0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t i = i0 + uint32_t(e);
+      if (i < m) {
+        uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
+        for (;;) {
+          const uint32_t old = atomicCAS(hk + sl, ~0u, tv[e]);
+          if (old == ~0u || old == tv[e]) {
+            atomicMin(hi + sl, i);
+            break;
+          }
+          sl = (sl + 1) & (TS - 1);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {  // C1: an earlier draw has the same value
+      const uint32_t i = i0 + uint32_t(e);
+      uint8_t c1 = 0;
+      if (i < m) {
+        uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
+        while (hk[sl] != tv[e]) sl = (sl + 1) & (TS - 1);
+        c1 = hi[sl] != i ? 1 : 0;
+      }
+      col[i] = c1;
+    }
+    __syncthreads();
+    for (;;) {  // D_i = C1_i or (J0 <= t_i < J0 + i and D_{t_i - J0}): monotone fixpoint
+      bool ch = false;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const uint32_t i = i0 + uint32_t(e);
+        if (i < m && !col[i] && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) {
+          col[i] = 1;
+          ch = true;
+        }
+      }
+      if (__syncthreads_or(ch) == 0) break;
+    }
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t i = i0 + uint32_t(e);
+      keys[i] = i < m ? order_key(__ldg(Vn + uint64_t(col[i] ? J0 + i : tv[e]) * Rp)) : 0xffffffffu;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t i = i0 + uint32_t(e);
+      keys[i] = i < m ? order_key(__ldg(Vn + uint64_t(i) * Rp)) : 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  for (uint32_t sz = 2; sz <= uint32_t(MP); sz <<= 1)  // bitonic sort, ascending
+    for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+      for (uint32_t i = tid; i < uint32_t(MP); i += kBndCtaThreads) {
+        const uint32_t j = i ^ st;
+        if (j > i) {
+          const uint32_t a = keys[i], b = keys[j];
+          if ((a > b) == ((i & sz) == 0)) {
+            keys[i] = b;
+            keys[j] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // midpoints of consecutive distinct values (float comparison: -0 == +0), compacted in order
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const uint32_t i = i0 + uint32_t(e);
+    cnt += (i >= 1 && i < m && order_key_inv(keys[i - 1]) < order_key_inv(keys[i])) ? 1u : 0u;
+  }
+  uint32_t wt;
+  const uint32_t wex = warp_excl_scan_u32(cnt, lane, &wt);
+  if (lane == 0) s_warp[w] = wt;
+  __syncthreads();
+  uint32_t pos = wex, total = 0;
+  for (int ww = 0; ww < kBndCtaThreads / 32; ++ww) {
+    if (ww < w) pos += s_warp[ww];
+    total += s_warp[ww];
+  }
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const uint32_t i = i0 + uint32_t(e);
+    if (i >= 1 && i < m && order_key_inv(keys[i - 1]) < order_key_inv(keys[i]))
+      out[pos++] = midpoint_down(order_key_inv(keys[i - 1]), order_key_inv(keys[i]));
+  }
+  if (tid == 0) nb_out[size_t(h) * R + r] = total;
+}
+
 }  // namespace dev
 
 // ---------------------------------------------------------------------------- launchers
@@ -554,6 +689,19 @@ cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nod
     case 256: return go(dev::k_hist_boundaries<8>);
     case 512: return go(dev::k_hist_boundaries<16>);
     case 1024: return go(dev::k_hist_boundaries<32>);
+    default: break;
+  }
+  auto go_cta = [&](auto kern) {  // more than 1024 bins: one CTA per (node, row)
+    const size_t smem_cta = size_t(mpad) * 21;  // hash 2 x 2 MP words, keys MP words, flags MP bytes
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
+    kern<<<unsigned(uint64_t(n_hist) * R), dev::kBndCtaThreads, smem_cta, st>>>(nodes, hist_nodes, n_hist, R, bins, draws,
+                                                                               gbase, G, bnd, nb);
+    return cudaGetLastError();
+  };
+  switch (mpad) {
+    case 2048: return go_cta(dev::k_hist_boundaries_cta<2048>);
+    case 4096: return go_cta(dev::k_hist_boundaries_cta<4096>);
+    case 8192: return go_cta(dev::k_hist_boundaries_cta<8192>);
     default: return cudaErrorInvalidValue;
   }
 }
