@@ -390,7 +390,10 @@ __global__ void __launch_bounds__(256) k_hist_count(
 // 32 x 32 tile by tile (conflict-free both ways) into skewed row-major rows and each warp scans 4
 // rows; multi-chunk nodes merge into the global counters first and the chunk that completes a
 // (node, row group) scans.
-constexpr int kLrU = 8;
+#ifndef SOFG_LRU
+#define SOFG_LRU 8
+#endif
+constexpr int kLrU = SOFG_LRU;  // searches in flight per lane (divides 32: a step's labels sit in one word)
 template <int LT>
 struct LrLayout {
   static constexpr int BP = 1 << LT;
