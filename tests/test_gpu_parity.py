@@ -365,3 +365,17 @@ def test_dense_projection_collision_resolution(gpu_ctx, oracle):
     gpu_ctx.upload(X, y, 2)
     gc, oc = _cfg(n_trees=2, mode="dynamic", breakeven=300, seed=9, cell_density=0.2)
     assert _forest_equal(gpu_ctx.train_forest(gc), oracle.train_forest(X, y, 2, oc)) == []
+
+
+def test_train_tree_repeated_active_longer_than_n(gpu_ctx, oracle):
+    # train_tree takes any active list (forest.hpp:250-262 checks only empty / out of range):
+    # repeated samples, more entries than the dataset has rows (xlogx tables grow with the list)
+    X, y = oracle.generate_trunk(700, 6, 17)
+    gpu_ctx.upload(X, y, 2)
+    rng = np.random.default_rng(5)
+    active = np.sort(rng.integers(0, 700, 1900)).astype(np.uint32)
+    for mode, breakeven in (("dynamic", 300), ("histogram", None), ("exact", None)):
+        gc, oc = _cfg(n_trees=1, mode=mode, breakeven=breakeven, seed=31)
+        t = gpu_ctx.train_tree(active, gc, 1234)
+        o = oracle.train_tree(X, y, 2, active, oc, 1234)
+        assert _forest_equal(t, o) == [], mode
