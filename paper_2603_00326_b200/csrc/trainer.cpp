@@ -96,6 +96,7 @@ void recycle_forest(FlatForest&& f) {
   if (g_recycled.size() < 2) g_recycled.push_back(std::move(f));
 }
 
+// Swaps recycled storage (capacity, no contents) into an empty forest.
 void adopt_recycled(FlatForest& out) {
   if (!out.left.empty()) return;  // appending to a non-empty forest: keep its arrays
   std::lock_guard<std::mutex> g(g_recycle_mu);
@@ -651,8 +652,8 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
     node_base[b + 1] = node_base[b] + trees[b].size();
     term_base[b + 1] = term_base[b] + pools[b].size();
   }
-  adopt_recycled(out);
   const size_t N0 = out.left.size(), Q0 = out.feat.size(), T0 = out.tree_off.size();
+  adopt_recycled(out);
   out.left.resize(N0 + node_base[B]);
   out.right.resize(N0 + node_base[B]);
   out.pred.resize(N0 + node_base[B]);
@@ -661,40 +662,54 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
   out.feat.resize(Q0 + term_base[B]);
   out.weight.resize(Q0 + term_base[B]);
   out.tree_off.resize(T0 + B);
+  out.term_off[N0] = int64_t(Q0);
+  // Node ids without a depth-first walk: the reference numbers the two children of a node when it
+  // splits, visiting nodes depth-first, left first (forest.hpp:214-229), so the left child of an
+  // internal node v gets id 1 + 2 * (internal nodes before v in preorder). Children are created
+  // after their parent (level order), so one reverse pass counts each subtree's internal nodes,
+  // one forward pass gives every node's id, and the output is written in id order by scattered
+  // stores while tr and the term pool are read sequentially.
   pool.parallel_for(B, [&](size_t b) {
     const std::vector<BNode>& tr = trees[b];
     const std::vector<uint32_t>& tp = pools[b];
-    std::vector<int32_t> id(tr.size(), -1), by_id(tr.size());
-    std::vector<int32_t> stack{0};
-    id[0] = 0;
-    int32_t next_id = 1;
-    while (!stack.empty()) {
-      const int32_t v = stack.back();
-      stack.pop_back();
-      const BNode& nv = tr[size_t(v)];
-      if (nv.left >= 0) {
-        id[size_t(nv.left)] = next_id;
-        id[size_t(nv.right)] = next_id + 1;
-        next_id += 2;
-        stack.push_back(nv.right);
-        stack.push_back(nv.left);
-      }
+    const size_t nn = tr.size();
+    std::vector<uint32_t> cnt(nn), id(nn);  // internal nodes in the subtree, then preorder rank
+    for (size_t v = nn; v-- > 0;) {
+      const BNode& nv = tr[v];
+      cnt[v] = nv.left >= 0 ? 1u + cnt[size_t(nv.left)] + cnt[size_t(nv.right)] : 0u;
     }
-    for (size_t v = 0; v < tr.size(); ++v) by_id[size_t(id[v])] = int32_t(v);
-    size_t q = N0 + node_base[b];
-    uint64_t tq = Q0 + term_base[b];
-    for (size_t u = 0; u < tr.size(); ++u, ++q) {
-      const BNode& nv = tr[size_t(by_id[u])];
-      out.left[q] = nv.left >= 0 ? id[size_t(nv.left)] : -1;
-      out.right[q] = nv.right >= 0 ? id[size_t(nv.right)] : -1;
+    std::vector<uint32_t> pre(nn);  // internal nodes before v in preorder
+    pre[0] = 0;
+    id[0] = 0;
+    std::vector<uint64_t> toff(nn + 1, 0);  // term_len by id, then exclusive prefix
+    for (size_t v = 0; v < nn; ++v) {
+      const BNode& nv = tr[v];
+      if (nv.left >= 0) {
+        const size_t L = size_t(nv.left), Rn = size_t(nv.right);
+        pre[L] = pre[v] + 1;
+        pre[Rn] = pre[v] + 1 + cnt[L];
+        id[L] = 1 + 2 * pre[v];
+        id[Rn] = id[L] + 1;
+      }
+      toff[id[v] + 1] = nv.term_len;
+    }
+    for (size_t u = 0; u < nn; ++u) toff[u + 1] += toff[u];
+    const size_t q0 = N0 + node_base[b];
+    const uint64_t tq0 = Q0 + term_base[b];
+    for (size_t v = 0; v < nn; ++v) {
+      const BNode& nv = tr[v];
+      const size_t q = q0 + id[v];
+      out.left[q] = nv.left >= 0 ? int32_t(id[size_t(nv.left)]) : -1;
+      out.right[q] = nv.right >= 0 ? int32_t(id[size_t(nv.right)]) : -1;
       out.pred[q] = nv.pred;
       out.thr[q] = nv.left >= 0 ? nv.thr : 0.f;
+      uint64_t tq = tq0 + toff[id[v]];
       for (uint32_t t = 0; t < nv.term_len; ++t, ++tq) {
         const uint32_t e = tp[nv.term_off + t];
         out.feat[tq] = e >> 1;
         out.weight[tq] = (e & 1u) ? -1.f : 1.f;
       }
-      out.term_off[q + 1] = int64_t(tq);
+      out.term_off[q + 1] = int64_t(tq0 + toff[id[v] + 1]);
     }
     out.tree_off[T0 + b] = int64_t(N0 + node_base[b + 1]);
   });
