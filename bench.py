@@ -55,7 +55,7 @@ def parse():
                    help="dynamic-switch threshold; 512 = B200 calibration (DESIGN.md 3, calibrate.py)")
     p.add_argument("--mode", default="dynamic", choices=["dynamic", "exact", "histogram"])
     p.add_argument("--seed", type=int, default=7)
-    p.add_argument("--e2e-steps", type=int, default=6)
+    p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--e2e-serial", action="store_true", help="e2e without the second-context input pipeline")
     p.add_argument("--cpu-trees", type=int, default=0, help="CPU baseline sample (0 = one per core)")
     p.add_argument("--holdout", type=int, default=20000, help="hold-out rows for the accuracy check")
