@@ -251,6 +251,7 @@ class WaveRunner {
   DevBuf<uint32_t> inv;
   DevBuf<uint64_t> tree_off;
   DevBuf<uint32_t> root_counts;
+  DevBuf<uint32_t> root_bits;  // root sets as bitmaps (one bit per dataset row, per tree)
 
  private:
   int device_;

@@ -136,6 +136,9 @@ cudaError_t launch_sector_count(const NodeIn* nodes, const Tile* tiles, int n_ti
                                 const uint32_t* idx, NodeRes* res, cudaStream_t st);
 
 // misc.cu
+// Tree b's sorted sample ids from its bitmap bits[b * W, (b + 1) * W) into ids[off[b] ...].
+cudaError_t launch_bits_to_ids(const uint32_t* bits, uint64_t W, uint32_t B, const uint64_t* off, uint32_t* ids,
+                               cudaStream_t st);
 // lab_out[p] = labels[idx[p]]; counts[b * k + c] = class-c count of tree b's root segment
 cudaError_t launch_root_labels(const uint32_t* idx, const uint64_t* off, uint32_t B,
                                uint64_t max_per_tree, const uint8_t* labels, uint8_t* lab_out,

@@ -102,6 +102,35 @@ __global__ void __launch_bounds__(256) k_root_labels(const uint32_t* __restrict_
     if (s_cnt[c]) atomicAdd(&counts[size_t(b) * k + c], s_cnt[c]);
 }
 
+
+// One CTA per tree: thread t takes words [t * per, (t + 1) * per), counts their bits, a block scan
+// gives its first rank, then it writes the ids of its set bits in order.
+__global__ void __launch_bounds__(1024) k_bits_to_ids(const uint32_t* __restrict__ bits, uint64_t W,
+                                                     const uint64_t* __restrict__ off, uint32_t* __restrict__ ids) {
+  __shared__ uint32_t s_warp[32];
+  const uint32_t b = blockIdx.x;
+  const uint32_t* bw = bits + uint64_t(b) * W;
+  const uint64_t per = (W + blockDim.x - 1) / blockDim.x;
+  const uint64_t w0 = uint64_t(threadIdx.x) * per, w1 = min(W, w0 + per);
+  uint32_t c = 0;
+  for (uint64_t i = w0; i < w1; ++i) c += __popc(bw[i]);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t wt;
+  const uint32_t ex = warp_excl_scan_u32(c, lane, &wt);
+  if (lane == 0) s_warp[w] = wt;
+  __syncthreads();
+  uint32_t pos = ex;
+  for (int i = 0; i < w; ++i) pos += s_warp[i];
+  uint32_t* out = ids + off[b];
+  for (uint64_t i = w0; i < w1; ++i) {
+    uint32_t x = bw[i];
+    while (x) {
+      const int t = __ffs(x) - 1;
+      x &= x - 1;
+      out[pos++] = uint32_t(i * 32 + uint64_t(t));
+    }
+  }
+}
 }  // namespace dev
 
 cudaError_t launch_root_labels(const uint32_t* idx, const uint64_t* off, uint32_t B,
@@ -146,6 +175,13 @@ cudaError_t launch_predict(const float* rows, uint64_t n_rows, uint64_t d, const
   if (work == 0) return cudaSuccess;
   dev::k_predict<<<unsigned((work + 255) / 256), 256, 0, st>>>(
       rows, n_rows, d, tree_off, n_trees, left, right, pred, thr, term_off, terms, k, votes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bits_to_ids(const uint32_t* bits, uint64_t W, uint32_t B, const uint64_t* off, uint32_t* ids,
+                               cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  dev::k_bits_to_ids<<<B, 1024, 0, st>>>(bits, W, off, ids);
   return cudaGetLastError();
 }
 

@@ -194,23 +194,53 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
     idx[i].ensure(total);
     lab[i].ensure(total);
   }
-  // Root segments: sample ids to the device; labels and class counts gathered there.
+  // Root segments: sample ids to the device; labels and class counts gathered there. Strictly
+  // increasing root lists (bootstrap samples: sorted sets) travel as one bit per dataset row and
+  // are expanded on the device (n/8 bytes per tree instead of 4 bytes per sample, ~20x fewer).
   uint64_t maxn = 0;
   for (size_t b = 0; b < B; ++b) maxn = std::max<uint64_t>(maxn, roots[b].size());
   DevBuf<uint64_t>& d_off = eng.tree_off;
   d_off.ensure(B + 1);
   std::vector<uint32_t> root_counts(B * size_t(k));
+  std::vector<unsigned char> increasing(B, 1);
+  pool.parallel_for(B, [&](size_t b) {
+    const std::vector<uint32_t>& r = roots[b];
+    for (size_t j = 1; j < r.size(); ++j)
+      if (!(r[j - 1] < r[j])) {
+        increasing[b] = 0;
+        break;
+      }
+  });
+  bool bitmap = true;
+  for (unsigned char x : increasing) bitmap = bitmap && x;
   {
-    unsigned char* stg = eng.staging.ensure(4 * total + 8 * (B + 1) + 4 * size_t(k) * B);
+    const uint64_t W = (D.n + 31) / 32;  // bitmap words per tree
+    const size_t id_bytes = bitmap ? 4 * W * B : 4 * total;
+    unsigned char* stg = eng.staging.ensure(id_bytes + 8 * (B + 1) + 4 * size_t(k) * B);
     uint32_t* hi = reinterpret_cast<uint32_t*>(stg);
-    uint64_t* ho = reinterpret_cast<uint64_t*>(stg + 4 * total);
-    uint32_t* hc = reinterpret_cast<uint32_t*>(stg + 4 * total + 8 * (B + 1));
-    pool.parallel_for(B, [&](size_t b) { std::memcpy(hi + off[b], roots[b].data(), 4 * roots[b].size()); });
+    uint64_t* ho = reinterpret_cast<uint64_t*>(stg + id_bytes);
+    uint32_t* hc = reinterpret_cast<uint32_t*>(stg + id_bytes + 8 * (B + 1));
+    if (bitmap) {
+      pool.parallel_for(B, [&](size_t b) {
+        uint32_t* bw = hi + b * W;
+        std::memset(bw, 0, 4 * W);
+        for (const uint32_t s : roots[b]) bw[s >> 5] |= 1u << (s & 31);
+      });
+    } else {
+      pool.parallel_for(B, [&](size_t b) { std::memcpy(hi + off[b], roots[b].data(), 4 * roots[b].size()); });
+    }
     std::memcpy(ho, off.data(), 8 * (B + 1));
     DevBuf<uint32_t>& d_cnt = eng.root_counts;
     d_cnt.ensure(size_t(k) * B);
-    cuda_check(cudaMemcpyAsync(idx[0].p, hi, 4 * total, cudaMemcpyHostToDevice, eng.stream()), "H2D idx");
     cuda_check(cudaMemcpyAsync(d_off.p, ho, 8 * (B + 1), cudaMemcpyHostToDevice, eng.stream()), "H2D off");
+    if (bitmap) {
+      DevBuf<uint32_t>& d_bits = eng.root_bits;
+      d_bits.ensure(W * B);
+      cuda_check(cudaMemcpyAsync(d_bits.p, hi, 4 * W * B, cudaMemcpyHostToDevice, eng.stream()), "H2D root bits");
+      cuda_check(launch_bits_to_ids(d_bits.p, W, uint32_t(B), d_off.p, idx[0].p, eng.stream()), "bits_to_ids");
+    } else {
+      cuda_check(cudaMemcpyAsync(idx[0].p, hi, 4 * total, cudaMemcpyHostToDevice, eng.stream()), "H2D idx");
+    }
     cuda_check(launch_root_labels(idx[0].p, d_off.p, uint32_t(B), maxn, D.lab.p, lab[0].p, k, d_cnt.p,
                                   eng.stream()),
                "root_labels");
@@ -227,9 +257,7 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
     std::vector<unsigned char> distinct(B, 1);
     pool.parallel_for(B, [&](size_t b) {
       const std::vector<uint32_t>& r = roots[b];
-      bool inc = true;
-      for (size_t j = 1; j < r.size() && inc; ++j) inc = r[j - 1] < r[j];
-      if (!inc) {
+      if (!increasing[b]) {
         std::vector<uint32_t> c(r);
         std::sort(c.begin(), c.end());
         distinct[b] = std::adjacent_find(c.begin(), c.end()) == c.end();
