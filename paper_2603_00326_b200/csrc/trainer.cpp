@@ -135,17 +135,21 @@ struct BNode {
   uint32_t term_off = 0, term_len = 0;  // into the tree's term pool
 };
 
-struct Open {
+// Class counts carried inline in Open (more classes: per-tree side arrays, see grow_trees).
+constexpr int kOpenClasses = 4;
+
+struct Open {  // 64 bytes: the per-level frontier is rewritten twice per node (post, prep)
+  uint64_t seed;
   uint32_t tree;
   int32_t bnode;
   uint32_t begin, n, depth, attempt;
-  uint64_t seed;
-  uint64_t pos;   // engine outputs consumed before this attempt's binomial draw
+  uint32_t pos;   // engine outputs consumed before this attempt's binomial draw
   uint32_t z;     // binomial draw for this attempt (valid when has_z)
   uint32_t zpos;  // stream position after it
   uint32_t has_z;
-  uint32_t counts[kMaxClasses];
+  uint32_t counts[kOpenClasses];
 };
+static_assert(sizeof(Open) == 64, "Open layout");
 
 // Host structures of grow_trees kept across calls (per calling thread): their capacity is
 // reused, so a training step does not fault in hundreds of MB of fresh pages.
@@ -274,9 +278,9 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
   static thread_local GrowScratch S;
   std::vector<std::vector<BNode>>& trees = S.trees;
   std::vector<std::vector<uint32_t>>& pools = S.pools;
-  // More than kMaxClasses classes: class counts live in per-tree side arrays (node v of tree b at
-  // wc[b][v * k, v * k + k)) instead of Open::counts; the wave returns left counts the same way.
-  const bool wide = k > kMaxClasses;
+  // More than kOpenClasses classes: class counts live in per-tree side arrays (node v of tree b at
+  // wc[b][v * k, v * k + k)) instead of Open::counts.
+  const bool wide = k > kOpenClasses;
   std::vector<std::vector<uint32_t>>& wc = S.wide;
   if (trees.size() < B) {
     trees.resize(B);
