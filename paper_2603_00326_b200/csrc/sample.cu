@@ -431,19 +431,20 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
     uint32_t done = 0;  // bit e: flag of draw i0+e known set
 #pragma unroll
     for (int e = 0; e < EPL; ++e) done |= uint32_t(col[i0 + e]) << e;
-    for (;;) {
-      bool ch = false;
+    for (;;) {  // each pass reads every flag, then writes the new ones (no read/write overlap)
+      uint32_t add = 0;
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
         const uint32_t i = i0 + uint32_t(e);
-        if (!(done >> e & 1u) && i < m && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) {
-          col[i] = 1;
-          done |= 1u << e;
-          ch = true;
-        }
+        if (!(done >> e & 1u) && i < m && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) add |= 1u << e;
       }
       __syncwarp();
-      if (!__any_sync(0xffffffffu, ch)) break;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e)
+        if (add >> e & 1u) col[i0 + uint32_t(e)] = 1;
+      done |= add;
+      __syncwarp();
+      if (!__any_sync(0xffffffffu, add != 0)) break;
     }
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
@@ -552,16 +553,17 @@ __global__ void __launch_bounds__(kBndCtaThreads) k_hist_boundaries_cta(
     }
     __syncthreads();
     for (;;) {  // D_i = C1_i or (J0 <= t_i < J0 + i and D_{t_i - J0}): monotone fixpoint
-      bool ch = false;
+      uint32_t add = 0;  // read every flag, then write the new ones
 #pragma unroll
       for (int e = 0; e < EPT; ++e) {
         const uint32_t i = i0 + uint32_t(e);
-        if (i < m && !col[i] && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) {
-          col[i] = 1;
-          ch = true;
-        }
+        if (i < m && !col[i] && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) add |= 1u << e;
       }
-      if (__syncthreads_or(ch) == 0) break;
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < EPT; ++e)
+        if (add >> e & 1u) col[i0 + uint32_t(e)] = 1;
+      if (__syncthreads_or(add != 0) == 0) break;
     }
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
