@@ -416,21 +416,19 @@ __global__ void __launch_bounds__(128) k_hist_boundaries(
       }
     }
     __syncwarp();
+    uint32_t done = 0;  // bit e: flag of draw i0+e known set (C1 first: all lookups, then the stores)
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       const uint32_t i = i0 + uint32_t(e);
-      uint8_t c1 = 0;
       if (i < m) {
         uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
         while (hk[sl] != tv[e]) sl = (sl + 1) & (TS - 1);
-        c1 = hi[sl] != i ? 1 : 0;
+        done |= (hi[sl] != i ? 1u : 0u) << e;
       }
-      col[i] = c1;
     }
-    __syncwarp();
-    uint32_t done = 0;  // bit e: flag of draw i0+e known set
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) done |= uint32_t(col[i0 + e]) << e;
+    for (int e = 0; e < EPL; ++e) col[i0 + uint32_t(e)] = uint8_t(done >> e & 1u);
+    __syncwarp();
     for (;;) {  // each pass reads every flag, then writes the new ones (no read/write overlap)
       uint32_t add = 0;
 #pragma unroll
@@ -540,36 +538,42 @@ __global__ void __launch_bounds__(kBndCtaThreads) k_hist_boundaries_cta(
       }
     }
     __syncthreads();
+    uint32_t c1 = 0;  // C1: an earlier draw has the same value (all lookups, then the stores)
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {  // C1: an earlier draw has the same value
+    for (int e = 0; e < EPT; ++e) {
       const uint32_t i = i0 + uint32_t(e);
-      uint8_t c1 = 0;
       if (i < m) {
         uint32_t sl = (tv[e] * 0x9E3779B1u) >> (32 - TB);
         while (hk[sl] != tv[e]) sl = (sl + 1) & (TS - 1);
-        c1 = hi[sl] != i ? 1 : 0;
+        c1 |= (hi[sl] != i ? 1u : 0u) << e;
       }
-      col[i] = c1;
     }
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) col[i0 + uint32_t(e)] = uint8_t(c1 >> e & 1u);
     __syncthreads();
+    uint32_t done = c1;  // this thread's flags, also kept in registers
     for (;;) {  // D_i = C1_i or (J0 <= t_i < J0 + i and D_{t_i - J0}): monotone fixpoint
       uint32_t add = 0;  // read every flag, then write the new ones
 #pragma unroll
       for (int e = 0; e < EPT; ++e) {
         const uint32_t i = i0 + uint32_t(e);
-        if (i < m && !col[i] && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) add |= 1u << e;
+        if (!(done >> e & 1u) && i < m && tv[e] >= J0 && tv[e] - J0 < i && col[tv[e] - J0]) add |= 1u << e;
       }
       __syncthreads();
 #pragma unroll
       for (int e = 0; e < EPT; ++e)
         if (add >> e & 1u) col[i0 + uint32_t(e)] = 1;
+      done |= add;
       if (__syncthreads_or(add != 0) == 0) break;
     }
+    uint32_t kv[EPT];  // all gathers in flight before the stores
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const uint32_t i = i0 + uint32_t(e);
-      keys[i] = i < m ? order_key(__ldg(Vn + uint64_t(col[i] ? J0 + i : tv[e]) * Rp)) : 0xffffffffu;
+      kv[e] = i < m ? order_key(__ldg(Vn + uint64_t((done >> e & 1u) ? J0 + i : tv[e]) * Rp)) : 0xffffffffu;
     }
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) keys[i0 + uint32_t(e)] = kv[e];
   } else {
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
