@@ -89,29 +89,45 @@ __global__ void __launch_bounds__(256) k_pair_build(const uint32_t* __restrict__
   const int lane = threadIdx.x & 31;
   const uint32_t Rp = vpitch(R);
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  constexpr int C = 4;  // 32-tree chunks whose dependent load chains (inv -> pos_node -> node) overlap
   for (uint32_t s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < N; s += warps) {
     uint32_t cnt = 0;
-    for (uint32_t b0 = 0; b0 < B; b0 += 32) {
-      const uint32_t b = b0 + uint32_t(lane);
-      uint32_t node = ~0u, p = ~0u;
-      if (b < B) {
-        p = __ldcs(inv + uint64_t(s) * B + b);
-        if (p != ~0u) node = __ldg(pos_node + p);
+    for (uint32_t b00 = 0; b00 < B; b00 += 32 * C) {
+      uint32_t p[C], node[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t b = b00 + 32 * c + uint32_t(lane);
+        p[c] = b < B ? __ldcs(inv + uint64_t(s) * B + b) : ~0u;
       }
-      const bool act = node != ~0u;
-      const unsigned m = __ballot_sync(0xffffffffu, act);
-      if (act) {
-        const uint32_t j = p - __ldg(&nodes[node].begin);
-        const uint2 qv = __ldg(reinterpret_cast<const uint2*>(qsplit) + node);
-        uint4 rec;
-        rec.x = uint32_t((__ldg(vbase + node) + uint64_t(j) * Rp) >> 3);
-        rec.y = uint32_t(aug_off<E>(__ldg(&nodes[node].term_off), node, R));
-        rec.z = qv.x;
-        rec.w = qv.y;
-        const uint32_t idx = cnt + __popc(m & ((1u << lane) - 1u));
-        *reinterpret_cast<uint4*>(recs + uint64_t(s) * PB + idx) = rec;
+#pragma unroll
+      for (int c = 0; c < C; ++c) node[c] = p[c] != ~0u ? __ldg(pos_node + p[c]) : ~0u;
+      uint32_t beg[C], toff[C];
+      uint64_t vb[C];
+      uint2 qv[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (node[c] != ~0u) {
+          beg[c] = __ldg(&nodes[node[c]].begin);
+          toff[c] = __ldg(&nodes[node[c]].term_off);
+          vb[c] = __ldg(vbase + node[c]);
+          qv[c] = __ldg(reinterpret_cast<const uint2*>(qsplit) + node[c]);
+        }
       }
-      cnt += __popc(m);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const bool act = node[c] != ~0u;
+        const unsigned m = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          uint4 rec;
+          rec.x = uint32_t((vb[c] + uint64_t(p[c] - beg[c]) * Rp) >> 3);
+          rec.y = uint32_t(aug_off<E>(toff[c], node[c], R));
+          rec.z = qv[c].x;
+          rec.w = qv[c].y;
+          const uint32_t idx = cnt + __popc(m & ((1u << lane) - 1u));
+          *reinterpret_cast<uint4*>(recs + uint64_t(s) * PB + idx) = rec;
+        }
+        cnt += __popc(m);
+      }
     }
     if (lane == 0) pcnt[s] = cnt;
   }
