@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(128) k_sample_projection(
   if (nd.flags & kNodeGivenCsr) return;  // host supplied the matrix and pos_after
 
   const uint32_t z = nd.z;
+  int zp = 32;  // this node's sort width (the shared arrays are sized for the wave's largest z)
+  while (zp < int(z)) zp <<= 1;
   const uint64_t cells = uint64_t(R) * d;
   WarpStream s;
   s.init_seeded(blk, nd.seed, lane);
@@ -125,9 +127,9 @@ __global__ void __launch_bounds__(128) k_sample_projection(
     for (int i = int(z) + lane; i < zpad; i += 32) keys[i] = 0xffffffffu;
     __syncwarp();
   } else {
-    for (int i = lane; i < zpad; i += 32) keys[i] = i < int(z) ? draws[i] : 0xffffffffu;
+    for (int i = lane; i < zp; i += 32) keys[i] = i < int(z) ? draws[i] : 0xffffffffu;
     __syncwarp();
-    if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
+    if (gkeys) warp_bitonic_sort(keys, zp, lane); else warp_sort_via_regs(keys, zp, lane);
   }
   bool dup = false;
   for (int i = lane + 1; i < int(z); i += 32) dup |= keys[i] == keys[i - 1];
@@ -227,10 +229,10 @@ __global__ void __launch_bounds__(128) k_sample_projection(
       if (lane == 0) keys[i] = hit ? uint32_t(cells - z + i) : t;
       __syncwarp();
     }
-    for (int i = lane; i < zpad; i += 32)
+    for (int i = lane; i < zp; i += 32)
       if (i >= int(z)) keys[i] = 0xffffffffu;
     __syncwarp();
-    if (gkeys) warp_bitonic_sort(keys, zpad, lane); else warp_sort_via_regs(keys, zpad, lane);
+    if (gkeys) warp_bitonic_sort(keys, zp, lane); else warp_sort_via_regs(keys, zp, lane);
   }
 
   // Coins: cell i (ascending) gets the top bit of the next output (uniform_int<int>(0,1)).
