@@ -1,5 +1,7 @@
 // Device context and the per-wave launch sequence.
 #pragma once
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -38,8 +40,9 @@ struct DevBuf {
   }
   T* ensure(size_t n) {
     if (n <= cap && p) return p;
-    release();
-    size_t want = n < 64 ? 64 : n + n / 4;
+    if (p && std::getenv("SOFG_GROW_LOG")) std::fprintf(stderr, "[grow] device %zu -> %zu bytes\n", cap * sizeof(T), n * sizeof(T));
+    release();  // cudaFree synchronizes the device: grow rarely (x2 up to 256 MB, +1/8 above)
+    const size_t want = n < 64 ? 64 : (n * sizeof(T) <= (size_t(256) << 20) ? 2 * n : n + n / 8);
     alloc(want);
     return p;
   }
@@ -75,9 +78,10 @@ struct PinnedBuf {
   }
   T* ensure(size_t n) {
     if (n <= cap && p) return p;
+    if (p && std::getenv("SOFG_GROW_LOG")) std::fprintf(stderr, "[grow] pinned %zu -> %zu bytes\n", cap * sizeof(T), n * sizeof(T));
     if (p) cudaFreeHost(p);
     p = nullptr;
-    size_t want = n < 64 ? 64 : n + n / 4;
+    const size_t want = n < 64 ? 64 : 2 * n;  // pinning is slow (~ms per 10 MB): grow rarely
     cuda_check(cudaMallocHost(&p, want * sizeof(T)), "cudaMallocHost");
     cap = want;
     return p;
