@@ -22,6 +22,16 @@
 #ifndef SOFG_TEAM_MINB
 #define SOFG_TEAM_MINB 3
 #endif
+// rows in flight per warp of the register splitters for n <= 32 / 64 / 128 (variant builds)
+#ifndef SOFG_GR32
+#define SOFG_GR32 2  // measured: 8 -> 35.9, 4 -> 34.9, 2 -> 31.2, 1 -> 32.0 ms per step
+#endif
+#ifndef SOFG_GR64
+#define SOFG_GR64 4   // 2 -> 49.1, 4 -> 48.5, 8 -> 56.1
+#endif
+#ifndef SOFG_GR128
+#define SOFG_GR128 1  // 2 -> 18.8, 1 -> 17.3
+#endif
 
 namespace sofg {
 namespace dev {
@@ -1064,9 +1074,9 @@ cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* li
   switch (bucket - 2) {
     case -2: return launch_seg<8, KC>(nodes, list, n, R, k, row_ptr, lab, gbase, G, xl, res, st);
     case -1: return launch_seg<16, KC>(nodes, list, n, R, k, row_ptr, lab, gbase, G, xl, res, st);
-    case 0: return launch_bucket<1, 8, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
-    case 1: return launch_bucket<2, 4, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
-    case 2: return launch_bucket<4, 2, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 0: return launch_bucket<1, SOFG_GR32, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 1: return launch_bucket<2, SOFG_GR64, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
+    case 2: return launch_bucket<4, SOFG_GR128, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 3: return launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);  // (a register E = 16 sort measured slower)
     case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
