@@ -1,5 +1,9 @@
 #include "engine.hpp"
 
+#ifndef SOFG_PRUNE32_MAXB
+#define SOFG_PRUNE32_MAXB 4  // exact buckets pruned with 32 value buckets (4: n <= 128), 64 above
+#endif
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
@@ -501,7 +505,7 @@ void WaveRunner::submit(const WaveSpec& w) {
       d_xstar = xstar_.ensure(prune_n);
       // 32 value buckets per row for n <= 128 (bounds tight enough, half the cost), 64 above
       size_t n_small = 0;
-      for (int b = kPruneFrom; b <= 4; ++b) n_small += exact_b_count[size_t(b)];
+      for (int b = kPruneFrom; b <= SOFG_PRUNE32_MAXB; ++b) n_small += exact_b_count[size_t(b)];
       cuda_check(launch_exact_prune(d_nodes, d_exact + prune_off, int(n_small), R, d_rp, w.lab_in,
                                     d_gbase, d_G, D.xl.p, d_rowlb, d_xstar, 32, k, st_),
                  "exact_prune");

@@ -23,6 +23,10 @@
 #define SOFG_TEAM_MINB 3
 #endif
 // rows in flight per warp of the register splitters for n <= 32 / 64 / 128 (variant builds)
+#ifndef SOFG_TEAM512
+#define SOFG_TEAM512 2  // warps per node of the radix splitter for 257..512 samples (4: 56.6 vs 40.2 ms per step)
+#endif
+static_assert(32 * 8 * SOFG_TEAM512 >= 512, "a team holds 256 W positions: 257..512 samples need W >= 2");
 #ifndef SOFG_GR32
 #define SOFG_GR32 2  // measured: 8 -> 35.9, 4 -> 34.9, 2 -> 31.2, 1 -> 32.0 ms per step
 #endif
@@ -1078,7 +1082,7 @@ cudaError_t launch_bucket_kc(int bucket, const NodeIn* nodes, const uint32_t* li
     case 1: return launch_bucket<2, SOFG_GR64, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 2: return launch_bucket<4, SOFG_GR128, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 3: return launch_bucket<8, 1, 1, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
-    case 4: return launch_team<2, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);  // (a register E = 16 sort measured slower)
+    case 4: return launch_team<SOFG_TEAM512, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);  // (a register E = 16 sort measured slower)
     case 5: return launch_team<4, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     case 6: return launch_team<8, KC>(nodes, list, n, R, k, terms, row_ptr, lab, gbase, G, xl, xlf, res, rowlb, xstar, st);
     default: return cudaErrorInvalidValue;

@@ -14,6 +14,10 @@
 #include "common.hpp"
 #include "dev_util.cuh"
 #include "kernels.hpp"
+
+#ifndef SOFG_SAMPLE_WARPS
+#define SOFG_SAMPLE_WARPS 2  // warps (nodes) per CTA of k_sample_projection (8: 54.6, 4: 47.8, 2: 45.1 ms per step)
+#endif
 #include "mt64.cuh"
 
 namespace sofg {
@@ -23,7 +27,7 @@ namespace dev {
 // Projection sampler: one warp per node.
 // smem per warp: 624 u64 (two engine blocks) + 2 * zpad u32 (sorted set, draw order).
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_sample_projection(
+__global__ void __launch_bounds__(32 * SOFG_SAMPLE_WARPS) k_sample_projection(
     const NodeIn* __restrict__ nodes, int n_nodes, uint32_t d, uint32_t R, int zpad,
     uint32_t* __restrict__ terms, uint32_t* __restrict__ row_ptr, uint32_t* __restrict__ pos_after,
     uint32_t* __restrict__ gkeys, uint32_t* __restrict__ gaux) {
@@ -639,7 +643,7 @@ cudaError_t launch_sample_projection(const NodeIn* nodes, int n_nodes, uint32_t 
   const int zpad = next_pow2(int(zmax));
   const bool global_sets = size_t(2 * dev::kMtN) * 8 + size_t(2 * zpad) * 4 > 96 * 1024;
   const size_t per_warp = size_t(2 * dev::kMtN) * 8 + (global_sets ? 0 : size_t(2 * zpad) * 4);
-  int warps = 4;
+  int warps = SOFG_SAMPLE_WARPS;
   while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
   const size_t smem = per_warp * warps;
   if (smem > 48 * 1024)
