@@ -13,6 +13,10 @@
 #include "dev_util.cuh"
 #include "kernels.hpp"
 
+#ifndef SOFG_PART_TPC
+#define SOFG_PART_TPC 8  // partition tiles (warps) per CTA
+#endif
+
 namespace sofg {
 namespace dev {
 
@@ -54,13 +58,13 @@ __global__ void k_part_scan(const NodeIn* __restrict__ nodes, int n_nodes, uint3
 // Flags and scatter, one warp per partition tile (flag word l / 32 of the tile's 32 words covers
 // elements [32 word, 32 word + 32)). A CTA takes 8 tiles, so the many small nodes of deep levels
 // do not each occupy a 256-thread CTA for a few dozen elements.
-__global__ void __launch_bounds__(256) k_part_flags_w(
+__global__ void __launch_bounds__(32 * SOFG_PART_TPC) k_part_flags_w(
     const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, int n_tiles, uint32_t R, int k,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase, const float* __restrict__ G,
     NodeRes* __restrict__ res, uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_left,
     uint32_t* __restrict__ class_left) {
   const int lane = threadIdx.x & 31;
-  const int ti = int(blockIdx.x) * 8 + int(threadIdx.x >> 5);
+  const int ti = int(blockIdx.x) * int(blockDim.x >> 5) + int(threadIdx.x >> 5);
   if (ti >= n_tiles) return;
   const Tile tl = tiles[ti];
   const int row = res[tl.node].row;
@@ -109,14 +113,14 @@ __global__ void __launch_bounds__(256) k_part_flags_w(
   }
 }
 
-__global__ void __launch_bounds__(256) k_part_scatter_w(
+__global__ void __launch_bounds__(32 * SOFG_PART_TPC) k_part_scatter_w(
     const NodeIn* __restrict__ nodes, const Tile* __restrict__ tiles, int n_tiles,
     const NodeRes* __restrict__ res, const uint32_t* __restrict__ flags,
     const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ idx_in,
     const uint8_t* __restrict__ lab_in, uint32_t* __restrict__ idx_out,
     uint8_t* __restrict__ lab_out, uint32_t* __restrict__ inv, uint32_t B) {
   const int lane = threadIdx.x & 31;
-  const int ti = int(blockIdx.x) * 8 + int(threadIdx.x >> 5);
+  const int ti = int(blockIdx.x) * int(blockDim.x >> 5) + int(threadIdx.x >> 5);
   if (ti >= n_tiles) return;
   const Tile tl = tiles[ti];
   if (res[tl.node].row < 0) return;
@@ -212,12 +216,12 @@ cudaError_t launch_partition(const NodeIn* nodes, int n_nodes, const Tile* tiles
                              cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
   if (n_tiles > 0)
-    dev::k_part_flags_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, R, k, lab_in, gbase, G, res,
+    dev::k_part_flags_w<<<(n_tiles + SOFG_PART_TPC - 1) / SOFG_PART_TPC, 32 * SOFG_PART_TPC, 0, st>>>(nodes, tiles, n_tiles, R, k, lab_in, gbase, G, res,
                                                            flags, tile_left, class_left);
   dev::k_part_scan<<<(n_nodes + 3) / 4, 128, 0, st>>>(nodes, n_nodes, R, tile_first, terms,
                                                       row_ptr, pos_proj, pos_split, tile_left, res);
   if (n_tiles > 0)
-    dev::k_part_scatter_w<<<(n_tiles + 7) / 8, 256, 0, st>>>(nodes, tiles, n_tiles, res, flags, tile_left, idx_in,
+    dev::k_part_scatter_w<<<(n_tiles + SOFG_PART_TPC - 1) / SOFG_PART_TPC, 32 * SOFG_PART_TPC, 0, st>>>(nodes, tiles, n_tiles, res, flags, tile_left, idx_in,
                                                              lab_in, idx_out, lab_out, inv, B);
   return cudaGetLastError();
 }

@@ -15,6 +15,12 @@
 #include "dev_util.cuh"
 #include "kernels.hpp"
 
+#ifndef SOFG_DRAW_THREADS
+#define SOFG_DRAW_THREADS 128  // threads per histogram node of k_hist_draws (64: 32.7, 128: 32.9, 256: 38.7, 512: 49.6 ms per step)
+#endif
+#ifndef SOFG_BND_WARPS
+#define SOFG_BND_WARPS 4  // (node, row) warps per CTA of k_hist_boundaries
+#endif
 #ifndef SOFG_SAMPLE_WARPS
 #define SOFG_SAMPLE_WARPS 2  // warps (nodes) per CTA of k_sample_projection (8: 54.6, 4: 47.8, 2: 45.1 ms per step)
 #endif
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(32 * SOFG_SAMPLE_WARPS) k_sample_projection(
 // draws of the R consecutive sample_boundaries calls. Output: draws[slot][R*m] (u32),
 // pos_split[node] = stream position after the picks.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_hist_draws(
+__global__ void __launch_bounds__(SOFG_DRAW_THREADS) k_hist_draws(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist,
     uint32_t R, uint32_t bins, const uint32_t* __restrict__ pos_after_proj,
     uint32_t* __restrict__ draws, uint32_t* __restrict__ pos_split) {
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(256) k_hist_draws(
 //      midpoints of consecutive distinct values, compacted in order.
 // ------------------------------------------------------------------------------------------
 template <int EPL>
-__global__ void __launch_bounds__(128) k_hist_boundaries(
+__global__ void __launch_bounds__(32 * SOFG_BND_WARPS) k_hist_boundaries(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist,
     uint32_t R, uint32_t bins, const uint32_t* __restrict__ draws,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
@@ -671,7 +677,7 @@ cudaError_t launch_hist_draws(const NodeIn* nodes, const uint32_t* hist_nodes, i
                               uint32_t R, uint32_t bins, const uint32_t* pos_after_proj,
                               uint32_t* draws, uint32_t* pos_split, cudaStream_t st) {
   if (n_hist == 0) return cudaSuccess;
-  dev::k_hist_draws<<<n_hist, 256, 0, st>>>(nodes, hist_nodes, n_hist, R, bins, pos_after_proj,
+  dev::k_hist_draws<<<n_hist, SOFG_DRAW_THREADS, 0, st>>>(nodes, hist_nodes, n_hist, R, bins, pos_after_proj,
                                             draws, pos_split);
   return cudaGetLastError();
 }
@@ -685,13 +691,13 @@ cudaError_t launch_hist_boundaries(const NodeIn* nodes, const uint32_t* hist_nod
   (void)row_ptr;
   if (n_hist == 0) return cudaSuccess;
   const int mpad = next_pow2(int(bins));
-  const size_t smem = size_t(mpad) * 17 * 4;  // 4 warps
+  const size_t smem = size_t(mpad) * 17 * SOFG_BND_WARPS;  // per warp: hash table + flags
   const uint64_t items = uint64_t(n_hist) * R;
-  const unsigned grid = unsigned((items + 3) / 4);
+  const unsigned grid = unsigned((items + SOFG_BND_WARPS - 1) / SOFG_BND_WARPS);
   auto go = [&](auto kern) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
-    kern<<<grid, 128, smem, st>>>(nodes, hist_nodes, n_hist, R, bins, draws, gbase, G, bnd, nb);
+    kern<<<grid, 32 * SOFG_BND_WARPS, smem, st>>>(nodes, hist_nodes, n_hist, R, bins, draws, gbase, G, bnd, nb);
     return cudaGetLastError();
   };
   switch (mpad) {
