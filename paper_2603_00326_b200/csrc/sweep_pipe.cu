@@ -38,7 +38,10 @@ struct PairRec {
 };
 static_assert(sizeof(PairRec) == 16, "PairRec layout");
 
-constexpr int kPipeConsumers = 16;                  // consumer warps per CTA
+#ifndef SOFG_PIPE_CONSUMERS
+#define SOFG_PIPE_CONSUMERS 16
+#endif
+constexpr int kPipeConsumers = SOFG_PIPE_CONSUMERS;  // consumer warps per CTA
 constexpr uint32_t kChunkPairs = 32u / kQ;          // pairs per consumer-warp ticket
 constexpr uint32_t kEndStage = 0xffffffffu;
 
