@@ -204,8 +204,11 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
       try {
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
         cudaEvent_t ev;
-        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-        const uint64_t cols = std::max<uint64_t>(1, (uint64_t(32) << 20) / (4 * n));  // ~32 MB slices
+        // blocking-sync event: the thread sleeps between slices instead of spinning on a core the
+        // trainers' host pools use
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+        static const uint64_t slice_mb = std::getenv("SOFG_UPLOAD_SLICE_MB") ? std::strtoull(std::getenv("SOFG_UPLOAD_SLICE_MB"), nullptr, 10) : 32;
+        const uint64_t cols = std::max<uint64_t>(1, (slice_mb << 20) / (4 * n));
         for (uint64_t f0 = 0; f0 < d; f0 += cols) {
           const uint64_t w = std::min(cols, d - f0);
           cuda_check(cudaMemcpy2DAsync(Dp->X.p + f0 * Dp->ld, Dp->ld * 4, src + f0 * n, n * 4, n * 4, w,
