@@ -23,6 +23,11 @@
 #define SOFG_TEAM_MINB 3
 #endif
 // rows in flight per warp of the register splitters for n <= 32 / 64 / 128 (variant builds)
+#ifndef SOFG_REG_MINB
+// min CTAs per SM of the register splitters, i.e. their register cap (ptxas' own choice at E = 1, 2,
+// 4, 8 -> 34.4 / 54.4 / 20.1 / 43.0 ms per step; 6 CTAs: 31.2 / 47.1 / 10.6 / 31.4; 8: 28.6 / 46.3 / 12.3 / 32.9)
+#define SOFG_REG_MINB(E) ((E) <= 2 ? 8 : 6)
+#endif
 #ifndef SOFG_TEAM512
 #define SOFG_TEAM512 2  // warps per node of the radix splitter for 257..512 samples (4: 56.6 vs 40.2 ms per step)
 #endif
@@ -436,7 +441,7 @@ __global__ void __launch_bounds__(128) k_exact_prune(
 
 // E keys per lane, G rows in flight per warp, WPN warps per node, KC class-count registers.
 template <int E, int GR, int WPN, int KC>
-__global__ void __launch_bounds__(128) k_exact_reg(
+__global__ void __launch_bounds__(128, SOFG_REG_MINB(E)) k_exact_reg(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     int k, const uint32_t* __restrict__ terms, const uint32_t* __restrict__ row_ptr,
     const uint8_t* __restrict__ lab, const uint64_t* __restrict__ gbase,
