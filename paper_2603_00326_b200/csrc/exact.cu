@@ -20,14 +20,14 @@
 #include "kernels.hpp"
 
 #ifndef SOFG_TEAM_MINB
-#define SOFG_TEAM_MINB 3
+#define SOFG_TEAM_MINB 4  // min CTAs per SM of the team splitters (3: 40.2, 4: 37.1 ms per step at <= 512 samples)
 #endif
-// rows in flight per warp of the register splitters for n <= 32 / 64 / 128 (variant builds)
 #ifndef SOFG_REG_MINB
 // min CTAs per SM of the register splitters, i.e. their register cap (ptxas' own choice at E = 1, 2,
 // 4, 8 -> 34.4 / 54.4 / 20.1 / 43.0 ms per step; 6 CTAs: 31.2 / 47.1 / 10.6 / 31.4; 8: 28.6 / 46.3 / 12.3 / 32.9)
 #define SOFG_REG_MINB(E) ((E) <= 2 ? 8 : 6)
 #endif
+// rows in flight per warp of the register splitters for n <= 32 / 64 / 128 (variant builds)
 #ifndef SOFG_TEAM512
 #define SOFG_TEAM512 2  // warps per node of the radix splitter for 257..512 samples (4: 56.6 vs 40.2 ms per step)
 #endif

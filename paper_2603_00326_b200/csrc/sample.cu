@@ -18,6 +18,10 @@
 #ifndef SOFG_DRAW_THREADS
 #define SOFG_DRAW_THREADS 128  // threads per histogram node of k_hist_draws (64: 32.7, 128: 32.9, 256: 38.7, 512: 49.6 ms per step)
 #endif
+#ifndef SOFG_BND_MINB_SMALL
+#define SOFG_BND_MINB_SMALL 10  // min CTAs per SM (register cap) of k_hist_boundaries for <= 256 picks (none: 86.2, 10: 82.5, 12: 123 ms per step)
+#endif
+#define SOFG_BND_MINB(EPL) ((EPL) <= 8 ? SOFG_BND_MINB_SMALL : 0)
 #ifndef SOFG_BND_WARPS
 #define SOFG_BND_WARPS 4  // (node, row) warps per CTA of k_hist_boundaries
 #endif
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(SOFG_DRAW_THREADS) k_hist_draws(
 //      midpoints of consecutive distinct values, compacted in order.
 // ------------------------------------------------------------------------------------------
 template <int EPL>
-__global__ void __launch_bounds__(32 * SOFG_BND_WARPS) k_hist_boundaries(
+__global__ void __launch_bounds__(32 * SOFG_BND_WARPS, SOFG_BND_MINB(EPL)) k_hist_boundaries(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ hist_nodes, int n_hist,
     uint32_t R, uint32_t bins, const uint32_t* __restrict__ draws,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
