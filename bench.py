@@ -397,7 +397,9 @@ def main():
     if not args.no_profile:
         ctx.set_stats(2)
         ctx.reset_stats()
-        ctx.train_forest(cfg_for(args.warmup + args.steps + args.e2e_steps))
+        # the last timed step's range again: context 0's next call (the first e2e step) then continues
+        # its range and finds its bootstrap samples drawn ahead, like every timed step
+        ctx.train_forest(cfg_for(args.warmup + args.steps - 1))
         st = ctx.stats()
         ctx.set_stats(0)
         roofline = roofline_block(st, args)
@@ -423,7 +425,8 @@ def main():
             try:
                 c2 = sofg.Context(local)
                 c2.upload_ptr(hptr, yh, args.n, args.d, args.classes)
-                c2.train_forest(cfg_for(args.warmup + args.steps + args.e2e_steps + 1))  # buffers (untimed)
+                # buffers (untimed); the range before context 1's first e2e range (see below)
+                c2.train_forest(cfg_for(args.warmup + args.steps + (args.e2e_steps + 1) // 2 - 1))
                 ctxs.append(c2)
             except Exception as exc:  # noqa: BLE001 - any allocation failure: serial pipeline
                 print(f"e2e: second context unavailable ({exc}); serial upload + train", file=sys.stderr)
@@ -432,12 +435,20 @@ def main():
         first = args.warmup + args.steps
         torch.cuda.synchronize()
         ts = time.perf_counter()
+        step_wall = [ts]
         ctxs[0].upload_ptr(hptr, yh, args.n, args.d, args.classes)
+        # With two contexts, each trains a contiguous half of the e2e tree ranges (context 0 the first
+        # half, context 1 the second, alternating steps), so a context's next call continues its
+        # previous range and finds that range's bootstrap samples already drawn in the idle time
+        # of its last call (api.cpp BootAhead). Same trees as ranges first .. first + steps - 1.
+        half = (args.e2e_steps + len(ctxs) - 1) // len(ctxs)
         for j in range(args.e2e_steps):
             cur = ctxs[j % len(ctxs)]
             if len(ctxs) > 1 and j + 1 < args.e2e_steps:  # next step's table, in flight during this step
                 ctxs[(j + 1) % len(ctxs)].upload_ptr(hptr, yh, args.n, args.d, args.classes)
-            f = cur.train_forest(cfg_for(first + j))
+            rng = first + (j % len(ctxs)) * half + j // len(ctxs)
+            f = cur.train_forest(cfg_for(rng))
+            step_wall.append(time.perf_counter())
             d2h = sum(a.nbytes for a in (f.tree_off, f.left, f.right, f.pred, f.thr, f.term_off, f.feat, f.weight))
             if len(ctxs) == 1 and j + 1 < args.e2e_steps:
                 cur.upload_ptr(hptr, yh, args.n, args.d, args.classes)
@@ -445,6 +456,7 @@ def main():
         e_s = max_over_ranks(time.perf_counter() - ts)
         e2e = {"value": world * T * args.e2e_steps / e_s, "unit": "trees/s", "h2d_bytes_per_step": nbytes + 4 * args.n,
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "step_ms": [round(1e3 * (b - a), 1) for a, b in zip(step_wall, step_wall[1:])],
                "timing": "host wall clock, cuda-synchronized, max over ranks",
                "pipeline": ("two contexts: step s+1's table upload overlaps step s's training"
                             if len(ctxs) > 1 else "serial: upload, then train")}

@@ -1,4 +1,5 @@
 // C ABI (include/sofg.h) and C++ API (include/sofg/soforest_gpu.hpp) over the level-wise trainer.
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -41,6 +42,15 @@ struct BootAhead {
     out.swap(r);
     return true;
   }
+};
+
+// Trainings in progress per device (all contexts of the process). A table upload keeps two
+// slices in flight while none is running and one otherwise (see upload).
+std::atomic<int> g_training[64];
+struct TrainingMark {
+  int dev;
+  explicit TrainingMark(int d) : dev(d & 63) { g_training[dev].fetch_add(1); }
+  ~TrainingMark() { g_training[dev].fetch_sub(1); }
 };
 
 struct sofg_ctx {
@@ -203,21 +213,31 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
     c->feeder = std::thread([c, Dp, src, n, d, st, dev, row_table] {
       try {
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
-        cudaEvent_t ev;
-        // blocking-sync event: the thread sleeps between slices instead of spinning on a core the
-        // trainers' host pools use
-        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+        // Slices in flight: two while no context of the process trains on this GPU, so the copy
+        // engine always has the next slice queued (one in flight leaves it idle while this thread
+        // wakes up: 16 GB in ~480 ms instead of ~300 at 32 MB slices); one while another context
+        // trains, whose per-wave copies otherwise starve behind the queued slices (measured:
+        // +300 ms per concurrent 100-tree step). Blocking-sync events: the thread sleeps between
+        // slices instead of spinning on a core the trainers' host pools use.
+        cudaEvent_t ev[2];
+        for (cudaEvent_t& e : ev)
+          cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync), "event");
         static const uint64_t slice_mb = std::getenv("SOFG_UPLOAD_SLICE_MB") ? std::strtoull(std::getenv("SOFG_UPLOAD_SLICE_MB"), nullptr, 10) : 32;
         const uint64_t cols = std::max<uint64_t>(1, (slice_mb << 20) / (4 * n));
-        for (uint64_t f0 = 0; f0 < d; f0 += cols) {
+        uint64_t i = 0;
+        for (uint64_t f0 = 0; f0 < d; f0 += cols, ++i) {
           const uint64_t w = std::min(cols, d - f0);
           cuda_check(cudaMemcpy2DAsync(Dp->X.p + f0 * Dp->ld, Dp->ld * 4, src + f0 * n, n * 4, n * 4, w,
                                        cudaMemcpyHostToDevice, st),
                      "H2D table slice");
-          cuda_check(cudaEventRecord(ev, st), "event");
-          cuda_check(cudaEventSynchronize(ev), "slice sync");
+          cuda_check(cudaEventRecord(ev[i & 1], st), "event");
+          if (g_training[dev & 63].load() > 0)
+            cuda_check(cudaEventSynchronize(ev[i & 1]), "slice sync");  // this slice: one in flight
+          else if (i > 0)
+            cuda_check(cudaEventSynchronize(ev[(i - 1) & 1]), "slice sync");
         }
-        cudaEventDestroy(ev);
+        if (i > 0) cuda_check(cudaEventSynchronize(ev[(i - 1) & 1]), "slice sync");
+        for (cudaEvent_t& e : ev) cudaEventDestroy(e);
         if (row_table)
           cuda_check(sofg::launch_transpose_rows(Dp->X.p, Dp->ld, n, d, Dp->XR.p, Dp->ldr, st), "transpose_rows");
       } catch (...) {
@@ -454,6 +474,7 @@ int sofg_download_dataset(sofg_ctx* c, float* X, int32_t* y) {
 int sofg_train_forest(sofg_ctx* c, const sofg_train_config* cfg, sofg_forest** out) {
   return guard([&] {
     require_data(c);
+    const TrainingMark busy(c->eng->device());
     const sofg::DeviceData& D = c->eng->data();
     validate_cfg(cfg, D);
     sofg::TrainParams P = params_for(cfg, D, true);
