@@ -44,9 +44,10 @@ struct BootAhead {
   }
 };
 
-// Trainings in progress per device (all contexts of the process). A table upload keeps two
-// slices in flight while none is running and one otherwise (see upload).
+// Per device, over all contexts of the process: trainings in progress, and table uploads some
+// call is waiting for (see upload: how many slices a feeder keeps in flight).
 std::atomic<int> g_training[64];
+std::atomic<int> g_waited[64];
 struct TrainingMark {
   int dev;
   explicit TrainingMark(int d) : dev(d & 63) { g_training[dev].fetch_add(1); }
@@ -65,8 +66,16 @@ struct sofg_ctx {
   // every later call on the context joins it first (its device work is stream-ordered after it).
   std::thread feeder;
   std::exception_ptr feeder_error;
+  std::atomic<bool> feeder_waited{false};  // a call of this context is waiting for the feeder
+  int feeder_dev = 0;
   void join_feeder() {
-    if (feeder.joinable()) feeder.join();
+    if (feeder.joinable()) {
+      feeder_waited = true;
+      g_waited[feeder_dev & 63].fetch_add(1);
+      feeder.join();
+      g_waited[feeder_dev & 63].fetch_sub(1);
+      feeder_waited = false;
+    }
     if (feeder_error) {
       std::exception_ptr e = feeder_error;
       feeder_error = nullptr;
@@ -210,28 +219,34 @@ void upload(sofg_ctx* c, uint64_t n, uint64_t d, const int32_t* labels, int32_t 
     sofg::DeviceData* Dp = &D;
     const float* src = pending_src;
     const int dev = c->eng->device();
+    c->feeder_dev = dev;
     c->feeder = std::thread([c, Dp, src, n, d, st, dev, row_table] {
       try {
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
-        // Slices in flight: two while no context of the process trains on this GPU, so the copy
-        // engine always has the next slice queued (one in flight leaves it idle while this thread
-        // wakes up: 16 GB in ~480 ms instead of ~300 at 32 MB slices); one while another context
-        // trains, whose per-wave copies otherwise starve behind the queued slices (measured:
-        // +300 ms per concurrent 100-tree step). Blocking-sync events: the thread sleeps between
-        // slices instead of spinning on a core the trainers' host pools use.
+        // Slices in flight: two when a call of this context waits for the table, or when nothing
+        // else uses the GPU, so the copy engine always has the next slice queued (one in flight
+        // leaves it idle while this thread wakes up: 16 GB in ~480 ms instead of ~300 at 32 MB
+        // slices); one while another context trains, whose per-wave copies otherwise starve
+        // behind the queued slices (measured: +300 ms per concurrent 100-tree step); none while
+        // another context's call waits for its own table (both would take twice as long).
+        // Blocking-sync events: the thread sleeps between slices instead of spinning on a core
+        // the trainers' host pools use.
         cudaEvent_t ev[2];
         for (cudaEvent_t& e : ev)
           cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync), "event");
         static const uint64_t slice_mb = std::getenv("SOFG_UPLOAD_SLICE_MB") ? std::strtoull(std::getenv("SOFG_UPLOAD_SLICE_MB"), nullptr, 10) : 32;
         const uint64_t cols = std::max<uint64_t>(1, (slice_mb << 20) / (4 * n));
         uint64_t i = 0;
+        const int dv = dev & 63;
         for (uint64_t f0 = 0; f0 < d; f0 += cols, ++i) {
+          while (!c->feeder_waited.load() && g_waited[dv].load() > 0)  // another table is awaited
+            std::this_thread::sleep_for(std::chrono::microseconds(100));
           const uint64_t w = std::min(cols, d - f0);
           cuda_check(cudaMemcpy2DAsync(Dp->X.p + f0 * Dp->ld, Dp->ld * 4, src + f0 * n, n * 4, n * 4, w,
                                        cudaMemcpyHostToDevice, st),
                      "H2D table slice");
           cuda_check(cudaEventRecord(ev[i & 1], st), "event");
-          if (g_training[dev & 63].load() > 0)
+          if (!c->feeder_waited.load() && g_training[dv].load() > 0)
             cuda_check(cudaEventSynchronize(ev[i & 1]), "slice sync");  // this slice: one in flight
           else if (i > 0)
             cuda_check(cudaEventSynchronize(ev[(i - 1) & 1]), "slice sync");
