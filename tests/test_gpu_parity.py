@@ -358,6 +358,43 @@ def test_pinned_upload_in_flight(gpu_ctx, oracle):
         L.sofg_host_free(ptr)
 
 
+def test_two_contexts_pipelined_pinned_uploads(gpu_ctx, oracle):
+    """The bench's end-to-end pipeline on small tables: two contexts on one GPU, each table
+    uploaded from its own page-locked buffer in several 32 MB slices while the other context
+    trains (one slice in flight), or while the other's call waits for its own table (paused), or
+    with nothing else running (two in flight); every training must see its own table."""
+    import ctypes as C
+
+    import paper_2603_00326_b200 as sofg
+
+    base, y = oracle.generate_trunk(100_000, 256, 23)  # 102 MB: four slices
+    d, n = base.shape
+    L = gpu_ctx.L
+    ptrs = [L.sofg_host_alloc(n * d * 4) for _ in range(2)]
+    assert all(ptrs)
+    other = sofg.Context(0)
+    try:
+        H = [np.ctypeslib.as_array((C.c_float * (n * d)).from_address(p)).reshape(d, n) for p in ptrs]
+        ctxs = [gpu_ctx, other]
+        tables = [base, -base, np.round(base * 2) / 2, base * np.float32(3.0)]
+        H[0][...] = tables[0]
+        H[1][...] = tables[1]
+        ctxs[0].upload_ptr(ptrs[0], y, n, d, 2)
+        ctxs[1].upload_ptr(ptrs[1], y, n, d, 2)  # both in flight; context 0's call waits first
+        for j, data in enumerate(tables):
+            cur = ctxs[j % 2]
+            gc, oc = _cfg(n_trees=2, mode="dynamic", breakeven=400, seed=41 + j)
+            f = cur.train_forest(gc)  # joins this context's upload
+            if j + 2 < len(tables):  # the buffer this step read, refilled for the step after next
+                H[j % 2][...] = tables[j + 2]
+                cur.upload_ptr(ptrs[j % 2], y, n, d, 2)  # in flight while the other context trains
+            assert _forest_equal(f, oracle.train_forest(np.ascontiguousarray(data, np.float32), y, 2, oc)) == [], j
+    finally:
+        other.close()
+        for p in ptrs:
+            L.sofg_host_free(p)
+
+
 def test_dense_projection_collision_resolution(gpu_ctx, oracle):
     """Matrices with thousands of cells (z ~ 10K of 49K cells): Floyd collisions are the rule, and
     are resolved by the parallel fixpoint (smallest index per sorted value, then the J0 + j chain)."""
