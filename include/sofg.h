@@ -103,8 +103,10 @@ int sofg_destroy(sofg_ctx* ctx);
  * labels: int32 in [0, class_count). Validates like the reference constructor; class_count <= 64
  * (more than 8 classes run the wide-class splitters, wide.cu; the reference has no bound).
  * X page-locked (e.g. from sofg_host_alloc): returns at once; a context thread feeds the copy to
- * the GPU in ~32 MB slices (one in flight, so other contexts' copies on the same GPU are not queued
- * behind it) and the next call on this context waits for it; keep X unchanged until the next
+ * the GPU in ~32 MB slices (two in flight when a call waits for it or the GPU is otherwise idle;
+ * one while another context of the process trains on the same GPU, so that context's copies are
+ * not queued behind it; paused while another context's call waits for its own table) and the next
+ * call on this context waits for it; keep X unchanged until the next
  * training / download call on this context returns. Pageable X: the copy has landed when this
  * returns. */
 int sofg_upload_dataset(sofg_ctx* ctx, const float* X, uint64_t n_samples, uint64_t n_features,
