@@ -36,7 +36,7 @@ static_assert(32 * 8 * SOFG_TEAM512 >= 512, "a team holds 256 W positions: 257..
 #define SOFG_GR32 2  // measured: 8 -> 35.9, 4 -> 34.9, 2 -> 31.2, 1 -> 32.0 ms per step
 #endif
 #ifndef SOFG_GR64
-#define SOFG_GR64 4   // 2 -> 49.1, 4 -> 48.5, 8 -> 56.1
+#define SOFG_GR64 2   // 2 -> 49.1, 4 -> 48.5, 8 -> 56.1; under the 8-CTA register cap: 2 -> 44.7, 4 -> 46.4, 8 -> 47.5
 #endif
 #ifndef SOFG_GR128
 #define SOFG_GR128 1  // 2 -> 18.8, 1 -> 17.3
