@@ -1,6 +1,7 @@
 #include "trainer.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -137,6 +138,8 @@ struct BNode {
 
 // Class counts carried inline in Open (more classes: per-tree side arrays, see grow_trees).
 constexpr int kOpenClasses = 4;
+
+constexpr uint32_t kNoSpec = 0xffffffffu;  // spec_pos of a child whose binomial was not drawn ahead
 
 struct Open {  // 64 bytes: the per-level frontier is rewritten twice per node (post, prep)
   uint64_t seed;
@@ -446,9 +449,33 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
       // binomial draws not done speculatively (roots, retries), parent entropies, node records
       const auto tb = Clock::now();
       pool.parallel_for(NP, [&](size_t p) {
+        {  // fresh engines (roots, children not drawn ahead): batched, their seedings primed together
+          constexpr size_t kB = 256;
+          uint64_t seeds[kB];
+          uint32_t zs[kB], us[kB];
+          size_t at[kB], c = 0;
+          auto flush = [&]() {
+            binom.batch(seeds, c, zs, us);
+            for (size_t q = 0; q < c; ++q) {
+              Open& o = sp[p][at[q]];
+              o.z = zs[q];
+              o.zpos = us[q];
+              o.has_z = 1;
+            }
+            c = 0;
+          };
+          for (size_t j = 0; j < sp[p].size(); ++j) {
+            const Open& o = sp[p][j];
+            if (o.has_z || o.pos != 0) continue;
+            seeds[c] = o.seed;
+            at[c++] = j;
+            if (c == kB) flush();
+          }
+          if (c) flush();
+        }
         for (size_t j = 0; j < sp[p].size(); ++j) {
           Open& o = sp[p][j];
-          if (!o.has_z) {
+          if (!o.has_z) {  // retries: the stream continues after the previous attempt
             uint64_t used;
             o.z = uint32_t(binom(o.seed, o.pos, &used));
             o.zpos = uint32_t(used);
@@ -500,20 +527,45 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
       times.ms_book += ms_since(t0);
 
       // While the GPU searches this wave: draw the children's attempt-0 binomials. They depend
-      // only on the child seeds derive_seed(seed, 1|2) (forest.hpp:226-228), known already.
+      // only on the child seeds derive_seed(seed, 1|2) (forest.hpp:226-228), known already. Drawn
+      // in chunks until the wave is done: a child whose draw was not reached by then gets it in
+      // the next prep, and only if it is split at all (about half of all children are leaves).
+      // With few host threads per GPU the draws outlast the waves of the widest levels.
       t0 = Clock::now();
       spec_z.resize(2 * N);
       spec_pos.resize(2 * N);
-      pool.parallel_for(NP, [&](size_t p) {
-        const size_t m = sp[p].size();
-        std::vector<uint64_t> seeds(2 * m);
-        for (size_t j = 0; j < m; ++j) {
-          const uint64_t seed = sp[p][j].seed;
-          seeds[2 * j] = host::derive_seed(seed, 1);
-          seeds[2 * j + 1] = host::derive_seed(seed, 2);
-        }
-        binom.batch(seeds.data(), 2 * m, spec_z.data() + 2 * poff[p], spec_pos.data() + 2 * poff[p]);
-      });
+      {
+        std::atomic<bool> stop{false};
+        std::atomic<int64_t> next_poll{0};
+        auto wave_over = [&]() {  // one thread queries the wave's event at a time, every >= 50 us
+          if (stop.load(std::memory_order_relaxed)) return true;
+          const int64_t now = std::chrono::duration_cast<std::chrono::microseconds>(
+                                  Clock::now().time_since_epoch()).count();
+          int64_t due = next_poll.load(std::memory_order_relaxed);
+          if (now < due || !next_poll.compare_exchange_strong(due, now + 50)) return false;
+          if (eng.wave_done()) stop.store(true, std::memory_order_relaxed);
+          return stop.load(std::memory_order_relaxed);
+        };
+        pool.parallel_for(NP, [&](size_t p) {
+          constexpr size_t kChunk = 128;  // parents per chunk
+          const size_t m = sp[p].size();
+          uint64_t seeds[2 * kChunk];
+          for (size_t j0 = 0; j0 < m; j0 += kChunk) {
+            if (wave_over()) {
+              std::fill(spec_pos.begin() + std::ptrdiff_t(2 * (poff[p] + j0)),
+                        spec_pos.begin() + std::ptrdiff_t(2 * (poff[p] + m)), kNoSpec);
+              return;
+            }
+            const size_t c = std::min(kChunk, m - j0);
+            for (size_t j = 0; j < c; ++j) {
+              const uint64_t seed = sp[p][j0 + j].seed;
+              seeds[2 * j] = host::derive_seed(seed, 1);
+              seeds[2 * j + 1] = host::derive_seed(seed, 2);
+            }
+            binom.batch(seeds, 2 * c, spec_z.data() + 2 * (poff[p] + j0), spec_pos.data() + 2 * (poff[p] + j0));
+          }
+        });
+      }
       const double lv_spec = ms_since(t0);
       times.ms_spec += lv_spec;
       t0 = Clock::now();
@@ -608,7 +660,8 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
             l.zpos = spec_pos[2 * i];
             rr.z = spec_z[2 * i + 1];
             rr.zpos = spec_pos[2 * i + 1];
-            l.has_z = rr.has_z = 1;
+            l.has_z = l.zpos != kNoSpec;  // else drawn in the next prep (if the child is split)
+            rr.has_z = rr.zpos != kNoSpec;
             if (wide) {  // children's counts at node ids L, L + 1 of the tree's side array
               std::vector<uint32_t>& v = wc[o.tree];
               if (v.size() < size_t(L + 2) * size_t(k)) v.resize(std::max(v.size() * 2, size_t(L + 2) * size_t(k)));

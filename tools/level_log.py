@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd())
 import paper_2603_00326_b200 as sofg
 with sofg.Context(0) as ctx:
     ctx.generate_trunk(1_000_000, 4096, 2, seed=1)
-    cfg = sofg.TrainConfig(n_trees=100, mode="dynamic", breakeven=512, seed=7, n_workers=0)
+    cfg = sofg.TrainConfig(n_trees=100, mode="dynamic", breakeven=512, seed=7, n_workers=int(os.environ.get("WORKERS", "0")))
     for i in range(3):
         t = time.perf_counter(); f = ctx.train_forest(cfg); print("STEP", i, (time.perf_counter()-t)*1e3, file=sys.stderr, flush=True)
     st = ctx.stats()
