@@ -210,14 +210,24 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
   d_off.ensure(B + 1);
   std::vector<uint32_t> root_counts(B * size_t(k));
   std::vector<unsigned char> increasing(B, 1);
-  pool.parallel_for(B, [&](size_t b) {
-    const std::vector<uint32_t>& r = roots[b];
-    for (size_t j = 1; j < r.size(); ++j)
-      if (!(r[j - 1] < r[j])) {
-        increasing[b] = 0;
-        break;
+  {
+    const uint64_t W = (D.n + 31) / 32;  // bitmap words per tree
+    const size_t tail = 8 * (B + 1) + 4 * size_t(k) * B;
+    // one pass per tree: its bitmap, and whether its list is strictly increasing
+    unsigned char* stg = eng.staging.ensure(4 * W * B + tail);
+    pool.parallel_for(B, [&](size_t b) {
+      uint32_t* bw = reinterpret_cast<uint32_t*>(stg) + b * W;
+      std::memset(bw, 0, 4 * W);
+      int64_t prev = -1;
+      bool inc = true;
+      for (const uint32_t s : roots[b]) {
+        inc &= int64_t(s) > prev;
+        prev = int64_t(s);
+        bw[s >> 5] |= 1u << (s & 31);
       }
-  });
+      increasing[b] = inc ? 1 : 0;
+    });
+  }
   bool bitmap = true;
   for (unsigned char x : increasing) bitmap = bitmap && x;
   {
@@ -227,15 +237,8 @@ void grow_trees(WaveRunner& eng, const TrainParams& P0, ThreadPool& pool,
     uint32_t* hi = reinterpret_cast<uint32_t*>(stg);
     uint64_t* ho = reinterpret_cast<uint64_t*>(stg + id_bytes);
     uint32_t* hc = reinterpret_cast<uint32_t*>(stg + id_bytes + 8 * (B + 1));
-    if (bitmap) {
-      pool.parallel_for(B, [&](size_t b) {
-        uint32_t* bw = hi + b * W;
-        std::memset(bw, 0, 4 * W);
-        for (const uint32_t s : roots[b]) bw[s >> 5] |= 1u << (s & 31);
-      });
-    } else {
+    if (!bitmap)  // some list is not a sorted set: the ids themselves
       pool.parallel_for(B, [&](size_t b) { std::memcpy(hi + off[b], roots[b].data(), 4 * roots[b].size()); });
-    }
     std::memcpy(ho, off.data(), 8 * (B + 1));
     DevBuf<uint32_t>& d_cnt = eng.root_counts;
     d_cnt.ensure(size_t(k) * B);
