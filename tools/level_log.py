@@ -1,3 +1,8 @@
+"""Per-wave host / GPU timeline of three 100-tree steps at 1M x 4096 (stderr):
+  SOFG_LEVEL_LOG=1 [WORKERS=<host threads>] python tools/level_log.py
+prints one line per wave (prep, submit, speculative draws, GPU wait, collect, child creation; the
+log synchronises each wave, so per-step times are slightly higher than in the bench) and the
+host phase totals (ctx.stats())."""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import paper_2603_00326_b200 as sofg
