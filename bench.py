@@ -11,7 +11,8 @@ value  device-timed trees/s over all ranks (CUDA events on the trainer's stream,
 e2e    the same through the C ABI with host buffers: every step uploads the 16.4 GB table from
        page-locked memory (sofg_upload_dataset), trains, and reads the forest back; a second context
        on the same GPU holds a second resident table so step s+1's upload overlaps step s's training
-       (--e2e-serial: upload, then train).
+       (--e2e-serial: upload, then train); each context trains a contiguous half of the tree
+       ranges. Per-step wall times in e2e.step_ms (the first step pays the unhidden upload).
 roofline  the dominant kernel, k_row_sweep (projection sweep): algorithmic bytes per launch (table
        rows streamed + projected rows written + term lists read) over its CUDA-event time, against
        MEASURED_PEAKS.json's HBM copy bandwidth, measured in one extra untimed profile step; traffic =
