@@ -323,25 +323,21 @@ __global__ void __launch_bounds__(SOFG_DRAW_THREADS) k_hist_draws(
     const uint64_t want = min(uint64_t(avail), total - q);
     if (tid == 0) s_first_bad = 0x7fffffff;
     __syncthreads();
-    // first pass: find the first rejection within [cur, cur+want)
+    // One pass over [cur, cur+want): every draw is written as if no earlier output in the window
+    // were rejected, and the first rejection is found. Draws at or after it are shifted by that
+    // rejected output; they are rewritten by the next windows, which start right after it and
+    // write every later position again in order (rejections are rare: range <= n << 2^64).
     for (int o = tid; o < int(want); o += blockDim.x) {
       const uint64_t x = mt_temper(cur_blk[cur + o]);
       const uint64_t qq = q + uint64_t(o);
       const uint32_t i = uint32_t(qq % m);
       uint64_t t;
       if (!lemire_accept(x, uint64_t(n - m + i) + 1, &t)) atomicMin(&s_first_bad, o);
+      out[qq] = uint32_t(t);
     }
     __syncthreads();
     const int fb = s_first_bad;
     const int take = fb == 0x7fffffff ? int(want) : fb;
-    for (int o = tid; o < take; o += blockDim.x) {
-      const uint64_t x = mt_temper(cur_blk[cur + o]);
-      const uint64_t qq = q + uint64_t(o);
-      const uint32_t i = uint32_t(qq % m);
-      uint64_t t;
-      lemire_accept(x, uint64_t(n - m + i) + 1, &t);
-      out[qq] = uint32_t(t);
-    }
     q += uint64_t(take);
     cur += take + (fb == 0x7fffffff ? 0 : 1);
     used += uint64_t(take) + (fb == 0x7fffffff ? 0 : 1);
