@@ -109,6 +109,16 @@ struct WarpStream {
     nxt_ready = false;
   }
 
+  // Same, for a state whose seeded words the caller already wrote to storage[312..624).
+  __device__ __forceinline__ void init_preseeded(uint64_t* storage, int lane) {
+    cur_blk = storage;
+    nxt_blk = storage + kMtN;
+    __syncwarp();
+    mt_twist_warp(nxt_blk, cur_blk, lane);
+    cur = 0;
+    nxt_ready = false;
+  }
+
   __device__ __forceinline__ void ensure_next(int lane) {
     if (!nxt_ready) {
       mt_twist_warp(cur_blk, nxt_blk, lane);

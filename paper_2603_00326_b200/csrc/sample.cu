@@ -26,7 +26,7 @@
 #define SOFG_BND_WARPS 4  // (node, row) warps per CTA of k_hist_boundaries
 #endif
 #ifndef SOFG_SAMPLE_WARPS
-#define SOFG_SAMPLE_WARPS 2  // warps (nodes) per CTA of k_sample_projection (8: 54.6, 4: 47.8, 2: 45.1 ms per step)
+#define SOFG_SAMPLE_WARPS 4  // warps (nodes) per CTA of k_sample_projection (8: 54.6, 4: 47.8, 2: 45.1 ms per step with per-warp seeding; seeded by one warp for the CTA: 8: 45.0, 4: 38.6, 2: 44.7)
 #endif
 #include "mt64.cuh"
 
@@ -45,9 +45,19 @@ __global__ void __launch_bounds__(32 * SOFG_SAMPLE_WARPS) k_sample_projection(
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int node = blockIdx.x * (blockDim.x >> 5) + wib;
-  if (node >= n_nodes) return;
   // dense matrices (large z): the cell sets live in global scratch instead of shared memory
   const size_t per_warp = size_t(2 * kMtN) * 8 + (gkeys ? 0 : size_t(2 * zpad) * 4);
+  // The engines' sequential seeding (311 dependent steps each) for all of the CTA's nodes at once,
+  // lane j of warp 0 for node j: one warp instruction advances every node's recurrence, where a
+  // lane-0-per-warp seeding spent the same instruction count on each node alone.
+  if (wib == 0 && lane < int(blockDim.x >> 5)) {
+    const int nj = int(blockIdx.x * (blockDim.x >> 5)) + lane;
+    if (nj < n_nodes && !(nodes[nj].flags & kNodeGivenCsr))
+      mt_seed_lane(reinterpret_cast<uint64_t*>(smem_raw + per_warp * size_t(lane)) + kMtN,
+                   split_mix64(nodes[nj].seed));
+  }
+  __syncthreads();
+  if (node >= n_nodes) return;
   unsigned char* base = smem_raw + per_warp * wib;
   uint64_t* blk = reinterpret_cast<uint64_t*>(base);
   uint32_t* keys = gkeys ? gkeys + size_t(node) * 2 * zpad
@@ -63,7 +73,7 @@ __global__ void __launch_bounds__(32 * SOFG_SAMPLE_WARPS) k_sample_projection(
   while (zp < int(z)) zp <<= 1;
   const uint64_t cells = uint64_t(R) * d;
   WarpStream s;
-  s.init_seeded(blk, nd.seed, lane);
+  s.init_preseeded(blk, lane);
   s.skip(nd.pos, lane);
   uint64_t used = nd.pos;
 
