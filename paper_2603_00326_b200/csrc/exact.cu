@@ -19,6 +19,9 @@
 #include "dev_util.cuh"
 #include "kernels.hpp"
 
+#ifndef SOFG_PRUNE_MINB
+#define SOFG_PRUNE_MINB 0  // min CTAs per SM of the prune pass (0: no register cap; 9: 120.6 vs 121.7 ms, within noise)
+#endif
 #ifndef SOFG_TEAM_MINB
 #define SOFG_TEAM_MINB 4  // min CTAs per SM of the team splitters (3: 40.2, 4: 37.1 ms per step at <= 512 samples)
 #endif
@@ -283,7 +286,7 @@ __device__ __forceinline__ double x_at(const double* __restrict__ xl, uint32_t l
 // shared memory.
 // kPB value buckets per row (32 or 64), kPBE per lane.
 template <int kPB, int KC>
-__global__ void __launch_bounds__(128) k_exact_prune(
+__global__ void __launch_bounds__(128, SOFG_PRUNE_MINB) k_exact_prune(
     const NodeIn* __restrict__ nodes, const uint32_t* __restrict__ list, int n_list, uint32_t R,
     const uint32_t* __restrict__ row_ptr, const uint8_t* __restrict__ lab,
     const uint64_t* __restrict__ gbase, const float* __restrict__ G,
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(128) k_exact_prune(
     int k) {
   constexpr int GR = 8;
   constexpr int kPBE = kPB / 32;
-  __shared__ uint32_t s_cnt[4][GR][kPB][KC];
+  __shared__ __align__(16) uint32_t s_cnt[4][GR][kPB][KC];
   // pivot i at word i + i/32: positions i and i+32 fall in different banks (a search step's probes
   // are spread over both halves)
   constexpr int kPP = kPB + kPB / 32;
@@ -360,6 +363,9 @@ __global__ void __launch_bounds__(128) k_exact_prune(
   __syncwarp();
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   double xbest = inf;
+  // Row g's lane partial bounds go to the row's own (then dead) bucket counters; one transposed
+  // reduction over all rows at the end replaces a warp-wide shuffle reduction per row.
+  unsigned scored = 0;
 #pragma unroll 1
   for (int g = 0; g < GR; ++g) {
     const uint32_t r = r0 + uint32_t(g);
@@ -431,9 +437,24 @@ __global__ void __launch_bounds__(128) k_exact_prune(
       xs0 = xat(z);
     }
     lb = fmin(lb, xs0);
-    lb = warp_min_f64(fmin(lb, xp));
     xbest = fmin(xbest, xp);
-    if (lane == 0) *out = __double2float_rd(lb);  // rounded down: a conservative bound
+    __syncwarp();  // every lane has read row g's counters
+    reinterpret_cast<double*>(&s_cnt[w][g][0][0])[lane] = fmin(lb, xp);  // 256 bytes: the whole row (kPB = 32, KC = 2) or part of it
+    scored |= 1u << g;
+  }
+  __syncwarp();
+  {  // lanes 4g .. 4g + 3 reduce row g's 32 partials: 8 each, then two shuffle steps
+    const int g = lane >> 2, part = lane & 3;
+    double m = inf;
+    if (g < GR && ((scored >> g) & 1u)) {
+      const double* pg = reinterpret_cast<const double*>(&s_cnt[w][g][0][0]) + 8 * part;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m = fmin(m, pg[i]);
+    }
+    m = fmin(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmin(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    if (part == 0 && g < GR && ((scored >> g) & 1u))
+      rowlb[size_t(li) * R + r0 + uint32_t(g)] = __double2float_rd(m);  // rounded down: a conservative bound
   }
   xbest = warp_min_f64(xbest);
   if (lane == 0 && xbest < inf) atomicMin(xstar + li, (unsigned long long)__double_as_longlong(xbest));
