@@ -414,12 +414,6 @@ void WaveRunner::submit(const WaveSpec& w) {
     void* d_aug = aug_.ensure(abytes);
     pend_sweep_bytes_ = double(D.n) * double(D.ldr) * 4.0 + double(g_total) * 4.0 + double(abytes);
     uint16_t* d_qs = qsplit_.ensure(size_t(N) * 4);
-    cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, d_qs, st_), "aug_build");
-    mark("sweep_prep");
-    if (uint64_t(N) > stats.sweep_widest_nodes) {
-      stats.sweep_widest_nodes = uint64_t(N);
-      row_sweep_variant(w.B, w.d, &stats.sweep_cta_threads, &stats.sweep_entry_bytes);
-    }
     // Pipelined sweep (sweep_pipe.cu) when samples carry enough pairs to fill a ticket stream;
     // the chunked kernel below it for sparse waves.
     static const double pipe_min = std::getenv("SOFG_SWEEP_PIPE_MIN") ? std::atof(std::getenv("SOFG_SWEEP_PIPE_MIN")) : 16.0;
@@ -427,12 +421,18 @@ void WaveRunner::submit(const WaveSpec& w) {
     // (pair records hold 32-bit V block (/ 8) and term-list offsets)
     const bool pipe = pairs_per_sample >= pipe_min && row_sweep_pipe_fits(D.ldr, w.B, R) &&
                       g_total / 8 < (uint64_t(1) << 32) && abytes / (aug_narrow(w.d) ? 2 : 4) < (uint64_t(1) << 32);
+    uint32_t* d_pn = pipe ? pnode_.ensure(size_t(N) * 4) : nullptr;
+    cuda_check(launch_aug_build(d_nodes, N, d_terms, d_rp, R, w.d, d_aug, d_qs, d_gbase, d_pn, st_), "aug_build");
+    mark("sweep_prep");
+    if (uint64_t(N) > stats.sweep_widest_nodes) {
+      stats.sweep_widest_nodes = uint64_t(N);
+      row_sweep_variant(w.B, w.d, &stats.sweep_cta_threads, &stats.sweep_entry_bytes);
+    }
     if (pipe) {
       const uint32_t PB = (w.B + 1u) & ~1u;
       void* d_recs = recs_.ensure(size_t(D.n) * PB * pair_rec_bytes());
       uint32_t* d_pcnt = pcnt_.ensure(size_t(D.n));
-      cuda_check(launch_pair_build(w.inv, w.B, uint32_t(D.n), d_pos_node, d_nodes, d_gbase, d_qs, R, w.d, d_recs,
-                                   d_pcnt, n_sm_, st_),
+      cuda_check(launch_pair_build(w.inv, w.B, uint32_t(D.n), d_pos_node, d_pn, R, w.d, d_recs, d_pcnt, n_sm_, st_),
                  "pair_build");
       mark("pair_build");
       cuda_check(launch_row_sweep_pipe(D.XR.p, D.ldr, uint32_t(D.n), d_recs, d_pcnt, w.B, d_aug, R, w.d, d_G,

@@ -292,6 +292,7 @@ class WaveRunner {
   DevBuf<uint32_t> pos_node_;  // level position -> wave node (sweep mode)
   DevBuf<unsigned char> aug_;  // augmented term lists (sweep mode)
   DevBuf<uint16_t> qsplit_;    // per node: the term lists' quarter boundaries (sweep mode)
+  DevBuf<uint32_t> pnode_;     // per node: 16-byte pair-record template (pipelined sweep)
   DevBuf<unsigned char> recs_;  // per-sample pair lists (pipelined sweep)
   DevBuf<uint32_t> pcnt_;       // pairs per sample (pipelined sweep)
   Scratch scratch_;                    // launch-sized temporaries (dense projections, exact_big)

@@ -72,9 +72,11 @@ cudaError_t launch_inv_init(const uint32_t* idx, const uint64_t* off, uint32_t B
 cudaError_t launch_pos_fill(const NodeIn* nodes, const Tile* tiles, int n_tiles, uint64_t total,
                             uint32_t* pos_node, cudaStream_t st);
 size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d);
+// pnode (optional, 16 bytes per node): what a pair record of the node needs, in one load —
+// {V block of the node's position 0 (/ 8, mod 2^32), term-list block offset, quarter boundaries}
 cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
                              const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
-                             uint16_t* qsplit, cudaStream_t st);
+                             uint16_t* qsplit, const uint64_t* vbase, uint32_t* pnode, cudaStream_t st);
 size_t row_sweep_smem(uint64_t ldr, uint32_t B, uint32_t R);
 void row_sweep_variant(uint32_t B, uint32_t d, uint32_t* cta_threads, uint32_t* entry_bytes);
 bool aug_narrow(uint32_t d);  // 16-bit term entries (d < 8192)
@@ -82,9 +84,8 @@ bool aug_narrow(uint32_t d);  // 16-bit term entries (d < 8192)
 bool row_sweep_pipe_fits(uint64_t ldr, uint32_t B, uint32_t R);
 size_t pair_rec_bytes();
 cudaError_t launch_pair_build(const uint32_t* inv, uint32_t B, uint32_t N, const uint32_t* pos_node,
-                              const NodeIn* nodes, const uint64_t* vbase, const uint16_t* qsplit,
-                              uint32_t R, uint32_t d, void* recs, uint32_t* pcnt, int n_sm,
-                              cudaStream_t st);
+                              const uint32_t* pnode, uint32_t R, uint32_t d, void* recs, uint32_t* pcnt,
+                              int n_sm, cudaStream_t st);
 cudaError_t launch_row_sweep_pipe(const float* XR, uint64_t ldr, uint32_t N, const void* recs,
                                   const uint32_t* pcnt, uint32_t B, const void* aug, uint32_t R,
                                   uint32_t d, float* V, int n_sm, cudaStream_t st);

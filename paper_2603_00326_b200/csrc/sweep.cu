@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
                                                    const uint32_t* __restrict__ terms,
                                                    const uint32_t* __restrict__ row_ptr, uint32_t R,
                                                    uint32_t d, E* __restrict__ aug,
-                                                   uint16_t* __restrict__ qsplit) {
+                                                   uint16_t* __restrict__ qsplit,
+                                                   const uint64_t* __restrict__ vbase,
+                                                   uint32_t* __restrict__ pnode) {
   constexpr uint32_t A = 16 / sizeof(E);
   extern __shared__ uint32_t s_empty_pre[];  // [4 warps][R + 1]: empty rows before row r
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -132,6 +134,16 @@ __global__ void __launch_bounds__(128) k_aug_build(const NodeIn* __restrict__ no
     qs[c] = min(below, R);
   }
   if (lane < kQ) qsplit[size_t(node) * kQ + lane] = uint16_t(lane + 1 < kQ ? qs[lane + 1] : R);
+  static_assert(kQ == 4, "pnode packs four quarter boundaries");
+  if (pnode && lane == 0) {  // pair record of level position p: x + p * Rp / 8, y, z, w
+    const uint32_t Rp8 = vpitch(R) / 8;
+    uint4 pn;
+    pn.x = uint32_t(__ldg(vbase + node) >> 3) - nd.begin * Rp8;  // mod 2^32: the records fit 32 bits
+    pn.y = uint32_t(aug_off<E>(nd.term_off, uint32_t(node), R));
+    pn.z = qs[1] | (qs[2] << 16);
+    pn.w = qs[3] | (R << 16);
+    reinterpret_cast<uint4*>(pnode)[node] = pn;
+  }
   // element e of list c -> entry ((e / A) * kQ + c) * A + e % A of the node block
   auto at = [&](uint32_t c, uint32_t e) { return ((e / A) * kQ + c) * A + (e % A); };
   for (uint32_t r = uint32_t(lane); r < R; r += 32) {
@@ -374,16 +386,16 @@ size_t aug_bytes(uint64_t total_terms, uint32_t n_nodes, uint32_t R, uint32_t d)
 
 cudaError_t launch_aug_build(const NodeIn* nodes, int n_nodes, const uint32_t* terms,
                              const uint32_t* row_ptr, uint32_t R, uint32_t d, void* aug,
-                             uint16_t* qsplit, cudaStream_t st) {
+                             uint16_t* qsplit, const uint64_t* vbase, uint32_t* pnode, cudaStream_t st) {
   if (n_nodes == 0) return cudaSuccess;
   if (R > 65535) return cudaErrorInvalidValue;
   const size_t smem = size_t(4) * (R + 1) * 4;
   if (aug_narrow(d))
     dev::k_aug_build<uint16_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
-        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint16_t*>(aug), qsplit);
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint16_t*>(aug), qsplit, vbase, pnode);
   else
     dev::k_aug_build<uint32_t><<<(n_nodes + 3) / 4, 128, smem, st>>>(
-        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint32_t*>(aug), qsplit);
+        nodes, n_nodes, terms, row_ptr, R, d, static_cast<uint32_t*>(aug), qsplit, vbase, pnode);
   return cudaGetLastError();
 }
 

@@ -81,18 +81,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ---- pair lists ----------------------------------------------------------------------------
-template <typename E>
 __global__ void __launch_bounds__(256) k_pair_build(const uint32_t* __restrict__ inv, uint32_t B,
                                                     uint32_t N, const uint32_t* __restrict__ pos_node,
-                                                    const NodeIn* __restrict__ nodes,
-                                                    const uint64_t* __restrict__ vbase,
-                                                    const uint16_t* __restrict__ qsplit, uint32_t R,
+                                                    const uint4* __restrict__ pnode, uint32_t R,
                                                     uint32_t PB, PairRec* __restrict__ recs,
                                                     uint32_t* __restrict__ pcnt) {
   const int lane = threadIdx.x & 31;
-  const uint32_t Rp = vpitch(R);
+  const uint32_t Rp8 = vpitch(R) / 8;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  constexpr int C = 4;  // 32-tree chunks whose dependent load chains (inv -> pos_node -> node) overlap
+  constexpr int C = 4;  // 32-tree chunks whose dependent load chains (inv -> pos_node -> pnode) overlap
   for (uint32_t s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < N; s += warps) {
     uint32_t cnt = 0;
     for (uint32_t b00 = 0; b00 < B; b00 += 32 * C) {
@@ -104,28 +101,17 @@ __global__ void __launch_bounds__(256) k_pair_build(const uint32_t* __restrict__
       }
 #pragma unroll
       for (int c = 0; c < C; ++c) node[c] = p[c] != ~0u ? __ldg(pos_node + p[c]) : ~0u;
-      uint32_t beg[C], toff[C];
-      uint64_t vb[C];
-      uint2 qv[C];
+      uint4 pn[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        if (node[c] != ~0u) {
-          beg[c] = __ldg(&nodes[node[c]].begin);
-          toff[c] = __ldg(&nodes[node[c]].term_off);
-          vb[c] = __ldg(vbase + node[c]);
-          qv[c] = __ldg(reinterpret_cast<const uint2*>(qsplit) + node[c]);
-        }
-      }
+      for (int c = 0; c < C; ++c)
+        if (node[c] != ~0u) pn[c] = __ldg(pnode + node[c]);  // one 16-byte record per node (aug_build)
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const bool act = node[c] != ~0u;
         const unsigned m = __ballot_sync(0xffffffffu, act);
         if (act) {
-          uint4 rec;
-          rec.x = uint32_t((vb[c] + uint64_t(p[c] - beg[c]) * Rp) >> 3);
-          rec.y = uint32_t(aug_off<E>(toff[c], node[c], R));
-          rec.z = qv[c].x;
-          rec.w = qv[c].y;
+          uint4 rec = pn[c];
+          rec.x += p[c] * Rp8;  // (V block of position 0 + p * Rp) / 8, mod 2^32
           const uint32_t idx = cnt + __popc(m & ((1u << lane) - 1u));
           *reinterpret_cast<uint4*>(recs + uint64_t(s) * PB + idx) = rec;
         }
@@ -289,16 +275,13 @@ bool row_sweep_pipe_fits(uint64_t ldr, uint32_t B, uint32_t R) { return pipe_sta
 size_t pair_rec_bytes() { return sizeof(dev::PairRec); }
 
 cudaError_t launch_pair_build(const uint32_t* inv, uint32_t B, uint32_t N, const uint32_t* pos_node,
-                              const NodeIn* nodes, const uint64_t* vbase, const uint16_t* qsplit, uint32_t R,
-                              uint32_t d, void* recs, uint32_t* pcnt, int n_sm, cudaStream_t st) {
+                              const uint32_t* pnode, uint32_t R, uint32_t d, void* recs, uint32_t* pcnt,
+                              int n_sm, cudaStream_t st) {
+  (void)d;
   const uint32_t PB = pipe_pb(B);
   const unsigned grid = unsigned(std::min<uint64_t>((uint64_t(N) + 7) / 8, uint64_t(n_sm) * 16));
-  if (aug_narrow(d))
-    dev::k_pair_build<uint16_t><<<grid, 256, 0, st>>>(inv, B, N, pos_node, nodes, vbase, qsplit, R, PB,
-                                                      static_cast<dev::PairRec*>(recs), pcnt);
-  else
-    dev::k_pair_build<uint32_t><<<grid, 256, 0, st>>>(inv, B, N, pos_node, nodes, vbase, qsplit, R, PB,
-                                                      static_cast<dev::PairRec*>(recs), pcnt);
+  dev::k_pair_build<<<grid, 256, 0, st>>>(inv, B, N, pos_node, reinterpret_cast<const uint4*>(pnode), R, PB,
+                                          static_cast<dev::PairRec*>(recs), pcnt);
   return cudaGetLastError();
 }
 
